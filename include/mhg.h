@@ -1,0 +1,142 @@
+/*
+ * mhg.h -- C ABI of the B200-native Morton-hybrid GF(p) matrix-multiply path.
+ *
+ * This is the drop-in boundary.  The reference (arxiv/paper_1705_04807,
+ * proj/include/mh) has no FFI: its interface is the header API
+ * `mh::mm_oblivious(const Problem&) -> Counters` (multiply.hpp:297-308) over
+ * three `Sub` views (submatrix.hpp:13-18) of `Matrix` containers
+ * (matrix.hpp:13-39).  Each entry point below names the reference interface it
+ * replaces.  A C++ mirror of the reference header API (namespace mh, same
+ * names) is layered on top in include/mh/ (C++ headers); INTEGRATION.md shows the
+ * bindings.
+ *
+ * Conventions
+ *  - Plain C types only: no torch, no CUDA types.  `stream` is a cudaStream_t
+ *    passed as void* (NULL = legacy default stream).
+ *  - Every call returns an mhg_status; MHG_OK == 0.  The status codes map one
+ *    to one onto the exception classes the reference throws
+ *    (std::invalid_argument, std::out_of_range, std::logic_error); the message
+ *    of the last failure on the calling thread is mhg_last_error().
+ *  - Device work is asynchronous on `stream` unless the name says otherwise.
+ *  - There is no CPU fallback: on a machine without an sm_100 GPU every compute
+ *    entry point fails with MHG_ERR_DEVICE.
+ */
+#ifndef MHG_H
+#define MHG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    MHG_OK = 0,
+    MHG_ERR_INVALID_ARGUMENT = 1, /* std::invalid_argument in the reference */
+    MHG_ERR_OUT_OF_RANGE = 2,     /* std::out_of_range */
+    MHG_ERR_LOGIC = 3,            /* std::logic_error */
+    MHG_ERR_DEVICE = 4,           /* CUDA failure / no sm_100 device */
+    MHG_ERR_UNSUPPORTED = 5       /* valid for the reference, not for this build */
+} mhg_status;
+
+/* Operation applied to the output view.  The reference only accumulates
+ * (multiply.hpp:9-10); SUB is the TU/TURBO Schur update C -= A*B and SET is
+ * C = A*B (view cells only). */
+typedef enum { MHG_OP_ADD = 0, MHG_OP_SUB = 1, MHG_OP_SET = 2 } mhg_op;
+
+/* Opaque device-resident Morton-hybrid container (replaces mh::Matrix,
+ * matrix.hpp:13-39): n x n uint32 residues mod q in the reference's flat
+ * order (tile Z-index * t*t + row-major offset inside the tile,
+ * layout.hpp:80-85), so uploads, downloads and parity compares are memcpys. */
+typedef struct mhg_matrix_s *mhg_matrix;
+
+/* A view: the reference's Sub 4-tuple (M, sigma, r, c), submatrix.hpp:13-18. */
+typedef struct {
+    mhg_matrix mat;
+    uint64_t origin; /* flat index of the first entry */
+    uint64_t rows;
+    uint64_t cols;
+} mhg_view;
+
+/* The reference's Counters (multiply.hpp:39-45), computed in closed form by
+ * the planner for the oblivious decomposition (identical values). */
+typedef struct {
+    uint64_t base_case_calls;
+    uint64_t scalar_macs;
+    uint64_t encode_calls;
+    uint64_t recursive_calls;
+    uint64_t max_consecutive_jump;
+} mhg_counters;
+
+/* ---- errors / device ---- */
+const char *mhg_last_error(void);
+/* Fails with MHG_ERR_DEVICE unless the current device is sm_100. */
+mhg_status mhg_device_check(void);
+const char *mhg_version(void);
+
+/* ---- layout codec (layout.hpp:42-99): host-side, no device needed ---- */
+mhg_status mhg_layout_check(uint64_t n, uint64_t t);                 /* Layout(n,t) ctor :50-62 */
+mhg_status mhg_encode(uint64_t n, uint64_t t, uint64_t i, uint64_t j, uint64_t *z); /* :80-85 */
+mhg_status mhg_extract(uint64_t n, uint64_t t, uint64_t z, uint64_t *i, uint64_t *j); /* :88-99 */
+mhg_status mhg_modulus_check(uint32_t q);                            /* Modulus(q), field.hpp:28-34 */
+
+/* ---- containers (matrix.hpp) ---- */
+/* Matrix(Layout(n,t), Modulus(q)): device allocation, zero filled. */
+mhg_status mhg_matrix_create(uint64_t n, uint64_t t, uint32_t q, mhg_matrix *out);
+/* Non-owning container over an existing device buffer of n*n uint32. */
+mhg_status mhg_matrix_wrap(uint64_t n, uint64_t t, uint32_t q, void *device_cells, mhg_matrix *out);
+mhg_status mhg_matrix_destroy(mhg_matrix m);
+mhg_status mhg_matrix_info(mhg_matrix m, uint64_t *n, uint64_t *t, uint32_t *q, void **device_cells);
+/* Flat Morton-hybrid order copies (Matrix::cells(), matrix.hpp:27-28). */
+mhg_status mhg_matrix_upload(mhg_matrix m, const uint32_t *host_cells, void *stream);
+mhg_status mhg_matrix_download(mhg_matrix m, uint32_t *host_cells, void *stream);
+/* from_row_major / to_row_major (matrix.hpp:44-67) on DEVICE buffers of n*n
+ * row-major uint32 (K1 conversion kernels).  from_row_major's residue check
+ * (:52-53) is applied on the device: an out-of-range residue fails the call
+ * with MHG_ERR_INVALID_ARGUMENT (synchronous on `stream`). */
+mhg_status mhg_rowmajor_to_mh(mhg_matrix dst, const uint32_t *device_rows, void *stream);
+mhg_status mhg_mh_to_rowmajor(mhg_matrix src, uint32_t *device_rows, void *stream);
+
+/* ---- multiply (multiply.hpp) ---- */
+/* out op= lhs * rhs over the three views, computed on the GPU with the int8
+ * limb-split tcgen05 kernels.  Validation follows check_problem
+ * (multiply.hpp:55-66) and mm_oblivious's layout guard (:299-301); an empty
+ * problem is a no-op with zero Counters (:303).  `ctr` may be NULL.
+ * Replaces mh::mm_oblivious (multiply.hpp:297-308). */
+mhg_status mhg_mm(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, mhg_counters *ctr,
+                  void *stream);
+
+/* Counters only (no device work): the closed form of the oblivious recursion. */
+mhg_status mhg_counters_oblivious(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_counters *ctr);
+/* Same, from the raw layout and view origins (three same-layout containers);
+ * pure host planner, usable without a GPU. */
+mhg_status mhg_counters_layout(uint64_t n, uint64_t t, uint64_t out_origin, uint64_t lhs_origin,
+                               uint64_t rhs_origin, uint64_t rows, uint64_t inner, uint64_t cols,
+                               mhg_counters *ctr);
+
+/* Reusable plan: validation, offset tables, packing workspace and a captured
+ * CUDA graph (pack lhs, pack rhs, GEMM + fused epilogue) replayed by
+ * mhg_plan_run.  The views' containers must outlive the plan. */
+typedef struct mhg_plan_s *mhg_plan;
+mhg_status mhg_plan_create(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, mhg_plan *plan);
+mhg_status mhg_plan_run(mhg_plan plan, void *stream);
+mhg_status mhg_plan_counters(mhg_plan plan, mhg_counters *ctr);
+/* Kernel launches per run and the planner's description (tiles, chunks, limbs). */
+mhg_status mhg_plan_info(mhg_plan plan, uint64_t *launches, uint64_t *tiles, uint32_t *limbs,
+                         uint32_t *k_chunks, uint64_t *workspace_bytes);
+mhg_status mhg_plan_destroy(mhg_plan plan);
+
+/* ---- diagnostics for tests / bench ---- */
+/* Host helper: the limb representation parameters the planner picks for q
+ * (number of int8 limbs, representative threshold, max K per int32 chunk). */
+mhg_status mhg_limb_params(uint32_t q, uint32_t *limbs, uint32_t *threshold, uint64_t *k_max);
+/* Times `iters` replays of a plan's GEMM kernel alone (CUDA events on
+ * `stream`), returns the mean ms per launch in *ms. */
+mhg_status mhg_plan_time_gemm(mhg_plan plan, int iters, void *stream, float *ms);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MHG_H */

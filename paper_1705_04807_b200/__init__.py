@@ -1,0 +1,401 @@
+"""B200-native Morton-hybrid GF(p) matrix multiplication (C <- C +/- A*B mod p).
+
+Python mirror of the reference's header API (arxiv/paper_1705_04807,
+proj/include/mh) over the C ABI of libmhg.so (include/mhg.h).  Names and
+argument meanings follow the reference:
+
+    Layout(n, t), encode / extract_i / extract_j        layout.hpp:42-99
+    Modulus(q), Fp arithmetic                            field.hpp:23-55
+    Matrix(layout, modulus), from_row_major, to_row_major  matrix.hpp:13-67
+    Sub(mat, origin, rows, cols)                         submatrix.hpp:13-18
+    Problem(a=out, b=lhs, c=rhs), Counters               multiply.hpp:39-53
+    mm_oblivious(problem) -> Counters                    multiply.hpp:297-308
+
+Error behaviour mirrors the reference's exception classes:
+    std::invalid_argument -> InvalidArgument (a ValueError)
+    std::out_of_range     -> OutOfRange      (an IndexError)
+    std::logic_error      -> LogicError      (a RuntimeError)
+
+All compute runs in the sm_100a kernels of libmhg.so.  There is no CPU
+fallback: importing works anywhere (codec/validation are host code), but any
+device call fails loudly with DeviceError when the library or an sm_100 GPU is
+missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional
+
+import numpy as np
+
+__all__ = [
+    "InvalidArgument", "OutOfRange", "LogicError", "DeviceError", "Unsupported",
+    "Layout", "Modulus", "Matrix", "Sub", "Problem", "Counters", "Plan",
+    "encode", "extract_i", "extract_j", "from_row_major", "to_row_major",
+    "mm_oblivious", "mm", "counters_oblivious", "counters_layout", "limb_params", "lib", "LIB_PATH",
+    "OP_ADD", "OP_SUB", "OP_SET",
+]
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libmhg.so")
+OP_ADD, OP_SUB, OP_SET = 0, 1, 2
+
+
+class InvalidArgument(ValueError):
+    """std::invalid_argument"""
+
+
+class OutOfRange(IndexError):
+    """std::out_of_range"""
+
+
+class LogicError(RuntimeError):
+    """std::logic_error"""
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure, missing library or no sm_100 device (no fallback)."""
+
+
+class Unsupported(RuntimeError):
+    """Valid for the reference, not supported by this build."""
+
+
+_ERR = {1: InvalidArgument, 2: OutOfRange, 3: LogicError, 4: DeviceError, 5: Unsupported}
+
+
+class _View(C.Structure):
+    _fields_ = [("mat", C.c_void_p), ("origin", C.c_uint64), ("rows", C.c_uint64),
+                ("cols", C.c_uint64)]
+
+
+class Counters(C.Structure):
+    """multiply.hpp:39-45"""
+
+    _fields_ = [("base_case_calls", C.c_uint64), ("scalar_macs", C.c_uint64),
+                ("encode_calls", C.c_uint64), ("recursive_calls", C.c_uint64),
+                ("max_consecutive_jump", C.c_uint64)]
+
+    def as_tuple(self):
+        return (self.base_case_calls, self.scalar_macs, self.encode_calls,
+                self.recursive_calls, self.max_consecutive_jump)
+
+    def __repr__(self):
+        return "Counters(%s)" % ", ".join(f"{n}={getattr(self, n)}" for n, _ in self._fields_)
+
+
+_lib = None
+
+
+def lib():
+    """Load libmhg.so (built in-tree by __graft_entry__.build() / make)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise DeviceError(f"{LIB_PATH} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = C.CDLL(LIB_PATH)
+    u64, u32, vp = C.c_uint64, C.c_uint32, C.c_void_p
+    P = C.POINTER
+    sigs = {
+        "mhg_last_error": ([], C.c_char_p),
+        "mhg_version": ([], C.c_char_p),
+        "mhg_device_check": ([], C.c_int),
+        "mhg_layout_check": ([u64, u64], C.c_int),
+        "mhg_modulus_check": ([u32], C.c_int),
+        "mhg_encode": ([u64, u64, u64, u64, P(u64)], C.c_int),
+        "mhg_extract": ([u64, u64, u64, P(u64), P(u64)], C.c_int),
+        "mhg_matrix_create": ([u64, u64, u32, P(vp)], C.c_int),
+        "mhg_matrix_wrap": ([u64, u64, u32, vp, P(vp)], C.c_int),
+        "mhg_matrix_destroy": ([vp], C.c_int),
+        "mhg_matrix_info": ([vp, P(u64), P(u64), P(u32), P(vp)], C.c_int),
+        "mhg_matrix_upload": ([vp, vp, vp], C.c_int),
+        "mhg_matrix_download": ([vp, vp, vp], C.c_int),
+        "mhg_rowmajor_to_mh": ([vp, vp, vp], C.c_int),
+        "mhg_mh_to_rowmajor": ([vp, vp, vp], C.c_int),
+        "mhg_mm": ([_View, _View, _View, C.c_int, P(Counters), vp], C.c_int),
+        "mhg_counters_oblivious": ([_View, _View, _View, P(Counters)], C.c_int),
+        "mhg_counters_layout": ([u64] * 8 + [P(Counters)], C.c_int),
+        "mhg_plan_create": ([_View, _View, _View, C.c_int, P(vp)], C.c_int),
+        "mhg_plan_run": ([vp, vp], C.c_int),
+        "mhg_plan_counters": ([vp, P(Counters)], C.c_int),
+        "mhg_plan_info": ([vp, P(u64), P(u64), P(u32), P(u32), P(u64)], C.c_int),
+        "mhg_plan_destroy": ([vp], C.c_int),
+        "mhg_limb_params": ([u32, P(u32), P(u32), P(u64)], C.c_int),
+        "mhg_plan_time_gemm": ([vp, C.c_int, vp, P(C.c_float)], C.c_int),
+    }
+    for name, (args, res) in sigs.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def _check(status: int):
+    if status:
+        msg = lib().mhg_last_error().decode(errors="replace")
+        raise _ERR.get(status, DeviceError)(msg)
+
+
+# ------------------------------------------------------------------ codec
+class Layout:
+    """layout.hpp:42-76: n = 2^m * t, tiles in Z order, row-major inside."""
+
+    def __init__(self, n: int, t: int):
+        _check(lib().mhg_layout_check(n, t))
+        self.n, self.t = int(n), int(t)
+        g = n // t
+        self.grid_log2 = g.bit_length() - 1
+        self.tile = t * t
+        self.total = n * n
+
+    def tdiv(self, v):
+        return v // self.t
+
+    def tmod(self, v):
+        return v % self.t
+
+    def __eq__(self, o):
+        return isinstance(o, Layout) and (self.n, self.t) == (o.n, o.t)
+
+    def __repr__(self):
+        return f"Layout(n={self.n}, t={self.t})"
+
+
+def encode(lay: Layout, i: int, j: int) -> int:
+    z = C.c_uint64()
+    _check(lib().mhg_encode(lay.n, lay.t, i, j, C.byref(z)))
+    return z.value
+
+
+def _extract(lay: Layout, z: int):
+    i, j = C.c_uint64(), C.c_uint64()
+    _check(lib().mhg_extract(lay.n, lay.t, z, C.byref(i), C.byref(j)))
+    return i.value, j.value
+
+
+def extract_i(lay: Layout, z: int) -> int:
+    return _extract(lay, z)[0]
+
+
+def extract_j(lay: Layout, z: int) -> int:
+    return _extract(lay, z)[1]
+
+
+class Modulus:
+    """field.hpp:23-35: prime 2 <= q < 2^31."""
+
+    def __init__(self, q: int):
+        _check(lib().mhg_modulus_check(q))
+        self.q = int(q)
+
+    def __repr__(self):
+        return f"Modulus({self.q})"
+
+
+def limb_params(q: int):
+    """(limbs, representative threshold H, max exact K per int32 chunk) for q."""
+    L, H, K = C.c_uint32(), C.c_uint32(), C.c_uint64()
+    _check(lib().mhg_limb_params(q, C.byref(L), C.byref(H), C.byref(K)))
+    return L.value, H.value, K.value
+
+
+def _stream_ptr(stream) -> Optional[int]:
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return int(getattr(stream, "cuda_stream", stream))
+
+
+# -------------------------------------------------------------- container
+class Matrix:
+    """matrix.hpp:13-39: device-resident n x n store in Morton-hybrid order.
+
+    `cells()` downloads the flat store (numpy uint32); `upload(cells)` replaces
+    it.  `device_ptr` exposes the device buffer (e.g. for torch interop).
+    """
+
+    def __init__(self, layout: Layout, modulus: Modulus, *, _wrap_ptr: Optional[int] = None,
+                 _owner=None):
+        self._h = C.c_void_p()
+        if _wrap_ptr is None:
+            _check(lib().mhg_matrix_create(layout.n, layout.t, modulus.q, C.byref(self._h)))
+        else:
+            _check(lib().mhg_matrix_wrap(layout.n, layout.t, modulus.q, C.c_void_p(_wrap_ptr),
+                                         C.byref(self._h)))
+        self._owner = _owner  # keeps a wrapped torch tensor alive
+        self._layout, self._mod = layout, modulus
+        ptr = C.c_void_p()
+        _check(lib().mhg_matrix_info(self._h, None, None, None, C.byref(ptr)))
+        self.device_ptr = ptr.value
+
+    @classmethod
+    def wrap(cls, layout: Layout, modulus: Modulus, device_ptr: int, owner=None) -> "Matrix":
+        """Non-owning container over an existing device buffer of n*n uint32."""
+        return cls(layout, modulus, _wrap_ptr=device_ptr, _owner=owner)
+
+    def layout(self) -> Layout:
+        return self._layout
+
+    def modulus(self) -> Modulus:
+        return self._mod
+
+    @property
+    def handle(self):
+        return self._h
+
+    def cells(self, stream=None) -> np.ndarray:
+        out = np.empty(self._layout.total, dtype=np.uint32)
+        _check(lib().mhg_matrix_download(self._h, out.ctypes.data, _stream_ptr(stream)))
+        if stream is not None:
+            import torch  # synchronise the caller's stream before reading host memory
+            torch.cuda.synchronize()
+        return out
+
+    def upload(self, cells: np.ndarray, stream=None) -> "Matrix":
+        a = np.ascontiguousarray(cells, dtype=np.uint32).reshape(-1)
+        if a.size != self._layout.total:
+            raise InvalidArgument("upload: expected n*n cells")
+        _check(lib().mhg_matrix_upload(self._h, a.ctypes.data, _stream_ptr(stream)))
+        if stream is not None:
+            import torch
+            torch.cuda.synchronize()
+        return self
+
+    def at(self, i: int, j: int) -> int:
+        return int(self.cells()[encode(self._layout, i, j)])
+
+    def __eq__(self, other) -> bool:  # matrix.hpp:30-33
+        return (isinstance(other, Matrix) and self._layout == other._layout
+                and self._mod.q == other._mod.q
+                and np.array_equal(self.cells(), other.cells()))
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().mhg_matrix_destroy(self._h)
+                self._h = C.c_void_p()
+        except Exception:
+            pass
+
+
+def from_row_major(grid: np.ndarray, t: int, mod: Modulus) -> Matrix:
+    """matrix.hpp:44-58, via the K1 conversion kernel (device)."""
+    import torch
+    g = np.ascontiguousarray(grid, dtype=np.uint32)
+    if g.ndim != 2 or g.shape[0] != g.shape[1]:
+        raise InvalidArgument("from_row_major: grid is not square")
+    n = g.shape[0]
+    lay = Layout(n, t)
+    m = Matrix(lay, mod)
+    dev = torch.from_numpy(g.view(np.int32)).cuda()
+    _check(lib().mhg_rowmajor_to_mh(m.handle, dev.data_ptr(), None))
+    return m
+
+
+def to_row_major(m: Matrix) -> np.ndarray:
+    """matrix.hpp:60-67, via the K1 conversion kernel (device)."""
+    import torch
+    n = m.layout().n
+    dev = torch.empty(n * n, dtype=torch.int32, device="cuda")
+    _check(lib().mhg_mh_to_rowmajor(m.handle, dev.data_ptr(), None))
+    torch.cuda.synchronize()
+    return dev.cpu().numpy().view(np.uint32).reshape(n, n)
+
+
+# ------------------------------------------------------------------ views
+@dataclass
+class Sub:
+    """submatrix.hpp:13-18: (container, flat origin, rows, cols)."""
+
+    mat: Optional[Matrix]
+    origin: int = 0
+    rows: int = 0
+    cols: int = 0
+
+    def _c(self) -> _View:
+        return _View(self.mat.handle if self.mat is not None else None, self.origin, self.rows,
+                     self.cols)
+
+
+@dataclass
+class Problem:
+    """multiply.hpp:49-53: a (output) += b (left) * c (right)."""
+
+    a: Sub
+    b: Sub
+    c: Sub
+
+
+def mm(problem: Problem, op: int = OP_ADD, stream=None) -> Counters:
+    """out op= lhs * rhs on the GPU (asynchronous on `stream`; None = default)."""
+    ctr = Counters()
+    _check(lib().mhg_mm(problem.a._c(), problem.b._c(), problem.c._c(), op, C.byref(ctr),
+                        _stream_ptr(stream)))
+    return ctr
+
+
+def mm_oblivious(problem: Problem, stream=None) -> Counters:
+    """Drop-in for mh::mm_oblivious (multiply.hpp:297-308): accumulate, then
+    synchronise so the result is visible like the reference's synchronous call."""
+    ctr = mm(problem, OP_ADD, stream)
+    import torch
+    torch.cuda.synchronize()
+    return ctr
+
+
+def counters_oblivious(problem: Problem) -> Counters:
+    ctr = Counters()
+    _check(lib().mhg_counters_oblivious(problem.a._c(), problem.b._c(), problem.c._c(),
+                                        C.byref(ctr)))
+    return ctr
+
+
+def counters_layout(n, t, out_origin, lhs_origin, rhs_origin, rows, inner, cols) -> Counters:
+    """Planner Counters from raw geometry (host only, no GPU needed)."""
+    ctr = Counters()
+    _check(lib().mhg_counters_layout(n, t, out_origin, lhs_origin, rhs_origin, rows, inner, cols,
+                                     C.byref(ctr)))
+    return ctr
+
+
+class Plan:
+    """Planned multiply replayed as one CUDA graph (pack lhs, pack rhs, GEMM)."""
+
+    def __init__(self, problem: Problem, op: int = OP_ADD):
+        self._h = C.c_void_p()
+        self._problem = problem  # keep containers alive
+        _check(lib().mhg_plan_create(problem.a._c(), problem.b._c(), problem.c._c(), op,
+                                     C.byref(self._h)))
+
+    def run(self, stream=None):
+        _check(lib().mhg_plan_run(self._h, _stream_ptr(stream)))
+
+    def counters(self) -> Counters:
+        c = Counters()
+        _check(lib().mhg_plan_counters(self._h, C.byref(c)))
+        return c
+
+    def info(self) -> dict:
+        la, ti, li, ch, wb = C.c_uint64(), C.c_uint64(), C.c_uint32(), C.c_uint32(), C.c_uint64()
+        _check(lib().mhg_plan_info(self._h, C.byref(la), C.byref(ti), C.byref(li), C.byref(ch),
+                                   C.byref(wb)))
+        return {"launches": la.value, "tiles": ti.value, "limbs": li.value, "k_chunks": ch.value,
+                "workspace_bytes": wb.value}
+
+    def time_gemm(self, iters: int = 10, stream=None) -> float:
+        ms = C.c_float()
+        _check(lib().mhg_plan_time_gemm(self._h, iters, _stream_ptr(stream), C.byref(ms)))
+        return ms.value
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().mhg_plan_destroy(self._h)
+                self._h = C.c_void_p()
+        except Exception:
+            pass

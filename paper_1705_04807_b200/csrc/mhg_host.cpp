@@ -1,0 +1,642 @@
+// mhg_host.cpp -- implementation of the C ABI declared in include/mhg.h.
+//
+// Host responsibilities: validation with the reference's error classes,
+// container handles, the planner (closed-form Counters + task grid), the
+// packing workspace and CUDA-graph capture of a plan.  All arithmetic runs in
+// the sm_100a kernels of mhg_kernels.cu; there is no CPU compute path.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+
+#include "mhg.h"
+#include "mhg_internal.hpp"
+#include "mhg_planner.hpp"
+
+struct mhg_matrix_s {
+    uint64_t n = 0, t = 0;
+    uint32_t q = 0;
+    uint32_t* cells = nullptr;  // device, n*n
+    bool owned = false;
+    int device = 0;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Failure {
+    mhg_status code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(mhg_status code, const std::string& msg) { throw Failure{code, msg}; }
+
+void cuda_check(int err, const char* what) {
+    if (err != 0)
+        fail(MHG_ERR_DEVICE, std::string(what) + ": " + cudaGetErrorString((cudaError_t)err));
+}
+
+template <typename F>
+mhg_status guarded(F&& f) {
+    try {
+        f();
+        return MHG_OK;
+    } catch (const Failure& e) {
+        g_last_error = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return MHG_ERR_DEVICE;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return MHG_ERR_DEVICE;
+    }
+}
+
+// ----------------------------------------------------------------- device
+struct DeviceInfo {
+    int sms = 0;
+    bool ok = false;
+    std::string why;
+};
+
+const DeviceInfo& device_info() {
+    static DeviceInfo info;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaError_t e = cudaGetDevice(&dev);
+        if (e != cudaSuccess) {
+            info.why = std::string("no CUDA device: ") + cudaGetErrorString(e);
+            cudaGetLastError();
+            return;
+        }
+        cudaDeviceProp prop{};
+        e = cudaGetDeviceProperties(&prop, dev);
+        if (e != cudaSuccess) {
+            info.why = std::string("cudaGetDeviceProperties: ") + cudaGetErrorString(e);
+            return;
+        }
+        if (prop.major != 10 || prop.minor != 0) {
+            info.why = "device " + std::string(prop.name) + " is sm_" + std::to_string(prop.major) +
+                       std::to_string(prop.minor) + "; this build only runs on sm_100 (B200)";
+            return;
+        }
+        info.sms = prop.multiProcessorCount;
+        const int ce = mhg::configure_kernels();
+        if (ce != 0) {
+            info.why = std::string("kernel configuration: ") + cudaGetErrorString((cudaError_t)ce);
+            return;
+        }
+        info.ok = true;
+    });
+    return info;
+}
+
+void require_device() {
+    const DeviceInfo& d = device_info();
+    if (!d.ok) fail(MHG_ERR_DEVICE, d.why);
+}
+
+// --------------------------------------------------------------- validation
+// submatrix.hpp:43-51
+mhg::Rect check_view(const mhg_view& v) {
+    if (v.mat == nullptr) fail(MHG_ERR_INVALID_ARGUMENT, "sub-matrix: null container");
+    const uint64_t n = v.mat->n, t = v.mat->t;
+    if (v.origin >= n * n) fail(MHG_ERR_OUT_OF_RANGE, "sub-matrix: origin outside the container");
+    const uint64_t i = mhg::extract_i(t, v.origin), j = mhg::extract_j(t, v.origin);
+    if (i + v.rows > n || j + v.cols > n)
+        fail(MHG_ERR_OUT_OF_RANGE, "sub-matrix: extends past the container edge");
+    return mhg::Rect{i, j, v.rows, v.cols};
+}
+
+bool overlap(const mhg_matrix_s* a, const mhg_matrix_s* b) {
+    const uintptr_t a0 = (uintptr_t)a->cells, a1 = a0 + a->n * a->n * 4;
+    const uintptr_t b0 = (uintptr_t)b->cells, b1 = b0 + b->n * b->n * 4;
+    return a0 < b1 && b0 < a1;
+}
+
+struct Checked {
+    mhg::Rect ro, rl, rr;
+};
+
+// check_problem (multiply.hpp:55-66) + mm_oblivious's layout guard (:299-301)
+Checked check_problem(const mhg_view& out, const mhg_view& lhs, const mhg_view& rhs) {
+    Checked c{check_view(out), check_view(lhs), check_view(rhs)};
+    if (out.mat == lhs.mat || out.mat == rhs.mat || lhs.mat == rhs.mat ||
+        overlap(out.mat, lhs.mat) || overlap(out.mat, rhs.mat) || overlap(lhs.mat, rhs.mat))
+        fail(MHG_ERR_LOGIC, "problem: the three views must live in distinct matrices");
+    if (out.rows != lhs.rows || out.cols != rhs.cols || lhs.cols != rhs.rows)
+        fail(MHG_ERR_LOGIC, "problem: view shapes do not chain");
+    if (out.mat->q != lhs.mat->q || out.mat->q != rhs.mat->q)
+        fail(MHG_ERR_LOGIC, "problem: operands use different moduli");
+    if (out.mat->n != lhs.mat->n || out.mat->n != rhs.mat->n || out.mat->t != lhs.mat->t ||
+        out.mat->t != rhs.mat->t)
+        fail(MHG_ERR_LOGIC, "mm_oblivious: operands must share layout parameters");
+    return c;
+}
+
+mhg::Counters counters_of(const mhg_view& out, const mhg_view&, const mhg_view&,
+                          const Checked& c) {
+    return mhg::oblivious_counters(out.mat->n, out.mat->t, c.ro, c.rl, c.rr);
+}
+
+void put_counters(const mhg::Counters& c, mhg_counters* dst) {
+    if (!dst) return;
+    dst->base_case_calls = c.base_case_calls;
+    dst->scalar_macs = c.scalar_macs;
+    dst->encode_calls = c.encode_calls;
+    dst->recursive_calls = c.recursive_calls;
+    dst->max_consecutive_jump = c.max_consecutive_jump;
+}
+
+// ---------------------------------------------------------------- execution
+// Device memory of one multiply: six offset tables and the two packed operands.
+struct Buffers {
+    uint64_t *out_row = nullptr, *out_col = nullptr, *lhs_row = nullptr, *lhs_col = nullptr,
+             *rhs_row = nullptr, *rhs_col = nullptr;
+    int8_t *apack = nullptr, *bpack = nullptr;
+};
+
+uint64_t align256(uint64_t v) { return (v + 255) & ~uint64_t(255); }
+
+uint64_t buffer_bytes(const Checked& c, const mhg::GemmGeometry& g) {
+    const uint64_t r = c.ro.rows, k = c.rl.cols, cc = c.ro.cols;
+    return align256(8 * r) + align256(8 * cc) + align256(8 * r) + align256(8 * k) + align256(8 * k) +
+           align256(8 * cc) + align256(g.apack_bytes) + align256(g.bpack_bytes);
+}
+
+Buffers carve(uint8_t* base, const Checked& c, const mhg::GemmGeometry& g) {
+    const uint64_t r = c.ro.rows, k = c.rl.cols, cc = c.ro.cols;
+    Buffers b;
+    uint8_t* p = base;
+    auto take = [&](uint64_t bytes) {
+        uint8_t* q = p;
+        p += align256(bytes);
+        return q;
+    };
+    b.out_row = (uint64_t*)take(8 * r);
+    b.out_col = (uint64_t*)take(8 * cc);
+    b.lhs_row = (uint64_t*)take(8 * r);
+    b.lhs_col = (uint64_t*)take(8 * k);
+    b.rhs_row = (uint64_t*)take(8 * k);
+    b.rhs_col = (uint64_t*)take(8 * cc);
+    b.apack = (int8_t*)take(g.apack_bytes);
+    b.bpack = (int8_t*)take(g.bpack_bytes);
+    return b;
+}
+
+void launch_offsets_all(const Buffers& b, const Checked& c, uint64_t t, void* stream) {
+    const mhg::TileGeom g = mhg::tile_geom(t);
+    cuda_check(mhg::launch_offsets(b.out_row, c.ro.i, c.ro.rows, g, 1, stream), "offsets");
+    cuda_check(mhg::launch_offsets(b.out_col, c.ro.j, c.ro.cols, g, 0, stream), "offsets");
+    cuda_check(mhg::launch_offsets(b.lhs_row, c.rl.i, c.rl.rows, g, 1, stream), "offsets");
+    cuda_check(mhg::launch_offsets(b.lhs_col, c.rl.j, c.rl.cols, g, 0, stream), "offsets");
+    cuda_check(mhg::launch_offsets(b.rhs_row, c.rr.i, c.rr.rows, g, 1, stream), "offsets");
+    cuda_check(mhg::launch_offsets(b.rhs_col, c.rr.j, c.rr.cols, g, 0, stream), "offsets");
+}
+
+mhg::GemmParams gemm_params(const Buffers& b, const mhg_view& out, const Checked& c,
+                            const mhg::GemmGeometry& g, mhg_op op) {
+    const uint32_t q = out.mat->q;
+    mhg::GemmParams p{};
+    p.apack = b.apack;
+    p.bpack = b.bpack;
+    p.out = out.mat->cells;
+    p.out_rowoff = b.out_row;
+    p.out_coloff = b.out_col;
+    p.rows = c.ro.rows;
+    p.cols = c.ro.cols;
+    p.Mt = g.Mt;
+    p.Nt = g.Nt;
+    p.Kt = g.Kt;
+    p.KC = g.KC;
+    p.q = q;
+    p.w32 = (uint32_t)((uint64_t(1) << 32) % q);
+    p.mu = ~uint64_t(0) / q;
+    const uint64_t two62 = uint64_t(1) << 62;
+    p.bias = ((two62 + q - 1) / q) * q;
+    p.mode = op == MHG_OP_SET ? 2 : 0;
+    p.vec_ok = out.mat->t % 4 == 0;
+    return p;
+}
+
+// Pack both operands and run the GEMM: 2 pack launches + 1 GEMM launch.
+void launch_multiply(const Buffers& b, const mhg_view& out, const mhg_view& lhs,
+                     const mhg_view& rhs, const Checked& c, const mhg::GemmGeometry& g,
+                     mhg_op op, void* stream) {
+    const mhg::LimbParams lp = mhg::limb_params(out.mat->q);
+    mhg::DigitParams dl{out.mat->q, lp.H, op == MHG_OP_SUB ? 1 : 0};
+    mhg::DigitParams dr{out.mat->q, lp.H, 0};
+    cuda_check(mhg::launch_pack((int)g.L, 0, lhs.mat->cells, b.lhs_row, b.lhs_col, c.rl.rows,
+                                c.rl.cols, mhg::kBM, g.Mt, g.Kt, b.apack, dl, stream),
+               "pack lhs");
+    cuda_check(mhg::launch_pack((int)g.L, 1, rhs.mat->cells, b.rhs_row, b.rhs_col, c.rr.cols,
+                                c.rr.rows, g.W, g.Nt, g.Kt, b.bpack, dr, stream),
+               "pack rhs");
+    const mhg::GemmParams p = gemm_params(b, out, c, g, op);
+    cuda_check(mhg::launch_gemm((int)g.L, p, device_info().sms, stream), "gemm");
+}
+
+// One-shot workspace for mhg_mm: grows on demand; an event orders reuse
+// across streams.
+struct Workspace {
+    std::mutex mu;
+    uint8_t* base = nullptr;
+    uint64_t bytes = 0;
+    cudaEvent_t last = nullptr;
+
+    uint8_t* acquire(uint64_t need, void* stream) {
+        if (!last) cuda_check(cudaEventCreateWithFlags(&last, cudaEventDisableTiming), "event");
+        if (need > bytes) {
+            cuda_check(cudaDeviceSynchronize(), "workspace sync");
+            if (base) cudaFree(base);
+            base = nullptr;
+            bytes = 0;
+            cuda_check(cudaMalloc(&base, need), "workspace alloc");
+            bytes = need;
+        } else {
+            cuda_check(cudaStreamWaitEvent((cudaStream_t)stream, last, 0), "workspace order");
+        }
+        return base;
+    }
+    void release(void* stream) { cuda_check(cudaEventRecord(last, (cudaStream_t)stream), "event"); }
+};
+
+Workspace& workspace() {
+    static Workspace* ws = new Workspace();  // leaked on purpose: no teardown-order issues
+    return *ws;
+}
+
+}  // namespace
+
+// ============================================================ plan object
+struct mhg_plan_s {
+    mhg_view out{}, lhs{}, rhs{};
+    mhg_op op = MHG_OP_ADD;
+    Checked chk{};
+    mhg::GemmGeometry geo{};
+    mhg::Counters ctr{};
+    uint8_t* mem = nullptr;
+    uint64_t mem_bytes = 0;
+    Buffers buf{};
+    bool empty = false;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraph_t graph = nullptr;
+};
+
+extern "C" {
+
+const char* mhg_last_error(void) { return g_last_error.c_str(); }
+
+const char* mhg_version(void) { return "mhg 0.1 (sm_100a tcgen05 kind::i8)"; }
+
+mhg_status mhg_device_check(void) {
+    return guarded([] { require_device(); });
+}
+
+mhg_status mhg_layout_check(uint64_t n, uint64_t t) {
+    return guarded([&] {
+        if (t == 0 || n == 0) fail(MHG_ERR_INVALID_ARGUMENT, "Layout: side lengths must be positive");
+        if (n >= (uint64_t(1) << 32))
+            fail(MHG_ERR_INVALID_ARGUMENT, "Layout: side too large for one-word indices");
+        if (!mhg::layout_ok(n, t)) fail(MHG_ERR_INVALID_ARGUMENT, "Layout: n must equal t * 2^m");
+    });
+}
+
+mhg_status mhg_modulus_check(uint32_t q) {
+    return guarded([&] {
+        if (q < 2 || q >= (uint32_t(1) << 31))
+            fail(MHG_ERR_INVALID_ARGUMENT, "Modulus: q must satisfy 2 <= q < 2^31");
+        if (!mhg::is_prime(q)) fail(MHG_ERR_INVALID_ARGUMENT, "Modulus: q must be prime");
+    });
+}
+
+mhg_status mhg_encode(uint64_t n, uint64_t t, uint64_t i, uint64_t j, uint64_t* z) {
+    mhg_status s = mhg_layout_check(n, t);
+    if (s) return s;
+    return guarded([&] {
+        if (i >= n || j >= n) fail(MHG_ERR_OUT_OF_RANGE, "encode: cell outside the matrix");
+        *z = mhg::encode(t, i, j);
+    });
+}
+
+mhg_status mhg_extract(uint64_t n, uint64_t t, uint64_t z, uint64_t* i, uint64_t* j) {
+    mhg_status s = mhg_layout_check(n, t);
+    if (s) return s;
+    return guarded([&] {
+        if (z >= n * n) fail(MHG_ERR_OUT_OF_RANGE, "extract: index outside the matrix");
+        *i = mhg::extract_i(t, z);
+        *j = mhg::extract_j(t, z);
+    });
+}
+
+mhg_status mhg_limb_params(uint32_t q, uint32_t* limbs, uint32_t* threshold, uint64_t* k_max) {
+    mhg_status s = mhg_modulus_check(q);
+    if (s) return s;
+    const mhg::LimbParams lp = mhg::limb_params(q);
+    if (limbs) *limbs = lp.L;
+    if (threshold) *threshold = lp.H;
+    if (k_max) *k_max = lp.k_max;
+    return MHG_OK;
+}
+
+// ------------------------------------------------------------- containers
+mhg_status mhg_matrix_create(uint64_t n, uint64_t t, uint32_t q, mhg_matrix* out) {
+    mhg_status s = mhg_layout_check(n, t);
+    if (s) return s;
+    if ((s = mhg_modulus_check(q))) return s;
+    return guarded([&] {
+        if (!out) fail(MHG_ERR_INVALID_ARGUMENT, "matrix_create: null out");
+        require_device();
+        auto* m = new mhg_matrix_s();
+        m->n = n;
+        m->t = t;
+        m->q = q;
+        m->owned = true;
+        cudaGetDevice(&m->device);
+        const uint64_t bytes = n * n * 4;
+        cudaError_t e = cudaMalloc(&m->cells, bytes);
+        if (e != cudaSuccess) {
+            delete m;
+            cuda_check((int)e, "matrix alloc");
+        }
+        e = cudaMemset(m->cells, 0, bytes);
+        if (e != cudaSuccess) {
+            cudaFree(m->cells);
+            delete m;
+            cuda_check((int)e, "matrix zero");
+        }
+        *out = m;
+    });
+}
+
+mhg_status mhg_matrix_wrap(uint64_t n, uint64_t t, uint32_t q, void* device_cells, mhg_matrix* out) {
+    mhg_status s = mhg_layout_check(n, t);
+    if (s) return s;
+    if ((s = mhg_modulus_check(q))) return s;
+    return guarded([&] {
+        if (!out || !device_cells) fail(MHG_ERR_INVALID_ARGUMENT, "matrix_wrap: null pointer");
+        if ((uintptr_t)device_cells % 16)
+            fail(MHG_ERR_INVALID_ARGUMENT, "matrix_wrap: cells must be 16-byte aligned");
+        auto* m = new mhg_matrix_s();
+        m->n = n;
+        m->t = t;
+        m->q = q;
+        m->cells = (uint32_t*)device_cells;
+        m->owned = false;
+        cudaGetDevice(&m->device);
+        *out = m;
+    });
+}
+
+mhg_status mhg_matrix_destroy(mhg_matrix m) {
+    return guarded([&] {
+        if (!m) return;
+        if (m->owned && m->cells) cudaFree(m->cells);
+        delete m;
+    });
+}
+
+mhg_status mhg_matrix_info(mhg_matrix m, uint64_t* n, uint64_t* t, uint32_t* q, void** cells) {
+    return guarded([&] {
+        if (!m) fail(MHG_ERR_INVALID_ARGUMENT, "matrix_info: null matrix");
+        if (n) *n = m->n;
+        if (t) *t = m->t;
+        if (q) *q = m->q;
+        if (cells) *cells = m->cells;
+    });
+}
+
+mhg_status mhg_matrix_upload(mhg_matrix m, const uint32_t* host, void* stream) {
+    return guarded([&] {
+        if (!m || !host) fail(MHG_ERR_INVALID_ARGUMENT, "matrix_upload: null pointer");
+        cuda_check(cudaMemcpyAsync(m->cells, host, m->n * m->n * 4, cudaMemcpyHostToDevice,
+                                   (cudaStream_t)stream),
+                   "upload");
+    });
+}
+
+mhg_status mhg_matrix_download(mhg_matrix m, uint32_t* host, void* stream) {
+    return guarded([&] {
+        if (!m || !host) fail(MHG_ERR_INVALID_ARGUMENT, "matrix_download: null pointer");
+        cuda_check(cudaMemcpyAsync(host, m->cells, m->n * m->n * 4, cudaMemcpyDeviceToHost,
+                                   (cudaStream_t)stream),
+                   "download");
+    });
+}
+
+mhg_status mhg_rowmajor_to_mh(mhg_matrix dst, const uint32_t* rows, void* stream) {
+    return guarded([&] {
+        if (!dst || !rows) fail(MHG_ERR_INVALID_ARGUMENT, "rowmajor_to_mh: null pointer");
+        require_device();
+        static int* flag = nullptr;
+        static std::mutex mu;
+        std::lock_guard<std::mutex> lock(mu);
+        if (!flag) cuda_check(cudaMalloc(&flag, sizeof(int)), "flag alloc");
+        cudaStream_t s = (cudaStream_t)stream;
+        cuda_check(cudaMemsetAsync(flag, 0, sizeof(int), s), "flag");
+        cuda_check(mhg::launch_rm_to_mh(rows, dst->cells, dst->n, mhg::tile_geom(dst->t), dst->q,
+                                        flag, stream),
+                   "rowmajor_to_mh");
+        int bad = 0;
+        cuda_check(cudaMemcpyAsync(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost, s), "flag");
+        cuda_check(cudaStreamSynchronize(s), "rowmajor_to_mh sync");
+        if (bad) fail(MHG_ERR_INVALID_ARGUMENT, "from_row_major: residue out of range");
+    });
+}
+
+mhg_status mhg_mh_to_rowmajor(mhg_matrix src, uint32_t* rows, void* stream) {
+    return guarded([&] {
+        if (!src || !rows) fail(MHG_ERR_INVALID_ARGUMENT, "mh_to_rowmajor: null pointer");
+        require_device();
+        cuda_check(mhg::launch_mh_to_rm(src->cells, rows, src->n, mhg::tile_geom(src->t), stream),
+                   "mh_to_rowmajor");
+    });
+}
+
+// --------------------------------------------------------------- multiply
+mhg_status mhg_counters_oblivious(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_counters* ctr) {
+    return guarded([&] {
+        const Checked c = check_problem(out, lhs, rhs);
+        put_counters(counters_of(out, lhs, rhs, c), ctr);
+    });
+}
+
+mhg_status mhg_counters_layout(uint64_t n, uint64_t t, uint64_t out_origin, uint64_t lhs_origin,
+                               uint64_t rhs_origin, uint64_t rows, uint64_t inner, uint64_t cols,
+                               mhg_counters* ctr) {
+    mhg_status s = mhg_layout_check(n, t);
+    if (s) return s;
+    return guarded([&] {
+        // three distinct host-side stand-ins: only geometry is inspected
+        mhg_matrix_s a, b, c;
+        a.n = b.n = c.n = n;
+        a.t = b.t = c.t = t;
+        a.q = b.q = c.q = 2;
+        a.cells = (uint32_t*)(uintptr_t)16;
+        b.cells = (uint32_t*)(uintptr_t)(16 + 4 * n * n);
+        c.cells = (uint32_t*)(uintptr_t)(16 + 8 * n * n);
+        const mhg_view vo{&a, out_origin, rows, cols}, vl{&b, lhs_origin, rows, inner},
+            vr{&c, rhs_origin, inner, cols};
+        const Checked k = check_problem(vo, vl, vr);
+        put_counters(counters_of(vo, vl, vr, k), ctr);
+    });
+}
+
+mhg_status mhg_mm(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, mhg_counters* ctr,
+                  void* stream) {
+    return guarded([&] {
+        if (op != MHG_OP_ADD && op != MHG_OP_SUB && op != MHG_OP_SET)
+            fail(MHG_ERR_INVALID_ARGUMENT, "mm: unknown op");
+        const Checked c = check_problem(out, lhs, rhs);
+        const mhg::Counters k = counters_of(out, lhs, rhs, c);
+        put_counters(k, ctr);
+        if (out.rows == 0 || out.cols == 0) return;
+        if (lhs.cols == 0) {
+            // empty inner dimension: += / -= leave the view alone (multiply.hpp:303);
+            // SET writes zeros, i.e. the product of empty factors
+            if (op != MHG_OP_SET) return;
+        }
+        require_device();
+        const mhg::GemmGeometry g = mhg::gemm_geometry(out.mat->q, c.ro.rows, c.rl.cols, c.ro.cols);
+        Workspace& ws = workspace();
+        std::lock_guard<std::mutex> lock(ws.mu);
+        uint8_t* base = ws.acquire(buffer_bytes(c, g), stream);
+        const Buffers b = carve(base, c, g);
+        launch_offsets_all(b, c, out.mat->t, stream);
+        if (lhs.cols == 0)  // SET with k == 0: the product of empty factors is zero
+            cuda_check(mhg::launch_fill_view(out.mat->cells, b.out_row, b.out_col, c.ro.rows,
+                                             c.ro.cols, 0u, stream),
+                       "fill view");
+        else
+            launch_multiply(b, out, lhs, rhs, c, g, op, stream);
+        ws.release(stream);
+    });
+}
+
+// ------------------------------------------------------------------- plans
+mhg_status mhg_plan_create(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, mhg_plan* plan) {
+    return guarded([&] {
+        if (!plan) fail(MHG_ERR_INVALID_ARGUMENT, "plan_create: null out");
+        if (op != MHG_OP_ADD && op != MHG_OP_SUB && op != MHG_OP_SET)
+            fail(MHG_ERR_INVALID_ARGUMENT, "plan_create: unknown op");
+        const Checked c = check_problem(out, lhs, rhs);
+        auto* p = new mhg_plan_s();
+        p->out = out;
+        p->lhs = lhs;
+        p->rhs = rhs;
+        p->op = op;
+        p->chk = c;
+        p->ctr = counters_of(out, lhs, rhs, c);
+        p->empty = out.rows == 0 || out.cols == 0 || lhs.cols == 0;
+        if (p->empty && op == MHG_OP_SET && out.rows && out.cols) {
+            delete p;
+            fail(MHG_ERR_UNSUPPORTED, "plan: SET with an empty inner dimension (use mhg_mm)");
+        }
+        if (!p->empty) {
+            try {
+                require_device();
+                p->geo = mhg::gemm_geometry(out.mat->q, c.ro.rows, c.rl.cols, c.ro.cols);
+                p->mem_bytes = buffer_bytes(c, p->geo);
+                cuda_check(cudaMalloc(&p->mem, p->mem_bytes), "plan workspace");
+                p->buf = carve(p->mem, c, p->geo);
+                launch_offsets_all(p->buf, c, out.mat->t, nullptr);
+                cuda_check(cudaStreamSynchronize(nullptr), "plan offsets");
+            } catch (...) {
+                if (p->mem) cudaFree(p->mem);
+                delete p;
+                throw;
+            }
+        }
+        *plan = p;
+    });
+}
+
+mhg_status mhg_plan_run(mhg_plan p, void* stream) {
+    return guarded([&] {
+        if (!p) fail(MHG_ERR_INVALID_ARGUMENT, "plan_run: null plan");
+        if (p->empty) return;
+        if (!p->exec) {
+            // capture pack(lhs), pack(rhs), gemm once; replay as one graph launch
+            cudaStream_t cap;
+            cuda_check(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "capture stream");
+            // make sure the kernels' one-time attributes are set outside capture
+            cuda_check(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "capture");
+            try {
+                launch_multiply(p->buf, p->out, p->lhs, p->rhs, p->chk, p->geo, p->op, cap);
+            } catch (...) {
+                cudaGraph_t g;
+                cudaStreamEndCapture(cap, &g);
+                if (g) cudaGraphDestroy(g);
+                cudaStreamDestroy(cap);
+                throw;
+            }
+            cuda_check(cudaStreamEndCapture(cap, &p->graph), "end capture");
+            cudaStreamDestroy(cap);
+            cuda_check(cudaGraphInstantiate(&p->exec, p->graph, 0), "graph instantiate");
+        }
+        cuda_check(cudaGraphLaunch(p->exec, (cudaStream_t)stream), "graph launch");
+    });
+}
+
+mhg_status mhg_plan_counters(mhg_plan p, mhg_counters* ctr) {
+    return guarded([&] {
+        if (!p) fail(MHG_ERR_INVALID_ARGUMENT, "plan_counters: null plan");
+        put_counters(p->ctr, ctr);
+    });
+}
+
+mhg_status mhg_plan_info(mhg_plan p, uint64_t* launches, uint64_t* tiles, uint32_t* limbs,
+                         uint32_t* k_chunks, uint64_t* workspace_bytes) {
+    return guarded([&] {
+        if (!p) fail(MHG_ERR_INVALID_ARGUMENT, "plan_info: null plan");
+        if (launches) *launches = p->empty ? 0 : 3;
+        if (tiles) *tiles = (uint64_t)p->geo.Mt * p->geo.Nt;
+        if (limbs) *limbs = p->geo.L;
+        if (k_chunks) *k_chunks = p->geo.chunks;
+        if (workspace_bytes) *workspace_bytes = p->mem_bytes;
+    });
+}
+
+mhg_status mhg_plan_time_gemm(mhg_plan p, int iters, void* stream, float* ms) {
+    return guarded([&] {
+        if (!p || iters < 1 || !ms) fail(MHG_ERR_INVALID_ARGUMENT, "plan_time_gemm: bad args");
+        if (p->empty) {
+            *ms = 0.f;
+            return;
+        }
+        // GEMM alone on the plan's packed operands (as left by the last run);
+        // repeated ADD/SUB keep `out` a valid residue container.
+        mhg::GemmParams prm = gemm_params(p->buf, p->out, p->chk, p->geo, p->op);
+        cudaEvent_t a, b;
+        cuda_check(cudaEventCreate(&a), "event");
+        cuda_check(cudaEventCreate(&b), "event");
+        cuda_check(cudaEventRecord(a, (cudaStream_t)stream), "event");
+        for (int i = 0; i < iters; ++i)
+            cuda_check(mhg::launch_gemm((int)p->geo.L, prm, device_info().sms, stream), "gemm");
+        cuda_check(cudaEventRecord(b, (cudaStream_t)stream), "event");
+        cuda_check(cudaEventSynchronize(b), "event sync");
+        float t = 0.f;
+        cudaEventElapsedTime(&t, a, b);
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        *ms = t / (float)iters;
+    });
+}
+
+mhg_status mhg_plan_destroy(mhg_plan p) {
+    return guarded([&] {
+        if (!p) return;
+        if (p->exec) cudaGraphExecDestroy(p->exec);
+        if (p->graph) cudaGraphDestroy(p->graph);
+        if (p->mem) cudaFree(p->mem);
+        delete p;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,83 @@
+// mhg_internal.hpp -- types shared by the host planner (mhg_host.cpp) and the
+// sm_100a kernels (mhg_kernels.cu).  Not part of the public ABI.
+#pragma once
+
+#include <cstdint>
+
+namespace mhg {
+
+// ---------------------------------------------------------------- geometry
+// Tile side of the Morton-hybrid layout (layout.hpp:42-76).  `shift` is
+// log2(t) when t is a power of two, else -1 (non-pow2 tiles such as
+// Layout(24, 3) are legal in the reference, layout_test.cpp:23).
+struct TileGeom {
+    uint64_t t;
+    uint64_t tt;  // t * t
+    int shift;
+};
+
+// ------------------------------------------------------------------ limbs
+// Residues are mapped to a signed representative x' (x' == x mod q) and split
+// into L signed 8-bit digits: x' = sum_s d_s 256^s, d_s in [-128, 127].
+// Representative: x' = x if x <= H else x - q.  With H = min((q-1)/2,
+// 127 (256^L - 1)/255) every x' fits L s8 digits whenever q <= 256^L.
+struct DigitParams {
+    uint32_t q;
+    uint32_t H;
+    int negate;  // 1: encode (q - x) mod q (C -= A.B as C += (-A).B)
+};
+
+struct LimbParams {
+    uint32_t L;          // digits per residue (1..4)
+    uint32_t H;          // representative threshold
+    uint32_t bound[4];   // max |digit| per position
+    uint64_t k_max;      // max inner length with every int32 class sum exact
+};
+
+LimbParams limb_params(uint32_t q);
+
+// ------------------------------------------------------------------- GEMM
+// CTA tile: BM = 128 output rows x W output columns, W = 128 (L <= 2) or 64.
+// K staged in BK = 128-byte slices (one SWIZZLE_128B atom row).
+constexpr int kBM = 128;
+constexpr int kBK = 128;
+constexpr int kPackRows = 32;  // pack kernel block rows
+
+inline int tile_width(int L) { return L <= 2 ? 128 : 64; }
+
+struct GemmParams {
+    const int8_t* apack;  // [Mt][Kt][L][128][128] swizzled
+    const int8_t* bpack;  // [Nt][Kt][L][W][128]  swizzled
+    uint32_t* out;        // Morton-hybrid container cells
+    const uint64_t* out_rowoff;  // rows entries
+    const uint64_t* out_coloff;  // cols entries
+    uint64_t rows, cols;
+    uint32_t Mt, Nt, Kt, KC;     // KC: k-tiles per exact int32 chunk
+    uint32_t q;
+    uint32_t w32;                // 2^32 mod q
+    uint64_t mu;                 // floor((2^64 - 1) / q)
+    uint64_t bias;               // multiple of q >= 2^62 (signed -> unsigned shift)
+    int mode;                    // 0: out += prod, 2: out = prod (first chunk)
+    int vec_ok;                  // t % 4 == 0: 16-byte epilogue accesses allowed
+};
+
+// --------------------------------------------------------------- launchers
+// All asynchronous on `stream`; return a cudaError_t value (0 = success).
+int launch_offsets(uint64_t* dst, uint64_t start, uint64_t count, TileGeom g, int is_row,
+                   void* stream);
+int launch_rm_to_mh(const uint32_t* rm, uint32_t* mh, uint64_t n, TileGeom g, uint32_t q,
+                    int* bad_flag, void* stream);
+int launch_mh_to_rm(const uint32_t* mh, uint32_t* rm, uint64_t n, TileGeom g, void* stream);
+// Pack an operand into limb planes.  trans = 0: pack rows are view rows, K is
+// view columns (lhs).  trans = 1: pack rows are view columns, K is view rows
+// (rhs, transposed to K-major).  rows_per_tile = 128 (lhs) or W (rhs).
+int launch_pack(int L, int trans, const uint32_t* src, const uint64_t* rowoff,
+                const uint64_t* coloff, uint64_t R, uint64_t K, uint32_t rows_per_tile,
+                uint32_t Rtiles, uint32_t Kt, int8_t* dst, DigitParams dp, void* stream);
+int launch_gemm(int L, const GemmParams& p, int num_sms, void* stream);
+int gemm_smem_bytes(int L);
+int configure_kernels();  // one-time kernel attributes (dynamic smem opt-in)
+int launch_fill_view(uint32_t* out, const uint64_t* rowoff, const uint64_t* coloff, uint64_t rows,
+                     uint64_t cols, uint32_t value, void* stream);
+
+}  // namespace mhg

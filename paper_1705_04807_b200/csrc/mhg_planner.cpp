@@ -1,0 +1,182 @@
+// mhg_planner.cpp -- see mhg_planner.hpp.
+#include "mhg_planner.hpp"
+
+#include <algorithm>
+#include <cstdlib>
+
+namespace mhg {
+
+bool layout_ok(uint64_t n, uint64_t t) {
+    if (n == 0 || t == 0 || n >= (uint64_t(1) << 32)) return false;
+    if (n % t != 0) return false;
+    const uint64_t g = n / t;
+    return (g & (g - 1)) == 0;
+}
+
+uint64_t dilate(uint64_t x) {  // interleave zeros: bit b -> bit 2b (low 32 bits)
+    x &= 0xffffffffull;
+    x = (x | (x << 16)) & 0x0000ffff0000ffffull;
+    x = (x | (x << 8)) & 0x00ff00ff00ff00ffull;
+    x = (x | (x << 4)) & 0x0f0f0f0f0f0f0f0full;
+    x = (x | (x << 2)) & 0x3333333333333333ull;
+    x = (x | (x << 1)) & 0x5555555555555555ull;
+    return x;
+}
+
+uint64_t undilate(uint64_t x) {
+    x &= 0x5555555555555555ull;
+    x = (x | (x >> 1)) & 0x3333333333333333ull;
+    x = (x | (x >> 2)) & 0x0f0f0f0f0f0f0f0full;
+    x = (x | (x >> 4)) & 0x00ff00ff00ff00ffull;
+    x = (x | (x >> 8)) & 0x0000ffff0000ffffull;
+    x = (x | (x >> 16)) & 0x00000000ffffffffull;
+    return x;
+}
+
+uint64_t encode(uint64_t t, uint64_t i, uint64_t j) {
+    return ((dilate(i / t) << 1) | dilate(j / t)) * t * t + (i % t) * t + (j % t);
+}
+
+uint64_t extract_i(uint64_t t, uint64_t z) { return undilate((z / (t * t)) >> 1) * t + (z % (t * t)) / t; }
+
+uint64_t extract_j(uint64_t t, uint64_t z) { return undilate(z / (t * t)) * t + (z % (t * t)) % t; }
+
+TileGeom tile_geom(uint64_t t) {
+    TileGeom g{t, t * t, -1};
+    if ((t & (t - 1)) == 0) {
+        int s = 0;
+        while ((uint64_t(1) << s) < t) ++s;
+        g.shift = s;
+    }
+    return g;
+}
+
+bool is_prime(uint32_t x) {
+    if (x < 2) return false;
+    if (x % 2 == 0) return x == 2;
+    for (uint64_t d = 3; d * d <= x; d += 2)
+        if (x % d == 0) return false;
+    return true;
+}
+
+// ------------------------------------------------------------------ limbs
+LimbParams limb_params(uint32_t q) {
+    LimbParams lp{};
+    uint32_t L = 1;
+    while ((uint64_t)q > (uint64_t(1) << (8 * L))) ++L;  // q <= 256^L
+    lp.L = L;
+    uint64_t R = 0;  // (256^(L-1) - 1) / 255 : weight sum of the lower digits
+    for (uint32_t s = 0; s + 1 < L; ++s) R = R * 256 + 1;
+    const uint64_t hmax = 127 * (R * 256 + 1);  // 127 (256^L - 1) / 255
+    const uint64_t half = (q - 1) / 2;
+    lp.H = (uint32_t)std::min<uint64_t>(half, hmax);
+    const int64_t lo = (int64_t)lp.H + 1 - (int64_t)q, hi = (int64_t)lp.H;
+    const uint64_t maxabs = (uint64_t)std::max<int64_t>(-lo, hi);
+    uint64_t base_top = 1;
+    for (uint32_t s = 0; s + 1 < L; ++s) base_top *= 256;
+    for (uint32_t s = 0; s < 4; ++s) lp.bound[s] = 0;
+    for (uint32_t s = 0; s + 1 < L; ++s) lp.bound[s] = 128;
+    lp.bound[L - 1] = (uint32_t)std::min<uint64_t>(128, (maxabs + 128 * R) / base_top);
+    uint64_t worst = 1;
+    for (uint32_t c = 0; c + 1 < 2 * L; ++c) {
+        uint64_t sum = 0;
+        for (uint32_t s = 0; s < L; ++s)
+            if (c >= s && c - s < L) sum += (uint64_t)lp.bound[s] * lp.bound[c - s];
+        worst = std::max(worst, sum);
+    }
+    lp.k_max = ((uint64_t(1) << 31) - 1) / worst;
+    return lp;
+}
+
+// ------------------------------------------------------- closed-form Counters
+uint64_t axis_segments(uint64_t off1, uint64_t off2, uint64_t len, uint64_t S) {
+    if (len == 0) return 0;
+    const uint64_t c1 = (off1 + len - 1) / S - off1 / S;
+    const uint64_t c2 = (off2 + len - 1) / S - off2 / S;
+    const bool same_phase = (off1 % S) == (off2 % S);
+    return 1 + c1 + c2 - (same_phase ? c1 : 0);
+}
+
+namespace {
+
+struct LeafAxis {
+    uint64_t count = 0, min_len = 0;
+    bool any_long = false;  // some leaf piece spans >= 2 cells
+};
+
+// Leaf-level pieces of one axis (cut at tile boundaries of either view).
+LeafAxis leaf_axis(uint64_t off1, uint64_t off2, uint64_t len, uint64_t t) {
+    LeafAxis a;
+    if (len == 0) return a;
+    std::vector<uint64_t> cuts;
+    for (uint64_t off : {off1, off2}) {
+        uint64_t x = t - off % t;  // first x >= 1 with (off + x) % t == 0
+        for (; x < len; x += t) cuts.push_back(x);
+    }
+    cuts.push_back(0);
+    cuts.push_back(len);
+    std::sort(cuts.begin(), cuts.end());
+    cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
+    a.count = cuts.size() - 1;
+    a.min_len = len;
+    for (size_t s = 1; s < cuts.size(); ++s) {
+        const uint64_t piece = cuts[s] - cuts[s - 1];
+        a.min_len = std::min(a.min_len, piece);
+        a.any_long = a.any_long || piece >= 2;
+    }
+    return a;
+}
+
+}  // namespace
+
+Counters oblivious_counters(uint64_t n, uint64_t t, const Rect& out, const Rect& lhs,
+                            const Rect& rhs) {
+    Counters c;
+    const uint64_t r = out.rows, cc = out.cols, k = lhs.cols;
+    if (r == 0 || cc == 0 || k == 0) return c;  // multiply.hpp:303
+    c.scalar_macs = r * k * cc;                 // multiply.hpp:171
+    // recursion nodes: depth d = 0..m, block side S = n >> d (multiply.hpp:233-263)
+    for (uint64_t S = n; S >= t; S /= 2) {
+        c.recursive_calls += axis_segments(out.i, lhs.i, r, S) * axis_segments(lhs.j, rhs.i, k, S) *
+                             axis_segments(out.j, rhs.j, cc, S);
+        if (S == t) break;
+    }
+    const LeafAxis X = leaf_axis(out.i, lhs.i, r, t);
+    const LeafAxis Z = leaf_axis(lhs.j, rhs.i, k, t);
+    const LeafAxis Y = leaf_axis(out.j, rhs.j, cc, t);
+    c.base_case_calls = X.count * Z.count * Y.count;
+    // JumpTracker (multiply.hpp:80-90) over base_case_mm's walks (:153-170):
+    //  out: +1 along a row, t - cols + 1 to the next row;
+    //  lhs: +1 along a row, t - inner + 1 to the next row;
+    //  rhs: +t down a column, +1 across columns only when inner == 1.
+    uint64_t jump = 0;
+    if (X.any_long) jump = std::max({jump, t - Y.min_len + 1, t - Z.min_len + 1});
+    if (Y.any_long || Z.any_long) jump = std::max<uint64_t>(jump, 1);
+    if (Z.any_long) jump = std::max(jump, t);
+    c.max_consecutive_jump = jump;
+    c.encode_calls = 0;  // contained leaves use offset arithmetic only
+    return c;
+}
+
+// -------------------------------------------------------------- task grid
+GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t cols) {
+    const LimbParams lp = limb_params(q);
+    GemmGeometry g{};
+    g.L = lp.L;
+    g.W = (uint32_t)tile_width((int)lp.L);
+    g.Mt = (uint32_t)((rows + kBM - 1) / kBM);
+    g.Nt = (uint32_t)((cols + g.W - 1) / g.W);
+    g.Kt = (uint32_t)((inner + kBK - 1) / kBK);
+    g.KC = (uint32_t)std::max<uint64_t>(1, lp.k_max / kBK);
+    // test hook: a smaller chunk exercises the multi-chunk path on small inputs
+    if (const char* force = std::getenv("MHG_FORCE_KCHUNK")) {
+        const long v = std::strtol(force, nullptr, 10);
+        if (v > 0 && (uint64_t)v < g.KC) g.KC = (uint32_t)v;
+    }
+    g.chunks = g.Kt ? (g.Kt + g.KC - 1) / g.KC : 0;
+    g.apack_bytes = (uint64_t)g.Mt * kBM * g.Kt * kBK * g.L;
+    g.bpack_bytes = (uint64_t)g.Nt * g.W * g.Kt * kBK * g.L;
+    return g;
+}
+
+}  // namespace mhg

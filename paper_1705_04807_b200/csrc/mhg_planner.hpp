@@ -1,0 +1,61 @@
+// mhg_planner.hpp -- host-side planner of the Morton-hybrid GF(p) MM path.
+//
+// The reference reaches its base cases through a recursion on the three
+// containers (oblivious_rec, multiply.hpp:232-264; split_sub,
+// submatrix.hpp:114-156; compatible_parts, multiply.hpp:177-198).  Its
+// decomposition has a closed form (pinned by the reference's own test,
+// multiply_test.cpp:79-86 and :252-256): the nodes at recursion depth d are the
+// Cartesian product of three 1-D segmentations, each axis cut wherever either
+// of the two views sharing it crosses a multiple of the depth-d block side
+// n / 2^d.  The planner evaluates that closed form (Counters) and turns the
+// problem into a flat grid of aligned tile-block GEMM tasks over packed operands
+// -- no device recursion, no index conversion inside the kernels.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "mhg_internal.hpp"
+
+namespace mhg {
+
+// ------------------------------------------------------------ codec (host)
+bool layout_ok(uint64_t n, uint64_t t);  // Layout(n, t) preconditions, layout.hpp:50-56
+uint64_t dilate(uint64_t x);
+uint64_t undilate(uint64_t x);
+uint64_t encode(uint64_t t, uint64_t i, uint64_t j);
+uint64_t extract_i(uint64_t t, uint64_t z);
+uint64_t extract_j(uint64_t t, uint64_t z);
+TileGeom tile_geom(uint64_t t);
+bool is_prime(uint32_t q);
+
+// ------------------------------------------------------ closed-form Counters
+struct Rect {
+    uint64_t i, j, rows, cols;  // container coordinates of the view
+};
+
+struct Counters {
+    uint64_t base_case_calls = 0, scalar_macs = 0, encode_calls = 0, recursive_calls = 0,
+             max_consecutive_jump = 0;
+};
+
+// Number of pieces of [0, len) cut where (off1 + x) % S == 0 or (off2 + x) % S == 0.
+uint64_t axis_segments(uint64_t off1, uint64_t off2, uint64_t len, uint64_t S);
+
+// Counters of mm_oblivious for out(r x c) += lhs(r x k) * rhs(k x c).
+Counters oblivious_counters(uint64_t n, uint64_t t, const Rect& out, const Rect& lhs,
+                            const Rect& rhs);
+
+// -------------------------------------------------------------- task grid
+struct GemmGeometry {
+    uint32_t L, W;        // limbs, output tile width
+    uint32_t Mt, Nt, Kt;  // tiles along rows / cols / inner (128-byte K slices)
+    uint32_t KC;          // K slices per exact int32 chunk
+    uint32_t chunks;
+    uint64_t apack_bytes, bpack_bytes;
+};
+
+GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t cols);
+
+}  // namespace mhg

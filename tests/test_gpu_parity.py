@@ -1,0 +1,263 @@
+"""GPU parity: libmhg.so (tcgen05 kind::i8 path) vs the CPU oracle / reference.
+
+Integer work mod q: the bar is bit-exact equality of the WHOLE output
+container (Matrix::operator==, matrix.hpp:30-33) wherever the oracle can
+finish in seconds; at benchmark sizes, size-independent checks (Freivalds'
+identity over the whole result + dense recompute of sampled output tiles that
+cover every top-level Morton quadrant and the view's edges and corners).
+"""
+import numpy as np
+import pytest
+
+from oracle.binding import OP_ADD, OP_SET, OP_SUB, Views
+
+pytestmark = pytest.mark.gpu
+
+P16 = 65521
+P31 = 2147483647
+P24 = 16777213  # a 24-bit prime: three limbs
+
+
+def _containers(mh, n, t, q, cells):
+    lay, mod = mh.Layout(n, t), mh.Modulus(q)
+    return [mh.Matrix(lay, mod).upload(c) for c in cells]
+
+
+def _run_gpu(mh, n, t, q, out, lhs, rhs, v: Views, op):
+    A, B, Cm = _containers(mh, n, t, q, (out, lhs, rhs))
+    prob = mh.Problem(mh.Sub(A, v.out_origin, v.rows, v.cols),
+                      mh.Sub(B, v.lhs_origin, v.rows, v.inner),
+                      mh.Sub(Cm, v.rhs_origin, v.inner, v.cols))
+    ctr = mh.mm(prob, op)
+    got = A.cells()
+    return got, ctr
+
+
+def _random_views(rng, n, r=None, k=None, c=None):
+    r = r or int(rng.integers(1, n + 1))
+    k = k or int(rng.integers(1, n + 1))
+    c = c or int(rng.integers(1, n + 1))
+    return r, k, c, [int(rng.integers(0, n - d + 1)) for d in (r, c, r, k, k, c)]
+
+
+def _views_from(oracle, n, t, r, k, c, corners):
+    ia, ja, ib, jb, ic, jc = corners
+    return Views(oracle.encode(n, t, ia, ja), oracle.encode(n, t, ib, jb),
+                 oracle.encode(n, t, ic, jc), r, k, c)
+
+
+def _fill(oracle, seed, n, q):
+    g = oracle.rng(seed)
+    return [oracle.fill_below(g, n * n, q) for _ in range(3)]
+
+
+def test_smoke_cfg1_shape(gpu, mh, oracle, reference):
+    """BASELINE cfg1: n=512, t=32, p=65521, C = A*B, full aligned views."""
+    n, t, q = 512, 32, P16
+    out, lhs, rhs = _fill(oracle, 0, n, q)
+    out[:] = 0
+    v = Views(0, 0, 0, n, n, n)
+    got, ctr = _run_gpu(mh, n, t, q, out, lhs, rhs, v, OP_ADD)
+    want = out.copy()
+    ref_ctr = reference.mm_oblivious(n, t, q, want, lhs, rhs, v)
+    assert np.array_equal(got, want)
+    assert ctr.as_tuple() == ref_ctr.as_tuple()
+
+
+@pytest.mark.parametrize("q", [2, 97, 257, P16, P24, P31])
+@pytest.mark.parametrize("op", [OP_ADD, OP_SUB, OP_SET])
+def test_random_misaligned_views(gpu, mh, oracle, q, op):
+    """Random (ragged, misaligned, rectangular) views; whole-container equality."""
+    rng = np.random.default_rng(q * 7 + op)
+    for it in range(6):
+        n = int(rng.choice([64, 128, 256]))
+        t = int(rng.choice([x for x in (4, 8, 16, 32, 64) if x <= n]))
+        r, k, c, corners = _random_views(rng, n)
+        v = _views_from(oracle, n, t, r, k, c, corners)
+        out, lhs, rhs = _fill(oracle, 1000 + it, n, q)
+        got, _ = _run_gpu(mh, n, t, q, out, lhs, rhs, v, op)
+        want = out.copy()
+        oracle.mm_dense(n, t, q, want, lhs, rhs, v, op=op)
+        assert np.array_equal(got, want), (n, t, q, op, v)
+
+
+def test_reference_acceptance_instances(gpu, mh, oracle, reference):
+    """acceptance_main.cpp:177-217 protocol: gen_problem draws, out += lhs*rhs,
+    whole container equal to the reference's mm_oblivious, Counters equal."""
+    for (n, t, q, seed, count) in [(64, 8, 2, 101, 40), (64, 8, 97, 102, 40), (256, 32, 2, 103, 12)]:
+        g = oracle.rng(seed)
+        for _ in range(count):
+            out, lhs, rhs, _, v = oracle.gen_problem(g, n, t, q)
+            got, ctr = _run_gpu(mh, n, t, q, out, lhs, rhs, v, OP_ADD)
+            want = out.copy()
+            ref = reference.mm_oblivious(n, t, q, want, lhs, rhs, v)
+            assert np.array_equal(got, want)
+            assert ctr.as_tuple() == ref.as_tuple()
+
+
+def test_empty_problems_are_noops(gpu, mh, oracle):
+    """multiply_test.cpp:187-193: empty problems leave the output, zero Counters."""
+    n, t, q = 8, 4, 2
+    out, lhs, rhs = _fill(oracle, 5, n, q)
+    for dims in [(0, 4, 4), (4, 0, 4), (4, 4, 0)]:
+        r, k, c = dims
+        got, ctr = _run_gpu(mh, n, t, q, out, lhs, rhs, Views(0, 0, 0, r, k, c), OP_ADD)
+        assert np.array_equal(got, out)
+        assert ctr.as_tuple() == (0, 0, 0, 0, 0)
+
+
+def test_validation_errors(gpu, mh):
+    """multiply_test.cpp:165-185: the reference's exception classes."""
+    two = mh.Modulus(2)
+    A, B, C = (mh.Matrix(mh.Layout(8, 4), two) for _ in range(3))
+    with pytest.raises(mh.LogicError):  # inner dimensions disagree
+        mh.mm(mh.Problem(mh.Sub(A, 0, 4, 4), mh.Sub(B, 0, 4, 3), mh.Sub(C, 0, 4, 4)))
+    with pytest.raises(mh.LogicError):  # shared container
+        mh.mm(mh.Problem(mh.Sub(A, 0, 4, 4), mh.Sub(A, 0, 4, 4), mh.Sub(C, 0, 4, 4)))
+    D = mh.Matrix(mh.Layout(8, 4), mh.Modulus(3))
+    with pytest.raises(mh.LogicError):  # mixed moduli
+        mh.mm(mh.Problem(mh.Sub(A, 0, 4, 4), mh.Sub(B, 0, 4, 4), mh.Sub(D, 0, 4, 4)))
+    E = mh.Matrix(mh.Layout(8, 2), two)
+    with pytest.raises(mh.LogicError):  # oblivious wants identical layouts
+        mh.mm(mh.Problem(mh.Sub(A, 0, 4, 4), mh.Sub(B, 0, 4, 4), mh.Sub(E, 0, 4, 4)))
+    with pytest.raises(mh.OutOfRange):
+        mh.mm(mh.Problem(mh.Sub(A, 64, 1, 1), mh.Sub(B, 0, 1, 1), mh.Sub(C, 0, 1, 1)))
+    with pytest.raises(mh.OutOfRange):
+        mh.mm(mh.Problem(mh.Sub(A, 0, 9, 1), mh.Sub(B, 0, 9, 1), mh.Sub(C, 0, 1, 1)))
+    with pytest.raises(mh.InvalidArgument):
+        mh.mm(mh.Problem(mh.Sub(None, 0, 1, 1), mh.Sub(B, 0, 1, 1), mh.Sub(C, 0, 1, 1)))
+
+
+def test_conversion_kernels_roundtrip(gpu, mh, oracle):
+    """K1: from_row_major / to_row_major (matrix.hpp:44-67) vs the oracle codec."""
+    for (n, t) in [(8, 4), (24, 3), (64, 8), (256, 64), (1024, 32)]:
+        rng = np.random.default_rng(n + t)
+        grid = rng.integers(0, 97, size=(n, n), dtype=np.uint32)
+        m = mh.from_row_major(grid, t, mh.Modulus(97))
+        assert np.array_equal(m.cells(), oracle.rowmajor_to_mh(n, t, grid))
+        assert np.array_equal(mh.to_row_major(m), grid)
+    with pytest.raises(mh.InvalidArgument):  # residue out of range (matrix.hpp:52-53)
+        mh.from_row_major(np.full((8, 8), 97, np.uint32), 4, mh.Modulus(97))
+
+
+# Residues whose signed limb digits are the extremes (+127 / -128 / -113 / +64 ...)
+EXTREMES = {P16: (32639, 32640, P16 - 1, 0x807F, 1),
+            P31: (1073741823, 1073741824, P31 - 1, 0x7F7F7F7F, 0x80808080 % P31)}
+
+
+def _constant_case(mh, n, t, q, a, b, c0, k, op):
+    """out (n x n, all c0) op= lhs (all a) * rhs (all b) over an r=c=n, inner k
+    problem: every output cell must equal c0 +/- k*a*b mod q (closed form)."""
+    lay, mod = mh.Layout(n, t), mh.Modulus(q)
+    A = mh.Matrix(lay, mod).upload(np.full(n * n, c0, np.uint32))
+    B = mh.Matrix(lay, mod).upload(np.full(n * n, a, np.uint32))
+    Cm = mh.Matrix(lay, mod).upload(np.full(n * n, b, np.uint32))
+    mh.mm(mh.Problem(mh.Sub(A, 0, n, n), mh.Sub(B, 0, n, k), mh.Sub(Cm, 0, k, n)), op)
+    prod = (k * a * b) % q
+    want = {OP_ADD: (c0 + prod) % q, OP_SUB: (c0 - prod) % q, OP_SET: prod}[op]
+    got = A.cells()
+    assert (got == want).all(), (q, a, b, op, int(got[0]), want)
+
+
+def test_adversarial_extreme_digits(gpu, mh):
+    """Extreme-magnitude signed digits in every limb position, all three ops."""
+    for q, vals in EXTREMES.items():
+        for a in vals:
+            for b in vals[:3]:
+                for op in (OP_ADD, OP_SUB, OP_SET):
+                    _constant_case(mh, 1024, 64, q, a, b, q - 1, 1024, op)
+
+
+@pytest.mark.slow
+def test_adversarial_int32_headroom(gpu, mh):
+    """K = 32768 (cfg5's inner length) with extreme digits: the int32 class
+    sums reach ~75% (q = 2^31-1) of the bound the planner sized chunks for."""
+    for q in (P16, P31):
+        for a, b in [(EXTREMES[q][0], EXTREMES[q][0]), (EXTREMES[q][1], EXTREMES[q][0])]:
+            _constant_case(mh, 32768, 64, q, a, b, 1, 32768, OP_SUB)
+
+
+def test_k_chunking(gpu, mh, oracle, monkeypatch):
+    """Multi-chunk accumulation (each exact int32 K-chunk drained and folded into
+    the output before the next): forced to 2 K-slices per chunk so small
+    problems take the path n >= 65536 would take for q = 2^31-1."""
+    monkeypatch.setenv("MHG_FORCE_KCHUNK", "2")
+    rng = np.random.default_rng(77)
+    for q in (P16, P31):
+        for op in (OP_ADD, OP_SUB, OP_SET):
+            n, t = 1024, 64
+            r, k, c, corners = _random_views(rng, n, r=300, k=1000, c=200)
+            v = _views_from(oracle, n, t, r, k, c, corners)
+            out, lhs, rhs = _fill(oracle, 9 + op, n, q)
+            got, _ = _run_gpu(mh, n, t, q, out, lhs, rhs, v, op)
+            want = out.copy()
+            oracle.mm_dense(n, t, q, want, lhs, rhs, v, op=op)
+            assert np.array_equal(got, want), (q, op)
+
+
+@pytest.mark.slow
+def test_cfg2_full_container(gpu, mh, oracle):
+    """BASELINE cfg2: n=4096, t=64, p=65521, C -= A*B, C uniform: whole container."""
+    n, t, q = 4096, 64, P16
+    out, lhs, rhs = _fill(oracle, 0, n, q)
+    v = Views(0, 0, 0, n, n, n)
+    got, _ = _run_gpu(mh, n, t, q, out, lhs, rhs, v, OP_SUB)
+    want = out.copy()
+    oracle.mm_dense(n, t, q, want, lhs, rhs, v, op=OP_SUB)
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.slow
+def test_cfg3_misaligned_schur_update(gpu, mh, oracle):
+    """BASELINE cfg3: C(6144x5120) -= A(6144x2048) B(2048x5120) in 8192^2 parents
+    at (96,160), t=64 -- exercises the alignment/containment decomposition."""
+    n, t, q = 8192, 64, P16
+    out, lhs, rhs = _fill(oracle, 3, n, q)
+    v = Views(oracle.encode(n, t, 96, 160), oracle.encode(n, t, 96, 160),
+              oracle.encode(n, t, 96, 160), 6144, 2048, 5120)
+    got, ctr = _run_gpu(mh, n, t, q, out, lhs, rhs, v, OP_SUB)
+    assert ctr.base_case_calls == 97 * 33 * 81  # 259,281 leaves
+    want = out.copy()
+    oracle.mm_dense(n, t, q, want, lhs, rhs, v, op=OP_SUB)
+    assert np.array_equal(got, want)
+
+
+def _sampled_tiles(oracle, n, t, q, out, lhs, rhs, got, v, op, tiles):
+    for (r0, c0) in tiles:
+        nr, nc = min(64, v.rows - r0), min(64, v.cols - c0)
+        want = oracle.mm_dense_block(n, t, q, out, lhs, rhs, v, r0, nr, c0, nc, op=op)
+        oi, oj = oracle.extract(n, t, v.out_origin)
+        for a in range(nr):
+            idx = [oracle.encode(n, t, oi + r0 + a, oj + c0 + b) for b in range(nc)]
+            assert np.array_equal(got[idx], want[a]), (r0, c0, a)
+
+
+@pytest.mark.slow
+def test_cfg4_large_prime(gpu, mh, oracle):
+    """BASELINE cfg4: n=8192, t=64, p=2^31-1, C = A*B: Freivalds + sampled tiles."""
+    n, t, q = 8192, 64, P31
+    out, lhs, rhs = _fill(oracle, 4, n, q)
+    v = Views(0, 0, 0, n, n, n)
+    got, _ = _run_gpu(mh, n, t, q, out, lhs, rhs, v, OP_SET)
+    assert oracle.freivalds(n, t, q, out, lhs, rhs, got, v, op=OP_SET, rounds=2)
+    h = n // 2
+    _sampled_tiles(oracle, n, t, q, out, lhs, rhs, got, v, OP_SET,
+                   [(0, 0), (0, h), (h, 0), (h, h), (n - 64, n - 64), (h - 32, h - 32)])
+    bad = got.copy()
+    bad[12345] = (bad[12345] + 1) % q
+    assert not oracle.freivalds(n, t, q, out, lhs, rhs, bad, v, op=OP_SET, rounds=1)
+
+
+@pytest.mark.slow
+def test_north_star_size(gpu, mh, oracle):
+    """n=16384, t=64, p=65521, C -= A*B (the bench workload): Freivalds over the
+    whole result + tiles in every top-level Morton quadrant, edges, corners."""
+    n, t, q = 16384, 64, P16
+    out, lhs, rhs = _fill(oracle, 0, n, q)
+    v = Views(0, 0, 0, n, n, n)
+    got, ctr = _run_gpu(mh, n, t, q, out, lhs, rhs, v, OP_SUB)
+    assert ctr.scalar_macs == n ** 3
+    assert oracle.freivalds(n, t, q, out, lhs, rhs, got, v, op=OP_SUB, rounds=2)
+    h = n // 2
+    _sampled_tiles(oracle, n, t, q, out, lhs, rhs, got, v, OP_SUB,
+                   [(0, 0), (0, h), (h, 0), (h, h), (0, n - 64), (n - 64, 0), (n - 64, n - 64)])
