@@ -1,0 +1,378 @@
+#!/usr/bin/env python
+"""Benchmark of the Morton-hybrid GF(p) MM hot path (BASELINE.json metric).
+
+Default workload (N=1): n=16384, T'=64, p=65521, C -= A*B over full views --
+the configuration BASELINE.json's metric is quoted on.  One step = one
+planned multiply: pack(lhs) + pack(rhs) + tcgen05 GEMM with the fused mod-p
+epilogue.  value = r*k*c GF(p) mult-adds per second (whole job).
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--workload cfg2]
+
+N > 1 runs under torchrun: C-stationary Morton-block partition, each rank
+all-gathers its A row panel / B column panel (NCCL) and updates its block.
+--impl reference times the reference's own CPU mm_oblivious (oracle/_ref) on
+the host cores, on a bounded sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+P16, P31 = 65521, 2147483647
+WORKLOADS = {
+    # name: (n, t, q, op, view) ; view None = full n x n x n
+    "ns16k": (16384, 64, P16, "sub", None),
+    "cfg1": (512, 32, P16, "set", None),
+    "cfg2": (4096, 64, P16, "sub", None),
+    "cfg3": (8192, 64, P16, "sub", (96, 160, 6144, 2048, 5120)),
+    "cfg4": (8192, 64, P31, "set", None),
+    "cfg5": (32768, 64, P16, "sub", None),
+}
+DESCR = {
+    "ns16k": "Morton-hybrid C -= A*B mod 65521, n=16384, T'=64 (north star)",
+    "cfg1": "C = A*B mod 65521, n=512, T'=32",
+    "cfg2": "C -= A*B mod 65521, n=4096, T'=64",
+    "cfg3": "C(6144x5120) -= A(6144x2048)*B(2048x5120) mod 65521 in 8192^2 parents at (96,160), T'=64",
+    "cfg4": "C = A*B mod 2^31-1, n=8192, T'=64",
+    "cfg5": "C -= A*B mod 65521, n=32768, T'=64",
+}
+METRIC = "GF(p) mult-adds/s, Morton-hybrid C-=A·B mod p, n=16384; % of TC roofline"
+UNIT = "GF(p) MAC/s"
+
+
+def limbs_of(q):
+    L = 1
+    while q > 256 ** L:
+        L += 1
+    return L
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["bf16_tflops"]), float(d.get("bf16_tflops_sustained", d["bf16_tflops"])), \
+            float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi-equivalent sampling (NVML) of SM clock + throttle reasons."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index=0, period=0.1):
+        self.samples, self.reasons = [], set()
+        self.period, self.stop_evt = period, threading.Event()
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+
+    def _run(self):
+        while not self.stop_evt.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                bits = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for b, name in self.REASONS.items():
+                    if bits & b and b != 0x1:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self.stop_evt.wait(self.period)
+
+    def __enter__(self):
+        if self.nv:
+            self.th = threading.Thread(target=self._run, daemon=True)
+            self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.nv:
+            self.stop_evt.set()
+            self.th.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unavailable"]}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------- reference CPU leg
+def reference_sample(n, t, q, threads, rows_per_thread=64, cols=512, view=None):
+    """Time the reference's mm_oblivious (oracle/_ref, compiled from the
+    reference's own headers) on a bounded sample of the workload: an output
+    block of (64 x threads) rows x `cols` columns with the FULL inner length,
+    split into one disjoint row strip per thread (multiply.hpp:25-29)."""
+    from oracle.binding import REF_SO, Reference
+    i0, j0, k0, inner = 0, 0, 0, n
+    if view is not None:
+        i0, j0, rr, inner, cc = view[0], view[1], view[2], view[3], view[4]
+        k0 = view[1]
+    if not os.path.exists(REF_SO):
+        return None
+    ref = Reference()
+    h = ref.bench_new(n, t, q, 0)
+    rows = min(rows_per_thread * threads, n - i0)
+    cols = min(cols, n - j0)
+    return ref, h, (i0, rows, j0, cols, k0, min(inner, n - k0))
+
+
+def cpu_baseline_json(args, n, t, q, view, steps=1, warmup=0):
+    threads = args.cpu_threads or os.cpu_count() or 1
+    got = reference_sample(n, t, q, threads, view=view)
+    if got is None:
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref/libmhref.so missing"}
+    ref, h, (i0, rows, j0, cols, k0, inner) = got
+    try:
+        for _ in range(warmup):
+            ref.bench_run(h, i0, rows, j0, cols, k0, inner, threads)
+        tot_ns, tot_macs = 0, 0
+        for _ in range(steps):
+            ns, macs = ref.bench_run(h, i0, rows, j0, cols, k0, inner, threads)
+            tot_ns += ns
+            tot_macs += macs
+    finally:
+        ref.bench_free(h)
+    val = tot_macs / (tot_ns * 1e-9)
+    return {"value": val, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"mh::mm_oblivious (reference headers, -O3 -DNDEBUG) on output rows "
+                      f"[{i0},{i0 + rows}) x cols [{j0},{j0 + cols}), inner {inner}, of the n={n} "
+                      f"containers; {threads} disjoint row strips on {threads} std::threads; "
+                      f"{steps} step(s) of {tot_macs // max(steps, 1)} MACs",
+            "ms_per_step": tot_ns / 1e6 / max(steps, 1)}
+
+
+def run_reference(args, rank, world):
+    n, t, q, op, view = WORKLOADS[args.workload]
+    if rank != 0:
+        return
+    W = max(args.warmup, 0)
+    cb = cpu_baseline_json(args, n, t, q, view, steps=args.steps, warmup=W)
+    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": W, "ms_per_step": cb.get("ms_per_step"),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic (uniform residues, splitmix stream)",
+            "config": {"workload": args.workload, "description": DESCR[args.workload], "n": n,
+                       "t": t, "p": q, "op": op},
+            "impl": "reference",
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "gpu_launches": 0}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- GPU leg
+def run_gpu(args, rank, world, local_rank):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1705_04807_b200 as mh
+    from paper_1705_04807_b200.dist import PanelExchange, slice_range
+
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
+    n, t, q, opname, view = WORKLOADS[args.workload]
+    op = {"add": mh.OP_ADD, "sub": mh.OP_SUB, "set": mh.OP_SET}[opname]
+    L = limbs_of(q)
+    lay, mod = mh.Layout(n, t), mh.Modulus(q)
+    stream = torch.cuda.current_stream()
+
+    # containers: full-size on every rank; each rank draws its own 1/P Morton slice
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    flats = []
+    b, e = slice_range(rank, world, n) if world > 1 else (0, n * n)
+    for _ in range(3):
+        f = torch.zeros(n * n, dtype=torch.int32, device=dev)
+        f[b:e] = torch.randint(0, q, (e - b,), dtype=torch.int32, device=dev, generator=gen)
+        flats.append(f)
+    out_f, lhs_f, rhs_f = flats
+    A, B, Cm = (mh.Matrix.wrap(lay, mod, f.data_ptr(), owner=f) for f in flats)
+
+    ex = PanelExchange(world, rank, n, t)
+    if world > 1:
+        blk = ex.block
+        oi, oj, rr, kk, cc = blk.i0, blk.j0, blk.rows, n, blk.cols
+        li, lj, ri, rj = blk.i0, 0, 0, blk.j0
+        if view is not None:
+            raise SystemExit("multi-GPU runs use full-view workloads")
+    elif view is not None:
+        oi, oj, rr, kk, cc = view
+        li, lj, ri, rj = oi, oj, oi, oj
+    else:
+        oi = oj = li = lj = ri = rj = 0
+        rr = kk = cc = n
+    prob = mh.Problem(mh.Sub(A, mh.encode(lay, oi, oj), rr, cc),
+                      mh.Sub(B, mh.encode(lay, li, lj), rr, kk),
+                      mh.Sub(Cm, mh.encode(lay, ri, rj), kk, cc))
+    plan = mh.Plan(prob, op)
+    info = plan.info()
+    macs_rank = rr * kk * cc
+    macs_total = n ** 3 if world > 1 else macs_rank
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def step():
+        ex.exchange(lhs_f, rhs_f)
+        plan.run(stream)
+
+    W = max(args.warmup, 3)
+    for _ in range(W):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---- timed region (device events, profiling mode brackets every GEMM)
+    plan.set_profiling(True)
+    plan.gemm_time()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        torch.cuda.synchronize()
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step()
+        ev1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms_local = ev0.elapsed_time(ev1) / args.steps
+    gemm_ms_total, gemm_launches = plan.gemm_time()
+    plan.set_profiling(False)
+    gemm_ms = gemm_ms_total / max(gemm_launches, 1)
+    t_ms = torch.tensor([ms_local, gemm_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms, gemm_ms_max = float(t_ms[0]), float(t_ms[1])
+    value = macs_total / (ms * 1e-3)
+
+    # ---- end to end through the public API with host buffers (pinned)
+    e2e = None
+    if not args.no_e2e:
+        hosts = [torch.empty(n * n, dtype=torch.int32, pin_memory=True) for _ in range(3)]
+        for h_, f in zip(hosts, flats):
+            h_.copy_(f)
+        res = torch.empty(n * n, dtype=torch.int32, pin_memory=True)
+        h2d = 3 * n * n * 4 if world == 1 else 3 * (e - b) * 4
+        d2h = n * n * 4 if world == 1 else (e - b) * 4
+        e2e_steps = max(1, min(args.steps, args.e2e_steps))
+        torch.cuda.synchronize()
+        barrier()
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x0.record(stream)
+        for _ in range(e2e_steps):
+            if world == 1:
+                for h_, m_ in zip(hosts, (A, B, Cm)):
+                    mh.lib().mhg_matrix_upload(m_.handle, h_.data_ptr(), stream.cuda_stream)
+            else:  # each rank uploads its own slices, then the panel exchange
+                for h_, f in zip(hosts, flats):
+                    f[b:e].copy_(h_[b:e], non_blocking=True)
+                ex.exchange(lhs_f, rhs_f)
+            plan.run(stream)
+            if world == 1:
+                mh.lib().mhg_matrix_download(A.handle, res.data_ptr(), stream.cuda_stream)
+            else:
+                res[b:e].copy_(out_f[b:e], non_blocking=True)
+        x1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms = torch.tensor([x0.elapsed_time(x1) / e2e_steps], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": macs_total / (float(e2e_ms[0]) * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps,
+               "ms_per_step": float(e2e_ms[0]),
+               "path": "mhg_matrix_upload x3 (pinned) -> mhg_plan_run -> mhg_matrix_download"}
+
+    if rank != 0:
+        return
+
+    bf16_burst, bf16_sus, hbm, peak_src = load_peaks()
+    int8_peak_tops = 2.0 * bf16_burst  # dense int8 = 2x dense bf16 on sm_100
+    algo_ops = 2.0 * L * L * macs_rank  # int8 ops per GEMM launch (2 per limb MAC)
+    achieved_tops = algo_ops / (gemm_ms_max * 1e-3) / 1e12
+    roof = {"bound": "tensor", "achieved": achieved_tops, "peak": int8_peak_tops,
+            "unit": "TFLOP/s", "frac": achieved_tops / int8_peak_tops, "traffic": None,
+            "kernel": f"k_gemm<{L}> (tcgen05.mma.cta_group::1.kind::i8)",
+            "peak_source": f"2 x {peak_src} bf16 burst {bf16_burst} TFLOP/s (MEASURED_PEAKS.json); "
+                           f"int8 ops counted as 2*L^2*r*k*c, L={L}",
+            "frac_of_spec_4500": achieved_tops / 4500.0,
+            "gemm_ms": gemm_ms_max, "gemm_share_of_step": gemm_ms_max / ms,
+            "gf_macs_per_s_gemm_only": macs_rank / (gemm_ms_max * 1e-3)}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline_json(args, n, t, q, view)
+        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": W, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "int8",
+            "data": "synthetic: uniform residues in [0,p) drawn on device (torch.Generator)",
+            "config": {"workload": args.workload, "description": DESCR[args.workload], "n": n,
+                       "t": t, "p": q, "op": opname, "limbs": L,
+                       "tiles": info["tiles"], "k_chunks": info["k_chunks"],
+                       "partition": f"C-stationary Morton blocks over {world} GPU(s)",
+                       "l2": "no flush: operands 3 x %.2f GiB >> 126 MB L2" % (n * n * 4 / 2 ** 30)},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": args.steps * info["launches"],
+            "clocks": clk.summary()}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="ns16k", choices=sorted(WORKLOADS))
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-threads", type=int, default=0)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_gpu(args, rank, world, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

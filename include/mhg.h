@@ -134,6 +134,12 @@ mhg_status mhg_limb_params(uint32_t q, uint32_t *limbs, uint32_t *threshold, uin
 /* Times `iters` replays of a plan's GEMM kernel alone (CUDA events on
  * `stream`), returns the mean ms per launch in *ms. */
 mhg_status mhg_plan_time_gemm(mhg_plan plan, int iters, void *stream, float *ms);
+/* Profiling mode: while enabled, mhg_plan_run launches the three kernels
+ * directly (no graph) and brackets the GEMM launch with CUDA events on
+ * `stream`; mhg_plan_gemm_time synchronises, returns the summed GEMM time and
+ * the number of GEMM launches recorded since the last call, and resets. */
+mhg_status mhg_plan_set_profiling(mhg_plan plan, int enable);
+mhg_status mhg_plan_gemm_time(mhg_plan plan, float *total_ms, uint64_t *launches);
 
 #ifdef __cplusplus
 }

@@ -125,6 +125,8 @@ def lib():
         "mhg_plan_destroy": ([vp], C.c_int),
         "mhg_limb_params": ([u32, P(u32), P(u32), P(u64)], C.c_int),
         "mhg_plan_time_gemm": ([vp, C.c_int, vp, P(C.c_float)], C.c_int),
+        "mhg_plan_set_profiling": ([vp, C.c_int], C.c_int),
+        "mhg_plan_gemm_time": ([vp, P(C.c_float), P(u64)], C.c_int),
     }
     for name, (args, res) in sigs.items():
         f = getattr(L, name)
@@ -391,6 +393,15 @@ class Plan:
         ms = C.c_float()
         _check(lib().mhg_plan_time_gemm(self._h, iters, _stream_ptr(stream), C.byref(ms)))
         return ms.value
+
+    def set_profiling(self, enable: bool = True):
+        _check(lib().mhg_plan_set_profiling(self._h, int(enable)))
+
+    def gemm_time(self):
+        """(summed GEMM ms, GEMM launches) since the last call (profiling mode)."""
+        ms, n = C.c_float(), C.c_uint64()
+        _check(lib().mhg_plan_gemm_time(self._h, C.byref(ms), C.byref(n)))
+        return ms.value, n.value
 
     def __del__(self):
         try:

@@ -11,6 +11,7 @@
 #include <mutex>
 #include <stdexcept>
 #include <string>
+#include <vector>
 
 #include "mhg.h"
 #include "mhg_internal.hpp"
@@ -228,7 +229,8 @@ mhg::GemmParams gemm_params(const Buffers& b, const mhg_view& out, const Checked
 // Pack both operands and run the GEMM: 2 pack launches + 1 GEMM launch.
 void launch_multiply(const Buffers& b, const mhg_view& out, const mhg_view& lhs,
                      const mhg_view& rhs, const Checked& c, const mhg::GemmGeometry& g,
-                     mhg_op op, void* stream) {
+                     mhg_op op, void* stream, cudaEvent_t gemm_begin = nullptr,
+                     cudaEvent_t gemm_end = nullptr) {
     const mhg::LimbParams lp = mhg::limb_params(out.mat->q);
     mhg::DigitParams dl{out.mat->q, lp.H, op == MHG_OP_SUB ? 1 : 0};
     mhg::DigitParams dr{out.mat->q, lp.H, 0};
@@ -239,7 +241,9 @@ void launch_multiply(const Buffers& b, const mhg_view& out, const mhg_view& lhs,
                                 c.rr.rows, g.W, g.Nt, g.Kt, b.bpack, dr, stream),
                "pack rhs");
     const mhg::GemmParams p = gemm_params(b, out, c, g, op);
+    if (gemm_begin) cuda_check(cudaEventRecord(gemm_begin, (cudaStream_t)stream), "event");
     cuda_check(mhg::launch_gemm((int)g.L, p, device_info().sms, stream), "gemm");
+    if (gemm_end) cuda_check(cudaEventRecord(gemm_end, (cudaStream_t)stream), "event");
 }
 
 // One-shot workspace for mhg_mm: grows on demand; an event orders reuse
@@ -287,6 +291,10 @@ struct mhg_plan_s {
     bool empty = false;
     cudaGraphExec_t exec = nullptr;
     cudaGraph_t graph = nullptr;
+    // profiling: event pairs bracketing each GEMM launch (ring, read + reset)
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev;
+    size_t ev_used = 0;
 };
 
 extern "C" {
@@ -561,6 +569,20 @@ mhg_status mhg_plan_run(mhg_plan p, void* stream) {
     return guarded([&] {
         if (!p) fail(MHG_ERR_INVALID_ARGUMENT, "plan_run: null plan");
         if (p->empty) return;
+        if (p->profiling) {
+            if (p->ev_used + 2 > p->ev.size()) {
+                const size_t grow = p->ev.size() ? p->ev.size() : 64;
+                for (size_t i = 0; i < grow; ++i) {
+                    cudaEvent_t e;
+                    cuda_check(cudaEventCreate(&e), "event");
+                    p->ev.push_back(e);
+                }
+            }
+            cudaEvent_t b = p->ev[p->ev_used], e = p->ev[p->ev_used + 1];
+            p->ev_used += 2;
+            launch_multiply(p->buf, p->out, p->lhs, p->rhs, p->chk, p->geo, p->op, stream, b, e);
+            return;
+        }
         if (!p->exec) {
             // capture pack(lhs), pack(rhs), gemm once; replay as one graph launch
             cudaStream_t cap;
@@ -629,9 +651,34 @@ mhg_status mhg_plan_time_gemm(mhg_plan p, int iters, void* stream, float* ms) {
     });
 }
 
+mhg_status mhg_plan_set_profiling(mhg_plan p, int enable) {
+    return guarded([&] {
+        if (!p) fail(MHG_ERR_INVALID_ARGUMENT, "plan_set_profiling: null plan");
+        p->profiling = enable != 0;
+        p->ev_used = 0;
+    });
+}
+
+mhg_status mhg_plan_gemm_time(mhg_plan p, float* total_ms, uint64_t* launches) {
+    return guarded([&] {
+        if (!p || !total_ms) fail(MHG_ERR_INVALID_ARGUMENT, "plan_gemm_time: bad args");
+        float sum = 0.f;
+        if (p->ev_used) cuda_check(cudaEventSynchronize(p->ev[p->ev_used - 1]), "event sync");
+        for (size_t i = 0; i + 1 < p->ev_used; i += 2) {
+            float ms = 0.f;
+            cuda_check(cudaEventElapsedTime(&ms, p->ev[i], p->ev[i + 1]), "elapsed");
+            sum += ms;
+        }
+        *total_ms = sum;
+        if (launches) *launches = p->ev_used / 2;
+        p->ev_used = 0;
+    });
+}
+
 mhg_status mhg_plan_destroy(mhg_plan p) {
     return guarded([&] {
         if (!p) return;
+        for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
         if (p->exec) cudaGraphExecDestroy(p->exec);
         if (p->graph) cudaGraphDestroy(p->graph);
         if (p->mem) cudaFree(p->mem);

@@ -1,0 +1,119 @@
+"""Multi-GPU partitioning of C <- C +/- A*B by top-level Morton blocks of C.
+
+One process per GPU (torch.distributed, NCCL on GPUs / gloo on CPU for tests).
+With P = 2^b ranks, rank r owns the r-th contiguous 1/P slice of every
+container's flat Morton-hybrid store.  Because the Z order visits quadrants
+NW, NE, SW, SE at every scale (layout.hpp:42-48), that slice is a rectangle:
+the bits of r, from the most significant, alternate (row half, column half)
+choices of successive quadrant levels.  P=2: north/south halves; P=4: the four
+quadrants; P=8: n/4 x n/2 blocks.
+
+C is stationary: rank r updates only its own block C[R_r, C_r].  It needs the
+A row panel A[R_r, :] and the B column panel B[:, C_r].  Those are the union of
+the A slices of the ranks sharing its row band ("row group") and the B slices of
+the ranks sharing its column band ("column group"), so the only exchange is an
+all-gather inside each group -- no reduction, since K is never split.  This is
+the reference's concurrency contract (disjoint output rectangles are
+independent, multiply.hpp:25-29) applied across devices.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Dict, List, Tuple
+
+
+@dataclass(frozen=True)
+class Block:
+    rank: int
+    i0: int
+    j0: int
+    rows: int
+    cols: int
+    row_band: int
+    col_band: int
+
+
+def _bits(P: int) -> int:
+    if P < 1 or P & (P - 1):
+        raise ValueError(f"rank count must be a power of two, got {P}")
+    return P.bit_length() - 1
+
+
+def morton_block(rank: int, P: int, n: int, t: int) -> Block:
+    """Rectangle covered by the rank-th 1/P slice of an n x n Morton-hybrid store."""
+    b = _bits(P)
+    if not 0 <= rank < P:
+        raise ValueError("rank out of range")
+    if (n // t) ** 2 < P:
+        raise ValueError("fewer tiles than ranks")
+    row_bits = (b + 1) // 2
+    col_bits = b // 2
+    rb = cb = 0
+    for k in range(b):  # from the most significant bit of rank
+        bit = (rank >> (b - 1 - k)) & 1
+        if k % 2 == 0:
+            rb = (rb << 1) | bit
+        else:
+            cb = (cb << 1) | bit
+    rows, cols = n >> row_bits, n >> col_bits
+    return Block(rank, rb * rows, cb * cols, rows, cols, rb, cb)
+
+
+def slice_range(rank: int, P: int, n: int) -> Tuple[int, int]:
+    """Flat [begin, end) of the rank's slice of the Morton store."""
+    per = n * n // P
+    return rank * per, (rank + 1) * per
+
+
+def groups(P: int, n: int, t: int) -> Tuple[Dict[int, List[int]], Dict[int, List[int]]]:
+    """row_band -> ranks sharing it, col_band -> ranks sharing it (ascending)."""
+    rows: Dict[int, List[int]] = {}
+    cols: Dict[int, List[int]] = {}
+    for r in range(P):
+        blk = morton_block(r, P, n, t)
+        rows.setdefault(blk.row_band, []).append(r)
+        cols.setdefault(blk.col_band, []).append(r)
+    return rows, cols
+
+
+class PanelExchange:
+    """Creates the row/column process groups once and all-gathers the panels
+    each rank needs directly into its full-size containers (flat tensors)."""
+
+    def __init__(self, P: int, rank: int, n: int, t: int):
+        import torch.distributed as dist
+
+        self.P, self.rank, self.n, self.t = P, rank, n, t
+        self.block = morton_block(rank, P, n, t)
+        rows, cols = groups(P, n, t)
+        self.row_members = rows[self.block.row_band]
+        self.col_members = cols[self.block.col_band]
+        self.row_group = self.col_group = None
+        if P > 1:
+            # every rank must create every group, in the same order
+            for band in sorted(rows):
+                g = dist.new_group(rows[band])
+                if band == self.block.row_band:
+                    self.row_group = g
+            for band in sorted(cols):
+                g = dist.new_group(cols[band])
+                if band == self.block.col_band:
+                    self.col_group = g
+
+    def exchange(self, lhs_flat, rhs_flat):
+        """lhs_flat / rhs_flat: the rank's full-size flat containers, holding its
+        own slice; afterwards they hold the A row panel / B column panel."""
+        import torch.distributed as dist
+
+        if self.P == 1:
+            return
+        for flat, members, group in ((lhs_flat, self.row_members, self.row_group),
+                                     (rhs_flat, self.col_members, self.col_group)):
+            if len(members) == 1:
+                continue
+            parts = []
+            for r in members:
+                b, e = slice_range(r, self.P, self.n)
+                parts.append(flat[b:e])
+            mine = parts[members.index(self.rank)]
+            dist.all_gather(parts, mine.clone(), group=group)
