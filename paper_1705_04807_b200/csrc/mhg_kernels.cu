@@ -127,84 +127,138 @@ __device__ __forceinline__ void to_digits(uint32_t v, const DigitParams& dp, int
     d[L - 1] = (int8_t)x;
 }
 
-constexpr int kPackStride = kBK + 4;  // smem row stride (bytes): conflict-free byte scatter
+// 4 residues -> 4 digits per limb packed little-endian into one 32-bit word
+template <int L>
+__device__ __forceinline__ void digits4(const uint32_t (&v)[4], const DigitParams& dp,
+                                        uint32_t (&w)[L]) {
+#pragma unroll
+    for (int s = 0; s < L; ++s) w[s] = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+        int8_t d[L];
+        to_digits<L>(v[e], dp, d);
+#pragma unroll
+        for (int s = 0; s < L; ++s) w[s] |= (uint32_t)(uint8_t)d[s] << (8 * e);
+    }
+}
 
-// One block = 32 pack rows x 128 K of one operand.  Output layout per
-// (row tile, k tile): [L][rows_per_tile][128 B] with the SWIZZLE_128B
-// pattern applied (16-byte chunk c of row r stored at chunk c ^ (r & 7)).
-template <int L, bool TRANS>
-__global__ void __launch_bounds__(256) k_pack(const uint32_t* __restrict__ src,
-                                              const uint64_t* __restrict__ rowoff,
-                                              const uint64_t* __restrict__ coloff, uint64_t R,
-                                              uint64_t K, uint32_t rows_per_tile, uint32_t Kt,
-                                              int8_t* __restrict__ dst, DigitParams dp) {
-    __shared__ __align__(16) int8_t sd[L][kPackRows][kPackStride];
-    const uint32_t kt = blockIdx.x % Kt;
-    const uint64_t rb = blockIdx.x / Kt;
-    const uint64_t pr0 = rb * kPackRows;
-    const uint64_t k0 = (uint64_t)kt * kBK;
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-
-    if (!TRANS) {
-        // lanes walk K (contiguous inside a Morton tile row of the source)
-        uint64_t co[4];
-        bool kok[4];
-#pragma unroll
-        for (int b = 0; b < 4; ++b) {
-            const uint64_t kk = k0 + tx + 32 * b;
-            kok[b] = kk < K;
-            co[b] = kok[b] ? __ldg(coloff + kk) : 0;
-        }
-#pragma unroll
-        for (int a = 0; a < 4; ++a) {
-            const int r = ty + 8 * a;
-            const uint64_t pr = pr0 + r;
-            const bool rok = pr < R;
-            const uint64_t ro = rok ? __ldg(rowoff + pr) : 0;
-            uint32_t v[4];
-#pragma unroll
-            for (int b = 0; b < 4; ++b) v[b] = (rok && kok[b]) ? __ldg(src + ro + co[b]) : 0u;
-#pragma unroll
-            for (int b = 0; b < 4; ++b) {
-                int8_t d[L];
-                to_digits<L>(v[b], dp, d);
-#pragma unroll
-                for (int s = 0; s < L; ++s) sd[s][r][tx + 32 * b] = d[s];
-            }
-        }
-    } else {
-        // lanes walk pack rows = source columns (contiguous in the source)
-        const uint64_t pr = pr0 + tx;
-        const bool rok = pr < R;
-        const uint64_t co = rok ? __ldg(coloff + pr) : 0;
-#pragma unroll 4
-        for (int b = 0; b < kBK / 8; ++b) {
-            const int kloc = ty + 8 * b;
-            const uint64_t kk = k0 + kloc;
-            const bool kok = kk < K;
-            const uint64_t ro = kok ? __ldg(rowoff + kk) : 0;
-            const uint32_t v = (rok && kok) ? __ldg(src + ro + co) : 0u;
-            int8_t d[L];
-            to_digits<L>(v, dp, d);
-#pragma unroll
-            for (int s = 0; s < L; ++s) sd[s][tx][kloc] = d[s];
+// Load 4 consecutive view cells along the source's column direction: one
+// 16-byte load when they are contiguous and aligned (t % 4 == 0 inside a tile
+// row), else per-cell loads; cells outside the view read as 0.
+__device__ __forceinline__ void load4(const uint32_t* __restrict__ src, uint64_t rbase, bool rok,
+                                      const uint64_t* __restrict__ coloff, uint64_t c0,
+                                      uint64_t ncols, uint32_t (&v)[4]) {
+    if (rok && c0 + 3 < ncols) {
+        const uint64_t a = __ldg(coloff + c0), b = __ldg(coloff + c0 + 3);
+        if (b == a + 3 && ((rbase + a) & 3) == 0) {
+            const uint4 x = __ldcs(reinterpret_cast<const uint4*>(src + rbase + a));
+            v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
+            return;
         }
     }
-    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+        v[e] = (rok && c0 + e < ncols) ? __ldcs(src + rbase + __ldg(coloff + c0 + e)) : 0u;
+}
 
-    const uint64_t rtile = pr0 / rows_per_tile;
-    const uint32_t rit0 = (uint32_t)(pr0 % rows_per_tile);
-    int8_t* base = dst + ((rtile * Kt + kt) * (uint64_t)L) * rows_per_tile * kBK;
+// Destination of the 16-byte chunk holding K bytes [kk, kk+16) of pack row pr,
+// limb s, in the [row tile][k tile][L][rows_per_tile][128 B] SWIZZLE_128B image.
+template <int L>
+__device__ __forceinline__ int8_t* pack_dst(int8_t* dst, uint64_t pr, uint64_t kk, int s,
+                                            uint32_t rpt, uint32_t Kt) {
+    const uint64_t tile = pr / rpt;
+    const uint32_t rit = (uint32_t)(pr - tile * rpt);
+    const uint64_t kt = kk / kBK;
+    const uint32_t ch = (uint32_t)(kk % kBK) >> 4;
+    return dst + ((tile * Kt + kt) * L + s) * (uint64_t)rpt * kBK + (uint64_t)rit * kBK +
+           ((ch ^ (rit & 7)) << 4);
+}
+
+// lhs: pack rows = view rows, K = view columns (contiguous in the source).
+// Block: 32 pack rows x 128 K; thread: 4 rows x 4 consecutive K (one 16-byte load
+// per row).  Smem holds the digit bytes [L][32][128 (+16 pad)].
+constexpr int kRowsStride = kBK + 16;
+
+template <int L>
+__global__ void __launch_bounds__(256) k_pack_rows(const uint32_t* __restrict__ src,
+                                                   const uint64_t* __restrict__ rowoff,
+                                                   const uint64_t* __restrict__ coloff, uint64_t R,
+                                                   uint64_t K, uint32_t rpt, uint32_t Kt,
+                                                   uint64_t Rpad, int8_t* __restrict__ dst,
+                                                   DigitParams dp) {
+    __shared__ __align__(16) uint8_t sd[L][32][kRowsStride];
+    const uint32_t kt = blockIdx.x % Kt;
+    const uint64_t pr0 = (uint64_t)(blockIdx.x / Kt) * 32;
+    const uint64_t k0 = (uint64_t)kt * kBK;
+    const int tk = threadIdx.x & 31, tr = threadIdx.x >> 5;
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        const int r = 4 * tr + a;
+        const uint64_t pr = pr0 + r;
+        const bool rok = pr < R;
+        const uint64_t rb = rok ? __ldg(rowoff + pr) : 0;
+        uint32_t v[4], w[L];
+        load4(src, rb, rok, coloff, k0 + 4 * tk, K, v);
+        digits4<L>(v, dp, w);
+#pragma unroll
+        for (int s = 0; s < L; ++s) *reinterpret_cast<uint32_t*>(&sd[s][r][4 * tk]) = w[s];
+    }
+    __syncthreads();
 #pragma unroll
     for (int e = 0; e < L; ++e) {
-        const int cid = threadIdx.x + 256 * e;  // L * 32 rows * 8 chunks
+        const int cid = threadIdx.x + 256 * e;  // L x 32 rows x 8 chunks
         const int s = cid >> 8, r = (cid >> 3) & 31, ch = cid & 7;
-        const uint32_t* w = reinterpret_cast<const uint32_t*>(&sd[s][r][ch * 16]);
-        const uint4 val = make_uint4(w[0], w[1], w[2], w[3]);
-        const uint32_t rit = rit0 + r;
-        int8_t* o = base + (uint64_t)s * rows_per_tile * kBK + (uint64_t)rit * kBK +
-                    ((ch ^ (rit & 7)) << 4);
-        *reinterpret_cast<uint4*>(o) = val;
+        const uint64_t pr = pr0 + r;
+        if (pr >= Rpad) continue;
+        const uint4 val = *reinterpret_cast<const uint4*>(&sd[s][r][ch * 16]);
+        *reinterpret_cast<uint4*>(pack_dst<L>(dst, pr, k0 + 16 * ch, s, rpt, Kt)) = val;
+    }
+}
+
+// rhs (transposed to K-major): pack rows = view columns (contiguous in the
+// source), K = view rows.  Block: 128 pack rows x 32 K; thread: 4 consecutive
+// pack rows (one 16-byte load) x 4 K rows, transposed in registers.
+constexpr int kColsStride = 36;  // 32 K bytes + 4 pad
+
+template <int L>
+__global__ void __launch_bounds__(256) k_pack_cols(const uint32_t* __restrict__ src,
+                                                   const uint64_t* __restrict__ rowoff,
+                                                   const uint64_t* __restrict__ coloff, uint64_t R,
+                                                   uint64_t K, uint32_t rpt, uint32_t Kt,
+                                                   uint64_t Rpad, int8_t* __restrict__ dst,
+                                                   DigitParams dp) {
+    __shared__ __align__(16) uint8_t sd[L][128][kColsStride];
+    const uint32_t kq = blockIdx.x % (Kt * 4);  // 32-wide K quarter of a k tile
+    const uint64_t pr0 = (uint64_t)(blockIdx.x / (Kt * 4)) * 128;
+    const uint64_t k0 = (uint64_t)kq * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+    uint32_t v[4][4];  // [k][pack row]
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const uint64_t kk = k0 + 4 * ty + i;
+        const bool kok = kk < K;
+        const uint64_t rb = kok ? __ldg(rowoff + kk) : 0;
+        load4(src, rb, kok, coloff, pr0 + 4 * tx, R, v[i]);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        const uint32_t col[4] = {v[0][c], v[1][c], v[2][c], v[3][c]};
+        uint32_t w[L];
+        digits4<L>(col, dp, w);
+#pragma unroll
+        for (int s = 0; s < L; ++s)
+            *reinterpret_cast<uint32_t*>(&sd[s][4 * tx + c][4 * ty]) = w[s];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < L; ++e) {
+        const int cid = threadIdx.x + 256 * e;  // L x 128 rows x 2 chunks
+        const int s = cid >> 8, r = (cid >> 1) & 127, h = cid & 1;
+        const uint64_t pr = pr0 + r;
+        if (pr >= Rpad) continue;
+        const uint32_t* w = reinterpret_cast<const uint32_t*>(&sd[s][r][16 * h]);
+        *reinterpret_cast<uint4*>(pack_dst<L>(dst, pr, k0 + 16 * h, s, rpt, Kt)) =
+            make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
@@ -245,6 +299,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
+
+// named barrier among the 4 epilogue warps (id 1; id 0 is __syncthreads)
+__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
 __device__ __forceinline__ void tc_fence_before() {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -332,7 +389,8 @@ struct GemmCfg {
     static constexpr int STAGE = A_STAGE + B_STAGE;
     static constexpr int STAGES_RAW = (200 * 1024) / STAGE;
     static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
-    static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE + 256 /*barriers*/;
+    static constexpr int SMEM =
+        1024 /*align slack*/ + STAGES * STAGE + 256 /*barriers*/ + 8 * W /*column offsets*/;
     static constexpr int THREADS = 192;                 // producer, MMA, 4 epilogue warps
     static_assert(CLASSES * W <= 512, "TMEM columns");
     static_assert(STAGES >= 2, "pipeline depth");
@@ -365,6 +423,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
     uint64_t* tmem_full = empty + STAGES;
     uint64_t* tmem_empty = tmem_full + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+    uint64_t* s_col = tmem_empty + 2;  // W column offsets of the current tile
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t num_tiles = p.Mt * p.Nt;
@@ -467,9 +526,17 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
         }
     } else {
         // ---------------- epilogue: TMEM -> registers -> fold mod q -> Morton stores
+        // Per tile: (1) stage the tile's column offsets in smem and prefetch the
+        // thread's output row segment (C_old) into registers -- this overlaps the
+        // tile's MMA main loop; (2) per exact K-chunk, drain the 2L-1 weight
+        // classes from TMEM, fold them mod q into the register copy, release
+        // TMEM; (3) store the row segment after TMEM is released, so the stores
+        // overlap the next tile's MMAs.
+        const int ew = warp - 2;    // epilogue warp 0..3
         const int quad = warp & 3;  // TMEM lane quadrant this warp may access
         const int row = quad * 32 + lane;
         const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+        constexpr uint64_t kNoCol = ~uint64_t(0);
         uint32_t acc_ph = 0;
         for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             uint32_t m, n;
@@ -477,66 +544,84 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
             const uint64_t gi = (uint64_t)m * kBM + row;
             const bool row_ok = gi < p.rows;
             const uint64_t rbase = row_ok ? __ldg(p.out_rowoff + gi) : 0;
+            epi_bar_sync();  // previous tile's readers of s_col are done
+            for (int j = ew * 32 + lane; j < W; j += 128) {
+                const uint64_t gj = (uint64_t)n * W + j;
+                s_col[j] = gj < p.cols ? __ldg(p.out_coloff + gj) : kNoCol;
+            }
+            epi_bar_sync();
+            uint32_t cur[W];
+            if (p.mode != 2 && row_ok) {
+#pragma unroll
+                for (int g = 0; g < W / 4; ++g) {
+                    const uint64_t c0 = s_col[4 * g], c3 = s_col[4 * g + 3];
+                    if (p.vec_ok && c3 == c0 + 3 && (c0 & 3) == 0) {
+                        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(p.out + rbase + c0));
+                        cur[4 * g] = v.x;
+                        cur[4 * g + 1] = v.y;
+                        cur[4 * g + 2] = v.z;
+                        cur[4 * g + 3] = v.w;
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const uint64_t c = s_col[4 * g + e];
+                            cur[4 * g + e] = c != kNoCol ? p.out[rbase + c] : 0u;
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < W; ++j) cur[j] = 0u;
+            }
             for (uint32_t c = 0; c < nchunks; ++c) {
-                const bool overwrite = (c == 0) && (p.mode == 2);
                 mbar_wait(tmem_full, acc_ph);
                 tc_fence_after();
-#pragma unroll 1
+#pragma unroll
                 for (int j0 = 0; j0 < W; j0 += 16) {
-                    const uint64_t gj0 = (uint64_t)n * W + j0;
-                    if (gj0 >= p.cols) break;  // warp-uniform
-                    const int nvalid = (p.cols - gj0) >= 16 ? 16 : (int)(p.cols - gj0);
-                    int32_t acc[Cfg::CLASSES][16];
+                    if ((uint64_t)n * W + j0 < p.cols) {  // warp-uniform
+                        int32_t acc[Cfg::CLASSES][16];
 #pragma unroll
-                    for (int k = 0; k < Cfg::CLASSES; ++k)
-                        tmem_ld16(tmem + lane_base + k * W + j0, acc[k]);
-                    tmem_wait_ld();
-                    uint32_t res[16];
+                        for (int k = 0; k < Cfg::CLASSES; ++k)
+                            tmem_ld16(tmem + lane_base + k * W + j0, acc[k]);
+                        tmem_wait_ld();
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        int64_t lo = 0, hi = 0;
+                        for (int j = 0; j < 16; ++j) {
+                            int64_t lo = 0, hi = 0;
 #pragma unroll
-                        for (int k = 0; k < Cfg::CLASSES; ++k) {
-                            if (k < 4) lo += (int64_t)acc[k][j] << (8 * k);
-                            else hi += (int64_t)acc[k][j] << (8 * (k - 4));
-                        }
-                        uint32_t r = red_signed(lo, p);
-                        if (Cfg::CLASSES > 4) {
-                            uint32_t h = mulmod(red_signed(hi, p), p.w32, p);
-                            r += h;
-                            r = r >= p.q ? r - p.q : r;
-                        }
-                        res[j] = r;
-                    }
-                    const uint64_t c0 = __ldg(p.out_coloff + gj0);
-                    bool vec = p.vec_ok && nvalid == 16 && (c0 & 3) == 0;
-                    if (vec) vec = __ldg(p.out_coloff + gj0 + 15) == c0 + 15;
-                    if (row_ok) {
-                        if (vec) {
-                            uint4* dst = reinterpret_cast<uint4*>(p.out + rbase + c0);
-#pragma unroll
-                            for (int v4 = 0; v4 < 4; ++v4) {
-                                uint4 o = overwrite ? make_uint4(0, 0, 0, 0) : dst[v4];
-                                uint32_t* ov = reinterpret_cast<uint32_t*>(&o);
-#pragma unroll
-                                for (int e = 0; e < 4; ++e) {
-                                    uint32_t s = ov[e] + res[4 * v4 + e];
-                                    ov[e] = s >= p.q ? s - p.q : s;
-                                }
-                                dst[v4] = o;
+                            for (int k = 0; k < Cfg::CLASSES; ++k) {
+                                if (k < 4) lo += (int64_t)acc[k][j] << (8 * k);
+                                else hi += (int64_t)acc[k][j] << (8 * (k - 4));
                             }
-                        } else {
-                            for (int j = 0; j < nvalid; ++j) {
-                                uint32_t* a = p.out + rbase + __ldg(p.out_coloff + gj0 + j);
-                                uint32_t s = (overwrite ? 0u : *a) + res[j];
-                                *a = s >= p.q ? s - p.q : s;
+                            uint32_t r = red_signed(lo, p);
+                            if (Cfg::CLASSES > 4) {
+                                const uint32_t h = mulmod(red_signed(hi, p), p.w32, p);
+                                r += h;
+                                r = r >= p.q ? r - p.q : r;
                             }
+                            const uint32_t sum = cur[j0 + j] + r;
+                            cur[j0 + j] = sum >= p.q ? sum - p.q : sum;
                         }
                     }
                 }
                 tc_fence_before();
                 mbar_arrive(tmem_empty);
                 acc_ph ^= 1;
+            }
+            if (row_ok) {
+#pragma unroll
+                for (int g = 0; g < W / 4; ++g) {
+                    const uint64_t c0 = s_col[4 * g], c3 = s_col[4 * g + 3];
+                    if (p.vec_ok && c3 == c0 + 3 && (c0 & 3) == 0) {
+                        __stcs(reinterpret_cast<uint4*>(p.out + rbase + c0),
+                               make_uint4(cur[4 * g], cur[4 * g + 1], cur[4 * g + 2], cur[4 * g + 3]));
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const uint64_t c = s_col[4 * g + e];
+                            if (c != kNoCol) p.out[rbase + c] = cur[4 * g + e];
+                        }
+                    }
+                }
             }
         }
     }
@@ -576,11 +661,16 @@ template <int L>
 int launch_pack_t(int trans, const uint32_t* src, const uint64_t* rowoff, const uint64_t* coloff,
                   uint64_t R, uint64_t K, uint32_t rpt, uint32_t Rtiles, uint32_t Kt, int8_t* dst,
                   DigitParams dp, cudaStream_t s) {
-    const uint64_t blocks = (uint64_t)Rtiles * (rpt / kPackRows) * Kt;
-    if (trans)
-        k_pack<L, true><<<(unsigned)blocks, 256, 0, s>>>(src, rowoff, coloff, R, K, rpt, Kt, dst, dp);
-    else
-        k_pack<L, false><<<(unsigned)blocks, 256, 0, s>>>(src, rowoff, coloff, R, K, rpt, Kt, dst, dp);
+    const uint64_t Rpad = (uint64_t)Rtiles * rpt;
+    if (trans) {
+        const uint64_t blocks = ((Rpad + 127) / 128) * Kt * 4;
+        k_pack_cols<L><<<(unsigned)blocks, 256, 0, s>>>(src, rowoff, coloff, R, K, rpt, Kt, Rpad,
+                                                        dst, dp);
+    } else {
+        const uint64_t blocks = (Rpad / 32) * Kt;
+        k_pack_rows<L><<<(unsigned)blocks, 256, 0, s>>>(src, rowoff, coloff, R, K, rpt, Kt, Rpad,
+                                                        dst, dp);
+    }
     return (int)cudaGetLastError();
 }
 

@@ -1,0 +1,16 @@
+#!/bin/bash
+# ncu evidence for the bench workload (run under gpurun, 1 GPU).
+# 1) plain run must exit 0; 2) launch list (per-kernel device time, serialized,
+# cold-cache: compare SHARES); 3) one full capture of each hot kernel.
+set -u
+CMD="python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu-baseline"
+TAG=${1:-r01}
+mkdir -p gpurun_out
+$CMD > gpurun_out/${TAG}_plain.log 2>&1 || { echo "plain run failed"; exit 1; }
+ncu --metrics gpu__time_duration.sum --clock-control none --csv \
+    --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launches.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 2 -c 1 \
+    -o gpurun_out/${TAG}_gemm_full $CMD > gpurun_out/${TAG}_ncu_gemm.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_pack -s 2 -c 2 \
+    -o gpurun_out/${TAG}_pack_full $CMD > gpurun_out/${TAG}_ncu_pack.log 2>&1
+echo "ncu done"

@@ -1,0 +1,164 @@
+"""Host-side tests (no GPU): the C-ABI library loads and exports every symbol
+include/mhg.h declares, the planner's closed-form Counters equal the
+reference's recursion, the limb representation is exact with the int32
+bound the planner claims, and device entry points fail loudly (no CPU
+fallback) when there is no B200."""
+import ctypes
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "mhg.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(mhg_[a-z_0-9]+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol(mh):
+    lib = ctypes.CDLL(mh.LIB_PATH)
+    syms = _declared_symbols()
+    assert len(syms) >= 25
+    missing = [s for s in syms if not hasattr(lib, s)]
+    assert not missing, missing
+
+
+def test_no_torch_types_in_abi():
+    src = open(os.path.join(ROOT, "include", "mhg.h")).read()
+    assert "torch" not in src.split("*/", 1)[1]
+    assert "cudaStream_t" not in re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+
+
+def test_layout_and_modulus_validation(mh):
+    """layout_test.cpp:20-28, field_test.cpp:10-19, layout_test.cpp:100-106."""
+    mh.Layout(8, 4), mh.Layout(1, 1), mh.Layout(24, 3)
+    for n, t in [(8, 3), (12, 4), (0, 1), (8, 0)]:
+        with pytest.raises(mh.InvalidArgument):
+            mh.Layout(n, t)
+    for q in (0, 1, 9, 2 ** 31, 65535):
+        with pytest.raises(mh.InvalidArgument):
+            mh.Modulus(q)
+    mh.Modulus(2), mh.Modulus(65521), mh.Modulus(2147483647)
+    lay = mh.Layout(8, 4)
+    assert mh.encode(lay, 2, 5) == 25 and mh.encode(lay, 5, 6) == 54
+    assert (mh.extract_i(lay, 47), mh.extract_j(lay, 47)) == (7, 3)
+    with pytest.raises(mh.OutOfRange):
+        mh.encode(lay, 8, 0)
+    with pytest.raises(mh.OutOfRange):
+        mh.extract_i(lay, 64)
+
+
+def test_codec_matches_oracle(mh, oracle):
+    for n, t in [(16, 4), (24, 3), (256, 32), (4096, 64)]:
+        lay = mh.Layout(n, t)
+        rng = np.random.default_rng(n)
+        for _ in range(200):
+            i, j = (int(x) for x in rng.integers(0, n, 2))
+            z = mh.encode(lay, i, j)
+            assert z == oracle.encode(n, t, i, j)
+            assert (mh.extract_i(lay, z), mh.extract_j(lay, z)) == (i, j)
+
+
+def test_planner_counters_equal_reference(mh, oracle, reference):
+    """Closed-form Counters (all five fields) == the reference's recursion."""
+    rng = np.random.default_rng(3)
+    for it in range(400):
+        n = int(rng.choice([8, 16, 32, 64, 128]))
+        t = int(rng.choice([x for x in (1, 2, 4, 8, 16, 32) if x <= n]))
+        if it % 9 == 0:
+            n, t = 48, 3
+        q = 2
+        out, lhs, rhs, _, v = oracle.gen_problem(oracle.rng(it), n, t, q)
+        got = mh.counters_layout(n, t, v.out_origin, v.lhs_origin, v.rhs_origin, v.rows, v.inner,
+                                 v.cols)
+        want = reference.mm_oblivious(n, t, q, out.copy(), lhs, rhs, v)
+        assert got.as_tuple() == want.as_tuple(), (n, t, v)
+
+
+def test_planner_counters_golden(mh):
+    """Reference-generated golden cases (tests/golden/cases.json) and the
+    20-trial batch of bench_test.cpp (oblivious calls + macs columns)."""
+    gold = json.load(open(os.path.join(ROOT, "tests", "golden", "cases.json")))
+    for c in gold:
+        o, l, r, rows, inner, cols = c["views"]
+        got = mh.counters_layout(c["n"], c["t"], o, l, r, rows, inner, cols)
+        assert list(got.as_tuple()) == c["counters"]
+    csv = open(os.path.join(ROOT, "tests", "golden", "bench_trials_seed0_n64_t8_q2.csv")).read()
+    for ln in csv.strip().splitlines()[1:]:
+        f = [int(x) for x in ln.split(",")]
+        got = mh.counters_layout(64, 8, f[1], f[4], f[7], f[2], f[6], f[3])
+        assert (got.base_case_calls, got.scalar_macs) == (f[11], f[12])
+
+
+def test_baseline_config_leaf_counts(mh):
+    """SURVEY 8(a) leaf counts at the BASELINE configurations."""
+    c = mh.counters_layout(512, 32, 0, 0, 0, 512, 512, 512)
+    assert c.base_case_calls == 16 ** 3 and c.recursive_calls == 1 + 8 + 64 + 512 + 4096
+    lay = mh.Layout(8192, 64)
+    z = mh.encode(lay, 96, 160)
+    c = mh.counters_layout(8192, 64, z, z, z, 6144, 2048, 5120)
+    assert c.base_case_calls == 97 * 33 * 81
+    c = mh.counters_layout(32768, 64, 0, 0, 0, 32768, 32768, 32768)
+    assert c.base_case_calls == 512 ** 3 and c.scalar_macs == 32768 ** 3
+
+
+def _digits(v, q, H, L, negate=False):
+    """Python restatement of the device digit split (mhg_kernels.cu to_digits)."""
+    if negate:
+        v = (q - v) % q
+    x = v if v <= H else v - q
+    d = []
+    for _ in range(L - 1):
+        lo = ((x & 0xFF) ^ 0x80) - 0x80
+        d.append(lo)
+        x = (x - lo) >> 8
+    d.append(x)
+    return d
+
+
+@pytest.mark.parametrize("q", [2, 3, 97, 251, 257, 65521, 65537, 16777213, 16777259,
+                               2147483629, 2147483647])
+def test_limb_representation_exact(mh, q):
+    L, H, kmax = mh.limb_params(q)
+    assert q <= 256 ** L and (L == 1 or q > 256 ** (L - 1))
+    rng = np.random.default_rng(q % 1000)
+    vals = {0, 1, q - 1, q // 2, q // 2 + 1, H, min(H + 1, q - 1)} | set(
+        int(x) for x in rng.integers(0, q, 3000))
+    vals = {v for v in vals if v < q}
+    top = 0
+    for v in vals:
+        for neg in (False, True):
+            d = _digits(v, q, H, L, neg)
+            assert all(-128 <= x <= 127 for x in d), (v, d)
+            val = sum(x * 256 ** s for s, x in enumerate(d))
+            assert val % q == ((q - v) % q if neg else v)
+            top = max(top, abs(d[-1]))
+    # the planner's K bound keeps every int32 class sum exact
+    bound = [128] * (L - 1) + [top]
+    worst = max(sum(bound[s] * bound[c - s] for s in range(L) if 0 <= c - s < L)
+                for c in range(2 * L - 1))
+    assert kmax * worst <= 2 ** 31 - 1
+
+
+def test_north_star_fits_one_chunk(mh):
+    """p=65521 needs 2 limbs and keeps K=32768 (cfg5) in one exact chunk;
+    p=2^31-1 needs 4 limbs and fits K=8192 (cfg4)."""
+    L, H, kmax = mh.limb_params(65521)
+    assert L == 2 and kmax >= 32768
+    L, H, kmax = mh.limb_params(2147483647)
+    assert L == 4 and kmax >= 8192
+
+
+def test_device_calls_fail_loudly_without_gpu(mh):
+    """No CPU fallback: without an sm_100 device every compute entry point raises."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises(mh.DeviceError):
+        mh.Matrix(mh.Layout(8, 4), mh.Modulus(2))
+    assert mh.lib().mhg_device_check() != 0
