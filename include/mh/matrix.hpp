@@ -1,0 +1,161 @@
+// mh/matrix.hpp -- Morton-hybrid container (reference: matrix.hpp:13-67).
+//
+// The authoritative copy lives in device memory (a libmhg container, same flat
+// order and bytes as the reference's std::vector<Fp>); a host mirror serves the
+// reference's element accessors.  Dirty tracking keeps them coherent:
+//   - non-const accessors (operator[], set, cells()) make the host copy newer;
+//   - a kernel that writes the container makes the device copy newer;
+//   - whichever side is read next is refreshed first (one bulk copy).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <utility>
+#include <vector>
+
+#include "mh/field.hpp"
+#include "mh/layout.hpp"
+
+namespace mh {
+
+class Matrix {
+public:
+    Matrix(const Layout& lay, const Modulus& mod) : lay_(lay), mod_(mod), host_(lay.total) {
+        gpu::check(mhg_matrix_create(lay.n, lay.t, mod.q, &dev_));  // zero filled
+    }
+
+    Matrix(const Matrix& o) : lay_(o.lay_), mod_(o.mod_) {
+        o.pull();
+        host_ = o.host_;
+        gpu::check(mhg_matrix_create(lay_.n, lay_.t, mod_.q, &dev_));
+        state_ = State::HostNewer;
+    }
+
+    Matrix(Matrix&& o) noexcept
+        : lay_(o.lay_), mod_(o.mod_), host_(std::move(o.host_)), dev_(o.dev_), state_(o.state_) {
+        o.dev_ = nullptr;
+    }
+
+    Matrix& operator=(const Matrix& o) {
+        if (this != &o) {
+            Matrix tmp(o);
+            swap(tmp);
+        }
+        return *this;
+    }
+
+    Matrix& operator=(Matrix&& o) noexcept {
+        swap(o);
+        return *this;
+    }
+
+    ~Matrix() {
+        if (dev_) mhg_matrix_destroy(dev_);
+    }
+
+    const Layout& layout() const { return lay_; }
+    const Modulus& modulus() const { return mod_; }
+
+    Fp operator[](Index z) const {
+        pull();
+        return host_[z];
+    }
+    Fp& operator[](Index z) {
+        pull();
+        state_ = State::HostNewer;
+        return host_[z];
+    }
+
+    Fp at(std::uint64_t i, std::uint64_t j) const { return (*this)[encode(lay_, i, j)]; }
+    void set(std::uint64_t i, std::uint64_t j, Fp v) { (*this)[encode(lay_, i, j)] = v; }
+
+    const std::vector<Fp>& cells() const {
+        pull();
+        return host_;
+    }
+    std::vector<Fp>& cells() {
+        pull();
+        state_ = State::HostNewer;
+        return host_;
+    }
+
+    friend bool operator==(const Matrix& x, const Matrix& y) {
+        return x.lay_.n == y.lay_.n && x.lay_.t == y.lay_.t && x.mod_.q == y.mod_.q &&
+               x.cells() == y.cells();
+    }
+    friend bool operator!=(const Matrix& x, const Matrix& y) { return !(x == y); }
+
+    // ---- device side (used by the multiply entry points)
+    /// Device container with any host-side edits uploaded first.
+    mhg_matrix device() const {
+        push();
+        return dev_;
+    }
+    /// Record that a kernel wrote the device copy.
+    void device_written() { state_ = State::DeviceNewer; }
+
+private:
+    enum class State { InSync, HostNewer, DeviceNewer };
+
+    void pull() const {
+        if (state_ == State::DeviceNewer) {
+            gpu::check(mhg_matrix_download(dev_, reinterpret_cast<std::uint32_t*>(host_.data()),
+                                           nullptr));
+            gpu::check(mhg_synchronize(nullptr));
+            state_ = State::InSync;
+        }
+    }
+    void push() const {
+        if (state_ == State::HostNewer) {
+            gpu::check(mhg_matrix_upload(dev_, reinterpret_cast<const std::uint32_t*>(host_.data()),
+                                         nullptr));
+            state_ = State::InSync;
+        }
+    }
+    void swap(Matrix& o) noexcept {
+        std::swap(lay_, o.lay_);
+        std::swap(mod_, o.mod_);
+        std::swap(host_, o.host_);
+        std::swap(dev_, o.dev_);
+        std::swap(state_, o.state_);
+    }
+
+    Layout lay_;
+    Modulus mod_;
+    mutable std::vector<Fp> host_;
+    mhg_matrix dev_ = nullptr;
+    mutable State state_ = State::InSync;
+};
+static_assert(sizeof(Fp) == sizeof(std::uint32_t), "Fp must be layout-compatible with uint32");
+
+/// Dense row-major grid used for ingestion and checking.
+using Grid = std::vector<std::vector<Fp>>;
+
+/// Row-major -> Morton-hybrid on the device (K1 conversion kernel, which also
+/// rejects residues >= q); shape checks as in the reference.
+inline Matrix from_row_major(const Grid& rows, std::uint64_t t, const Modulus& mod) {
+    const std::uint64_t n = rows.size();
+    Layout lay(n, t);
+    std::vector<std::uint32_t> flat;
+    flat.reserve(n * n);
+    for (const auto& r : rows) {
+        if (r.size() != n) throw std::invalid_argument("from_row_major: grid is not square");
+        for (Fp v : r) flat.push_back(v.v);
+    }
+    Matrix m(lay, mod);
+    gpu::check(mhg_rowmajor_host_to_mh(m.device(), flat.data()));
+    m.device_written();
+    return m;
+}
+
+inline Grid to_row_major(const Matrix& m) {
+    const std::uint64_t n = m.layout().n;
+    std::vector<std::uint32_t> flat(n * n);
+    gpu::check(mhg_mh_to_rowmajor_host(m.device(), flat.data()));
+    Grid rows(n, std::vector<Fp>(n));
+    for (std::uint64_t i = 0; i < n; ++i)
+        for (std::uint64_t j = 0; j < n; ++j) rows[i][j] = Fp{flat[i * n + j]};
+    return rows;
+}
+
+}  // namespace mh

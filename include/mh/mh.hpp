@@ -1,0 +1,9 @@
+// mh/mh.hpp -- umbrella header of the C++ mirror of the reference API
+// (reference: proj/include/mh/mh.hpp), backed by libmhg.so on a B200.
+#pragma once
+
+#include "mh/field.hpp"
+#include "mh/layout.hpp"
+#include "mh/matrix.hpp"
+#include "mh/multiply.hpp"
+#include "mh/submatrix.hpp"

@@ -97,6 +97,12 @@ mhg_status mhg_matrix_download(mhg_matrix m, uint32_t *host_cells, void *stream)
  * with MHG_ERR_INVALID_ARGUMENT (synchronous on `stream`). */
 mhg_status mhg_rowmajor_to_mh(mhg_matrix dst, const uint32_t *device_rows, void *stream);
 mhg_status mhg_mh_to_rowmajor(mhg_matrix src, uint32_t *device_rows, void *stream);
+/* Same two conversions from / to HOST row-major buffers (staged through a
+ * device scratch buffer, K1 on the device); synchronous. */
+mhg_status mhg_rowmajor_host_to_mh(mhg_matrix dst, const uint32_t *host_rows);
+mhg_status mhg_mh_to_rowmajor_host(mhg_matrix src, uint32_t *host_rows);
+/* cudaStreamSynchronize(stream) for callers that do not link the CUDA runtime. */
+mhg_status mhg_synchronize(void *stream);
 
 /* ---- multiply (multiply.hpp) ---- */
 /* out op= lhs * rhs over the three views, computed on the GPU with the int8

@@ -467,6 +467,44 @@ mhg_status mhg_mh_to_rowmajor(mhg_matrix src, uint32_t* rows, void* stream) {
     });
 }
 
+mhg_status mhg_synchronize(void* stream) {
+    return guarded([&] {
+        require_device();
+        cuda_check(cudaStreamSynchronize((cudaStream_t)stream), "synchronize");
+    });
+}
+
+mhg_status mhg_rowmajor_host_to_mh(mhg_matrix dst, const uint32_t* host_rows) {
+    return guarded([&] {
+        if (!dst || !host_rows) fail(MHG_ERR_INVALID_ARGUMENT, "rowmajor_host_to_mh: null pointer");
+        require_device();
+        uint32_t* tmp = nullptr;
+        const uint64_t bytes = dst->n * dst->n * 4;
+        cuda_check(cudaMalloc(&tmp, bytes), "scratch alloc");
+        mhg_status st = MHG_OK;
+        const cudaError_t e = cudaMemcpy(tmp, host_rows, bytes, cudaMemcpyHostToDevice);
+        if (e == cudaSuccess) st = mhg_rowmajor_to_mh(dst, tmp, nullptr);
+        const std::string msg = g_last_error;
+        cudaFree(tmp);
+        cuda_check((int)e, "rowmajor upload");
+        if (st) fail(st, msg);
+    });
+}
+
+mhg_status mhg_mh_to_rowmajor_host(mhg_matrix src, uint32_t* host_rows) {
+    return guarded([&] {
+        if (!src || !host_rows) fail(MHG_ERR_INVALID_ARGUMENT, "mh_to_rowmajor_host: null pointer");
+        require_device();
+        uint32_t* tmp = nullptr;
+        const uint64_t bytes = src->n * src->n * 4;
+        cuda_check(cudaMalloc(&tmp, bytes), "scratch alloc");
+        int err = mhg::launch_mh_to_rm(src->cells, tmp, src->n, mhg::tile_geom(src->t), nullptr);
+        if (!err) err = (int)cudaMemcpy(host_rows, tmp, bytes, cudaMemcpyDeviceToHost);
+        cudaFree(tmp);
+        cuda_check(err, "mh_to_rowmajor_host");
+    });
+}
+
 // --------------------------------------------------------------- multiply
 mhg_status mhg_counters_oblivious(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_counters* ctr) {
     return guarded([&] {

@@ -1,0 +1,25 @@
+"""The reference's unit-test scenarios compiled against the C++ mirror
+(include/mh/*.hpp) and run on the GPU through libmhg.so."""
+import os
+import subprocess
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "tests", "cpp", "dropin_test")
+
+
+def test_cpp_headers_compile():
+    """The C++ mirror compiles and links against libmhg.so (no GPU needed)."""
+    subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
+    assert os.path.exists(BIN)
+
+
+@pytest.mark.gpu
+def test_cpp_dropin_on_gpu(gpu):
+    if not os.path.exists(BIN):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
+    r = subprocess.run([BIN], capture_output=True, text=True, timeout=300)
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failures" in r.stdout
