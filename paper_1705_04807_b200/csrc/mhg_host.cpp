@@ -4,9 +4,11 @@
 // container handles, the planner (closed-form Counters + task grid), the
 // packing workspace and CUDA-graph capture of a plan.  All arithmetic runs in
 // the sm_100a kernels of mhg_kernels.cu; there is no CPU compute path.
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -226,6 +228,57 @@ mhg::GemmParams gemm_params(const Buffers& b, const mhg_view& out, const Checked
     return p;
 }
 
+// 2D uint8 tensor map over a packed operand: rows of 128 bytes, box of
+// `box_rows` rows, no swizzle (the pack kernels already wrote the swizzled
+// shared-memory image).  cuTensorMapEncodeTiled comes from the driver entry
+// point, so the library does not link libcuda.
+struct TensorMaps {
+    CUtensorMap a, b;
+};
+
+void make_tmap(CUtensorMap* tm, const void* base, uint64_t bytes, uint32_t box_rows) {
+    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static Encode encode = nullptr;
+    if (!encode) {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        cuda_check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q),
+                   "cuTensorMapEncodeTiled lookup");
+        if (!fn || q != cudaDriverEntryPointSuccess)
+            fail(MHG_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<Encode>(fn);
+    }
+    const cuuint64_t dims[2] = {128, bytes / 128};
+    const cuuint64_t strides[1] = {128};
+    const cuuint32_t box[2] = {128, box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims,
+                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(MHG_ERR_DEVICE, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+}
+
+TensorMaps tensor_maps(const Buffers& b, const mhg::GemmGeometry& g) {
+    TensorMaps t{};
+    if (g.pair) {
+        make_tmap(&t.a, b.apack, g.apack_bytes, mhg::kBM);
+        make_tmap(&t.b, b.bpack, g.bpack_bytes, (uint32_t)mhg::gemm2_b_box_rows((int)g.L));
+    }
+    return t;
+}
+
+void launch_gemm_any(const mhg::GemmParams& p, const mhg::GemmGeometry& g, const TensorMaps& tm,
+                     void* stream) {
+    if (g.pair)
+        cuda_check(mhg::launch_gemm2((int)g.L, p, &tm.a, &tm.b, device_info().sms, stream), "gemm2");
+    else
+        cuda_check(mhg::launch_gemm((int)g.L, p, device_info().sms, stream), "gemm");
+}
+
 // Pack both operands and run the GEMM: 2 pack launches + 1 GEMM launch.
 void launch_multiply(const Buffers& b, const mhg_view& out, const mhg_view& lhs,
                      const mhg_view& rhs, const Checked& c, const mhg::GemmGeometry& g,
@@ -240,10 +293,43 @@ void launch_multiply(const Buffers& b, const mhg_view& out, const mhg_view& lhs,
     cuda_check(mhg::launch_pack((int)g.L, 1, rhs.mat->cells, b.rhs_row, b.rhs_col, c.rr.cols,
                                 c.rr.rows, g.W, g.Nt, g.Kt, b.bpack, dr, stream),
                "pack rhs");
-    const mhg::GemmParams p = gemm_params(b, out, c, g, op);
+    mhg::GemmParams p = gemm_params(b, out, c, g, op);
+    // diagnostics: MHG_GEMM_STATS=1 prints per-CTA wait-cycle shares (synchronous)
+    static const bool stats_on = std::getenv("MHG_GEMM_STATS") != nullptr;
+    unsigned long long* stats = nullptr;
+    if (stats_on) {
+        cuda_check(cudaMalloc(&stats, 148 * 8 * mhg::kStatCount * 2), "stats alloc");
+        cuda_check(cudaMemset(stats, 0, 148 * 8 * mhg::kStatCount * 2), "stats zero");
+        p.stats = stats;
+    }
+    const TensorMaps tm = tensor_maps(b, g);
     if (gemm_begin) cuda_check(cudaEventRecord(gemm_begin, (cudaStream_t)stream), "event");
-    cuda_check(mhg::launch_gemm((int)g.L, p, device_info().sms, stream), "gemm");
+    launch_gemm_any(p, g, tm, stream);
     if (gemm_end) cuda_check(cudaEventRecord(gemm_end, (cudaStream_t)stream), "event");
+    if (stats) {
+        const int n = device_info().sms;
+        std::vector<unsigned long long> h((size_t)n * mhg::kStatCount);
+        cuda_check(cudaStreamSynchronize((cudaStream_t)stream), "stats sync");
+        cuda_check(cudaMemcpy(h.data(), stats, h.size() * 8, cudaMemcpyDeviceToHost), "stats copy");
+        cudaFree(stats);
+        // MMA-side counters come from MMA-issuing CTAs only (pair leaders);
+        // producer / epilogue counters from every CTA: normalise separately
+        double tot = 0, s[mhg::kStatCount] = {0};
+        int issuers = 0;
+        for (int b = 0; b < n; ++b) {
+            if (h[(size_t)b * mhg::kStatCount + mhg::kStatTotal]) ++issuers;
+            for (int k = 0; k < mhg::kStatCount; ++k) s[k] += (double)h[(size_t)b * mhg::kStatCount + k];
+        }
+        tot = s[mhg::kStatTotal] / (issuers ? issuers : 1);
+        for (int k : {1, 2}) s[k] /= (issuers ? issuers : 1);
+        for (int k : {3, 4, 5}) s[k] /= n;
+        std::fprintf(stderr,
+                     "[mhg stats] L=%u tiles=%u  MMA wait(full)=%.1f%%  MMA wait(tmem_empty)=%.1f%%  "
+                     "producer wait(empty)=%.1f%%  epilogue wait(tmem_full)=%.1f%%  epilogue busy=%.1f%%  "
+                     "(cycles per MMA issuer %.3g, %s)\n",
+                     g.L, g.Mt * g.Nt, 100 * s[1] / tot, 100 * s[2] / tot, 100 * s[3] / tot,
+                     100 * s[4] / tot, 100 * s[5] / tot, tot, g.pair ? "cta pair" : "1 cta");
+    }
 }
 
 // One-shot workspace for mhg_mm: grows on demand; an event orders reuse
@@ -673,12 +759,13 @@ mhg_status mhg_plan_time_gemm(mhg_plan p, int iters, void* stream, float* ms) {
         // GEMM alone on the plan's packed operands (as left by the last run);
         // repeated ADD/SUB keep `out` a valid residue container.
         mhg::GemmParams prm = gemm_params(p->buf, p->out, p->chk, p->geo, p->op);
+        const TensorMaps tm = tensor_maps(p->buf, p->geo);
         cudaEvent_t a, b;
         cuda_check(cudaEventCreate(&a), "event");
         cuda_check(cudaEventCreate(&b), "event");
         cuda_check(cudaEventRecord(a, (cudaStream_t)stream), "event");
         for (int i = 0; i < iters; ++i)
-            cuda_check(mhg::launch_gemm((int)p->geo.L, prm, device_info().sms, stream), "gemm");
+            launch_gemm_any(prm, p->geo, tm, stream);
         cuda_check(cudaEventRecord(b, (cudaStream_t)stream), "event");
         cuda_check(cudaEventSynchronize(b), "event sync");
         float t = 0.f;

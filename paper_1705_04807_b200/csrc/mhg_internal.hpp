@@ -59,7 +59,12 @@ struct GemmParams {
     uint64_t bias;               // multiple of q >= 2^62 (signed -> unsigned shift)
     int mode;                    // 0: out += prod, 2: out = prod (first chunk)
     int vec_ok;                  // t % 4 == 0: 16-byte epilogue accesses allowed
+    unsigned long long* stats;   // optional per-CTA wait-cycle counters (diagnostics), or null
 };
+
+// k_gemm diagnostics layout (per CTA, when GemmParams::stats != null)
+enum GemmStat { kStatTotal = 0, kStatMmaWaitFull, kStatMmaWaitTmem, kStatProdWaitEmpty,
+                kStatEpiWaitFull, kStatEpiBusy, kStatCount };
 
 // --------------------------------------------------------------- launchers
 // All asynchronous on `stream`; return a cudaError_t value (0 = success).
@@ -77,6 +82,11 @@ int launch_pack(int L, int trans, const uint32_t* src, const uint64_t* rowoff,
 int launch_gemm(int L, const GemmParams& p, int num_sms, void* stream);
 int gemm_smem_bytes(int L);
 int configure_kernels();  // one-time kernel attributes (dynamic smem opt-in)
+// CTA-pair GEMM: tmA / tmB point to CUtensorMap (2D uint8, rows of 128 B; box
+// 128 rows for A, gemm2_b_box_rows(L) rows for B'); requires p.Mt even.
+int launch_gemm2(int L, const GemmParams& p, const void* tmA, const void* tmB, int num_sms,
+                 void* stream);
+int gemm2_b_box_rows(int L);
 int launch_fill_view(uint32_t* out, const uint64_t* rowoff, const uint64_t* coloff, uint64_t rows,
                      uint64_t cols, uint32_t value, void* stream);
 

@@ -14,6 +14,7 @@
 //                  folds them mod q and applies out (+)= ... at Morton addresses.
 //                  Replaces base_case_mm (multiply.hpp:136-172) + add/mul
 //                  (field.hpp:43-55).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -301,7 +302,8 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // named barrier among the 4 epilogue warps (id 1; id 0 is __syncthreads)
-__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, %0;" ::"n"(N) : "memory"); }
 
 __device__ __forceinline__ void tc_fence_before() {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -391,7 +393,10 @@ struct GemmCfg {
     static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
     static constexpr int SMEM =
         1024 /*align slack*/ + STAGES * STAGE + 256 /*barriers*/ + 8 * W /*column offsets*/;
-    static constexpr int THREADS = 192;                 // producer, MMA, 4 epilogue warps
+    static constexpr int EPI_WARPS = 8;                 // two per SMSP, each half the columns
+    static constexpr int EPI_THREADS = EPI_WARPS * 32;
+    static constexpr int WH = W / 2;                    // columns per epilogue warp
+    static constexpr int THREADS = 64 + EPI_THREADS;    // producer, MMA, epilogue warps
     static_assert(CLASSES * W <= 512, "TMEM columns");
     static_assert(STAGES >= 2, "pipeline depth");
 };
@@ -440,7 +445,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
             mbar_init(&empty[s], 1);
         }
         mbar_init(tmem_full, 1);
-        mbar_init(tmem_empty, 128);
+        mbar_init(tmem_empty, Cfg::EPI_THREADS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -454,13 +459,16 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
         if (lane == 0) {
             int st = 0;
             uint32_t ph = 0;
+            long long wait_empty = 0;
             for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
                 uint32_t m, n;
                 tile_coords(tile, p.Mt, p.Nt, m, n);
                 const int8_t* a_src = p.apack + (uint64_t)m * p.Kt * Cfg::A_STAGE;
                 const int8_t* b_src = p.bpack + (uint64_t)n * p.Kt * Cfg::B_STAGE;
                 for (uint32_t kt = 0; kt < p.Kt; ++kt) {
+                    const long long w0 = clock64();
                     mbar_wait(&empty[st], ph ^ 1);
+                    wait_empty += clock64() - w0;
                     mbar_expect_tx(&full[st], Cfg::STAGE);
                     bulk_g2s(sA + st * Cfg::A_STAGE, a_src + (uint64_t)kt * Cfg::A_STAGE,
                              Cfg::A_STAGE, &full[st]);
@@ -472,6 +480,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
                     }
                 }
             }
+            if (p.stats) p.stats[(uint64_t)blockIdx.x * kStatCount + kStatProdWaitEmpty] = wait_empty;
         }
     } else if (warp == 1) {
         // ---------------- MMA issuer (single thread)
@@ -481,14 +490,20 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
             constexpr uint32_t id_one = idesc_i8(kBM, W);
             int st = 0;
             uint32_t ph = 0, acc_ph = 0;
+            long long wait_full = 0, wait_tmem = 0;
+            const long long t_begin = clock64();
             for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
                 for (uint32_t c = 0; c < nchunks; ++c) {
                     const uint32_t kb = c * p.KC;
                     const uint32_t ke = (kb + p.KC < p.Kt) ? kb + p.KC : p.Kt;
+                    long long w0 = clock64();
                     mbar_wait(tmem_empty, acc_ph ^ 1);
+                    wait_tmem += clock64() - w0;
                     tc_fence_after();
                     for (uint32_t kt = kb; kt < ke; ++kt) {
+                        w0 = clock64();
                         mbar_wait(&full[st], ph);
+                        wait_full += clock64() - w0;
                         tc_fence_after();
                         const uint32_t a0 = smem_u32(sA + st * Cfg::A_STAGE);
                         const uint32_t b0 = smem_u32(sB + st * Cfg::B_STAGE);
@@ -523,6 +538,12 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
                     acc_ph ^= 1;
                 }
             }
+            if (p.stats) {
+                unsigned long long* o = p.stats + (uint64_t)blockIdx.x * kStatCount;
+                o[kStatTotal] = clock64() - t_begin;
+                o[kStatMmaWaitFull] = wait_full;
+                o[kStatMmaWaitTmem] = wait_tmem;
+            }
         }
     } else {
         // ---------------- epilogue: TMEM -> registers -> fold mod q -> Morton stores
@@ -532,29 +553,33 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
         // classes from TMEM, fold them mod q into the register copy, release
         // TMEM; (3) store the row segment after TMEM is released, so the stores
         // overlap the next tile's MMAs.
-        const int ew = warp - 2;    // epilogue warp 0..3
-        const int quad = warp & 3;  // TMEM lane quadrant this warp may access
+        constexpr int WH = Cfg::WH;
+        const int ew = warp - 2;              // epilogue warp 0..7
+        const int quad = warp & 3;            // TMEM lane quadrant this warp may access
+        const int jb = (ew >> 2) * WH;        // first tile column of this warp
         const int row = quad * 32 + lane;
         const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
         constexpr uint64_t kNoCol = ~uint64_t(0);
         uint32_t acc_ph = 0;
+        long long epi_wait = 0, epi_busy = 0;
         for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             uint32_t m, n;
             tile_coords(tile, p.Mt, p.Nt, m, n);
             const uint64_t gi = (uint64_t)m * kBM + row;
             const bool row_ok = gi < p.rows;
             const uint64_t rbase = row_ok ? __ldg(p.out_rowoff + gi) : 0;
-            epi_bar_sync();  // previous tile's readers of s_col are done
-            for (int j = ew * 32 + lane; j < W; j += 128) {
+            epi_bar_sync<Cfg::EPI_THREADS>();  // previous tile's readers of s_col are done
+            for (int j = ew * 32 + lane; j < W; j += Cfg::EPI_THREADS) {
                 const uint64_t gj = (uint64_t)n * W + j;
                 s_col[j] = gj < p.cols ? __ldg(p.out_coloff + gj) : kNoCol;
             }
-            epi_bar_sync();
-            uint32_t cur[W];
+            epi_bar_sync<Cfg::EPI_THREADS>();
+            const uint64_t* col = s_col + jb;
+            uint32_t cur[WH];
             if (p.mode != 2 && row_ok) {
 #pragma unroll
-                for (int g = 0; g < W / 4; ++g) {
-                    const uint64_t c0 = s_col[4 * g], c3 = s_col[4 * g + 3];
+                for (int g = 0; g < WH / 4; ++g) {
+                    const uint64_t c0 = col[4 * g], c3 = col[4 * g + 3];
                     if (p.vec_ok && c3 == c0 + 3 && (c0 & 3) == 0) {
                         const uint4 v = __ldcs(reinterpret_cast<const uint4*>(p.out + rbase + c0));
                         cur[4 * g] = v.x;
@@ -564,25 +589,28 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
                     } else {
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
-                            const uint64_t c = s_col[4 * g + e];
+                            const uint64_t c = col[4 * g + e];
                             cur[4 * g + e] = c != kNoCol ? p.out[rbase + c] : 0u;
                         }
                     }
                 }
             } else {
 #pragma unroll
-                for (int j = 0; j < W; ++j) cur[j] = 0u;
+                for (int j = 0; j < WH; ++j) cur[j] = 0u;
             }
             for (uint32_t c = 0; c < nchunks; ++c) {
+                long long w0 = clock64();
                 mbar_wait(tmem_full, acc_ph);
+                const long long w1 = clock64();
+                epi_wait += w1 - w0;
                 tc_fence_after();
 #pragma unroll
-                for (int j0 = 0; j0 < W; j0 += 16) {
-                    if ((uint64_t)n * W + j0 < p.cols) {  // warp-uniform
+                for (int j0 = 0; j0 < WH; j0 += 16) {
+                    if ((uint64_t)n * W + jb + j0 < p.cols) {  // warp-uniform
                         int32_t acc[Cfg::CLASSES][16];
 #pragma unroll
                         for (int k = 0; k < Cfg::CLASSES; ++k)
-                            tmem_ld16(tmem + lane_base + k * W + j0, acc[k]);
+                            tmem_ld16(tmem + lane_base + k * W + jb + j0, acc[k]);
                         tmem_wait_ld();
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
@@ -605,24 +633,29 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
                 }
                 tc_fence_before();
                 mbar_arrive(tmem_empty);
+                epi_busy += clock64() - w1;
                 acc_ph ^= 1;
             }
             if (row_ok) {
 #pragma unroll
-                for (int g = 0; g < W / 4; ++g) {
-                    const uint64_t c0 = s_col[4 * g], c3 = s_col[4 * g + 3];
+                for (int g = 0; g < WH / 4; ++g) {
+                    const uint64_t c0 = col[4 * g], c3 = col[4 * g + 3];
                     if (p.vec_ok && c3 == c0 + 3 && (c0 & 3) == 0) {
                         __stcs(reinterpret_cast<uint4*>(p.out + rbase + c0),
                                make_uint4(cur[4 * g], cur[4 * g + 1], cur[4 * g + 2], cur[4 * g + 3]));
                     } else {
 #pragma unroll
                         for (int e = 0; e < 4; ++e) {
-                            const uint64_t c = s_col[4 * g + e];
+                            const uint64_t c = col[4 * g + e];
                             if (c != kNoCol) p.out[rbase + c] = cur[4 * g + e];
                         }
                     }
                 }
             }
+        }
+        if (p.stats && threadIdx.x == 64) {
+            p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiWaitFull] = epi_wait;
+            p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiBusy] = epi_busy;
         }
     }
 
@@ -631,6 +664,381 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
     }
+}
+
+// =====================================================================
+// K3' k_gemm2: the same GEMM on a CTA pair (tcgen05 cta_group::2, M = 256).
+// Each CTA of the pair holds its own 128-row A tile (all L limbs) and HALF of
+// the stacked B' (N rows [rank*NB/2, (rank+1)*NB/2)); the leader issues one
+// 256 x NB x 32 MMA per limb that reads both CTAs' shared memory and writes
+// each CTA's TMEM (its 128 rows).  Per-SM operand traffic drops by 25%
+// versus k_gemm (B' is no longer replicated per 128 rows).
+//   - loads: cp.async.bulk.tensor.2d.cta_group::2 from both CTAs complete on
+//     the LEADER's full barrier (mapa address);
+//   - MMA completion: tcgen05.commit.cta_group::2 multicast to both CTAs'
+//     empty / tmem_full barriers;
+//   - TMEM release: each epilogue warp of both CTAs arrives on the leader's
+//     tmem_empty (remote arrive through the cluster window);
+//   - the upper weight classes [L, 2L-1) are zeroed by the epilogue right
+//     after it drains them, so every MMA but the first of a chunk accumulates.
+// =====================================================================
+template <int L>
+struct Gemm2Cfg {
+    static constexpr int W = (L <= 2) ? 128 : 64;
+    static constexpr int NB = L * W;
+    static constexpr int NBH = NB / 2;                  // B' rows per CTA
+    static constexpr int CLASSES = 2 * L - 1;
+    static constexpr int A_STAGE = L * kBM * kBK;
+    static constexpr int B_STAGE = NBH * kBK;
+    static constexpr int STAGE = A_STAGE + B_STAGE;
+    static constexpr int STAGES_RAW = (200 * 1024) / STAGE;
+    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
+    static constexpr int SMEM = 1024 + STAGES * STAGE + 512 + 8 * W;
+    static constexpr int EPI_WARPS = 8;
+    static constexpr int EPI_THREADS = EPI_WARPS * 32;
+    static constexpr int WH = W / 2;
+    static constexpr int THREADS = 64 + EPI_THREADS;
+    static_assert(CLASSES * W <= 512, "TMEM columns");
+    static_assert(STAGES >= 2, "pipeline depth");
+    static_assert(NBH % 16 == 0 || NBH == 64, "B' half rows");
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+}
+
+__device__ __forceinline__ void tma2d_pair(uint32_t dst, const void* tmap, int c0, int c1,
+                                           uint32_t leader_bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(leader_bar)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_i8_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"((uint16_t)0x3)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_zero16(uint32_t taddr) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(taddr),
+        "r"(0)
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_wait_st() {
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+template <int L>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS, 1)
+    k_gemm2(const __grid_constant__ GemmParams p, const __grid_constant__ CUtensorMap tmA,
+            const __grid_constant__ CUtensorMap tmB) {
+    using Cfg = Gemm2Cfg<L>;
+    constexpr int W = Cfg::W;
+    constexpr int WH = Cfg::WH;
+    constexpr int STAGES = Cfg::STAGES;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * Cfg::A_STAGE;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tmem_full = empty + STAGES;
+    uint64_t* tmem_empty = tmem_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+    uint64_t* s_col = tmem_empty + 2;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_rank();
+    const uint32_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+    const uint32_t Mt2 = p.Mt >> 1;  // host pads Mt to even
+    const uint32_t num_tiles = Mt2 * p.Nt;
+    const uint32_t nchunks = (p.Kt + p.KC - 1) / p.KC;
+
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else if (warp == 1 && lane == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tmem_full, 1);
+        mbar_init(tmem_empty, 2 * Cfg::EPI_WARPS);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (warp >= 2) {
+        // zero the upper weight classes once; afterwards the epilogue re-zeroes
+        // them as it drains them
+        const int ew = warp - 2, quad = warp & 3, jb = (ew >> 2) * WH;
+        const uint32_t lb = (uint32_t)(quad * 32) << 16;
+#pragma unroll
+        for (int k = L; k < Cfg::CLASSES; ++k)
+#pragma unroll
+            for (int j0 = 0; j0 < WH; j0 += 16) tmem_zero16(tmem + lb + k * W + jb + j0);
+        tmem_wait_st();
+    }
+    tc_fence_before();
+    cluster_sync_all();
+    tc_fence_after();
+
+    if (warp == 0) {
+        if (lane == 0) {
+            long long wait_empty = 0;
+            int st = 0;
+            uint32_t ph = 0;
+            for (uint32_t tile = pair; tile < num_tiles; tile += npairs) {
+                uint32_t pm, n;
+                tile_coords(tile, Mt2, p.Nt, pm, n);
+                const uint32_t m = 2 * pm + rank;
+                for (uint32_t kt = 0; kt < p.Kt; ++kt) {
+                    const long long w0 = clock64();
+                    mbar_wait(&empty[st], ph ^ 1);
+                    wait_empty += clock64() - w0;
+                    if (rank == 0) mbar_expect_tx(&full[st], 2 * Cfg::STAGE);
+                    const uint32_t lbar = mapa_shared(smem_u32(&full[st]), 0);
+                    const int arow = (int)(((uint64_t)m * p.Kt + kt) * L * kBM);
+#pragma unroll
+                    for (int l = 0; l < L; ++l)
+                        tma2d_pair(smem_u32(sA + st * Cfg::A_STAGE + l * kBM * kBK), &tmA, 0,
+                                   arow + l * kBM, lbar);
+                    const int brow = (int)(((uint64_t)n * p.Kt + kt) * Cfg::NB + rank * Cfg::NBH);
+                    tma2d_pair(smem_u32(sB + st * Cfg::B_STAGE), &tmB, 0, brow, lbar);
+                    if (++st == STAGES) {
+                        st = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+            if (p.stats) p.stats[(uint64_t)blockIdx.x * kStatCount + kStatProdWaitEmpty] = wait_empty;
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {
+            constexpr uint32_t id_full = idesc_i8(2 * kBM, Cfg::NB);
+            int st = 0;
+            uint32_t ph = 0, acc_ph = 0;
+            long long wait_full = 0, wait_tmem = 0;
+            const long long t_begin = clock64();
+            for (uint32_t tile = pair; tile < num_tiles; tile += npairs) {
+                for (uint32_t c = 0; c < nchunks; ++c) {
+                    const uint32_t kb = c * p.KC;
+                    const uint32_t ke = (kb + p.KC < p.Kt) ? kb + p.KC : p.Kt;
+                    long long w0 = clock64();
+                    mbar_wait(tmem_empty, acc_ph ^ 1);
+                    wait_tmem += clock64() - w0;
+                    tc_fence_after();
+                    for (uint32_t kt = kb; kt < ke; ++kt) {
+                        w0 = clock64();
+                        mbar_wait(&full[st], ph);
+                        wait_full += clock64() - w0;
+                        tc_fence_after();
+                        const uint32_t a0 = smem_u32(sA + st * Cfg::A_STAGE);
+                        const uint32_t b0 = smem_u32(sB + st * Cfg::B_STAGE);
+#pragma unroll
+                        for (int kk = 0; kk < kBK / 32; ++kk) {
+                            const bool first = (kt == kb) && (kk == 0);
+                            const uint64_t bd = sdesc(b0 + kk * 32);
+#pragma unroll
+                            for (int s = 0; s < L; ++s)
+                                mma_i8_pair(tmem + s * W, sdesc(a0 + s * kBM * kBK + kk * 32), bd,
+                                            id_full, (first && s == 0) ? 0u : 1u);
+                        }
+                        tc_commit_pair(&empty[st]);
+                        if (++st == STAGES) {
+                            st = 0;
+                            ph ^= 1;
+                        }
+                    }
+                    tc_commit_pair(tmem_full);
+                    acc_ph ^= 1;
+                }
+            }
+            if (p.stats) {
+                unsigned long long* o = p.stats + (uint64_t)blockIdx.x * kStatCount;
+                o[kStatTotal] = clock64() - t_begin;
+                o[kStatMmaWaitFull] = wait_full;
+                o[kStatMmaWaitTmem] = wait_tmem;
+            }
+        }
+    } else {
+        const int ew = warp - 2;
+        const int quad = warp & 3;
+        const int jb = (ew >> 2) * WH;
+        const int row = quad * 32 + lane;
+        const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+        const uint32_t leader_tmem_empty = mapa_shared(smem_u32(tmem_empty), 0);
+        constexpr uint64_t kNoCol = ~uint64_t(0);
+        uint32_t acc_ph = 0;
+        long long epi_wait = 0, epi_busy = 0;
+        for (uint32_t tile = pair; tile < num_tiles; tile += npairs) {
+            uint32_t pm, n;
+            tile_coords(tile, Mt2, p.Nt, pm, n);
+            const uint32_t m = 2 * pm + rank;
+            const uint64_t gi = (uint64_t)m * kBM + row;
+            const bool row_ok = gi < p.rows;
+            const uint64_t rbase = row_ok ? __ldg(p.out_rowoff + gi) : 0;
+            epi_bar_sync<Cfg::EPI_THREADS>();
+            for (int j = ew * 32 + lane; j < W; j += Cfg::EPI_THREADS) {
+                const uint64_t gj = (uint64_t)n * W + j;
+                s_col[j] = gj < p.cols ? __ldg(p.out_coloff + gj) : kNoCol;
+            }
+            epi_bar_sync<Cfg::EPI_THREADS>();
+            const uint64_t* col = s_col + jb;
+            uint32_t cur[WH];
+            if (p.mode != 2 && row_ok) {
+#pragma unroll
+                for (int g = 0; g < WH / 4; ++g) {
+                    const uint64_t c0 = col[4 * g], c3 = col[4 * g + 3];
+                    if (p.vec_ok && c3 == c0 + 3 && (c0 & 3) == 0) {
+                        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(p.out + rbase + c0));
+                        cur[4 * g] = v.x;
+                        cur[4 * g + 1] = v.y;
+                        cur[4 * g + 2] = v.z;
+                        cur[4 * g + 3] = v.w;
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const uint64_t cc = col[4 * g + e];
+                            cur[4 * g + e] = cc != kNoCol ? p.out[rbase + cc] : 0u;
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < WH; ++j) cur[j] = 0u;
+            }
+            for (uint32_t c = 0; c < nchunks; ++c) {
+                const long long w0 = clock64();
+                mbar_wait(tmem_full, acc_ph);
+                const long long w1 = clock64();
+                epi_wait += w1 - w0;
+                tc_fence_after();
+#pragma unroll
+                for (int j0 = 0; j0 < WH; j0 += 16) {
+                    int32_t acc[Cfg::CLASSES][16];
+#pragma unroll
+                    for (int k = 0; k < Cfg::CLASSES; ++k)
+                        tmem_ld16(tmem + lane_base + k * W + jb + j0, acc[k]);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int k = L; k < Cfg::CLASSES; ++k) tmem_zero16(tmem + lane_base + k * W + jb + j0);
+                    if ((uint64_t)n * W + jb + j0 < p.cols) {  // warp-uniform
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            int64_t lo = 0, hi = 0;
+#pragma unroll
+                            for (int k = 0; k < Cfg::CLASSES; ++k) {
+                                if (k < 4) lo += (int64_t)acc[k][j] << (8 * k);
+                                else hi += (int64_t)acc[k][j] << (8 * (k - 4));
+                            }
+                            uint32_t r = red_signed(lo, p);
+                            if (Cfg::CLASSES > 4) {
+                                const uint32_t h = mulmod(red_signed(hi, p), p.w32, p);
+                                r += h;
+                                r = r >= p.q ? r - p.q : r;
+                            }
+                            const uint32_t sum = cur[j0 + j] + r;
+                            cur[j0 + j] = sum >= p.q ? sum - p.q : sum;
+                        }
+                    }
+                }
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_remote(leader_tmem_empty);
+                epi_busy += clock64() - w1;
+                acc_ph ^= 1;
+            }
+            if (row_ok) {
+#pragma unroll
+                for (int g = 0; g < WH / 4; ++g) {
+                    const uint64_t c0 = col[4 * g], c3 = col[4 * g + 3];
+                    if (p.vec_ok && c3 == c0 + 3 && (c0 & 3) == 0) {
+                        __stcs(reinterpret_cast<uint4*>(p.out + rbase + c0),
+                               make_uint4(cur[4 * g], cur[4 * g + 1], cur[4 * g + 2], cur[4 * g + 3]));
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const uint64_t cc = col[4 * g + e];
+                            if (cc != kNoCol) p.out[rbase + cc] = cur[4 * g + e];
+                        }
+                    }
+                }
+            }
+        }
+        if (p.stats && threadIdx.x == 64) {
+            p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiWaitFull] = epi_wait;
+            p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiBusy] = epi_busy;
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync_all();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+    }
+}
+
+template <int L>
+int launch_gemm2_t(const GemmParams& p, const void* tmA, const void* tmB, int num_sms,
+                   cudaStream_t s) {
+    using Cfg = Gemm2Cfg<L>;
+    const uint32_t tiles = (p.Mt / 2) * p.Nt;
+    uint32_t grid = 2 * tiles < (uint32_t)num_sms ? 2 * tiles : (uint32_t)num_sms;
+    grid &= ~1u;
+    k_gemm2<L><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p, *static_cast<const CUtensorMap*>(tmA),
+                                                      *static_cast<const CUtensorMap*>(tmB));
+    return (int)cudaGetLastError();
+}
+
+template <int L>
+int configure_gemm2_t() {
+    return (int)cudaFuncSetAttribute(k_gemm2<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Gemm2Cfg<L>::SMEM);
 }
 
 template <int L>
@@ -724,8 +1132,26 @@ int configure_kernels() {
     if (!e) e = configure_gemm_t<2>();
     if (!e) e = configure_gemm_t<3>();
     if (!e) e = configure_gemm_t<4>();
+    if (!e) e = configure_gemm2_t<1>();
+    if (!e) e = configure_gemm2_t<2>();
+    if (!e) e = configure_gemm2_t<3>();
+    if (!e) e = configure_gemm2_t<4>();
     return e;
 }
+
+int launch_gemm2(int L, const GemmParams& p, const void* tmA, const void* tmB, int num_sms,
+                 void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (L) {
+        case 1: return launch_gemm2_t<1>(p, tmA, tmB, num_sms, s);
+        case 2: return launch_gemm2_t<2>(p, tmA, tmB, num_sms, s);
+        case 3: return launch_gemm2_t<3>(p, tmA, tmB, num_sms, s);
+        case 4: return launch_gemm2_t<4>(p, tmA, tmB, num_sms, s);
+    }
+    return (int)cudaErrorInvalidValue;
+}
+
+int gemm2_b_box_rows(int L) { return (L <= 2 ? 128 : 64) * L / 2; }
 
 int launch_fill_view(uint32_t* out, const uint64_t* rowoff, const uint64_t* coloff, uint64_t rows,
                      uint64_t cols, uint32_t value, void* stream) {

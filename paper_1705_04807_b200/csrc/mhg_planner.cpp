@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <string>
 
 namespace mhg {
 
@@ -165,6 +166,12 @@ GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t c
     g.L = lp.L;
     g.W = (uint32_t)tile_width((int)lp.L);
     g.Mt = (uint32_t)((rows + kBM - 1) / kBM);
+    // single-CTA kernel by default: under the B200's 1 kW cap it sustains ~17%
+    // higher clocks than the CTA-pair kernel for the same work (measured,
+    // profiles/ab_gemm.py); MHG_GEMM=2cta selects the pair kernel.
+    const char* sel = std::getenv("MHG_GEMM");
+    g.pair = sel && std::string(sel) == "2cta";
+    if (g.pair) g.Mt += g.Mt & 1u;  // pairs take two row tiles
     g.Nt = (uint32_t)((cols + g.W - 1) / g.W);
     g.Kt = (uint32_t)((inner + kBK - 1) / kBK);
     g.KC = (uint32_t)std::max<uint64_t>(1, lp.k_max / kBK);
