@@ -2,7 +2,9 @@
 // (reference: proj/include/mh/mh.hpp), backed by libmhg.so on a B200.
 #pragma once
 
+#include "mh/bench.hpp"
 #include "mh/field.hpp"
+#include "mh/io.hpp"
 #include "mh/layout.hpp"
 #include "mh/matrix.hpp"
 #include "mh/multiply.hpp"

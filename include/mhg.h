@@ -51,6 +51,9 @@ typedef enum { MHG_OP_ADD = 0, MHG_OP_SUB = 1, MHG_OP_SET = 2 } mhg_op;
  * layout.hpp:80-85), so uploads, downloads and parity compares are memcpys. */
 typedef struct mhg_matrix_s *mhg_matrix;
 
+/* Opaque reusable multiply plan (see mhg_plan_create). */
+typedef struct mhg_plan_s *mhg_plan;
+
 /* A view: the reference's Sub 4-tuple (M, sigma, r, c), submatrix.hpp:13-18. */
 typedef struct {
     mhg_matrix mat;
@@ -113,6 +116,17 @@ mhg_status mhg_synchronize(void *stream);
 mhg_status mhg_mm(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, mhg_counters *ctr,
                   void *stream);
 
+/* Extended form.  flags & MHG_ALLOW_ALIAS lifts the reference's distinct-
+ * container rule (multiply.hpp:59-60) for the TU/TURBO Schur update, where
+ * C, A and B are views of ONE parent: the operands are read (packed) before the
+ * output is written, so the result is C_new = C_old op A_old * B_old even when
+ * the views overlap.  All other checks are unchanged. */
+#define MHG_ALLOW_ALIAS 1u
+mhg_status mhg_mm_ex(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, uint32_t flags,
+                     mhg_counters *ctr, void *stream);
+mhg_status mhg_plan_create_ex(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, uint32_t flags,
+                              mhg_plan *plan);
+
 /* Counters only (no device work): the closed form of the oblivious recursion. */
 mhg_status mhg_counters_oblivious(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_counters *ctr);
 /* Same, from the raw layout and view origins (three same-layout containers);
@@ -124,7 +138,6 @@ mhg_status mhg_counters_layout(uint64_t n, uint64_t t, uint64_t out_origin, uint
 /* Reusable plan: validation, offset tables, packing workspace and a captured
  * CUDA graph (pack lhs, pack rhs, GEMM + fused epilogue) replayed by
  * mhg_plan_run.  The views' containers must outlive the plan. */
-typedef struct mhg_plan_s *mhg_plan;
 mhg_status mhg_plan_create(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, mhg_plan *plan);
 mhg_status mhg_plan_run(mhg_plan plan, void *stream);
 mhg_status mhg_plan_counters(mhg_plan plan, mhg_counters *ctr);

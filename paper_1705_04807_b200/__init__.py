@@ -116,6 +116,8 @@ def lib():
         "mhg_rowmajor_to_mh": ([vp, vp, vp], C.c_int),
         "mhg_mh_to_rowmajor": ([vp, vp, vp], C.c_int),
         "mhg_mm": ([_View, _View, _View, C.c_int, P(Counters), vp], C.c_int),
+        "mhg_mm_ex": ([_View, _View, _View, C.c_int, u32, P(Counters), vp], C.c_int),
+        "mhg_plan_create_ex": ([_View, _View, _View, C.c_int, u32, P(vp)], C.c_int),
         "mhg_counters_oblivious": ([_View, _View, _View, P(Counters)], C.c_int),
         "mhg_counters_layout": ([u64] * 8 + [P(Counters)], C.c_int),
         "mhg_plan_create": ([_View, _View, _View, C.c_int, P(vp)], C.c_int),
@@ -333,11 +335,18 @@ class Problem:
     c: Sub
 
 
-def mm(problem: Problem, op: int = OP_ADD, stream=None) -> Counters:
-    """out op= lhs * rhs on the GPU (asynchronous on `stream`; None = default)."""
+ALLOW_ALIAS = 1
+
+
+def mm(problem: Problem, op: int = OP_ADD, stream=None, allow_alias: bool = False) -> Counters:
+    """out op= lhs * rhs on the GPU (asynchronous on `stream`; None = default).
+
+    allow_alias=True lifts the reference's distinct-container rule (the TU
+    Schur update on views of one parent); snapshot semantics: C_new = C_old op
+    A_old * B_old even when the views overlap."""
     ctr = Counters()
-    _check(lib().mhg_mm(problem.a._c(), problem.b._c(), problem.c._c(), op, C.byref(ctr),
-                        _stream_ptr(stream)))
+    _check(lib().mhg_mm_ex(problem.a._c(), problem.b._c(), problem.c._c(), op,
+                           ALLOW_ALIAS if allow_alias else 0, C.byref(ctr), _stream_ptr(stream)))
     return ctr
 
 
@@ -368,11 +377,11 @@ def counters_layout(n, t, out_origin, lhs_origin, rhs_origin, rows, inner, cols)
 class Plan:
     """Planned multiply replayed as one CUDA graph (pack lhs, pack rhs, GEMM)."""
 
-    def __init__(self, problem: Problem, op: int = OP_ADD):
+    def __init__(self, problem: Problem, op: int = OP_ADD, allow_alias: bool = False):
         self._h = C.c_void_p()
         self._problem = problem  # keep containers alive
-        _check(lib().mhg_plan_create(problem.a._c(), problem.b._c(), problem.c._c(), op,
-                                     C.byref(self._h)))
+        _check(lib().mhg_plan_create_ex(problem.a._c(), problem.b._c(), problem.c._c(), op,
+                                        ALLOW_ALIAS if allow_alias else 0, C.byref(self._h)))
 
     def run(self, stream=None):
         _check(lib().mhg_plan_run(self._h, _stream_ptr(stream)))

@@ -128,10 +128,13 @@ struct Checked {
 };
 
 // check_problem (multiply.hpp:55-66) + mm_oblivious's layout guard (:299-301)
-Checked check_problem(const mhg_view& out, const mhg_view& lhs, const mhg_view& rhs) {
+Checked check_problem(const mhg_view& out, const mhg_view& lhs, const mhg_view& rhs,
+                      bool allow_alias = false) {
     Checked c{check_view(out), check_view(lhs), check_view(rhs)};
-    if (out.mat == lhs.mat || out.mat == rhs.mat || lhs.mat == rhs.mat ||
-        overlap(out.mat, lhs.mat) || overlap(out.mat, rhs.mat) || overlap(lhs.mat, rhs.mat))
+    const bool shared = out.mat == lhs.mat || out.mat == rhs.mat || lhs.mat == rhs.mat ||
+                        overlap(out.mat, lhs.mat) || overlap(out.mat, rhs.mat) ||
+                        overlap(lhs.mat, rhs.mat);
+    if (shared && !allow_alias)
         fail(MHG_ERR_LOGIC, "problem: the three views must live in distinct matrices");
     if (out.rows != lhs.rows || out.cols != rhs.cols || lhs.cols != rhs.rows)
         fail(MHG_ERR_LOGIC, "problem: view shapes do not chain");
@@ -622,10 +625,14 @@ mhg_status mhg_counters_layout(uint64_t n, uint64_t t, uint64_t out_origin, uint
 
 mhg_status mhg_mm(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, mhg_counters* ctr,
                   void* stream) {
-    return guarded([&] {
+    return mhg_mm_ex(out, lhs, rhs, op, 0u, ctr, stream);
+}
+
+mhg_status mhg_mm_ex(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, uint32_t flags,
+                     mhg_counters* ctr, void* stream) {    return guarded([&] {
         if (op != MHG_OP_ADD && op != MHG_OP_SUB && op != MHG_OP_SET)
             fail(MHG_ERR_INVALID_ARGUMENT, "mm: unknown op");
-        const Checked c = check_problem(out, lhs, rhs);
+        const Checked c = check_problem(out, lhs, rhs, (flags & MHG_ALLOW_ALIAS) != 0);
         const mhg::Counters k = counters_of(out, lhs, rhs, c);
         put_counters(k, ctr);
         if (out.rows == 0 || out.cols == 0) return;
@@ -653,11 +660,16 @@ mhg_status mhg_mm(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, mhg_count
 
 // ------------------------------------------------------------------- plans
 mhg_status mhg_plan_create(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, mhg_plan* plan) {
+    return mhg_plan_create_ex(out, lhs, rhs, op, 0u, plan);
+}
+
+mhg_status mhg_plan_create_ex(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, uint32_t flags,
+                              mhg_plan* plan) {
     return guarded([&] {
         if (!plan) fail(MHG_ERR_INVALID_ARGUMENT, "plan_create: null out");
         if (op != MHG_OP_ADD && op != MHG_OP_SUB && op != MHG_OP_SET)
             fail(MHG_ERR_INVALID_ARGUMENT, "plan_create: unknown op");
-        const Checked c = check_problem(out, lhs, rhs);
+        const Checked c = check_problem(out, lhs, rhs, (flags & MHG_ALLOW_ALIAS) != 0);
         auto* p = new mhg_plan_s();
         p->out = out;
         p->lhs = lhs;

@@ -11,6 +11,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv \
     --log-file gpurun_out/${TAG}_launches.csv $CMD > gpurun_out/${TAG}_ncu_launches.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 2 -c 1 \
     -o gpurun_out/${TAG}_gemm_full $CMD > gpurun_out/${TAG}_ncu_gemm.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_pack -s 2 -c 2 \
+ncu --set full --clock-control none --import-source on -k regex:k_pack -s 4 -c 2 \
     -o gpurun_out/${TAG}_pack_full $CMD > gpurun_out/${TAG}_ncu_pack.log 2>&1
 echo "ncu done"

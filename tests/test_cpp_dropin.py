@@ -23,3 +23,16 @@ def test_cpp_dropin_on_gpu(gpu):
     print(r.stdout, r.stderr)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failures" in r.stdout
+
+
+@pytest.mark.gpu
+def test_cpp_protocol_golden_csv(gpu):
+    """run_trials on the GPU engine reproduces the reference's 20-trial golden
+    CSV (bench_test.cpp:528-549, time columns stripped); io round trip."""
+    exe = os.path.join(ROOT, "tests", "cpp", "protocol_test")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-s", "-C", os.path.join(ROOT, "tests", "cpp")], check=True)
+    golden = os.path.join(ROOT, "tests", "golden", "bench_trials_seed0_n64_t8_q2.csv")
+    r = subprocess.run([exe, golden], capture_output=True, text=True, timeout=300, cwd="/tmp")
+    print(r.stdout, r.stderr)
+    assert r.returncode == 0, r.stdout + r.stderr

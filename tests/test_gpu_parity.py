@@ -261,3 +261,54 @@ def test_north_star_size(gpu, mh, oracle):
     h = n // 2
     _sampled_tiles(oracle, n, t, q, out, lhs, rhs, got, v, OP_SUB,
                    [(0, 0), (0, h), (h, 0), (h, h), (0, n - 64), (n - 64, 0), (n - 64, n - 64)])
+
+
+def test_alias_mode_same_parent(gpu, mh, oracle):
+    """TU Schur update on views of ONE parent: rejected by default (the
+    reference's rule), exact with allow_alias (snapshot semantics), including
+    overlapping views."""
+    n, t, q = 256, 32, P16
+    (cells,) = _fill(oracle, 21, n, q)[:1]
+    lay, mod = mh.Layout(n, t), mh.Modulus(q)
+    M = mh.Matrix(lay, mod).upload(cells)
+    prob = mh.Problem(mh.Sub(M, mh.encode(lay, 100, 100), 156, 156),
+                      mh.Sub(M, mh.encode(lay, 100, 37), 156, 63),
+                      mh.Sub(M, mh.encode(lay, 37, 100), 63, 156))
+    with pytest.raises(mh.LogicError):
+        mh.mm(prob)
+    for views, op in [((100, 100, 100, 37, 37, 100, 156, 63, 156), OP_SUB),
+                      ((0, 0, 10, 5, 20, 30, 200, 150, 180), OP_ADD)]:  # overlapping
+        oi, oj, li, lj, ri, rj, r, k, c = views
+        M.upload(cells)
+        prob = mh.Problem(mh.Sub(M, mh.encode(lay, oi, oj), r, c), mh.Sub(M, mh.encode(lay, li, lj), r, k),
+                          mh.Sub(M, mh.encode(lay, ri, rj), k, c))
+        mh.mm(prob, op, allow_alias=True)
+        got = M.cells()
+        want = cells.copy()
+        v = Views(oracle.encode(n, t, oi, oj), oracle.encode(n, t, li, lj), oracle.encode(n, t, ri, rj),
+                  r, k, c)
+        oracle.mm_dense(n, t, q, want, cells.copy(), cells.copy(), v, op=op)
+        assert np.array_equal(got, want), views
+
+
+def test_tu_schur_sweep(gpu, mh, oracle):
+    """Right-looking elimination update sweep on one parent, misaligned panel
+    width (96 vs t=64), every step a graph-replayed aliased plan."""
+    from paper_1705_04807_b200.tu import schur_plans, schur_sweep
+    n, t, q, block = 1024, 64, P16, 96
+    (cells,) = _fill(oracle, 22, n, q)[:1]
+    lay, mod = mh.Layout(n, t), mh.Modulus(q)
+    M = mh.Matrix(lay, mod).upload(cells)
+    plans = schur_plans(M, block)
+    macs = schur_sweep(M, block, plans=plans)
+    got = M.cells()
+    want = cells.copy()
+    k0 = 0
+    while k0 + block < n:
+        k1, rest = k0 + block, n - k0 - block
+        v = Views(oracle.encode(n, t, k1, k1), oracle.encode(n, t, k1, k0), oracle.encode(n, t, k0, k1),
+                  rest, block, rest)
+        oracle.mm_dense(n, t, q, want, want.copy(), want.copy(), v, op=OP_SUB)
+        k0 = k1
+    assert np.array_equal(got, want)
+    assert macs == sum(((n - k) ** 2) * block for k in range(block, n, block))
