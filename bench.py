@@ -185,6 +185,93 @@ def run_reference(args, rank, world):
 
 
 # ---------------------------------------------------------------- GPU leg
+def e2e_pipelined(mh, torch, lay, mod, flats, set0, prob0, op, n, steps, macs):
+    """End to end through the public C ABI with pinned HOST buffers: every step
+    uploads its three inputs (mhg_matrix_upload), runs the plan, and downloads
+    the result (mhg_matrix_download).  Two container sets alternate so step i's
+    result download and step i+1's uploads overlap step i's compute: H2D,
+    compute and D2H run on three streams ordered by events."""
+    hosts = []
+    for f in flats:
+        h = torch.empty(n * n, dtype=torch.int32, pin_memory=True)
+        h.copy_(f)
+        hosts.append(h)
+    res = [torch.empty(n * n, dtype=torch.int32, pin_memory=True) for _ in range(2)]
+    fl2 = [torch.empty_like(f) for f in flats]
+    A2, B2, C2 = (mh.Matrix.wrap(lay, mod, f.data_ptr(), owner=f) for f in fl2)
+    plan2 = mh.Plan(mh.Problem(mh.Sub(A2, prob0.a.origin, prob0.a.rows, prob0.a.cols),
+                               mh.Sub(B2, prob0.b.origin, prob0.b.rows, prob0.b.cols),
+                               mh.Sub(C2, prob0.c.origin, prob0.c.rows, prob0.c.cols)), op)
+    sets = [set0, (A2, B2, C2, plan2)]
+    s_up, s_cmp, s_dn = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
+    ev_up = [torch.cuda.Event() for _ in range(2)]
+    ev_cmp = [torch.cuda.Event() for _ in range(2)]
+    ev_dn = [torch.cuda.Event() for _ in range(2)]
+    lib = mh.lib()
+
+    def one(i):
+        k = i % 2
+        A_, B_, C_, pl = sets[k]
+        if i >= 2:  # container set k is free once its previous step was computed and read back
+            s_up.wait_event(ev_cmp[k])
+            s_up.wait_event(ev_dn[k])
+        for h_, m_ in zip(hosts, (A_, B_, C_)):
+            mh._check(lib.mhg_matrix_upload(m_.handle, h_.data_ptr(), s_up.cuda_stream))
+        ev_up[k].record(s_up)
+        s_cmp.wait_event(ev_up[k])
+        pl.run(s_cmp)
+        ev_cmp[k].record(s_cmp)
+        s_dn.wait_event(ev_cmp[k])
+        mh._check(lib.mhg_matrix_download(A_.handle, res[k].data_ptr(), s_dn.cuda_stream))
+        ev_dn[k].record(s_dn)
+
+    for i in range(2):  # warm-up of both sets / graphs
+        one(i)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(s_up)
+    for i in range(steps):
+        one(i)
+    t1.record(s_dn)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1) / steps
+    return {"value": macs / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 3 * n * n * 4,
+            "d2h_bytes_per_step": n * n * 4, "steps": steps, "ms_per_step": ms,
+            "path": "pinned host -> mhg_matrix_upload x3 -> mhg_plan_run -> mhg_matrix_download "
+                    "-> pinned host; 2 container sets, H2D / compute / D2H streams overlapped"}
+
+
+def e2e_ranked(mh, torch, dist, flats, out_f, lhs_f, rhs_f, ex, plan, stream, b, e, steps, macs,
+               dev, barrier):
+    """Multi-GPU end to end: each rank uploads its own 1/P slices from pinned
+    host memory, exchanges panels, updates its C block, reads its slice back."""
+    hosts = []
+    for f in flats:
+        h = torch.empty(e - b, dtype=torch.int32, pin_memory=True)
+        h.copy_(f[b:e])
+        hosts.append(h)
+    res = torch.empty(e - b, dtype=torch.int32, pin_memory=True)
+    torch.cuda.synchronize()
+    barrier()
+    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    x0.record(stream)
+    for _ in range(steps):
+        for h_, f in zip(hosts, flats):
+            f[b:e].copy_(h_, non_blocking=True)
+        ex.exchange(lhs_f, rhs_f)
+        plan.run(stream)
+        res.copy_(out_f[b:e], non_blocking=True)
+    x1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    t = torch.tensor([x0.elapsed_time(x1) / steps], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return {"value": macs / (float(t[0]) * 1e-3), "unit": UNIT,
+            "h2d_bytes_per_step": 3 * (e - b) * 4, "d2h_bytes_per_step": (e - b) * 4,
+            "steps": steps, "ms_per_step": float(t[0]),
+            "path": "per-rank pinned slices -> panel all-gather -> mhg_plan_run -> slice read-back"}
+
+
 def run_gpu(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
@@ -273,40 +360,13 @@ def run_gpu(args, rank, world, local_rank):
     # ---- end to end through the public API with host buffers (pinned)
     e2e = None
     if not args.no_e2e:
-        hosts = [torch.empty(n * n, dtype=torch.int32, pin_memory=True) for _ in range(3)]
-        for h_, f in zip(hosts, flats):
-            h_.copy_(f)
-        res = torch.empty(n * n, dtype=torch.int32, pin_memory=True)
-        h2d = 3 * n * n * 4 if world == 1 else 3 * (e - b) * 4
-        d2h = n * n * 4 if world == 1 else (e - b) * 4
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
-        torch.cuda.synchronize()
-        barrier()
-        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        x0.record(stream)
-        for _ in range(e2e_steps):
-            if world == 1:
-                for h_, m_ in zip(hosts, (A, B, Cm)):
-                    mh.lib().mhg_matrix_upload(m_.handle, h_.data_ptr(), stream.cuda_stream)
-            else:  # each rank uploads its own slices, then the panel exchange
-                for h_, f in zip(hosts, flats):
-                    f[b:e].copy_(h_[b:e], non_blocking=True)
-                ex.exchange(lhs_f, rhs_f)
-            plan.run(stream)
-            if world == 1:
-                mh.lib().mhg_matrix_download(A.handle, res.data_ptr(), stream.cuda_stream)
-            else:
-                res[b:e].copy_(out_f[b:e], non_blocking=True)
-        x1.record(stream)
-        torch.cuda.synchronize()
-        barrier()
-        e2e_ms = torch.tensor([x0.elapsed_time(x1) / e2e_steps], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-        e2e = {"value": macs_total / (float(e2e_ms[0]) * 1e-3), "unit": UNIT,
-               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "steps": e2e_steps,
-               "ms_per_step": float(e2e_ms[0]),
-               "path": "mhg_matrix_upload x3 (pinned) -> mhg_plan_run -> mhg_matrix_download"}
+        if world == 1:
+            e2e = e2e_pipelined(mh, torch, lay, mod, flats, (A, B, Cm, plan), prob, op, n, e2e_steps,
+                                macs_total)
+        else:
+            e2e = e2e_ranked(mh, torch, dist, flats, out_f, lhs_f, rhs_f, ex, plan, stream, b, e,
+                             e2e_steps, macs_total, dev, barrier)
 
     if rank != 0:
         return
@@ -349,7 +409,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="ns16k", choices=sorted(WORKLOADS))
-    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--e2e-steps", type=int, default=8)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
