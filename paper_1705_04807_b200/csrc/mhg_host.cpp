@@ -226,6 +226,10 @@ mhg::GemmParams gemm_params(const Buffers& b, const mhg_view& out, const Checked
     p.mu = ~uint64_t(0) / q;
     const uint64_t two62 = uint64_t(1) << 62;
     p.bias = ((two62 + q - 1) / q) * q;
+    p.m32 = (uint32_t)((uint64_t(1) << 32) / q);
+    p.bias32 = (uint32_t)(((uint64_t(1) << 31) / q) * q);
+    p.w16 = (uint32_t)((uint64_t(1) << 16) % q);
+    p.w16_small = p.w16 < 256;
     p.mode = op == MHG_OP_SET ? 2 : 0;
     p.vec_ok = out.mat->t % 4 == 0;
     return p;

@@ -31,7 +31,7 @@ struct LimbParams {
     uint32_t L;          // digits per residue (1..4)
     uint32_t H;          // representative threshold
     uint32_t bound[4];   // max |digit| per position
-    uint64_t k_max;      // max inner length with every int32 class sum exact
+    uint64_t k_max;      // max inner length with every int32 class sum <= 2^31 - 2^17
 };
 
 LimbParams limb_params(uint32_t q);
@@ -57,6 +57,11 @@ struct GemmParams {
     uint32_t w32;                // 2^32 mod q
     uint64_t mu;                 // floor((2^64 - 1) / q)
     uint64_t bias;               // multiple of q >= 2^62 (signed -> unsigned shift)
+    // 32-bit fold (L <= 2, q <= 2^16): class sums obey |a_c| <= 2^31 - 2^17
+    uint32_t m32;                // floor(2^32 / q)
+    uint32_t bias32;             // q * floor(2^31 / q): a_c + bias32 in [0, 2^32)
+    uint32_t w16;                // 2^16 mod q
+    int w16_small;               // w16 < 256: fold the top class without a mulmod
     int mode;                    // 0: out += prod, 2: out = prod (first chunk)
     int vec_ok;                  // t % 4 == 0: 16-byte epilogue accesses allowed
     unsigned long long* stats;   // optional per-CTA wait-cycle counters (diagnostics), or null

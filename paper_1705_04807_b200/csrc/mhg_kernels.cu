@@ -358,6 +358,26 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
         : "r"(taddr));
 }
 
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+        "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+          "=r"(v[31])
+        : "r"(taddr));
+}
+
+template <int N>
+__device__ __forceinline__ void tmem_ld(uint32_t taddr, int32_t (&v)[N]) {
+    if constexpr (N == 32) tmem_ld32(taddr, v);
+    else tmem_ld16(taddr, v);
+}
+
 __device__ __forceinline__ void tmem_wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
@@ -381,6 +401,46 @@ __device__ __forceinline__ uint32_t mulmod(uint32_t a, uint32_t b, const GemmPar
     return (uint32_t)r;
 }
 
+// u mod q for u < 2^32, q <= 2^16: Barrett with m = floor(2^32/q) is off by at
+// most one multiple of q.
+__device__ __forceinline__ uint32_t red32(uint32_t u, const GemmParams& p) {
+    const uint32_t r = u - __umulhi(u, p.m32) * p.q;
+    return r >= p.q ? r - p.q : r;
+}
+
+// Fold the 2L-1 weight classes of one output element to a canonical residue:
+// S = sum_c acc_c 256^c (mod q).  L <= 2 (q <= 2^16) stays in 32 bits (class 0
+// and class 2L-2 are single-product sums, |a| <= 2^30; every class is within
+// 2^31 - 2^17 by the planner's K bound); wider primes fold exactly in int64.
+template <int L, int CW>
+__device__ __forceinline__ uint32_t fold_classes(const int32_t (&acc)[2 * L - 1][CW], int j,
+                                                 const GemmParams& p) {
+    if constexpr (L == 1) {
+        return red32((uint32_t)acc[0][j] + p.bias32, p);
+    } else if constexpr (L == 2) {
+        const uint32_t r1 = red32((uint32_t)acc[1][j] + p.bias32, p);
+        const uint32_t r2 = red32((uint32_t)acc[2][j] + p.bias32, p);
+        const uint32_t u = (uint32_t)acc[0][j] + p.bias32 + (r1 << 8);
+        if (p.w16_small) return red32(u + p.w16 * r2, p);
+        const uint32_t x = red32(u, p) + red32(p.w16 * r2, p);
+        return x >= p.q ? x - p.q : x;
+    } else {
+        int64_t lo = 0, hi = 0;
+#pragma unroll
+        for (int k = 0; k < 2 * L - 1; ++k) {
+            if (k < 4) lo += (int64_t)acc[k][j] << (8 * k);
+            else hi += (int64_t)acc[k][j] << (8 * (k - 4));
+        }
+        uint32_t r = red_signed(lo, p);
+        if (2 * L - 1 > 4) {
+            const uint32_t h = mulmod(red_signed(hi, p), p.w32, p);
+            r += h;
+            r = r >= p.q ? r - p.q : r;
+        }
+        return r;
+    }
+}
+
 template <int L>
 struct GemmCfg {
     static constexpr int W = (L <= 2) ? 128 : 64;       // output columns per tile
@@ -396,6 +456,7 @@ struct GemmCfg {
     static constexpr int EPI_WARPS = 8;                 // two per SMSP, each half the columns
     static constexpr int EPI_THREADS = EPI_WARPS * 32;
     static constexpr int WH = W / 2;                    // columns per epilogue warp
+    static constexpr int CW = 16;                       // TMEM columns per drain step (x16: 168-register cap of 10-warp CTAs)
     static constexpr int THREADS = 64 + EPI_THREADS;    // producer, MMA, epilogue warps
     static_assert(CLASSES * W <= 512, "TMEM columns");
     static_assert(STAGES >= 2, "pipeline depth");
@@ -605,27 +666,16 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
                 epi_wait += w1 - w0;
                 tc_fence_after();
 #pragma unroll
-                for (int j0 = 0; j0 < WH; j0 += 16) {
+                for (int j0 = 0; j0 < WH; j0 += Cfg::CW) {
                     if ((uint64_t)n * W + jb + j0 < p.cols) {  // warp-uniform
-                        int32_t acc[Cfg::CLASSES][16];
+                        int32_t acc[Cfg::CLASSES][Cfg::CW];
 #pragma unroll
                         for (int k = 0; k < Cfg::CLASSES; ++k)
-                            tmem_ld16(tmem + lane_base + k * W + jb + j0, acc[k]);
+                            tmem_ld<Cfg::CW>(tmem + lane_base + k * W + jb + j0, acc[k]);
                         tmem_wait_ld();
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            int64_t lo = 0, hi = 0;
-#pragma unroll
-                            for (int k = 0; k < Cfg::CLASSES; ++k) {
-                                if (k < 4) lo += (int64_t)acc[k][j] << (8 * k);
-                                else hi += (int64_t)acc[k][j] << (8 * (k - 4));
-                            }
-                            uint32_t r = red_signed(lo, p);
-                            if (Cfg::CLASSES > 4) {
-                                const uint32_t h = mulmod(red_signed(hi, p), p.w32, p);
-                                r += h;
-                                r = r >= p.q ? r - p.q : r;
-                            }
+                        for (int j = 0; j < Cfg::CW; ++j) {
+                            const uint32_t r = fold_classes<L, Cfg::CW>(acc, j, p);
                             const uint32_t sum = cur[j0 + j] + r;
                             cur[j0 + j] = sum >= p.q ? sum - p.q : sum;
                         }
@@ -960,25 +1010,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS
                     int32_t acc[Cfg::CLASSES][16];
 #pragma unroll
                     for (int k = 0; k < Cfg::CLASSES; ++k)
-                        tmem_ld16(tmem + lane_base + k * W + jb + j0, acc[k]);
+                        tmem_ld<16>(tmem + lane_base + k * W + jb + j0, acc[k]);
                     tmem_wait_ld();
 #pragma unroll
                     for (int k = L; k < Cfg::CLASSES; ++k) tmem_zero16(tmem + lane_base + k * W + jb + j0);
                     if ((uint64_t)n * W + jb + j0 < p.cols) {  // warp-uniform
 #pragma unroll
                         for (int j = 0; j < 16; ++j) {
-                            int64_t lo = 0, hi = 0;
-#pragma unroll
-                            for (int k = 0; k < Cfg::CLASSES; ++k) {
-                                if (k < 4) lo += (int64_t)acc[k][j] << (8 * k);
-                                else hi += (int64_t)acc[k][j] << (8 * (k - 4));
-                            }
-                            uint32_t r = red_signed(lo, p);
-                            if (Cfg::CLASSES > 4) {
-                                const uint32_t h = mulmod(red_signed(hi, p), p.w32, p);
-                                r += h;
-                                r = r >= p.q ? r - p.q : r;
-                            }
+                            const uint32_t r = fold_classes<L, 16>(acc, j, p);
                             const uint32_t sum = cur[j0 + j] + r;
                             cur[j0 + j] = sum >= p.q ? sum - p.q : sum;
                         }

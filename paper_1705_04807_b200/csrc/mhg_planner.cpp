@@ -85,7 +85,9 @@ LimbParams limb_params(uint32_t q) {
             if (c >= s && c - s < L) sum += (uint64_t)lp.bound[s] * lp.bound[c - s];
         worst = std::max(worst, sum);
     }
-    lp.k_max = ((uint64_t(1) << 31) - 1) / worst;
+    // 2^17 of headroom keeps every class sum plus a q-multiple bias inside
+    // 32 bits for the epilogue's 32-bit fold
+    lp.k_max = ((uint64_t(1) << 31) - (uint64_t(1) << 17)) / worst;
     return lp;
 }
 
