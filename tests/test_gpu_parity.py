@@ -312,3 +312,103 @@ def test_tu_schur_sweep(gpu, mh, oracle):
         k0 = k1
     assert np.array_equal(got, want)
     assert macs == sum(((n - k) ** 2) * block for k in range(block, n, block))
+
+
+@pytest.mark.parametrize("kernel", ["1cta", "2cta"])
+def test_both_gemm_kernels(gpu, mh, oracle, monkeypatch, kernel):
+    """The single-CTA (default) and CTA-pair (cta_group::2, MHG_GEMM=2cta)
+    kernels on ragged views, every limb count, all ops, forced K-chunking."""
+    monkeypatch.setenv("MHG_GEMM", kernel)
+    rng = np.random.default_rng(5)
+    for q in (97, P16, P24, P31):
+        for op in (OP_ADD, OP_SUB, OP_SET):
+            n = 512
+            t = int(rng.choice([16, 32, 64]))
+            r, k, c, corners = _random_views(rng, n)
+            v = _views_from(oracle, n, t, r, k, c, corners)
+            out, lhs, rhs = _fill(oracle, 40 + op, n, q)
+            if op == OP_SUB:
+                monkeypatch.setenv("MHG_FORCE_KCHUNK", "1")
+            got, _ = _run_gpu(mh, n, t, q, out, lhs, rhs, v, op)
+            monkeypatch.delenv("MHG_FORCE_KCHUNK", raising=False)
+            want = out.copy()
+            oracle.mm_dense(n, t, q, want, lhs, rhs, v, op=op)
+            assert np.array_equal(got, want), (kernel, q, op, t, v)
+
+
+def test_edge_shapes(gpu, mh, oracle):
+    """Degenerate and boundary shapes: 1x1 containers, t = 1, t = n, views
+    that touch every container edge, single rows / columns / inner length 1,
+    non-power-of-two tiles."""
+    cases = [
+        (1, 1, 97, (0, 0, 0, 0, 0, 0), 1, 1, 1),
+        (2, 1, 97, (0, 0, 0, 0, 0, 0), 2, 2, 2),
+        (64, 64, 65521, (0, 0, 0, 0, 0, 0), 64, 64, 64),       # one tile
+        (128, 1, 65521, (3, 5, 7, 9, 11, 13), 100, 90, 80),    # t = 1 (pure Z order)
+        (96, 3, 257, (0, 1, 2, 3, 3, 5), 91, 93, 90),          # non-pow2 tile side
+        (256, 64, P31, (255, 0, 0, 255, 0, 0), 1, 1, 256),     # single row, inner 1
+        (256, 64, P31, (0, 255, 0, 0, 0, 255), 256, 256, 1),   # single column
+        (256, 32, P16, (1, 1, 1, 1, 1, 1), 255, 255, 255),     # touches the far edges
+    ]
+    for (n, t, q, corners, r, k, c) in cases:
+        v = _views_from(oracle, n, t, r, k, c, corners)
+        out, lhs, rhs = _fill(oracle, n + t, n, q)
+        for op in (OP_ADD, OP_SUB, OP_SET):
+            got, _ = _run_gpu(mh, n, t, q, out, lhs, rhs, v, op)
+            want = out.copy()
+            oracle.mm_dense(n, t, q, want, lhs, rhs, v, op=op)
+            assert np.array_equal(got, want), (n, t, q, corners, r, k, c, op)
+
+
+def test_plan_graph_replay_matches_direct(gpu, mh, oracle):
+    """A plan replayed as a CUDA graph (several runs) equals repeated direct
+    calls, and its Counters equal the direct call's."""
+    n, t, q = 512, 32, P16
+    out, lhs, rhs = _fill(oracle, 77, n, q)
+    v = _views_from(oracle, n, t, 300, 200, 250, (10, 20, 30, 40, 50, 60))
+    A, B, Cm = _containers(mh, n, t, q, (out, lhs, rhs))
+    prob = mh.Problem(mh.Sub(A, v.out_origin, v.rows, v.cols), mh.Sub(B, v.lhs_origin, v.rows, v.inner),
+                      mh.Sub(Cm, v.rhs_origin, v.inner, v.cols))
+    plan = mh.Plan(prob, mh.OP_SUB)
+    for _ in range(3):
+        plan.run()
+    got = A.cells()
+    want = out.copy()
+    for _ in range(3):
+        oracle.mm_dense(n, t, q, want, lhs, rhs, v, op=OP_SUB)
+    assert np.array_equal(got, want)
+    assert plan.counters().as_tuple() == mh.counters_oblivious(prob).as_tuple()
+    assert plan.info()["launches"] == 3
+
+
+@pytest.mark.parametrize("kernel", ["1cta", "2cta"])
+def test_guard_bands(gpu, mh, oracle, monkeypatch, kernel):
+    """Out-of-bounds detector (compute-sanitizer is unavailable on this pool):
+    each container is wrapped in the middle of a larger device buffer whose
+    guard zones hold a sentinel; after multiplies with ragged views, every
+    guard word is intact and the result equals the oracle."""
+    import torch
+    monkeypatch.setenv("MHG_GEMM", kernel)
+    n, t, guard = 256, 32, 1 << 16
+    sentinel = 0x5A5A5A5A
+    for q in (97, P16, P31):
+        lay, mod = mh.Layout(n, t), mh.Modulus(q)
+        cells = _fill(oracle, q % 1000, n, q)
+        bufs, mats = [], []
+        for c in cells:
+            b = torch.full((n * n + 2 * guard,), sentinel, dtype=torch.int64, device="cuda").to(torch.int32)
+            b[guard:guard + n * n] = torch.from_numpy(c.view(np.int32)).cuda()
+            bufs.append(b)
+            mats.append(mh.Matrix.wrap(lay, mod, b[guard:].data_ptr(), owner=b))
+        v = _views_from(oracle, n, t, 250, 131, 7, (5, 249, 1, 3, 120, 240))
+        for op in (OP_SUB, OP_SET, OP_ADD):
+            mh.mm(mh.Problem(mh.Sub(mats[0], v.out_origin, v.rows, v.cols),
+                             mh.Sub(mats[1], v.lhs_origin, v.rows, v.inner),
+                             mh.Sub(mats[2], v.rhs_origin, v.inner, v.cols)), op)
+            oracle.mm_dense(n, t, q, cells[0], cells[1], cells[2], v, op=op)
+        torch.cuda.synchronize()
+        for b in bufs:
+            h = b.cpu().numpy().view(np.uint32)
+            assert (h[:guard] == sentinel).all() and (h[guard + n * n:] == sentinel).all()
+        assert np.array_equal(bufs[0][guard:guard + n * n].cpu().numpy().view(np.uint32), cells[0])
+        assert np.array_equal(bufs[1][guard:guard + n * n].cpu().numpy().view(np.uint32), cells[1])
