@@ -64,6 +64,7 @@ struct GemmParams {
     int w16_small;               // w16 < 256: fold the top class without a mulmod
     int mode;                    // 0: out += prod, 2: out = prod (first chunk)
     int vec_ok;                  // t % 4 == 0: 16-byte epilogue accesses allowed
+    uint32_t group;              // raster: row tiles per group sharing rhs panels in L2
     unsigned long long* stats;   // optional per-CTA wait-cycle counters (diagnostics), or null
 };
 

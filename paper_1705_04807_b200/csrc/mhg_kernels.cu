@@ -462,9 +462,10 @@ struct GemmCfg {
     static_assert(STAGES >= 2, "pipeline depth");
 };
 
-__device__ __forceinline__ void tile_coords(uint32_t tile, uint32_t Mt, uint32_t Nt, uint32_t& m,
-                                            uint32_t& n) {
-    constexpr uint32_t G = 16;  // grouped raster: 16 row tiles share B panels in L2
+__device__ __forceinline__ void tile_coords(uint32_t tile, uint32_t Mt, uint32_t Nt, uint32_t G,
+                                            uint32_t& m, uint32_t& n) {
+    // grouped raster: G row tiles iterate over the column tiles together, so the
+    // tiles in flight share lhs and rhs panels in L2
     const uint32_t group = G * Nt;
     const uint32_t gid = tile / group;
     const uint32_t first_m = gid * G;
@@ -523,7 +524,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
             long long wait_empty = 0;
             for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
                 uint32_t m, n;
-                tile_coords(tile, p.Mt, p.Nt, m, n);
+                tile_coords(tile, p.Mt, p.Nt, p.group, m, n);
                 const int8_t* a_src = p.apack + (uint64_t)m * p.Kt * Cfg::A_STAGE;
                 const int8_t* b_src = p.bpack + (uint64_t)n * p.Kt * Cfg::B_STAGE;
                 for (uint32_t kt = 0; kt < p.Kt; ++kt) {
@@ -625,7 +626,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
         long long epi_wait = 0, epi_busy = 0;
         for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
             uint32_t m, n;
-            tile_coords(tile, p.Mt, p.Nt, m, n);
+            tile_coords(tile, p.Mt, p.Nt, p.group, m, n);
             const uint64_t gi = (uint64_t)m * kBM + row;
             const bool row_ok = gi < p.rows;
             const uint64_t rbase = row_ok ? __ldg(p.out_rowoff + gi) : 0;
@@ -881,7 +882,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS
             uint32_t ph = 0;
             for (uint32_t tile = pair; tile < num_tiles; tile += npairs) {
                 uint32_t pm, n;
-                tile_coords(tile, Mt2, p.Nt, pm, n);
+                tile_coords(tile, Mt2, p.Nt, p.group, pm, n);
                 const uint32_t m = 2 * pm + rank;
                 for (uint32_t kt = 0; kt < p.Kt; ++kt) {
                     const long long w0 = clock64();
@@ -964,7 +965,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS
         long long epi_wait = 0, epi_busy = 0;
         for (uint32_t tile = pair; tile < num_tiles; tile += npairs) {
             uint32_t pm, n;
-            tile_coords(tile, Mt2, p.Nt, pm, n);
+            tile_coords(tile, Mt2, p.Nt, p.group, pm, n);
             const uint32_t m = 2 * pm + rank;
             const uint64_t gi = (uint64_t)m * kBM + row;
             const bool row_ok = gi < p.rows;

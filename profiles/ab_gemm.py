@@ -58,8 +58,24 @@ def sample(stop, clocks, watts):
 
 
 res = {name: [] for name, _ in variants}
+class env_set:
+    def __init__(self, spec):
+        self.k, self.v = spec.split("=", 1)
+
+    def __enter__(self):
+        self.old = os.environ.get(self.k)
+        os.environ[self.k] = self.v
+
+    def __exit__(self, *a):
+        if self.old is None:
+            del os.environ[self.k]
+        else:
+            os.environ[self.k] = self.old
+
+
 for r in range(rounds):
-    for name, _ in variants:
+    for name, spec in variants:
+      with env_set(spec):
         pl = plans[name]
         pl.time_gemm(2)
         ms_one = pl.time_gemm(2)
