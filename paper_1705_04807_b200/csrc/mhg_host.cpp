@@ -231,6 +231,8 @@ mhg::GemmParams gemm_params(const Buffers& b, const mhg_view& out, const Checked
     p.w16 = (uint32_t)((uint64_t(1) << 16) % q);
     p.w16_small = p.w16 < 256;
     p.group = 8;  // measured best at the power cap (profiles/r01_raster_groups.txt)
+    p.serpentine = 1;
+    if (const char* sp = std::getenv("MHG_SERPENTINE")) p.serpentine = std::atoi(sp) != 0;
     if (const char* gs = std::getenv("MHG_GROUP")) {  // tuning hook (raster group size)
         const long v = std::strtol(gs, nullptr, 10);
         if (v > 0) p.group = (uint32_t)v;

@@ -65,6 +65,7 @@ struct GemmParams {
     int mode;                    // 0: out += prod, 2: out = prod (first chunk)
     int vec_ok;                  // t % 4 == 0: 16-byte epilogue accesses allowed
     uint32_t group;              // raster: row tiles per group sharing rhs panels in L2
+    int serpentine;              // alternate the K direction per tile (L2 reuse across waves)
     unsigned long long* stats;   // optional per-CTA wait-cycle counters (diagnostics), or null
 };
 

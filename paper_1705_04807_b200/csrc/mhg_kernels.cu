@@ -522,12 +522,17 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
             int st = 0;
             uint32_t ph = 0;
             long long wait_empty = 0;
-            for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            uint32_t ord = 0;
+            for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++ord) {
                 uint32_t m, n;
                 tile_coords(tile, p.Mt, p.Nt, p.group, m, n);
                 const int8_t* a_src = p.apack + (uint64_t)m * p.Kt * Cfg::A_STAGE;
                 const int8_t* b_src = p.bpack + (uint64_t)n * p.Kt * Cfg::B_STAGE;
-                for (uint32_t kt = 0; kt < p.Kt; ++kt) {
+                // serpentine K: odd tiles of a CTA sweep K backwards, so the next wave
+                // starts on the panel slices the previous wave just left in L2
+                const bool rev = p.serpentine && (ord & 1);
+                for (uint32_t j = 0; j < p.Kt; ++j) {
+                    const uint32_t kt = rev ? p.Kt - 1 - j : j;
                     const long long w0 = clock64();
                     mbar_wait(&empty[st], ph ^ 1);
                     wait_empty += clock64() - w0;
@@ -880,11 +885,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS
             long long wait_empty = 0;
             int st = 0;
             uint32_t ph = 0;
-            for (uint32_t tile = pair; tile < num_tiles; tile += npairs) {
+            uint32_t ord = 0;
+            for (uint32_t tile = pair; tile < num_tiles; tile += npairs, ++ord) {
                 uint32_t pm, n;
                 tile_coords(tile, Mt2, p.Nt, p.group, pm, n);
                 const uint32_t m = 2 * pm + rank;
-                for (uint32_t kt = 0; kt < p.Kt; ++kt) {
+                const bool rev = p.serpentine && (ord & 1);
+                for (uint32_t j = 0; j < p.Kt; ++j) {
+                    const uint32_t kt = rev ? p.Kt - 1 - j : j;
                     const long long w0 = clock64();
                     mbar_wait(&empty[st], ph ^ 1);
                     wait_empty += clock64() - w0;
