@@ -372,10 +372,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, int32_t (&v)[32]) {
         : "r"(taddr));
 }
 
+__device__ __forceinline__ void tmem_ld8(uint32_t taddr, int32_t (&v)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                   "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+}
+
 template <int N>
 __device__ __forceinline__ void tmem_ld(uint32_t taddr, int32_t (&v)[N]) {
     if constexpr (N == 32) tmem_ld32(taddr, v);
-    else tmem_ld16(taddr, v);
+    else if constexpr (N == 16) tmem_ld16(taddr, v);
+    else tmem_ld8(taddr, v);
 }
 
 __device__ __forceinline__ void tmem_wait_ld() {
@@ -456,7 +464,6 @@ struct GemmCfg {
     static constexpr int EPI_WARPS = 8;                 // two per SMSP, each half the columns
     static constexpr int EPI_THREADS = EPI_WARPS * 32;
     static constexpr int WH = W / 2;                    // columns per epilogue warp
-    static constexpr int CW = 16;                       // TMEM columns per drain step (x16: 168-register cap of 10-warp CTAs)
     static constexpr int THREADS = 64 + EPI_THREADS;    // producer, MMA, epilogue warps
     static_assert(CLASSES * W <= 512, "TMEM columns");
     static_assert(STAGES >= 2, "pipeline depth");
@@ -473,6 +480,209 @@ __device__ __forceinline__ void tile_coords(uint32_t tile, uint32_t Mt, uint32_t
     const uint32_t local = tile - gid * group;
     m = first_m + local % gm;
     n = local / gm;
+}
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+
+__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+    return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+}
+
+__device__ __forceinline__ void tma2d_pair(uint32_t dst, const void* tmap, int c0, int c1,
+                                           uint32_t leader_bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(leader_bar)
+        : "memory");
+}
+
+__device__ __forceinline__ void mma_i8_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+    asm volatile(
+        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"((uint16_t)0x3)
+        : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+                 : "memory");
+}
+
+__device__ __forceinline__ void tmem_zero16(uint32_t taddr) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
+        "{%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(taddr),
+        "r"(0)
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_zero8(uint32_t taddr) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(
+                     taddr),
+                 "r"(0)
+                 : "memory");
+}
+
+template <int N>
+__device__ __forceinline__ void tmem_zero(uint32_t taddr) {
+    if constexpr (N == 16) tmem_zero16(taddr);
+    else tmem_zero8(taddr);
+}
+
+__device__ __forceinline__ void tmem_wait_st() {
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// Epilogue role of both GEMM kernels (warps 2 .. 2+EPI_WARPS-1).  Per tile:
+// (1) stage the tile's column offsets in smem and prefetch the thread's output
+// row segment (C_old) into registers -- overlapping the tile's MMA main loop;
+// (2) per exact K-chunk, drain the 2L-1 weight classes from TMEM
+// (tcgen05.ld 32x32b.x16), fold them mod q into the register copy, release
+// TMEM; (3) store the row segment after the release, overlapping the next
+// tile's MMAs.  One TMEM lane (= output row) per thread; warp w may only
+// access lane quadrant w % 4, and the two warps of a quadrant split the
+// columns.  PAIR (k_gemm2): the tile's row block is 2*pm + rank, the upper
+// classes [L, 2L-1) are re-zeroed as they are drained (every MMA but the first
+// of a chunk accumulates), and TMEM is released on the LEADER's barrier.
+template <int L, int W, int EPI_WARPS, bool PAIR>
+__device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t first_tile,
+                                              uint32_t tile_stride, uint32_t num_tiles,
+                                              uint32_t row_groups, uint32_t rank, uint32_t nchunks,
+                                              uint32_t tmem, uint64_t* s_col, uint64_t* tmem_full,
+                                              uint64_t* tmem_empty, int warp, int lane) {
+    constexpr int EPI_THREADS = EPI_WARPS * 32;
+    constexpr int WH = W / 2;
+    constexpr int CLASSES = 2 * L - 1;
+    constexpr int CW = L <= 2 ? 16 : 8;  // TMEM columns per drain step (register budget)
+    constexpr uint64_t kNoCol = ~uint64_t(0);
+    const int ew = warp - 2;
+    const int quad = warp & 3;
+    const int jb = (ew >> 2) * WH;  // first tile column of this warp
+    const int row = quad * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    const uint32_t release_bar =
+        PAIR ? mapa_shared(smem_u32(tmem_empty), 0) : smem_u32(tmem_empty);
+    uint32_t acc_ph = 0;
+    long long epi_wait = 0, epi_busy = 0;
+    for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride) {
+        uint32_t tm, n;
+        tile_coords(tile, row_groups, p.Nt, p.group, tm, n);
+        const uint32_t m = PAIR ? 2 * tm + rank : tm;
+        const uint64_t gi = (uint64_t)m * kBM + row;
+        const bool row_ok = gi < p.rows;
+        const uint64_t rbase = row_ok ? __ldg(p.out_rowoff + gi) : 0;
+        epi_bar_sync<EPI_THREADS>();  // previous tile's readers of s_col are done
+        for (int j = ew * 32 + lane; j < W; j += EPI_THREADS) {
+            const uint64_t gj = (uint64_t)n * W + j;
+            s_col[j] = gj < p.cols ? __ldg(p.out_coloff + gj) : kNoCol;
+        }
+        epi_bar_sync<EPI_THREADS>();
+        const uint64_t* col = s_col + jb;
+        uint32_t cur[WH];
+        if (p.mode != 2 && row_ok) {
+#pragma unroll
+            for (int g = 0; g < WH / 4; ++g) {
+                const uint64_t c0 = col[4 * g], c3 = col[4 * g + 3];
+                if (p.vec_ok && c3 == c0 + 3 && (c0 & 3) == 0) {
+                    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(p.out + rbase + c0));
+                    cur[4 * g] = v.x;
+                    cur[4 * g + 1] = v.y;
+                    cur[4 * g + 2] = v.z;
+                    cur[4 * g + 3] = v.w;
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const uint64_t cc = col[4 * g + e];
+                        cur[4 * g + e] = cc != kNoCol ? p.out[rbase + cc] : 0u;
+                    }
+                }
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < WH; ++j) cur[j] = 0u;
+        }
+        for (uint32_t c = 0; c < nchunks; ++c) {
+            const long long w0 = clock64();
+            mbar_wait(tmem_full, acc_ph);
+            const long long w1 = clock64();
+            epi_wait += w1 - w0;
+            tc_fence_after();
+#pragma unroll
+            for (int j0 = 0; j0 < WH; j0 += CW) {
+                const bool live = (uint64_t)n * W + jb + j0 < p.cols;  // warp-uniform
+                if (!PAIR && !live) continue;
+                int32_t acc[CLASSES][CW];
+#pragma unroll
+                for (int k = 0; k < CLASSES; ++k)
+                    tmem_ld<CW>(tmem + lane_base + k * W + jb + j0, acc[k]);
+                tmem_wait_ld();
+                if constexpr (PAIR) {
+#pragma unroll
+                    for (int k = L; k < CLASSES; ++k) tmem_zero<CW>(tmem + lane_base + k * W + jb + j0);
+                }
+                if (live) {
+#pragma unroll
+                    for (int j = 0; j < CW; ++j) {
+                        const uint32_t r = fold_classes<L, CW>(acc, j, p);
+                        const uint32_t sum = cur[j0 + j] + r;
+                        cur[j0 + j] = sum >= p.q ? sum - p.q : sum;
+                    }
+                }
+            }
+            if constexpr (PAIR) tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if constexpr (PAIR) mbar_arrive_remote(release_bar);
+                else mbar_arrive(tmem_empty);
+            }
+            epi_busy += clock64() - w1;
+            acc_ph ^= 1;
+        }
+        if (row_ok) {
+#pragma unroll
+            for (int g = 0; g < WH / 4; ++g) {
+                const uint64_t c0 = col[4 * g], c3 = col[4 * g + 3];
+                if (p.vec_ok && c3 == c0 + 3 && (c0 & 3) == 0) {
+                    __stcs(reinterpret_cast<uint4*>(p.out + rbase + c0),
+                           make_uint4(cur[4 * g], cur[4 * g + 1], cur[4 * g + 2], cur[4 * g + 3]));
+                } else {
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const uint64_t cc = col[4 * g + e];
+                        if (cc != kNoCol) p.out[rbase + cc] = cur[4 * g + e];
+                    }
+                }
+            }
+        }
+    }
+    if (p.stats && warp == 2 && lane == 0) {
+        p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiWaitFull] = epi_wait;
+        p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiBusy] = epi_busy;
+    }
 }
 
 template <int L>
@@ -507,7 +717,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
             mbar_init(&empty[s], 1);
         }
         mbar_init(tmem_full, 1);
-        mbar_init(tmem_empty, Cfg::EPI_THREADS);
+        mbar_init(tmem_empty, Cfg::EPI_WARPS);  // one arrive per epilogue warp
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
@@ -613,106 +823,9 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
             }
         }
     } else {
-        // ---------------- epilogue: TMEM -> registers -> fold mod q -> Morton stores
-        // Per tile: (1) stage the tile's column offsets in smem and prefetch the
-        // thread's output row segment (C_old) into registers -- this overlaps the
-        // tile's MMA main loop; (2) per exact K-chunk, drain the 2L-1 weight
-        // classes from TMEM, fold them mod q into the register copy, release
-        // TMEM; (3) store the row segment after TMEM is released, so the stores
-        // overlap the next tile's MMAs.
-        constexpr int WH = Cfg::WH;
-        const int ew = warp - 2;              // epilogue warp 0..7
-        const int quad = warp & 3;            // TMEM lane quadrant this warp may access
-        const int jb = (ew >> 2) * WH;        // first tile column of this warp
-        const int row = quad * 32 + lane;
-        const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-        constexpr uint64_t kNoCol = ~uint64_t(0);
-        uint32_t acc_ph = 0;
-        long long epi_wait = 0, epi_busy = 0;
-        for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
-            uint32_t m, n;
-            tile_coords(tile, p.Mt, p.Nt, p.group, m, n);
-            const uint64_t gi = (uint64_t)m * kBM + row;
-            const bool row_ok = gi < p.rows;
-            const uint64_t rbase = row_ok ? __ldg(p.out_rowoff + gi) : 0;
-            epi_bar_sync<Cfg::EPI_THREADS>();  // previous tile's readers of s_col are done
-            for (int j = ew * 32 + lane; j < W; j += Cfg::EPI_THREADS) {
-                const uint64_t gj = (uint64_t)n * W + j;
-                s_col[j] = gj < p.cols ? __ldg(p.out_coloff + gj) : kNoCol;
-            }
-            epi_bar_sync<Cfg::EPI_THREADS>();
-            const uint64_t* col = s_col + jb;
-            uint32_t cur[WH];
-            if (p.mode != 2 && row_ok) {
-#pragma unroll
-                for (int g = 0; g < WH / 4; ++g) {
-                    const uint64_t c0 = col[4 * g], c3 = col[4 * g + 3];
-                    if (p.vec_ok && c3 == c0 + 3 && (c0 & 3) == 0) {
-                        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(p.out + rbase + c0));
-                        cur[4 * g] = v.x;
-                        cur[4 * g + 1] = v.y;
-                        cur[4 * g + 2] = v.z;
-                        cur[4 * g + 3] = v.w;
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const uint64_t c = col[4 * g + e];
-                            cur[4 * g + e] = c != kNoCol ? p.out[rbase + c] : 0u;
-                        }
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < WH; ++j) cur[j] = 0u;
-            }
-            for (uint32_t c = 0; c < nchunks; ++c) {
-                long long w0 = clock64();
-                mbar_wait(tmem_full, acc_ph);
-                const long long w1 = clock64();
-                epi_wait += w1 - w0;
-                tc_fence_after();
-#pragma unroll
-                for (int j0 = 0; j0 < WH; j0 += Cfg::CW) {
-                    if ((uint64_t)n * W + jb + j0 < p.cols) {  // warp-uniform
-                        int32_t acc[Cfg::CLASSES][Cfg::CW];
-#pragma unroll
-                        for (int k = 0; k < Cfg::CLASSES; ++k)
-                            tmem_ld<Cfg::CW>(tmem + lane_base + k * W + jb + j0, acc[k]);
-                        tmem_wait_ld();
-#pragma unroll
-                        for (int j = 0; j < Cfg::CW; ++j) {
-                            const uint32_t r = fold_classes<L, Cfg::CW>(acc, j, p);
-                            const uint32_t sum = cur[j0 + j] + r;
-                            cur[j0 + j] = sum >= p.q ? sum - p.q : sum;
-                        }
-                    }
-                }
-                tc_fence_before();
-                mbar_arrive(tmem_empty);
-                epi_busy += clock64() - w1;
-                acc_ph ^= 1;
-            }
-            if (row_ok) {
-#pragma unroll
-                for (int g = 0; g < WH / 4; ++g) {
-                    const uint64_t c0 = col[4 * g], c3 = col[4 * g + 3];
-                    if (p.vec_ok && c3 == c0 + 3 && (c0 & 3) == 0) {
-                        __stcs(reinterpret_cast<uint4*>(p.out + rbase + c0),
-                               make_uint4(cur[4 * g], cur[4 * g + 1], cur[4 * g + 2], cur[4 * g + 3]));
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const uint64_t c = col[4 * g + e];
-                            if (c != kNoCol) p.out[rbase + c] = cur[4 * g + e];
-                        }
-                    }
-                }
-            }
-        }
-        if (p.stats && threadIdx.x == 64) {
-            p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiWaitFull] = epi_wait;
-            p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiBusy] = epi_busy;
-        }
+        epilogue_role<L, W, Cfg::EPI_WARPS, false>(p, blockIdx.x, gridDim.x, num_tiles, p.Mt, 0,
+                                                   nchunks, tmem, s_col, tmem_full, tmem_empty,
+                                                   warp, lane);
     }
 
     __syncthreads();
@@ -758,67 +871,6 @@ struct Gemm2Cfg {
     static_assert(STAGES >= 2, "pipeline depth");
     static_assert(NBH % 16 == 0 || NBH == 64, "B' half rows");
 };
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-    uint32_t r;
-    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-    return r;
-}
-
-__device__ __forceinline__ uint32_t mapa_shared(uint32_t addr, uint32_t rank) {
-    uint32_t r;
-    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
-    return r;
-}
-
-__device__ __forceinline__ void cluster_sync_all() {
-    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
-                     : "memory");
-}
-
-__device__ __forceinline__ void tma2d_pair(uint32_t dst, const void* tmap, int c0, int c1,
-                                           uint32_t leader_bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
-        "l"(reinterpret_cast<uint64_t>(tmap)), "r"(c0), "r"(c1), "r"(leader_bar)
-        : "memory");
-}
-
-__device__ __forceinline__ void mma_i8_pair(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
-                                            uint32_t idesc, uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-
-__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
-    asm volatile(
-        "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-        " [%0], %1;" ::"r"(smem_u32(bar)),
-        "h"((uint16_t)0x3)
-        : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
-    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
-                 : "memory");
-}
-
-__device__ __forceinline__ void tmem_zero16(uint32_t taddr) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-        "{%1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1, %1};" ::"r"(taddr),
-        "r"(0)
-        : "memory");
-}
-
-__device__ __forceinline__ void tmem_wait_st() {
-    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-}
 
 template <int L>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS, 1)
@@ -962,104 +1014,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS
             }
         }
     } else {
-        const int ew = warp - 2;
-        const int quad = warp & 3;
-        const int jb = (ew >> 2) * WH;
-        const int row = quad * 32 + lane;
-        const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-        const uint32_t leader_tmem_empty = mapa_shared(smem_u32(tmem_empty), 0);
-        constexpr uint64_t kNoCol = ~uint64_t(0);
-        uint32_t acc_ph = 0;
-        long long epi_wait = 0, epi_busy = 0;
-        for (uint32_t tile = pair; tile < num_tiles; tile += npairs) {
-            uint32_t pm, n;
-            tile_coords(tile, Mt2, p.Nt, p.group, pm, n);
-            const uint32_t m = 2 * pm + rank;
-            const uint64_t gi = (uint64_t)m * kBM + row;
-            const bool row_ok = gi < p.rows;
-            const uint64_t rbase = row_ok ? __ldg(p.out_rowoff + gi) : 0;
-            epi_bar_sync<Cfg::EPI_THREADS>();
-            for (int j = ew * 32 + lane; j < W; j += Cfg::EPI_THREADS) {
-                const uint64_t gj = (uint64_t)n * W + j;
-                s_col[j] = gj < p.cols ? __ldg(p.out_coloff + gj) : kNoCol;
-            }
-            epi_bar_sync<Cfg::EPI_THREADS>();
-            const uint64_t* col = s_col + jb;
-            uint32_t cur[WH];
-            if (p.mode != 2 && row_ok) {
-#pragma unroll
-                for (int g = 0; g < WH / 4; ++g) {
-                    const uint64_t c0 = col[4 * g], c3 = col[4 * g + 3];
-                    if (p.vec_ok && c3 == c0 + 3 && (c0 & 3) == 0) {
-                        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(p.out + rbase + c0));
-                        cur[4 * g] = v.x;
-                        cur[4 * g + 1] = v.y;
-                        cur[4 * g + 2] = v.z;
-                        cur[4 * g + 3] = v.w;
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const uint64_t cc = col[4 * g + e];
-                            cur[4 * g + e] = cc != kNoCol ? p.out[rbase + cc] : 0u;
-                        }
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < WH; ++j) cur[j] = 0u;
-            }
-            for (uint32_t c = 0; c < nchunks; ++c) {
-                const long long w0 = clock64();
-                mbar_wait(tmem_full, acc_ph);
-                const long long w1 = clock64();
-                epi_wait += w1 - w0;
-                tc_fence_after();
-#pragma unroll
-                for (int j0 = 0; j0 < WH; j0 += 16) {
-                    int32_t acc[Cfg::CLASSES][16];
-#pragma unroll
-                    for (int k = 0; k < Cfg::CLASSES; ++k)
-                        tmem_ld<16>(tmem + lane_base + k * W + jb + j0, acc[k]);
-                    tmem_wait_ld();
-#pragma unroll
-                    for (int k = L; k < Cfg::CLASSES; ++k) tmem_zero16(tmem + lane_base + k * W + jb + j0);
-                    if ((uint64_t)n * W + jb + j0 < p.cols) {  // warp-uniform
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const uint32_t r = fold_classes<L, 16>(acc, j, p);
-                            const uint32_t sum = cur[j0 + j] + r;
-                            cur[j0 + j] = sum >= p.q ? sum - p.q : sum;
-                        }
-                    }
-                }
-                tmem_wait_st();
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive_remote(leader_tmem_empty);
-                epi_busy += clock64() - w1;
-                acc_ph ^= 1;
-            }
-            if (row_ok) {
-#pragma unroll
-                for (int g = 0; g < WH / 4; ++g) {
-                    const uint64_t c0 = col[4 * g], c3 = col[4 * g + 3];
-                    if (p.vec_ok && c3 == c0 + 3 && (c0 & 3) == 0) {
-                        __stcs(reinterpret_cast<uint4*>(p.out + rbase + c0),
-                               make_uint4(cur[4 * g], cur[4 * g + 1], cur[4 * g + 2], cur[4 * g + 3]));
-                    } else {
-#pragma unroll
-                        for (int e = 0; e < 4; ++e) {
-                            const uint64_t cc = col[4 * g + e];
-                            if (cc != kNoCol) p.out[rbase + cc] = cur[4 * g + e];
-                        }
-                    }
-                }
-            }
-        }
-        if (p.stats && threadIdx.x == 64) {
-            p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiWaitFull] = epi_wait;
-            p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiBusy] = epi_busy;
-        }
+        epilogue_role<L, W, Cfg::EPI_WARPS, true>(p, pair, npairs, num_tiles, Mt2, rank, nchunks, tmem,
+                                                  s_col, tmem_full, tmem_empty, warp, lane);
     }
 
     tc_fence_before();
