@@ -76,6 +76,44 @@ def groups(P: int, n: int, t: int) -> Tuple[Dict[int, List[int]], Dict[int, List
     return rows, cols
 
 
+@dataclass(frozen=True)
+class Segment:
+    """One K segment of rank r's update: C[R_r, C_r] op= A[R_r, k0:k1] B[k0:k1, C_r].
+
+    The A part is a contiguous flat range of the row-group member `a_owner`'s
+    Morton slice and the B part is the whole slice of column-group member
+    `b_owner` (dyadic bands: the row bands refine the column bands, so K is cut
+    at row-band boundaries)."""
+
+    index: int
+    k0: int
+    k1: int
+    a_owner: int
+    a_range: Tuple[int, int]
+    b_owner: int
+    b_range: Tuple[int, int]
+
+
+def segments(rank: int, P: int, n: int, t: int) -> List[Segment]:
+    b = _bits(P)
+    blk = morton_block(rank, P, n, t)
+    row_bits, col_bits = (b + 1) // 2, b // 2
+    h, w = n >> row_bits, n >> col_bits  # row-band height, column-band width (w in {h, 2h})
+    owners = {(morton_block(r, P, n, t).row_band, morton_block(r, P, n, t).col_band): r
+              for r in range(P)}
+    segs = []
+    for i in range(1 << row_bits):
+        k0, k1 = i * h, (i + 1) * h
+        a_owner = owners[(blk.row_band, k0 // w)]
+        lo, hi = slice_range(a_owner, P, n)
+        half = (hi - lo) // (w // h)  # the slice is (w // h) h x h quadrants, Z order
+        part = (k0 % w) // h
+        b_owner = owners[(i, blk.col_band)]
+        segs.append(Segment(i, k0, k1, a_owner, (lo + part * half, lo + (part + 1) * half),
+                            b_owner, slice_range(b_owner, P, n)))
+    return segs
+
+
 class PanelExchange:
     """Creates the row/column process groups once and all-gathers the panels
     each rank needs directly into its full-size containers (flat tensors)."""
@@ -99,6 +137,29 @@ class PanelExchange:
                 g = dist.new_group(cols[band])
                 if band == self.block.col_band:
                     self.col_group = g
+
+    # -- pipelined form: one K segment at a time (overlaps the previous segment's GEMM)
+    def segments(self) -> List[Segment]:
+        return segments(self.rank, self.P, self.n, self.t)
+
+    def exchange_segment(self, seg: Segment, lhs_flat, rhs_flat, async_op: bool = False):
+        """Broadcast the segment's A part inside the row group and its B part
+        inside the column group, in place in the full-size flat containers.
+        Returns the pending work handles when async_op."""
+        import torch.distributed as dist
+
+        works = []
+        if self.P == 1:
+            return works
+        for flat, owner, (b, e), members, group in (
+                (lhs_flat, seg.a_owner, seg.a_range, self.row_members, self.row_group),
+                (rhs_flat, seg.b_owner, seg.b_range, self.col_members, self.col_group)):
+            if len(members) == 1:
+                continue
+            wk = dist.broadcast(flat[b:e], src=owner, group=group, async_op=async_op)
+            if async_op:
+                works.append(wk)
+        return works
 
     def exchange(self, lhs_flat, rhs_flat):
         """lhs_flat / rhs_flat: the rank's full-size flat containers, holding its
