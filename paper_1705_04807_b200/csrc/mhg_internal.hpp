@@ -66,6 +66,7 @@ struct GemmParams {
     int vec_ok;                  // t % 4 == 0: 16-byte epilogue accesses allowed
     uint32_t group;              // raster: row tiles per group sharing rhs panels in L2
     int serpentine;              // alternate the K direction per tile (L2 reuse across waves)
+    int l2_hints;                // evict_last for lhs stages, evict_first for rhs stages
     unsigned long long* stats;   // optional per-CTA wait-cycle counters (diagnostics), or null
 };
 

@@ -305,6 +305,28 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 template <int N>
 __device__ __forceinline__ void epi_bar_sync() { asm volatile("bar.sync 1, %0;" ::"n"(N) : "memory"); }
 
+// Bulk copy with an L2 eviction-priority policy (createpolicy result).
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes,
+                                              uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1], %2, [%3], %4;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
 __device__ __forceinline__ void tc_fence_before() {
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
 }
@@ -733,6 +755,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
             uint32_t ph = 0;
             long long wait_empty = 0;
             uint32_t ord = 0;
+            const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
             for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++ord) {
                 uint32_t m, n;
                 tile_coords(tile, p.Mt, p.Nt, p.group, m, n);
@@ -747,10 +770,19 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
                     mbar_wait(&empty[st], ph ^ 1);
                     wait_empty += clock64() - w0;
                     mbar_expect_tx(&full[st], Cfg::STAGE);
-                    bulk_g2s(sA + st * Cfg::A_STAGE, a_src + (uint64_t)kt * Cfg::A_STAGE,
-                             Cfg::A_STAGE, &full[st]);
-                    bulk_g2s(sB + st * Cfg::B_STAGE, b_src + (uint64_t)kt * Cfg::B_STAGE,
-                             Cfg::B_STAGE, &full[st]);
+                    if (p.l2_hints) {
+                        // lhs panels of the raster group are re-read by the next waves;
+                        // rhs panels only by the current one
+                        bulk_g2s_hint(sA + st * Cfg::A_STAGE, a_src + (uint64_t)kt * Cfg::A_STAGE,
+                                      Cfg::A_STAGE, &full[st], pol_keep);
+                        bulk_g2s_hint(sB + st * Cfg::B_STAGE, b_src + (uint64_t)kt * Cfg::B_STAGE,
+                                      Cfg::B_STAGE, &full[st], pol_stream);
+                    } else {
+                        bulk_g2s(sA + st * Cfg::A_STAGE, a_src + (uint64_t)kt * Cfg::A_STAGE,
+                                 Cfg::A_STAGE, &full[st]);
+                        bulk_g2s(sB + st * Cfg::B_STAGE, b_src + (uint64_t)kt * Cfg::B_STAGE,
+                                 Cfg::B_STAGE, &full[st]);
+                    }
                     if (++st == STAGES) {
                         st = 0;
                         ph ^= 1;
