@@ -404,8 +404,17 @@ def run_gpu(args, rank, world, local_rank):
     int8_peak_tops = 2.0 * bf16_burst  # dense int8 = 2x dense bf16 on sm_100
     algo_ops = 2.0 * L * L * macs_rank  # int8 ops per GEMM launch (2 per limb MAC)
     achieved_tops = algo_ops / (gemm_ms_max * 1e-3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            rec = json.load(f).get(args.workload)
+        if rec and world == 1:
+            traffic = rec["dram_read"] + rec["dram_write"]
+    except Exception:
+        traffic = None
     roof = {"bound": "tensor", "achieved": achieved_tops, "peak": int8_peak_tops,
-            "unit": "TFLOP/s", "frac": achieved_tops / int8_peak_tops, "traffic": None,
+            "unit": "TFLOP/s", "frac": achieved_tops / int8_peak_tops, "traffic": traffic,
+            "traffic_source": "profiles/traffic.json (ncu --set full, bytes per launch)",
             "kernel": f"k_gemm<{L}> (tcgen05.mma.cta_group::1.kind::i8)",
             "peak_source": f"2 x {peak_src} bf16 burst {bf16_burst} TFLOP/s (MEASURED_PEAKS.json); "
                            f"int8 ops counted as 2*L^2*r*k*c, L={L}",
