@@ -1,6 +1,20 @@
-// mh/mh.hpp -- umbrella header of the C++ mirror of the reference API
-// (reference: proj/include/mh/mh.hpp), backed by libmhg.so on a B200.
+// mh/mh.hpp -- everything of the C++ mirror of the reference's header API
+// (namespace mh), backed by libmhg.so on an sm_100 GPU.
+//
+//   geometry      mh/layout.hpp     Layout, encode, extract_i / extract_j
+//   field         mh/field.hpp      Modulus, Fp, add, mul
+//   containers    mh/matrix.hpp     Matrix (device store + host mirror), Grid,
+//                                   from_row_major / to_row_major (device kernels)
+//   views         mh/submatrix.hpp  Sub, Aligned, split_sub, quadrants, predicates
+//   multiply      mh/multiply.hpp   Problem, Counters, mm_oblivious (+ Op::Sub / Op::Set),
+//                                   mm_naive, mm_default, compatible_parts
+//   protocol      mh/bench.hpp      Config, Rng, gen_problem, run_trials, CSV writers
+//   fixtures      mh/io.hpp         load_matrix / save_matrix text format
+//
+// Link with -lmhg (paper_1705_04807_b200/libmhg.so).
 #pragma once
+
+#define MH_B200_MIRROR 1
 
 #include "mh/bench.hpp"
 #include "mh/field.hpp"
