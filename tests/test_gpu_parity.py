@@ -412,3 +412,24 @@ def test_guard_bands(gpu, mh, oracle, monkeypatch, kernel):
             assert (h[:guard] == sentinel).all() and (h[guard + n * n:] == sentinel).all()
         assert np.array_equal(bufs[0][guard:guard + n * n].cpu().numpy().view(np.uint32), cells[0])
         assert np.array_equal(bufs[1][guard:guard + n * n].cpu().numpy().view(np.uint32), cells[1])
+
+
+def test_reference_golden_cases(gpu, mh, oracle):
+    """tests/golden/cases.json (generated by running the reference library,
+    tests/golden/make_golden.py): for every case the GPU's whole output
+    container hashes to the reference's SHA-256 and the Counters match."""
+    import hashlib
+    import json
+    import os
+    cases = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "cases.json")))
+    assert len(cases) >= 60
+    for c in cases:
+        n, t, q = c["n"], c["t"], c["q"]
+        g = oracle.rng(c["seed"])
+        for _ in range(c["draw"]):
+            oracle.gen_problem(g, n, t, q)
+        out, lhs, rhs, _, v = oracle.gen_problem(g, n, t, q)
+        assert [v.out_origin, v.lhs_origin, v.rhs_origin, v.rows, v.inner, v.cols] == c["views"]
+        got, ctr = _run_gpu(mh, n, t, q, out, lhs, rhs, v, c["op"])
+        assert hashlib.sha256(got.tobytes()).hexdigest() == c["out_sha256"], c
+        assert list(ctr.as_tuple()) == c["counters"], c
