@@ -232,6 +232,8 @@ mhg::GemmParams gemm_params(const Buffers& b, const mhg_view& out, const Checked
     p.w16_small = p.w16 < 256;
     p.group = 8;  // measured best at the power cap (profiles/r01_raster_groups.txt)
     p.serpentine = 1;
+    p.early_release = 1;
+    if (const char* er = std::getenv("MHG_EARLY_RELEASE")) p.early_release = std::atoi(er) != 0;
     p.l2_hints = 1;  // measured: -1.3% (n=16384), -2% (n=32768)
     if (const char* lh = std::getenv("MHG_L2HINTS")) p.l2_hints = std::atoi(lh) != 0;
     if (const char* sp = std::getenv("MHG_SERPENTINE")) p.serpentine = std::atoi(sp) != 0;

@@ -67,6 +67,7 @@ struct GemmParams {
     uint32_t group;              // raster: row tiles per group sharing rhs panels in L2
     int serpentine;              // alternate the K direction per tile (L2 reuse across waves)
     int l2_hints;                // evict_last for lhs stages, evict_first for rhs stages
+    int early_release;           // alternate TMEM bases and release before the last class group
     unsigned long long* stats;   // optional per-CTA wait-cycle counters (diagnostics), or null
 };
 

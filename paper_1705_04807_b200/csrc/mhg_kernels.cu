@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "mhg_internal.hpp"
 
@@ -471,6 +472,53 @@ __device__ __forceinline__ uint32_t fold_classes(const int32_t (&acc)[2 * L - 1]
     }
 }
 
+// Whether accumulation jobs alternate TMEM bases 0 / W so that the epilogue can
+// release TMEM before draining the last class group (single-CTA kernel).  Pays
+// when the early group is cheap: L = 1 (full double buffering) and L = 2 with
+// 2^16 mod q < 256; wider primes keep the fused single-phase drain.
+template <int L>
+__device__ __forceinline__ bool early_release(const GemmParams& p) {
+    return p.early_release && (L == 1 || (L == 2 && p.w16_small));
+}
+
+// Partial fold over the weight classes [C0, C1): sum_c acc[c - C0] 256^c mod q
+// (the epilogue drains a job's classes in two groups, see epilogue_role).
+template <int L, int CW, int C0, int C1>
+__device__ __forceinline__ uint32_t fold_part(const int32_t (&acc)[C1 - C0][CW], int j,
+                                              const GemmParams& p) {
+    if constexpr (L <= 2) {
+        uint32_t x = 0;
+#pragma unroll
+        for (int c = C0; c < C1; ++c) {
+            const uint32_t r = red32((uint32_t)acc[c - C0][j] + p.bias32, p);
+            uint32_t term = r;
+            if (c == 1) term = red32(r << 8, p);          // 256 r < 2^24
+            if (c == 2) term = red32(p.w16 * r, p);       // (2^16 mod q) r < 2^32
+            x += term;
+            x = x >= p.q ? x - p.q : x;
+        }
+        return x;
+    } else {
+        int64_t lo = 0, hi = 0;
+        bool any_hi = false;
+#pragma unroll
+        for (int c = C0; c < C1; ++c) {
+            if (c < 4) lo += (int64_t)acc[c - C0][j] << (8 * c);
+            else {
+                hi += (int64_t)acc[c - C0][j] << (8 * (c - 4));
+                any_hi = true;
+            }
+        }
+        uint32_t r = red_signed(lo, p);
+        if (any_hi) {
+            const uint32_t h = mulmod(red_signed(hi, p), p.w32, p);
+            r += h;
+            r = r >= p.q ? r - p.q : r;
+        }
+        return r;
+    }
+}
+
 template <int L>
 struct GemmCfg {
     static constexpr int W = (L <= 2) ? 128 : 64;       // output columns per tile
@@ -609,6 +657,81 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         PAIR ? mapa_shared(smem_u32(tmem_empty), 0) : smem_u32(tmem_empty);
     uint32_t acc_ph = 0;
     long long epi_wait = 0, epi_busy = 0;
+    // hand the accumulator columns back to the MMA issuer (one arrive per warp)
+    auto release = [&]() {
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+            if constexpr (PAIR) mbar_arrive_remote(release_bar);
+            else mbar_arrive(tmem_empty);
+        }
+    };
+    // L = 2 with w16 = 2^16 mod q < 256.  Base 0: classes {1,2} first --
+    // cur += 256 r1 + w16 r2 (unreduced, < 2^25) -- release, then class 0:
+    // cur = red(cur + a0 + bias).  Base W: classes {0,1} first -- cur += a0 +
+    // bias + 256 r1 (unreduced, < 2^32 - 2^24) -- release, then class 2:
+    // cur = red(cur + w16 r2).  Every class sum is within 2^31 - 2^17 (class 0
+    // and class 2 within 2^30), so no step wraps 32 bits.
+    auto drain_l2_small = [&](uint32_t tbase, uint32_t n_tile, uint32_t* cur_, uint32_t layout) {
+        const int lo_cls = layout ? 0 : 1;  // first group: {lo_cls, lo_cls + 1}
+#pragma unroll
+        for (int j0 = 0; j0 < WH; j0 += CW) {
+            if ((uint64_t)n_tile * W + jb + j0 >= p.cols) continue;  // warp-uniform
+            int32_t a[2][CW];
+            tmem_ld<CW>(tbase + lo_cls * W + j0, a[0]);
+            tmem_ld<CW>(tbase + (lo_cls + 1) * W + j0, a[1]);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < CW; ++j) {
+                const uint32_t r1 = red32((uint32_t)a[layout ? 1 : 0][j] + p.bias32, p);
+                if (layout == 0) {
+                    const uint32_t r2 = red32((uint32_t)a[1][j] + p.bias32, p);
+                    cur_[j0 + j] += (r1 << 8) + p.w16 * r2;
+                } else {
+                    cur_[j0 + j] += (uint32_t)a[0][j] + p.bias32 + (r1 << 8);
+                }
+            }
+        }
+        release();
+#pragma unroll
+        for (int j0 = 0; j0 < WH; j0 += CW) {
+            if ((uint64_t)n_tile * W + jb + j0 >= p.cols) continue;
+            int32_t a[1][CW];
+            tmem_ld<CW>(tbase + (layout ? 2 : 0) * W + j0, a[0]);
+            tmem_wait_ld();
+#pragma unroll
+            for (int j = 0; j < CW; ++j) {
+                if (layout == 0) {
+                    cur_[j0 + j] = red32(cur_[j0 + j] + (uint32_t)a[0][j] + p.bias32, p);
+                } else {
+                    const uint32_t r2 = red32((uint32_t)a[0][j] + p.bias32, p);
+                    cur_[j0 + j] = red32(cur_[j0 + j] + p.w16 * r2, p);
+                }
+            }
+        }
+    };
+    // drain weight classes [C0, C1) of this warp's columns and fold them into cur
+    auto drain = [&](auto c0_tag, auto c1_tag, uint32_t tbase, uint32_t n_tile, uint32_t* cur_) {
+        constexpr int C0 = decltype(c0_tag)::value, C1 = decltype(c1_tag)::value;
+        if constexpr (C1 > C0) {
+#pragma unroll
+            for (int j0 = 0; j0 < WH; j0 += CW) {
+                if ((uint64_t)n_tile * W + jb + j0 >= p.cols) continue;  // warp-uniform
+                int32_t acc[C1 - C0][CW];
+#pragma unroll
+                for (int k = C0; k < C1; ++k) tmem_ld<CW>(tbase + k * W + j0, acc[k - C0]);
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < CW; ++j) {
+                    uint32_t r;
+                    if constexpr (C0 == 0 && C1 == CLASSES) r = fold_classes<L, CW>(acc, j, p);
+                    else r = fold_part<L, CW, C0, C1>(acc, j, p);
+                    const uint32_t sum = cur_[j0 + j] + r;
+                    cur_[j0 + j] = sum >= p.q ? sum - p.q : sum;
+                }
+            }
+        }
+    };
     for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride) {
         uint32_t tm, n;
         tile_coords(tile, row_groups, p.Nt, p.group, tm, n);
@@ -652,36 +775,65 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
             const long long w1 = clock64();
             epi_wait += w1 - w0;
             tc_fence_after();
+            if constexpr (PAIR) {
 #pragma unroll
-            for (int j0 = 0; j0 < WH; j0 += CW) {
-                const bool live = (uint64_t)n * W + jb + j0 < p.cols;  // warp-uniform
-                if (!PAIR && !live) continue;
-                int32_t acc[CLASSES][CW];
+                for (int j0 = 0; j0 < WH; j0 += CW) {
+                    const bool live = (uint64_t)n * W + jb + j0 < p.cols;  // warp-uniform
+                    int32_t acc[CLASSES][CW];
 #pragma unroll
-                for (int k = 0; k < CLASSES; ++k)
-                    tmem_ld<CW>(tmem + lane_base + k * W + jb + j0, acc[k]);
-                tmem_wait_ld();
-                if constexpr (PAIR) {
+                    for (int k = 0; k < CLASSES; ++k)
+                        tmem_ld<CW>(tmem + lane_base + k * W + jb + j0, acc[k]);
+                    tmem_wait_ld();
 #pragma unroll
                     for (int k = L; k < CLASSES; ++k) tmem_zero<CW>(tmem + lane_base + k * W + jb + j0);
-                }
-                if (live) {
+                    if (live) {
 #pragma unroll
-                    for (int j = 0; j < CW; ++j) {
-                        const uint32_t r = fold_classes<L, CW>(acc, j, p);
-                        const uint32_t sum = cur[j0 + j] + r;
-                        cur[j0 + j] = sum >= p.q ? sum - p.q : sum;
+                        for (int j = 0; j < CW; ++j) {
+                            const uint32_t r = fold_classes<L, CW>(acc, j, p);
+                            const uint32_t sum = cur[j0 + j] + r;
+                            cur[j0 + j] = sum >= p.q ? sum - p.q : sum;
+                        }
                     }
                 }
+                tmem_wait_st();
+                release();
+                epi_busy += clock64() - w1;
+            } else {
+                // Jobs alternate TMEM bases 0 / W.  The next job (other base) needs
+                // this job's classes [1, C) (base 0) or [0, C-1) (base W) plus the
+                // free region, so those are drained and folded first, TMEM is
+                // released, and the remaining class is drained while the next
+                // job's MMAs run.
+                const bool alt = early_release<L>(p);
+                const uint32_t tb = tmem + lane_base + ((alt && acc_ph) ? W : 0) + jb;
+                if (!alt) {
+                    // fixed layout: drain and fold every class, then release
+                    drain(std::integral_constant<int, 0>{}, std::integral_constant<int, CLASSES>{}, tb, n, cur);
+                    release();
+                    epi_busy += clock64() - w1;
+                    acc_ph ^= 1;
+                    continue;
+                }
+                if constexpr (L == 2) {
+                    // lean split for q = 2^16 - small (e.g. 65521): the first group
+                    // leaves cur unreduced (< 2^32 - 2^24); the second group finishes
+                    drain_l2_small(tb, n, cur, acc_ph);
+                    epi_busy += clock64() - w1;
+                    acc_ph ^= 1;
+                    continue;
+                }
+                if (acc_ph == 0) {
+                    drain(std::integral_constant<int, 1>{}, std::integral_constant<int, CLASSES>{}, tb, n, cur);
+                    release();
+                    epi_busy += clock64() - w1;
+                    drain(std::integral_constant<int, 0>{}, std::integral_constant<int, 1>{}, tb, n, cur);
+                } else {
+                    drain(std::integral_constant<int, 0>{}, std::integral_constant<int, CLASSES - 1>{}, tb, n, cur);
+                    release();
+                    epi_busy += clock64() - w1;
+                    drain(std::integral_constant<int, CLASSES - 1>{}, std::integral_constant<int, CLASSES>{}, tb, n, cur);
+                }
             }
-            if constexpr (PAIR) tmem_wait_st();
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                if constexpr (PAIR) mbar_arrive_remote(release_bar);
-                else mbar_arrive(tmem_empty);
-            }
-            epi_busy += clock64() - w1;
             acc_ph ^= 1;
         }
         if (row_ok) {
@@ -797,6 +949,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
             constexpr uint32_t id_full = idesc_i8(kBM, Cfg::NB);
             constexpr uint32_t id_head = idesc_i8(kBM, (L > 1 ? L - 1 : 1) * W);
             constexpr uint32_t id_one = idesc_i8(kBM, W);
+            const bool alt_layout = early_release<L>(p);
             int st = 0;
             uint32_t ph = 0, acc_ph = 0;
             long long wait_full = 0, wait_tmem = 0;
@@ -823,7 +976,9 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
 #pragma unroll
                             for (int s = 0; s < L; ++s) {
                                 const uint64_t ad = sdesc(a0 + s * kBM * kBK + kk * 32);
-                                const uint32_t d = tmem + s * W;
+                                // accumulation jobs alternate TMEM bases 0 / W where the
+                                // epilogue uses the early release (see epilogue_role)
+                                const uint32_t d = tmem + ((alt_layout && acc_ph) ? W : 0) + s * W;
                                 if (!first) {
                                     mma_i8(d, ad, bd, id_full, 1u);
                                 } else if (s == 0) {
