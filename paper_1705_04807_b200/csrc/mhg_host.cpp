@@ -232,6 +232,8 @@ mhg::GemmParams gemm_params(const Buffers& b, const mhg_view& out, const Checked
     p.w16_small = p.w16 < 256;
     p.group = 8;  // measured best at the power cap (profiles/r01_raster_groups.txt)
     p.serpentine = 1;
+    p.ring = 0;
+    if (const char* rg = std::getenv("MHG_RING")) p.ring = std::atoi(rg);
     p.early_release = 1;
     if (const char* er = std::getenv("MHG_EARLY_RELEASE")) p.early_release = std::atoi(er) != 0;
     p.l2_hints = 1;  // measured: -1.3% (n=16384), -2% (n=32768)
@@ -246,7 +248,7 @@ mhg::GemmParams gemm_params(const Buffers& b, const mhg_view& out, const Checked
     return p;
 }
 
-// 2D uint8 tensor map over a packed operand: rows of 128 bytes, box of
+// 2D uint8 tensor map over a packed operand: rows of kBK bytes, box of
 // `box_rows` rows, no swizzle (the pack kernels already wrote the swizzled
 // shared-memory image).  cuTensorMapEncodeTiled comes from the driver entry
 // point, so the library does not link libcuda.
@@ -269,9 +271,9 @@ void make_tmap(CUtensorMap* tm, const void* base, uint64_t bytes, uint32_t box_r
             fail(MHG_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
         encode = reinterpret_cast<Encode>(fn);
     }
-    const cuuint64_t dims[2] = {128, bytes / 128};
-    const cuuint64_t strides[1] = {128};
-    const cuuint32_t box[2] = {128, box_rows};
+    const cuuint64_t dims[2] = {(cuuint64_t)mhg::kBK, bytes / mhg::kBK};
+    const cuuint64_t strides[1] = {(cuuint64_t)mhg::kBK};
+    const cuuint32_t box[2] = {(cuuint32_t)mhg::kBK, box_rows};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims,
                               strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,

@@ -38,9 +38,12 @@ LimbParams limb_params(uint32_t q);
 
 // ------------------------------------------------------------------- GEMM
 // CTA tile: BM = 128 output rows x W output columns, W = 128 (L <= 2) or 64.
-// K staged in BK = 128-byte slices (one SWIZZLE_128B atom row).
+// K staged in BK-byte slices (one swizzle-atom row).  BK = 128 (SWIZZLE_128B):
+// BK = 64 would allow a deeper ring of smaller stages, but SWIZZLE_64B operands
+// slow the tensor pipe by ~20% (profiles/r01_ab_ring.txt).
 constexpr int kBM = 128;
-constexpr int kBK = 128;
+constexpr int kBK = 128;       // bytes of K per pipeline stage = one SWIZZLE_128B atom row
+constexpr int kPackK = 128;    // K elements per k_pack_rows block
 constexpr int kPackRows = 32;  // pack kernel block rows
 
 inline int tile_width(int L) { return L <= 2 ? 128 : 64; }
@@ -67,6 +70,7 @@ struct GemmParams {
     uint32_t group;              // raster: row tiles per group sharing rhs panels in L2
     int serpentine;              // alternate the K direction per tile (L2 reuse across waves)
     int l2_hints;                // evict_last for lhs stages, evict_first for rhs stages
+    int ring;                    // pipeline stages in use (0 = all); diagnostics
     int early_release;           // alternate TMEM bases and release before the last class group
     unsigned long long* stats;   // optional per-CTA wait-cycle counters (diagnostics), or null
 };

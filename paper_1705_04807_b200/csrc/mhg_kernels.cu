@@ -163,8 +163,14 @@ __device__ __forceinline__ void load4(const uint32_t* __restrict__ src, uint64_t
         v[e] = (rok && c0 + e < ncols) ? __ldcs(src + rbase + __ldg(coloff + c0 + e)) : 0u;
 }
 
+// Swizzle of the K-major UMMA operand image with BK-byte rows (SWIZZLE_<BK>B):
+// the 16-byte chunk c of row r sits at chunk c ^ ((r * BK >> 7) & (BK/16 - 1)).
+__host__ __device__ constexpr uint32_t swizzled_chunk(uint32_t row, uint32_t chunk) {
+    return chunk ^ (((row * (uint32_t)kBK) >> 7) & (uint32_t)(kBK / 16 - 1));
+}
+
 // Destination of the 16-byte chunk holding K bytes [kk, kk+16) of pack row pr,
-// limb s, in the [row tile][k tile][L][rows_per_tile][128 B] SWIZZLE_128B image.
+// limb s, in the [row tile][k tile][L][rows_per_tile][BK B] swizzled image.
 template <int L>
 __device__ __forceinline__ int8_t* pack_dst(int8_t* dst, uint64_t pr, uint64_t kk, int s,
                                             uint32_t rpt, uint32_t Kt) {
@@ -173,13 +179,13 @@ __device__ __forceinline__ int8_t* pack_dst(int8_t* dst, uint64_t pr, uint64_t k
     const uint64_t kt = kk / kBK;
     const uint32_t ch = (uint32_t)(kk % kBK) >> 4;
     return dst + ((tile * Kt + kt) * L + s) * (uint64_t)rpt * kBK + (uint64_t)rit * kBK +
-           ((ch ^ (rit & 7)) << 4);
+           (swizzled_chunk(rit, ch) << 4);
 }
 
 // lhs: pack rows = view rows, K = view columns (contiguous in the source).
 // Block: 32 pack rows x 128 K; thread: 4 rows x 4 consecutive K (one 16-byte load
 // per row).  Smem holds the digit bytes [L][32][128 (+16 pad)].
-constexpr int kRowsStride = kBK + 16;
+constexpr int kRowsStride = kPackK + 16;
 
 template <int L>
 __global__ void __launch_bounds__(256) k_pack_rows(const uint32_t* __restrict__ src,
@@ -189,9 +195,11 @@ __global__ void __launch_bounds__(256) k_pack_rows(const uint32_t* __restrict__ 
                                                    uint64_t Rpad, int8_t* __restrict__ dst,
                                                    DigitParams dp) {
     __shared__ __align__(16) uint8_t sd[L][32][kRowsStride];
-    const uint32_t kt = blockIdx.x % Kt;
-    const uint64_t pr0 = (uint64_t)(blockIdx.x / Kt) * 32;
-    const uint64_t k0 = (uint64_t)kt * kBK;
+    const uint64_t kpad = (uint64_t)Kt * kBK;
+    const uint32_t nkb = (uint32_t)((kpad + kPackK - 1) / kPackK);
+    const uint32_t kb = blockIdx.x % nkb;
+    const uint64_t pr0 = (uint64_t)(blockIdx.x / nkb) * 32;
+    const uint64_t k0 = (uint64_t)kb * kPackK;
     const int tk = threadIdx.x & 31, tr = threadIdx.x >> 5;
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
@@ -211,7 +219,7 @@ __global__ void __launch_bounds__(256) k_pack_rows(const uint32_t* __restrict__ 
         const int cid = threadIdx.x + 256 * e;  // L x 32 rows x 8 chunks
         const int s = cid >> 8, r = (cid >> 3) & 31, ch = cid & 7;
         const uint64_t pr = pr0 + r;
-        if (pr >= Rpad) continue;
+        if (pr >= Rpad || k0 + 16 * ch >= kpad) continue;
         const uint4 val = *reinterpret_cast<const uint4*>(&sd[s][r][ch * 16]);
         *reinterpret_cast<uint4*>(pack_dst<L>(dst, pr, k0 + 16 * ch, s, rpt, Kt)) = val;
     }
@@ -230,8 +238,9 @@ __global__ void __launch_bounds__(256) k_pack_cols(const uint32_t* __restrict__ 
                                                    uint64_t Rpad, int8_t* __restrict__ dst,
                                                    DigitParams dp) {
     __shared__ __align__(16) uint8_t sd[L][128][kColsStride];
-    const uint32_t kq = blockIdx.x % (Kt * 4);  // 32-wide K quarter of a k tile
-    const uint64_t pr0 = (uint64_t)(blockIdx.x / (Kt * 4)) * 128;
+    const uint32_t nkq = Kt * (kBK / 32);         // 32-wide K slices
+    const uint32_t kq = blockIdx.x % nkq;
+    const uint64_t pr0 = (uint64_t)(blockIdx.x / nkq) * 128;
     const uint64_t k0 = (uint64_t)kq * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     uint32_t v[4][4];  // [k][pack row]
@@ -352,14 +361,16 @@ __device__ __forceinline__ void mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t
         : "memory");
 }
 
-// K-major operand, SWIZZLE_128B: 8-row x 128-byte atoms, 1024 B apart (SBO).
+// K-major operand, SWIZZLE_<BK>B: 8-row x BK-byte atoms, 8*BK bytes apart (SBO).
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
+    static_assert(kBK == 128 || kBK == 64, "swizzle width");
+    constexpr uint64_t layout = kBK == 128 ? 2 : 4;  // SWIZZLE_128B / SWIZZLE_64B
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-    d |= (uint64_t)1 << 16;              // LBO (unused for swizzled K-major)
-    d |= (uint64_t)(1024 >> 4) << 32;    // SBO
-    d |= (uint64_t)1 << 46;              // descriptor version (sm_100)
-    d |= (uint64_t)2 << 61;              // SWIZZLE_128B
+    d |= (uint64_t)1 << 16;                    // LBO (unused for swizzled K-major)
+    d |= (uint64_t)((8 * kBK) >> 4) << 32;     // SBO
+    d |= (uint64_t)1 << 46;                    // descriptor version (sm_100)
+    d |= layout << 61;
     return d;
 }
 
@@ -527,10 +538,11 @@ struct GemmCfg {
     static constexpr int A_STAGE = L * kBM * kBK;       // bytes
     static constexpr int B_STAGE = NB * kBK;            // bytes
     static constexpr int STAGE = A_STAGE + B_STAGE;
-    static constexpr int STAGES_RAW = (200 * 1024) / STAGE;
-    static constexpr int STAGES = STAGES_RAW > 6 ? 6 : STAGES_RAW;
+    static constexpr int STAGES_RAW = (224 * 1024) / STAGE;
+    static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
     static constexpr int SMEM =
         1024 /*align slack*/ + STAGES * STAGE + 256 /*barriers*/ + 8 * W /*column offsets*/;
+    static_assert(SMEM <= 232448, "227 KB dynamic shared memory limit");
     static constexpr int EPI_WARPS = 8;                 // two per SMSP, each half the columns
     static constexpr int EPI_THREADS = EPI_WARPS * 32;
     static constexpr int WH = W / 2;                    // columns per epilogue warp
@@ -879,6 +891,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t num_tiles = p.Mt * p.Nt;
     const uint32_t nchunks = (p.Kt + p.KC - 1) / p.KC;
+    const int ring = (p.ring > 0 && p.ring < STAGES) ? p.ring : STAGES;  // tuning hook
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -935,7 +948,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
                         bulk_g2s(sB + st * Cfg::B_STAGE, b_src + (uint64_t)kt * Cfg::B_STAGE,
                                  Cfg::B_STAGE, &full[st]);
                     }
-                    if (++st == STAGES) {
+                    if (++st == ring) {
                         st = 0;
                         ph ^= 1;
                     }
@@ -993,7 +1006,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
                             }
                         }
                         tc_commit(&empty[st]);
-                        if (++st == STAGES) {
+                        if (++st == ring) {
                             st = 0;
                             ph ^= 1;
                         }
@@ -1047,9 +1060,10 @@ struct Gemm2Cfg {
     static constexpr int A_STAGE = L * kBM * kBK;
     static constexpr int B_STAGE = NBH * kBK;
     static constexpr int STAGE = A_STAGE + B_STAGE;
-    static constexpr int STAGES_RAW = (200 * 1024) / STAGE;
+    static constexpr int STAGES_RAW = (220 * 1024) / STAGE;
     static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
     static constexpr int SMEM = 1024 + STAGES * STAGE + 512 + 8 * W;
+    static_assert(SMEM <= 232448, "227 KB dynamic shared memory limit");
     static constexpr int EPI_WARPS = 8;
     static constexpr int EPI_THREADS = EPI_WARPS * 32;
     static constexpr int WH = W / 2;
@@ -1262,11 +1276,11 @@ int launch_pack_t(int trans, const uint32_t* src, const uint64_t* rowoff, const 
                   DigitParams dp, cudaStream_t s) {
     const uint64_t Rpad = (uint64_t)Rtiles * rpt;
     if (trans) {
-        const uint64_t blocks = ((Rpad + 127) / 128) * Kt * 4;
+        const uint64_t blocks = ((Rpad + 127) / 128) * Kt * (kBK / 32);
         k_pack_cols<L><<<(unsigned)blocks, 256, 0, s>>>(src, rowoff, coloff, R, K, rpt, Kt, Rpad,
                                                         dst, dp);
     } else {
-        const uint64_t blocks = (Rpad / 32) * Kt;
+        const uint64_t blocks = (Rpad / 32) * (((uint64_t)Kt * kBK + kPackK - 1) / kPackK);
         k_pack_rows<L><<<(unsigned)blocks, 256, 0, s>>>(src, rowoff, coloff, R, K, rpt, Kt, Rpad,
                                                         dst, dp);
     }
