@@ -299,20 +299,38 @@ void launch_gemm_any(const mhg::GemmParams& p, const mhg::GemmGeometry& g, const
         cuda_check(mhg::launch_gemm((int)g.L, p, device_info().sms, stream), "gemm");
 }
 
+// Side stream + events that turn the two pack launches into parallel graph branches.
+struct Fork {
+    cudaStream_t side;
+    cudaEvent_t split, join;
+};
+
 // Pack both operands and run the GEMM: 2 pack launches + 1 GEMM launch.
 void launch_multiply(const Buffers& b, const mhg_view& out, const mhg_view& lhs,
                      const mhg_view& rhs, const Checked& c, const mhg::GemmGeometry& g,
                      mhg_op op, void* stream, cudaEvent_t gemm_begin = nullptr,
-                     cudaEvent_t gemm_end = nullptr) {
+                     cudaEvent_t gemm_end = nullptr, const Fork* fork = nullptr) {
     const mhg::LimbParams lp = mhg::limb_params(out.mat->q);
     mhg::DigitParams dl{out.mat->q, lp.H, op == MHG_OP_SUB ? 1 : 0};
     mhg::DigitParams dr{out.mat->q, lp.H, 0};
+    // with a fork (graph capture), the two independent packs become parallel
+    // branches joined before the GEMM
+    void* rhs_stream = stream;
+    if (fork) {
+        cuda_check(cudaEventRecord(fork->split, (cudaStream_t)stream), "fork");
+        cuda_check(cudaStreamWaitEvent(fork->side, fork->split, 0), "fork");
+        rhs_stream = fork->side;
+    }
     cuda_check(mhg::launch_pack((int)g.L, 0, lhs.mat->cells, b.lhs_row, b.lhs_col, c.rl.rows,
                                 c.rl.cols, mhg::kBM, g.Mt, g.Kt, b.apack, dl, stream),
                "pack lhs");
     cuda_check(mhg::launch_pack((int)g.L, 1, rhs.mat->cells, b.rhs_row, b.rhs_col, c.rr.cols,
-                                c.rr.rows, g.W, g.Nt, g.Kt, b.bpack, dr, stream),
+                                c.rr.rows, g.W, g.Nt, g.Kt, b.bpack, dr, rhs_stream),
                "pack rhs");
+    if (fork) {
+        cuda_check(cudaEventRecord(fork->join, fork->side), "join");
+        cuda_check(cudaStreamWaitEvent((cudaStream_t)stream, fork->join, 0), "join");
+    }
     mhg::GemmParams p = gemm_params(b, out, c, g, op);
     // diagnostics: MHG_GEMM_STATS=1 prints per-CTA wait-cycle shares (synchronous)
     static const bool stats_on = std::getenv("MHG_GEMM_STATS") != nullptr;
@@ -742,9 +760,20 @@ mhg_status mhg_plan_run(mhg_plan p, void* stream) {
             cuda_check(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "capture stream");
             // make sure the kernels' one-time attributes are set outside capture
             cuda_check(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "capture");
+            Fork fork{};
+            cuda_check(cudaStreamCreateWithFlags(&fork.side, cudaStreamNonBlocking), "fork stream");
+            cuda_check(cudaEventCreateWithFlags(&fork.split, cudaEventDisableTiming), "fork event");
+            cuda_check(cudaEventCreateWithFlags(&fork.join, cudaEventDisableTiming), "fork event");
+            auto drop_fork = [&] {
+                cudaEventDestroy(fork.split);
+                cudaEventDestroy(fork.join);
+                cudaStreamDestroy(fork.side);
+            };
             try {
-                launch_multiply(p->buf, p->out, p->lhs, p->rhs, p->chk, p->geo, p->op, cap);
+                launch_multiply(p->buf, p->out, p->lhs, p->rhs, p->chk, p->geo, p->op, cap, nullptr,
+                                nullptr, &fork);
             } catch (...) {
+                drop_fork();
                 cudaGraph_t g;
                 cudaStreamEndCapture(cap, &g);
                 if (g) cudaGraphDestroy(g);
@@ -752,6 +781,7 @@ mhg_status mhg_plan_run(mhg_plan p, void* stream) {
                 throw;
             }
             cuda_check(cudaStreamEndCapture(cap, &p->graph), "end capture");
+            drop_fork();
             cudaStreamDestroy(cap);
             cuda_check(cudaGraphInstantiate(&p->exec, p->graph, 0), "graph instantiate");
         }
