@@ -433,3 +433,19 @@ def test_reference_golden_cases(gpu, mh, oracle):
         got, ctr = _run_gpu(mh, n, t, q, out, lhs, rhs, v, c["op"])
         assert hashlib.sha256(got.tobytes()).hexdigest() == c["out_sha256"], c
         assert list(ctr.as_tuple()) == c["counters"], c
+
+
+@pytest.mark.slow
+def test_cfg5_box_scale(gpu, mh, oracle):
+    """BASELINE cfg5 shape on one GPU: n=32768, t=64, p=65521, C -= A*B (K=32768
+    in a single exact int32 chunk): Freivalds over the whole result + tiles in
+    the four top-level quadrants and the far corner."""
+    n, t, q = 32768, 64, P16
+    out, lhs, rhs = _fill(oracle, 5, n, q)
+    v = Views(0, 0, 0, n, n, n)
+    got, ctr = _run_gpu(mh, n, t, q, out, lhs, rhs, v, OP_SUB)
+    assert ctr.base_case_calls == 512 ** 3
+    assert oracle.freivalds(n, t, q, out, lhs, rhs, got, v, op=OP_SUB, rounds=1)
+    h = n // 2
+    _sampled_tiles(oracle, n, t, q, out, lhs, rhs, got, v, OP_SUB,
+                   [(0, 0), (0, h), (h, 0), (h, h), (n - 64, n - 64)])
