@@ -449,3 +449,19 @@ def test_cfg5_box_scale(gpu, mh, oracle):
     h = n // 2
     _sampled_tiles(oracle, n, t, q, out, lhs, rhs, got, v, OP_SUB,
                    [(0, 0), (0, h), (h, 0), (h, h), (n - 64, n - 64)])
+
+
+@pytest.mark.slow
+def test_two_exact_chunks_at_scale(gpu, mh, oracle):
+    """n = 65536: K = 65536 exceeds the exact int32 chunk for p = 65521
+    (k_max = 65532), so the GEMM really drains and folds two K-chunks per tile.
+    Whole-result Freivalds check (inputs from numpy; 16 GiB per container)."""
+    n, t, q = 65536, 64, P16
+    L, H, kmax = mh.limb_params(q)
+    assert n > kmax
+    rng = np.random.default_rng(65536)
+    out, lhs, rhs = (rng.integers(0, q, n * n, dtype=np.uint32) for _ in range(3))
+    v = Views(0, 0, 0, n, n, n)
+    got, ctr = _run_gpu(mh, n, t, q, out, lhs, rhs, v, OP_SUB)
+    assert ctr.scalar_macs == n ** 3
+    assert oracle.freivalds(n, t, q, out, lhs, rhs, got, v, op=OP_SUB, rounds=1)
