@@ -39,7 +39,8 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libmhg.so")
+# MHG_LIB: an alternative build of the same library (kernel A/B diagnostics only)
+LIB_PATH = os.environ.get("MHG_LIB") or os.path.join(HERE, "libmhg.so")
 OP_ADD, OP_SUB, OP_SET = 0, 1, 2
 
 

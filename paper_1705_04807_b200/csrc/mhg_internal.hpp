@@ -55,6 +55,8 @@ struct GemmParams {
     const uint64_t* out_rowoff;  // rows entries
     const uint64_t* out_coloff;  // cols entries
     uint64_t rows, cols;
+    uint64_t out_i0, out_j0;     // view origin in the output container
+    TileGeom out_geom;           // output container tile geometry (offsets in-kernel)
     uint32_t Mt, Nt, Kt, KC;     // KC: k-tiles per exact int32 chunk
     uint32_t q;
     uint32_t w32;                // 2^32 mod q
@@ -72,12 +74,14 @@ struct GemmParams {
     int l2_hints;                // evict_last for lhs stages, evict_first for rhs stages
     int ring;                    // pipeline stages in use (0 = all); diagnostics
     int early_release;           // alternate TMEM bases and release before the last class group
+    int off_tables;              // epilogue output offsets from the tables (1) or computed (0)
+    uint32_t wait_hint;          // mbarrier try_wait suspend-time hint, ns (k_gemm roles)
     unsigned long long* stats;   // optional per-CTA wait-cycle counters (diagnostics), or null
 };
 
 // k_gemm diagnostics layout (per CTA, when GemmParams::stats != null)
 enum GemmStat { kStatTotal = 0, kStatMmaWaitFull, kStatMmaWaitTmem, kStatProdWaitEmpty,
-                kStatEpiWaitFull, kStatEpiBusy, kStatCount };
+                kStatEpiWaitFull, kStatEpiBusy, kStatEpiPrologue, kStatEpiTail, kStatEpiLdWait, kStatCount };
 
 // --------------------------------------------------------------- launchers
 // All asynchronous on `stream`; return a cudaError_t value (0 = success).

@@ -302,6 +302,49 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// Blocking wait with a suspend-time hint (ns): the thread sleeps in the
+// barrier until the phase completes instead of re-polling, which keeps the
+// single-thread producer / MMA roles off the issue slots their SMSP shares with
+// epilogue warps.
+__device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
+    if (hint_ns == 0) {
+        mbar_wait(bar, parity);
+        return;
+    }
+    asm volatile(
+        "{\n\t.reg .pred P1;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1, %2;\n\t"
+        "@!P1 bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(hint_ns)
+        : "memory");
+}
+
+__device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
+    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
+                 "r"(v.w)
+                 : "memory");
+}
+
+__device__ __forceinline__ uint4 lds128(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "r"(addr)
+                 : "memory");
+    return v;
+}
+
+__device__ __forceinline__ void sts32(uint32_t addr, uint32_t v) {
+    asm volatile("st.shared.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.b32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
                                          uint64_t* bar) {
     asm volatile(
@@ -538,14 +581,18 @@ struct GemmCfg {
     static constexpr int A_STAGE = L * kBM * kBK;       // bytes
     static constexpr int B_STAGE = NB * kBK;            // bytes
     static constexpr int STAGE = A_STAGE + B_STAGE;
-    static constexpr int STAGES_RAW = (224 * 1024) / STAGE;
+    // two epilogue warps per SMSP, 64 columns each; W = 128 uses the coalesced
+    // C path with a 4 KB per-warp transpose buffer, the narrow-tile primes keep
+    // row-per-thread C access (see epilogue_role)
+    static constexpr bool XPOSE = (W == 128);
+    static constexpr int EPI_WARPS = 8;
+    static constexpr int XBUF = XPOSE ? EPI_WARPS * 4096 : 0;
+    static constexpr int FIXED = 1024 /*align slack*/ + 256 /*barriers*/ + 8 * W /*column offsets*/ + XBUF;
+    static constexpr int STAGES_RAW = (232448 - FIXED) / STAGE;
     static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-    static constexpr int SMEM =
-        1024 /*align slack*/ + STAGES * STAGE + 256 /*barriers*/ + 8 * W /*column offsets*/;
+    static constexpr int SMEM = FIXED + STAGES * STAGE;
     static_assert(SMEM <= 232448, "227 KB dynamic shared memory limit");
-    static constexpr int EPI_WARPS = 8;                 // two per SMSP, each half the columns
     static constexpr int EPI_THREADS = EPI_WARPS * 32;
-    static constexpr int WH = W / 2;                    // columns per epilogue warp
     static constexpr int THREADS = 64 + EPI_THREADS;    // producer, MMA, epilogue warps
     static_assert(CLASSES * W <= 512, "TMEM columns");
     static_assert(STAGES >= 2, "pipeline depth");
@@ -639,24 +686,34 @@ __device__ __forceinline__ void tmem_wait_st() {
 }
 
 // Epilogue role of both GEMM kernels (warps 2 .. 2+EPI_WARPS-1).  Per tile:
-// (1) stage the tile's column offsets in smem and prefetch the thread's output
-// row segment (C_old) into registers -- overlapping the tile's MMA main loop;
-// (2) per exact K-chunk, drain the 2L-1 weight classes from TMEM
-// (tcgen05.ld 32x32b.x16), fold them mod q into the register copy, release
-// TMEM; (3) store the row segment after the release, overlapping the next
-// tile's MMAs.  One TMEM lane (= output row) per thread; warp w may only
-// access lane quadrant w % 4, and the two warps of a quadrant split the
-// columns.  PAIR (k_gemm2): the tile's row block is 2*pm + rank, the upper
-// classes [L, 2L-1) are re-zeroed as they are drained (every MMA but the first
-// of a chunk accumulates), and TMEM is released on the LEADER's barrier.
-template <int L, int W, int EPI_WARPS, bool PAIR>
+// (1) bring the tile's output rows (C_old) into a register copy; (2) per exact
+// K-chunk, drain the 2L-1 weight classes from TMEM (tcgen05.ld 32x32b), fold
+// them mod q into the copy and release TMEM; (3) store the copy after the
+// release, overlapping the next tile's MMAs.  One TMEM lane (= output row) per
+// thread; warp w may only access lane quadrant w % 4, and the EPI_WARPS / 4
+// warps of a quadrant split the columns.  PAIR (k_gemm2): the tile's row block
+// is 2*pm + rank, the upper classes [L, 2L-1) are re-zeroed as they are drained
+// (every MMA but the first of a chunk accumulates), and TMEM is released on the
+// LEADER's barrier.
+//
+// XPOSE (k_gemm, W = 128, 8 warps x 64 columns): C_old is loaded and C is
+// stored in a coalesced order -- per warp instruction 8 lanes cover one
+// 128-byte row run (32 columns), 4 rows at a time -- and moved to / from the
+// row-per-thread copy through a 4 KB per-warp shared buffer (32 rows x 8
+// 16-byte chunks, chunk index XOR row%8: both orders bank-conflict free), one
+// 32-column pass at a time.  Output offsets are computed from the Morton
+// geometry (no table loads).  Otherwise (narrow tiles, CTA pair) the row's
+// C_old is prefetched into registers at tile start, addressed through smem
+// column offsets.
+template <int L, int W, int EPI_WARPS, bool PAIR, bool XPOSE = false>
 __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t first_tile,
                                               uint32_t tile_stride, uint32_t num_tiles,
                                               uint32_t row_groups, uint32_t rank, uint32_t nchunks,
                                               uint32_t tmem, uint64_t* s_col, uint64_t* tmem_full,
-                                              uint64_t* tmem_empty, int warp, int lane) {
+                                              uint64_t* tmem_empty, int warp, int lane,
+                                              uint8_t* xbuf = nullptr) {
     constexpr int EPI_THREADS = EPI_WARPS * 32;
-    constexpr int WH = W / 2;
+    constexpr int WH = W * 4 / EPI_WARPS;  // columns per epilogue warp
     constexpr int CLASSES = 2 * L - 1;
     constexpr int CW = L <= 2 ? 16 : 8;  // TMEM columns per drain step (register budget)
     constexpr uint64_t kNoCol = ~uint64_t(0);
@@ -668,7 +725,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     const uint32_t release_bar =
         PAIR ? mapa_shared(smem_u32(tmem_empty), 0) : smem_u32(tmem_empty);
     uint32_t acc_ph = 0;
-    long long epi_wait = 0, epi_busy = 0;
+    long long epi_wait = 0, epi_busy = 0, epi_ldw = 0;
     // hand the accumulator columns back to the MMA issuer (one arrive per warp)
     auto release = [&]() {
         tc_fence_before();
@@ -690,9 +747,11 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         for (int j0 = 0; j0 < WH; j0 += CW) {
             if ((uint64_t)n_tile * W + jb + j0 >= p.cols) continue;  // warp-uniform
             int32_t a[2][CW];
+            const long long l0 = clock64();
             tmem_ld<CW>(tbase + lo_cls * W + j0, a[0]);
             tmem_ld<CW>(tbase + (lo_cls + 1) * W + j0, a[1]);
             tmem_wait_ld();
+            epi_ldw += clock64() - l0;
 #pragma unroll
             for (int j = 0; j < CW; ++j) {
                 const uint32_t r1 = red32((uint32_t)a[layout ? 1 : 0][j] + p.bias32, p);
@@ -709,8 +768,10 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         for (int j0 = 0; j0 < WH; j0 += CW) {
             if ((uint64_t)n_tile * W + jb + j0 >= p.cols) continue;
             int32_t a[1][CW];
+            const long long l0 = clock64();
             tmem_ld<CW>(tbase + (layout ? 2 : 0) * W + j0, a[0]);
             tmem_wait_ld();
+            epi_ldw += clock64() - l0;
 #pragma unroll
             for (int j = 0; j < CW; ++j) {
                 if (layout == 0) {
@@ -744,46 +805,177 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
             }
         }
     };
+    long long epi_pro = 0, epi_tail = 0;
+    // ---- XPOSE helpers: coalesced order = rows RPI*i + sr (i < NI), 16-byte
+    // chunk ch of a PW-column pass h (NH passes)
+    constexpr int PW = 32, CPR = PW / 4, RPI = 32 / CPR, NI = 32 / RPI, NH = WH / PW;
+    const int sr = lane / CPR, ch = lane % CPR;
+    const uint32_t xb = XPOSE ? smem_u32(xbuf) + ew * (32 * PW * 4) : 0u;
+    auto xaddr = [&](int r, int c) -> uint32_t { return xb + r * (PW * 4) + ((c ^ (r & (CPR - 1))) << 4); };
+    // container offset of output row m*128 + r (kNoCol past the view)
+    auto row_at = [&](uint32_t m, int r) -> uint64_t {
+        const uint64_t gi = (uint64_t)m * kBM + r;
+        if (gi >= p.rows) return kNoCol;
+        return p.off_tables ? __ldg(p.out_rowoff + gi) : rowpart(p.out_i0 + gi, p.out_geom);
+    };
+    // container offset of output column n*W + jb + j; vec: j..j+3 is one aligned
+    // 16-byte run of a tile row
+    auto col_at = [&](uint32_t n, int j, bool& vec) -> uint64_t {
+        const uint64_t gj = (uint64_t)n * W + jb + j;
+        if (gj >= p.cols) {
+            vec = false;
+            return kNoCol;
+        }
+        if (p.off_tables) {
+            const uint64_t c = __ldg(p.out_coloff + gj);
+            const uint64_t c3 = gj + 3 < p.cols ? __ldg(p.out_coloff + gj + 3) : kNoCol;
+            vec = p.vec_ok && c3 == c + 3 && (c & 3) == 0;
+            return c;
+        }
+        uint64_t b, r;
+        tdivmod(p.out_j0 + gj, p.out_geom, b, r);
+        vec = p.vec_ok && (r & 3) == 0 && r + 3 < p.out_geom.t && gj + 3 < p.cols;
+        return dilate32(b) * p.out_geom.tt + r;
+    };
+    // edge path (a lane whose 4-column run is not one aligned 16-byte run): the
+    // pass's rows element by element, staged through the transpose buffer
+    auto edge_load = [&](uint32_t m, uint32_t n, int h) {
+#pragma unroll 1
+        for (int i = 0; i < NI; ++i) {
+            const uint64_t rb = row_at(m, quad * 32 + RPI * i + sr);
+            const uint32_t dst = xaddr(RPI * i + sr, ch);
+#pragma unroll 1
+            for (int e = 0; e < 4; ++e) {
+                bool unused;
+                const uint64_t cc = col_at(n, PW * h + 4 * ch + e, unused);
+                sts32(dst + 4 * e, (rb != kNoCol && cc != kNoCol) ? p.out[rb + cc] : 0u);
+            }
+        }
+    };
+    auto edge_store = [&](uint32_t m, uint32_t n, int h) {
+#pragma unroll 1
+        for (int i = 0; i < NI; ++i) {
+            const uint64_t rb = row_at(m, quad * 32 + RPI * i + sr);
+            const uint32_t src = xaddr(RPI * i + sr, ch);
+#pragma unroll 1
+            for (int e = 0; e < 4; ++e) {
+                bool unused;
+                const uint64_t cc = col_at(n, PW * h + 4 * ch + e, unused);
+                if (rb != kNoCol && cc != kNoCol) p.out[rb + cc] = lds32(src + 4 * e);
+            }
+        }
+    };
+    // coalesced C_old loads of `tile` for the vector lanes (no waits; edge
+    // lanes are filled element-wise when the tile is staged)
+    uint4 cold[XPOSE ? NH : 1][XPOSE ? NI : 1];
+    // (always assigns cold -- past the last tile or for SET it is zeros -- so
+    // cold is dead between the staging and the next load)
+    auto load_cold = [&](uint32_t tile) {
+        const bool live = tile < num_tiles && p.mode != 2;
+        uint32_t lm = 0, ln = 0;
+        if (live) tile_coords(tile, row_groups, p.Nt, p.group, lm, ln);
+        const uint64_t own = row_at(lm, row);
+        uint64_t c0[NH];
+        bool vec[NH];
+#pragma unroll
+        for (int h = 0; h < NH; ++h) {
+            c0[h] = col_at(ln, PW * h + 4 * ch, vec[h]);
+            vec[h] = vec[h] && live;
+        }
+#pragma unroll
+        for (int i = 0; i < NI; ++i) {
+            const uint64_t rb = __shfl_sync(0xffffffffu, own, RPI * i + sr);
+#pragma unroll
+            for (int h = 0; h < NH; ++h)
+                cold[h][i] = (vec[h] && rb != kNoCol)
+                                 ? __ldcs(reinterpret_cast<const uint4*>(p.out + rb + c0[h]))
+                                 : make_uint4(0u, 0u, 0u, 0u);
+        }
+    };
+#ifndef MHG_COLD_EARLY
+#define MHG_COLD_EARLY 0
+#endif
+    // MHG_COLD_EARLY: 1 = the next tile's C_old is loaded during this tile's
+    // stores; 0 = each tile loads its own C_old at tile start.  Measured
+    // (profiles/r01_epilogue_ab.txt): 0 is 21% faster at K = 1024.
+    if constexpr (XPOSE && MHG_COLD_EARLY) load_cold(first_tile);
     for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride) {
+        const long long tp0 = clock64();
         uint32_t tm, n;
         tile_coords(tile, row_groups, p.Nt, p.group, tm, n);
         const uint32_t m = PAIR ? 2 * tm + rank : tm;
-        const uint64_t gi = (uint64_t)m * kBM + row;
-        const bool row_ok = gi < p.rows;
-        const uint64_t rbase = row_ok ? __ldg(p.out_rowoff + gi) : 0;
-        epi_bar_sync<EPI_THREADS>();  // previous tile's readers of s_col are done
-        for (int j = ew * 32 + lane; j < W; j += EPI_THREADS) {
-            const uint64_t gj = (uint64_t)n * W + j;
-            s_col[j] = gj < p.cols ? __ldg(p.out_coloff + gj) : kNoCol;
-        }
-        epi_bar_sync<EPI_THREADS>();
-        const uint64_t* col = s_col + jb;
         uint32_t cur[WH];
-        if (p.mode != 2 && row_ok) {
+        uint64_t rbase = 0;
+        bool row_ok = false;
+        const uint64_t* col = s_col + jb;
+        if constexpr (XPOSE) {
+            if (!MHG_COLD_EARLY) load_cold(tile);
+            if (p.mode != 2) {
+                // cold holds this tile's C_old (vector lanes; issued before the
+                // previous tile's stores): per pass stage it in the buffer, fill
+                // the edge lanes, read back in row order
 #pragma unroll
-            for (int g = 0; g < WH / 4; ++g) {
-                const uint64_t c0 = col[4 * g], c3 = col[4 * g + 3];
-                if (p.vec_ok && c3 == c0 + 3 && (c0 & 3) == 0) {
-                    const uint4 v = __ldcs(reinterpret_cast<const uint4*>(p.out + rbase + c0));
-                    cur[4 * g] = v.x;
-                    cur[4 * g + 1] = v.y;
-                    cur[4 * g + 2] = v.z;
-                    cur[4 * g + 3] = v.w;
-                } else {
+                for (int h = 0; h < NH; ++h) {
+                    bool vec;
+                    (void)col_at(n, PW * h + 4 * ch, vec);
+                    if (vec) {
 #pragma unroll
-                    for (int e = 0; e < 4; ++e) {
-                        const uint64_t cc = col[4 * g + e];
-                        cur[4 * g + e] = cc != kNoCol ? p.out[rbase + cc] : 0u;
+                        for (int i = 0; i < NI; ++i) sts128(xaddr(RPI * i + sr, ch), cold[h][i]);
+                    } else {
+                        edge_load(m, n, h);
                     }
+                    __syncwarp();
+#pragma unroll
+                    for (int g = 0; g < CPR; ++g) {
+                        const uint4 v = lds128(xaddr(lane, g));
+                        cur[PW * h + 4 * g] = v.x;
+                        cur[PW * h + 4 * g + 1] = v.y;
+                        cur[PW * h + 4 * g + 2] = v.z;
+                        cur[PW * h + 4 * g + 3] = v.w;
+                    }
+                    __syncwarp();
                 }
+            } else {
+#pragma unroll
+                for (int j = 0; j < WH; ++j) cur[j] = 0u;
             }
         } else {
+            const uint64_t gi = (uint64_t)m * kBM + row;
+            row_ok = gi < p.rows;
+            rbase = row_ok ? __ldg(p.out_rowoff + gi) : 0;
+            epi_bar_sync<EPI_THREADS>();  // previous tile's readers of s_col are done
+            for (int j = ew * 32 + lane; j < W; j += EPI_THREADS) {
+                const uint64_t gj = (uint64_t)n * W + j;
+                s_col[j] = gj < p.cols ? __ldg(p.out_coloff + gj) : kNoCol;
+            }
+            epi_bar_sync<EPI_THREADS>();
+            if (p.mode != 2 && row_ok) {
 #pragma unroll
-            for (int j = 0; j < WH; ++j) cur[j] = 0u;
+                for (int g = 0; g < WH / 4; ++g) {
+                    const uint64_t c0 = col[4 * g], c3 = col[4 * g + 3];
+                    if (p.vec_ok && c3 == c0 + 3 && (c0 & 3) == 0) {
+                        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(p.out + rbase + c0));
+                        cur[4 * g] = v.x;
+                        cur[4 * g + 1] = v.y;
+                        cur[4 * g + 2] = v.z;
+                        cur[4 * g + 3] = v.w;
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const uint64_t cc = col[4 * g + e];
+                            cur[4 * g + e] = cc != kNoCol ? p.out[rbase + cc] : 0u;
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < WH; ++j) cur[j] = 0u;
+            }
         }
+        epi_pro += clock64() - tp0;
         for (uint32_t c = 0; c < nchunks; ++c) {
             const long long w0 = clock64();
-            mbar_wait(tmem_full, acc_ph);
+            mbar_wait_hint(tmem_full, acc_ph, p.wait_hint);
             const long long w1 = clock64();
             epi_wait += w1 - w0;
             tc_fence_after();
@@ -848,7 +1040,31 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
             }
             acc_ph ^= 1;
         }
-        if (row_ok) {
+        const long long tt0 = clock64();
+        if constexpr (XPOSE) {
+            const uint64_t own = row_at(m, row);
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+#pragma unroll
+                for (int g = 0; g < CPR; ++g)
+                    sts128(xaddr(lane, g), make_uint4(cur[PW * h + 4 * g], cur[PW * h + 4 * g + 1],
+                                                      cur[PW * h + 4 * g + 2], cur[PW * h + 4 * g + 3]));
+                __syncwarp();
+                // once the first pass is staged, the next tile's C_old loads go
+                // out and land during the remaining stores
+                if (MHG_COLD_EARLY && h == 0) load_cold(tile + tile_stride);
+                bool vec;
+                const uint64_t c0 = col_at(n, PW * h + 4 * ch, vec);
+#pragma unroll
+                for (int i = 0; i < NI; ++i) {
+                    const uint64_t rb = __shfl_sync(0xffffffffu, own, RPI * i + sr);
+                    if (vec && rb != kNoCol)
+                        __stcs(reinterpret_cast<uint4*>(p.out + rb + c0), lds128(xaddr(RPI * i + sr, ch)));
+                }
+                if (!vec) edge_store(m, n, h);
+                __syncwarp();
+            }
+        } else if (row_ok) {
 #pragma unroll
             for (int g = 0; g < WH / 4; ++g) {
                 const uint64_t c0 = col[4 * g], c3 = col[4 * g + 3];
@@ -864,10 +1080,14 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
                 }
             }
         }
+        epi_tail += clock64() - tt0;
     }
     if (p.stats && warp == 2 && lane == 0) {
         p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiWaitFull] = epi_wait;
         p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiBusy] = epi_busy;
+        p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiPrologue] = epi_pro;
+        p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiTail] = epi_tail;
+        p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiLdWait] = epi_ldw;
     }
 }
 
@@ -886,7 +1106,8 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
     uint64_t* tmem_full = empty + STAGES;
     uint64_t* tmem_empty = tmem_full + 1;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
-    uint64_t* s_col = tmem_empty + 2;  // W column offsets of the current tile
+    uint64_t* s_col = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE + 256);  // W column offsets
+    uint8_t* xbuf = reinterpret_cast<uint8_t*>(s_col + W);  // per-warp C transpose buffers
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t num_tiles = p.Mt * p.Nt;
@@ -932,7 +1153,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
                 for (uint32_t j = 0; j < p.Kt; ++j) {
                     const uint32_t kt = rev ? p.Kt - 1 - j : j;
                     const long long w0 = clock64();
-                    mbar_wait(&empty[st], ph ^ 1);
+                    mbar_wait_hint(&empty[st], ph ^ 1, p.wait_hint);
                     wait_empty += clock64() - w0;
                     mbar_expect_tx(&full[st], Cfg::STAGE);
                     if (p.l2_hints) {
@@ -972,12 +1193,12 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
                     const uint32_t kb = c * p.KC;
                     const uint32_t ke = (kb + p.KC < p.Kt) ? kb + p.KC : p.Kt;
                     long long w0 = clock64();
-                    mbar_wait(tmem_empty, acc_ph ^ 1);
+                    mbar_wait_hint(tmem_empty, acc_ph ^ 1, p.wait_hint);
                     wait_tmem += clock64() - w0;
                     tc_fence_after();
                     for (uint32_t kt = kb; kt < ke; ++kt) {
                         w0 = clock64();
-                        mbar_wait(&full[st], ph);
+                        mbar_wait_hint(&full[st], ph, p.wait_hint);
                         wait_full += clock64() - w0;
                         tc_fence_after();
                         const uint32_t a0 = smem_u32(sA + st * Cfg::A_STAGE);
@@ -1023,9 +1244,9 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
             }
         }
     } else {
-        epilogue_role<L, W, Cfg::EPI_WARPS, false>(p, blockIdx.x, gridDim.x, num_tiles, p.Mt, 0,
-                                                   nchunks, tmem, s_col, tmem_full, tmem_empty,
-                                                   warp, lane);
+        epilogue_role<L, W, Cfg::EPI_WARPS, false, Cfg::XPOSE>(p, blockIdx.x, gridDim.x, num_tiles,
+                                                               p.Mt, 0, nchunks, tmem, s_col, tmem_full,
+                                                               tmem_empty, warp, lane, xbuf);
     }
 
     __syncthreads();
@@ -1248,8 +1469,9 @@ int configure_gemm2_t() {
 
 template <int L>
 int configure_gemm_t() {
-    return (int)cudaFuncSetAttribute(k_gemm<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     GemmCfg<L>::SMEM);
+    int e = (int)cudaFuncSetAttribute(k_gemm<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      GemmCfg<L>::SMEM);
+    return e;
 }
 
 // Writes `value` into every cell of a view (SET with an empty inner dimension).
