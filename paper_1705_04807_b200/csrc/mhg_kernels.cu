@@ -18,6 +18,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "mhg_internal.hpp"
@@ -90,6 +91,45 @@ __global__ void k_rm_to_mh(const uint32_t* __restrict__ rm, uint32_t* __restrict
             const uint32_t v = rm[x];
             saw_bad |= v >= q;
             mh[rowpart(i, g) + colpart(j, g)] = v;
+        }
+    }
+    if (saw_bad) atomicOr(bad, 1);
+}
+
+// Inverse of dilate32 on the even bits: compact(dilate32(x)) == x.
+__device__ __forceinline__ uint32_t compact32(uint64_t x) {
+    x &= 0x5555555555555555ull;
+    x = (x | (x >> 1)) & 0x3333333333333333ull;
+    x = (x | (x >> 2)) & 0x0f0f0f0f0f0f0f0full;
+    x = (x | (x >> 4)) & 0x00ff00ff00ff00ffull;
+    x = (x | (x >> 8)) & 0x0000ffff0000ffffull;
+    x = (x | (x >> 16)) & 0x00000000ffffffffull;
+    return (uint32_t)x;
+}
+
+// K1 in Morton order (power-of-two t, t % 4 == 0): thread x owns the 16-byte
+// group at Morton offset 4x, so the Morton side is one contiguous stream and
+// the row-major side moves t*4-byte row runs; no divisions.  to_mh = 1:
+// row-major -> Morton (+ residue check), 0: Morton -> row-major.
+__global__ void k_conv_z(const uint32_t* __restrict__ src, uint32_t* __restrict__ dst, uint64_t n,
+                         TileGeom g, uint32_t q, int* __restrict__ bad, int to_mh) {
+    const uint64_t groups = n * n / 4;
+    const int sh = g.shift;
+    int saw_bad = 0;
+    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < groups;
+         x += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t z = 4 * x;
+        const uint64_t tile = z >> (2 * sh);
+        const uint64_t rem = z & (g.tt - 1);
+        const uint64_t i = ((uint64_t)compact32(tile >> 1) << sh) + (rem >> sh);
+        const uint64_t j = ((uint64_t)compact32(tile) << sh) + (rem & (g.t - 1));
+        const uint64_t r = i * n + j;
+        if (to_mh) {
+            const uint4 v = __ldcs(reinterpret_cast<const uint4*>(src + r));
+            saw_bad |= (v.x >= q) | (v.y >= q) | (v.z >= q) | (v.w >= q);
+            __stcs(reinterpret_cast<uint4*>(dst) + x, v);
+        } else {
+            __stcs(reinterpret_cast<uint4*>(dst + r), __ldcs(reinterpret_cast<const uint4*>(src) + x));
         }
     }
     if (saw_bad) atomicOr(bad, 1);
@@ -467,6 +507,14 @@ __device__ __forceinline__ void tmem_wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// Orders every later use of v after the preceding tcgen05.wait::ld: the empty
+// volatile asms "rewrite" the registers and cannot move above the wait.
+template <int N>
+__device__ __forceinline__ void reg_fence(int32_t (&v)[N]) {
+#pragma unroll
+    for (int i = 0; i < N; ++i) asm volatile("" : "+r"(v[i]));
+}
+
 // x mod q for |x| < 2^62 (bias = multiple of q >= 2^62 makes it non-negative)
 __device__ __forceinline__ uint32_t red_signed(int64_t x, const GemmParams& p) {
     const uint64_t u = (uint64_t)x + p.bias;
@@ -584,9 +632,12 @@ struct GemmCfg {
     // two epilogue warps per SMSP, 64 columns each; W = 128 uses the coalesced
     // C path with a 4 KB per-warp transpose buffer, the narrow-tile primes keep
     // row-per-thread C access (see epilogue_role)
+#ifndef MHG_EPI_WARPS
+#define MHG_EPI_WARPS 8
+#endif
     static constexpr bool XPOSE = (W == 128);
-    static constexpr int EPI_WARPS = 8;
-    static constexpr int XBUF = XPOSE ? EPI_WARPS * 4096 : 0;
+    static constexpr int EPI_WARPS = XPOSE ? MHG_EPI_WARPS : 8;
+    static constexpr int XBUF = XPOSE ? EPI_WARPS * (W * 4 / EPI_WARPS >= 64 ? 4096 : 2048) : 0;
     static constexpr int FIXED = 1024 /*align slack*/ + 256 /*barriers*/ + 8 * W /*column offsets*/ + XBUF;
     static constexpr int STAGES_RAW = (232448 - FIXED) / STAGE;
     static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
@@ -715,7 +766,10 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     constexpr int EPI_THREADS = EPI_WARPS * 32;
     constexpr int WH = W * 4 / EPI_WARPS;  // columns per epilogue warp
     constexpr int CLASSES = 2 * L - 1;
-    constexpr int CW = L <= 2 ? 16 : 8;  // TMEM columns per drain step (register budget)
+#ifndef MHG_CW
+#define MHG_CW 16
+#endif
+    constexpr int CW = L <= 2 ? MHG_CW : 8;  // TMEM columns per drain step (register budget)
     constexpr uint64_t kNoCol = ~uint64_t(0);
     const int ew = warp - 2;
     const int quad = warp & 3;
@@ -741,8 +795,70 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     // bias + 256 r1 (unreduced, < 2^32 - 2^24) -- release, then class 2:
     // cur = red(cur + w16 r2).  Every class sum is within 2^31 - 2^17 (class 0
     // and class 2 within 2^30), so no step wraps 32 bits.
+#ifndef MHG_DRAIN_PIPE
+#define MHG_DRAIN_PIPE 0
+#endif
     auto drain_l2_small = [&](uint32_t tbase, uint32_t n_tile, uint32_t* cur_, uint32_t layout) {
         const int lo_cls = layout ? 0 : 1;  // first group: {lo_cls, lo_cls + 1}
+        if constexpr (MHG_DRAIN_PIPE != 0) {
+            // software-pipelined: the TMEM loads of step t+1 are in flight while
+            // step t folds (columns past the view are folded too, never stored)
+            constexpr int NS = WH / CW;
+            int32_t a[2][2][CW];
+            tmem_ld<CW>(tbase + lo_cls * W, a[0][0]);
+            tmem_ld<CW>(tbase + (lo_cls + 1) * W, a[0][1]);
+            tmem_wait_ld();
+            reg_fence(a[0][0]);
+            reg_fence(a[0][1]);
+#pragma unroll
+            for (int t = 0; t < NS; ++t) {
+                if (t + 1 < NS) {
+                    tmem_ld<CW>(tbase + lo_cls * W + (t + 1) * CW, a[(t + 1) & 1][0]);
+                    tmem_ld<CW>(tbase + (lo_cls + 1) * W + (t + 1) * CW, a[(t + 1) & 1][1]);
+                }
+#pragma unroll
+                for (int j = 0; j < CW; ++j) {
+                    const int32_t* x = a[t & 1][0];
+                    const int32_t* y = a[t & 1][1];
+                    const uint32_t r1 = red32((uint32_t)(layout ? y[j] : x[j]) + p.bias32, p);
+                    if (layout == 0) {
+                        const uint32_t r2 = red32((uint32_t)y[j] + p.bias32, p);
+                        cur_[t * CW + j] += (r1 << 8) + p.w16 * r2;
+                    } else {
+                        cur_[t * CW + j] += (uint32_t)x[j] + p.bias32 + (r1 << 8);
+                    }
+                }
+                if (t + 1 < NS) {
+                    tmem_wait_ld();
+                    reg_fence(a[(t + 1) & 1][0]);
+                    reg_fence(a[(t + 1) & 1][1]);
+                }
+            }
+            release();
+            int32_t b[2][CW];
+            tmem_ld<CW>(tbase + (layout ? 2 : 0) * W, b[0]);
+            tmem_wait_ld();
+            reg_fence(b[0]);
+#pragma unroll
+            for (int t = 0; t < NS; ++t) {
+                if (t + 1 < NS) tmem_ld<CW>(tbase + (layout ? 2 : 0) * W + (t + 1) * CW, b[(t + 1) & 1]);
+#pragma unroll
+                for (int j = 0; j < CW; ++j) {
+                    const int32_t v = b[t & 1][j];
+                    if (layout == 0) {
+                        cur_[t * CW + j] = red32(cur_[t * CW + j] + (uint32_t)v + p.bias32, p);
+                    } else {
+                        const uint32_t r2 = red32((uint32_t)v + p.bias32, p);
+                        cur_[t * CW + j] = red32(cur_[t * CW + j] + p.w16 * r2, p);
+                    }
+                }
+                if (t + 1 < NS) {
+                    tmem_wait_ld();
+                    reg_fence(b[(t + 1) & 1]);
+                }
+            }
+            return;
+        }
 #pragma unroll
         for (int j0 = 0; j0 < WH; j0 += CW) {
             if ((uint64_t)n_tile * W + jb + j0 >= p.cols) continue;  // warp-uniform
@@ -808,10 +924,15 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     long long epi_pro = 0, epi_tail = 0;
     // ---- XPOSE helpers: coalesced order = rows RPI*i + sr (i < NI), 16-byte
     // chunk ch of a PW-column pass h (NH passes)
-    constexpr int PW = 32, CPR = PW / 4, RPI = 32 / CPR, NI = 32 / RPI, NH = WH / PW;
+    constexpr int PW = WH >= 64 ? 32 : 16, CPR = PW / 4, RPI = 32 / CPR, NI = 32 / RPI, NH = WH / PW;
     const int sr = lane / CPR, ch = lane % CPR;
     const uint32_t xb = XPOSE ? smem_u32(xbuf) + ew * (32 * PW * 4) : 0u;
-    auto xaddr = [&](int r, int c) -> uint32_t { return xb + r * (PW * 4) + ((c ^ (r & (CPR - 1))) << 4); };
+    // chunk swizzle: 8 chunks per row -> c ^ r%8; 4 chunks -> c ^ (r/2)%4 (each
+    // 8-lane phase of a 16-byte access hits 8 distinct bank groups in both orders)
+    auto xaddr = [&](int r, int c) -> uint32_t {
+        const int sw = CPR == 8 ? (r & 7) : ((r >> 1) & 3);
+        return xb + r * (PW * 4) + ((c ^ sw) << 4);
+    };
     // container offset of output row m*128 + r (kNoCol past the view)
     auto row_at = [&](uint32_t m, int r) -> uint64_t {
         const uint64_t gi = (uint64_t)m * kBM + r;
@@ -1519,14 +1640,31 @@ int launch_offsets(uint64_t* dst, uint64_t start, uint64_t count, TileGeom g, in
     return (int)cudaGetLastError();
 }
 
+// Conversion direction choice (measured, profiles/r01_conversion.txt): the
+// Morton-order kernel for row-major -> Morton (contiguous Morton writes, 0.73
+// of HBM vs 0.68), the row-major-order kernel for Morton -> row-major
+// (contiguous row-major writes, 0.86 vs 0.74).  MHG_CONV: 0 both row-order,
+// 2 both Morton-order (A/B only).
+static int conv_mode() {
+    static const int mode = [] {
+        const char* e = std::getenv("MHG_CONV");
+        return e ? std::atoi(e) : 1;
+    }();
+    return mode;
+}
+
 int launch_rm_to_mh(const uint32_t* rm, uint32_t* mh, uint64_t n, TileGeom g, uint32_t q,
                     int* bad_flag, void* stream) {
-    k_rm_to_mh<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(rm, mh, n, g, q, bad_flag);
+    const bool z = g.shift >= 0 && g.t % 4 == 0 && conv_mode() >= 1;
+    if (z) k_conv_z<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(rm, mh, n, g, q, bad_flag, 1);
+    else k_rm_to_mh<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(rm, mh, n, g, q, bad_flag);
     return (int)cudaGetLastError();
 }
 
 int launch_mh_to_rm(const uint32_t* mh, uint32_t* rm, uint64_t n, TileGeom g, void* stream) {
-    k_mh_to_rm<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(mh, rm, n, g);
+    const bool z = g.shift >= 0 && g.t % 4 == 0 && conv_mode() >= 2;
+    if (z) k_conv_z<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(mh, rm, n, g, 0u, nullptr, 0);
+    else k_mh_to_rm<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(mh, rm, n, g);
     return (int)cudaGetLastError();
 }
 

@@ -81,6 +81,22 @@ def test_random_misaligned_views(gpu, mh, oracle, q, op):
         assert np.array_equal(got, want), (n, t, q, op, v)
 
 
+@pytest.mark.parametrize("n,t", [(48, 3), (96, 6), (192, 12), (64, 2), (320, 10), (384, 24)])
+def test_non_power_of_two_tiles(gpu, mh, oracle, n, t):
+    """Tile sides that are not powers of two (layout_test.cpp:23 allows them):
+    the in-kernel Morton offsets take the division path, and t % 4 != 0 forces
+    the element-wise epilogue edge path for every output."""
+    rng = np.random.default_rng(n * 31 + t)
+    for it, (q, op) in enumerate([(P16, OP_SUB), (97, OP_ADD), (P31, OP_SET), (P24, OP_SUB)]):
+        r, k, c, corners = _random_views(rng, n)
+        v = _views_from(oracle, n, t, r, k, c, corners)
+        out, lhs, rhs = _fill(oracle, 2000 + it, n, q)
+        got, _ = _run_gpu(mh, n, t, q, out, lhs, rhs, v, op)
+        want = out.copy()
+        oracle.mm_dense(n, t, q, want, lhs, rhs, v, op=op)
+        assert np.array_equal(got, want), (n, t, q, op, v)
+
+
 def test_reference_acceptance_instances(gpu, mh, oracle, reference):
     """acceptance_main.cpp:177-217 protocol: gen_problem draws, out += lhs*rhs,
     whole container equal to the reference's mm_oblivious, Counters equal."""
