@@ -239,8 +239,6 @@ mhg::GemmParams gemm_params(const Buffers& b, const mhg_view& out, const Checked
     if (const char* rg = std::getenv("MHG_RING")) p.ring = std::atoi(rg);
     p.early_release = 1;
     if (const char* er = std::getenv("MHG_EARLY_RELEASE")) p.early_release = std::atoi(er) != 0;
-    p.off_tables = 0;
-    if (const char* ot = std::getenv("MHG_OFFTAB")) p.off_tables = std::atoi(ot) != 0;
     p.wait_hint = 0;
     if (const char* wh = std::getenv("MHG_WAIT_HINT")) p.wait_hint = (uint32_t)std::atoi(wh);
     p.l2_hints = 1;  // measured: -1.3% (n=16384), -2% (n=32768)
@@ -367,14 +365,15 @@ void launch_multiply(const Buffers& b, const mhg_view& out, const mhg_view& lhs,
         }
         tot = s[mhg::kStatTotal] / (issuers ? issuers : 1);
         for (int k : {1, 2}) s[k] /= (issuers ? issuers : 1);
-        for (int k : {3, 4, 5, 6, 7, 8}) s[k] /= n;
+        for (int k : {3, 4, 5, 6, 7, 8, 9, 10}) s[k] /= n;
         std::fprintf(stderr,
                      "[mhg stats] L=%u tiles=%u  MMA wait(full)=%.1f%%  MMA wait(tmem_empty)=%.1f%%  "
                      "producer wait(empty)=%.1f%%  epilogue wait(tmem_full)=%.1f%%  epilogue busy=%.1f%%  "
-                     "epilogue prologue=%.1f%%  epilogue stores=%.1f%%  tmem ld wait=%.1f%%  "
+                     "epilogue prologue=%.1f%% (issue %.1f%%, C_old landing %.1f%%)  epilogue stores=%.1f%%  "
+                     "tmem ld wait=%.1f%%  "
                      "(cycles per MMA issuer %.3g, %s)\n",
                      g.L, g.Mt * g.Nt, 100 * s[1] / tot, 100 * s[2] / tot, 100 * s[3] / tot,
-                     100 * s[4] / tot, 100 * s[5] / tot, 100 * s[6] / tot, 100 * s[7] / tot, 100 * s[8] / tot, tot,
+                     100 * s[4] / tot, 100 * s[5] / tot, 100 * s[6] / tot, 100 * s[9] / tot, 100 * s[10] / tot, 100 * s[7] / tot, 100 * s[8] / tot, tot,
                      g.pair ? "cta pair" : "1 cta");
     }
 }

@@ -74,14 +74,14 @@ struct GemmParams {
     int l2_hints;                // evict_last for lhs stages, evict_first for rhs stages
     int ring;                    // pipeline stages in use (0 = all); diagnostics
     int early_release;           // alternate TMEM bases and release before the last class group
-    int off_tables;              // epilogue output offsets from the tables (1) or computed (0)
     uint32_t wait_hint;          // mbarrier try_wait suspend-time hint, ns (k_gemm roles)
     unsigned long long* stats;   // optional per-CTA wait-cycle counters (diagnostics), or null
 };
 
 // k_gemm diagnostics layout (per CTA, when GemmParams::stats != null)
 enum GemmStat { kStatTotal = 0, kStatMmaWaitFull, kStatMmaWaitTmem, kStatProdWaitEmpty,
-                kStatEpiWaitFull, kStatEpiBusy, kStatEpiPrologue, kStatEpiTail, kStatEpiLdWait, kStatCount };
+                kStatEpiWaitFull, kStatEpiBusy, kStatEpiPrologue, kStatEpiTail, kStatEpiLdWait, kStatEpiIssue,
+                kStatEpiLand, kStatCount };
 
 // --------------------------------------------------------------- launchers
 // All asynchronous on `stream`; return a cudaError_t value (0 = success).

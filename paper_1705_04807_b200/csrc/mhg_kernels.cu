@@ -360,6 +360,40 @@ __device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity, u
         : "memory");
 }
 
+// global C_old / C accesses of the coalesced epilogue (cache-hint variants:
+// MHG_CHINT 0 = .cs streaming, 1 = default caching, 2 = L1 no-allocate loads)
+#ifndef MHG_CHINT
+#define MHG_CHINT 0
+#endif
+__device__ __forceinline__ uint4 c_load(const uint4* a) {
+    if constexpr (MHG_CHINT == 0) return __ldcs(a);
+    else if constexpr (MHG_CHINT == 1) return *a;
+    else {
+        uint4 v;
+        asm volatile("ld.global.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                     : "l"(a));
+        return v;
+    }
+}
+
+// Predicated streaming 16-byte load straight into v (left unchanged when
+// !pred).  Written as one predicated PTX load so that no register move -- which
+// would wait for the data -- follows it: all of a tile's C_old loads go out
+// back to back.
+__device__ __forceinline__ void c_load_pred(uint4& v, const uint32_t* a, bool pred) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "@p ld.global.cs.v4.u32 {%0, %1, %2, %3}, [%5];\n\t}"
+        : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
+        : "r"((uint32_t)pred), "l"(a));
+}
+
+__device__ __forceinline__ void c_store(uint4* a, uint4 v) {
+    if constexpr (MHG_CHINT == 0) __stcs(a, v);
+    else *a = v;
+}
+
 __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
                  "r"(v.w)
@@ -921,7 +955,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
             }
         }
     };
-    long long epi_pro = 0, epi_tail = 0;
+    long long epi_pro = 0, epi_tail = 0, epi_issue = 0, epi_land = 0;
     // ---- XPOSE helpers: coalesced order = rows RPI*i + sr (i < NI), 16-byte
     // chunk ch of a PW-column pass h (NH passes)
     constexpr int PW = WH >= 64 ? 32 : 16, CPR = PW / 4, RPI = 32 / CPR, NI = 32 / RPI, NH = WH / PW;
@@ -936,8 +970,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     // container offset of output row m*128 + r (kNoCol past the view)
     auto row_at = [&](uint32_t m, int r) -> uint64_t {
         const uint64_t gi = (uint64_t)m * kBM + r;
-        if (gi >= p.rows) return kNoCol;
-        return p.off_tables ? __ldg(p.out_rowoff + gi) : rowpart(p.out_i0 + gi, p.out_geom);
+        return gi < p.rows ? rowpart(p.out_i0 + gi, p.out_geom) : kNoCol;
     };
     // container offset of output column n*W + jb + j; vec: j..j+3 is one aligned
     // 16-byte run of a tile row
@@ -946,12 +979,6 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         if (gj >= p.cols) {
             vec = false;
             return kNoCol;
-        }
-        if (p.off_tables) {
-            const uint64_t c = __ldg(p.out_coloff + gj);
-            const uint64_t c3 = gj + 3 < p.cols ? __ldg(p.out_coloff + gj + 3) : kNoCol;
-            vec = p.vec_ok && c3 == c + 3 && (c & 3) == 0;
-            return c;
         }
         uint64_t b, r;
         tdivmod(p.out_j0 + gj, p.out_geom, b, r);
@@ -989,6 +1016,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     // coalesced C_old loads of `tile` for the vector lanes (no waits; edge
     // lanes are filled element-wise when the tile is staged)
     uint4 cold[XPOSE ? NH : 1][XPOSE ? NI : 1];
+    uint32_t cmask = 0;  // bit h*NI+i: cold[h][i] holds real data
     // (always assigns cold -- past the last tile or for SET it is zeros -- so
     // cold is dead between the staging and the next load)
     auto load_cold = [&](uint32_t tile) {
@@ -1003,14 +1031,19 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
             c0[h] = col_at(ln, PW * h + 4 * ch, vec[h]);
             vec[h] = vec[h] && live;
         }
+        cmask = 0;
 #pragma unroll
         for (int i = 0; i < NI; ++i) {
             const uint64_t rb = __shfl_sync(0xffffffffu, own, RPI * i + sr);
 #pragma unroll
-            for (int h = 0; h < NH; ++h)
-                cold[h][i] = (vec[h] && rb != kNoCol)
-                                 ? __ldcs(reinterpret_cast<const uint4*>(p.out + rb + c0[h]))
-                                 : make_uint4(0u, 0u, 0u, 0u);
+            for (int h = 0; h < NH; ++h) {
+                // unconditional load (a dead lane reads cell 0 and is masked when
+                // staged): a predicated load would be followed by register moves
+                // that wait for it, serialising the loads
+                const bool ok = vec[h] && rb != kNoCol;
+                cmask |= (uint32_t)ok << (h * NI + i);
+                cold[h][i] = c_load(reinterpret_cast<const uint4*>(p.out + (ok ? rb + c0[h] : 0)));
+            }
         }
     };
 #ifndef MHG_COLD_EARLY
@@ -1031,6 +1064,8 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         const uint64_t* col = s_col + jb;
         if constexpr (XPOSE) {
             if (!MHG_COLD_EARLY) load_cold(tile);
+            const long long ta = clock64();
+            epi_issue += ta - tp0;
             if (p.mode != 2) {
                 // cold holds this tile's C_old (vector lanes; issued before the
                 // previous tile's stores): per pass stage it in the buffer, fill
@@ -1041,10 +1076,14 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
                     (void)col_at(n, PW * h + 4 * ch, vec);
                     if (vec) {
 #pragma unroll
-                        for (int i = 0; i < NI; ++i) sts128(xaddr(RPI * i + sr, ch), cold[h][i]);
+                        for (int i = 0; i < NI; ++i)
+                            sts128(xaddr(RPI * i + sr, ch), ((cmask >> (h * NI + i)) & 1u)
+                                                                ? cold[h][i]
+                                                                : make_uint4(0u, 0u, 0u, 0u));
                     } else {
                         edge_load(m, n, h);
                     }
+                    if (h == 0) epi_land += clock64() - ta;
                     __syncwarp();
 #pragma unroll
                     for (int g = 0; g < CPR; ++g) {
@@ -1180,7 +1219,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
                 for (int i = 0; i < NI; ++i) {
                     const uint64_t rb = __shfl_sync(0xffffffffu, own, RPI * i + sr);
                     if (vec && rb != kNoCol)
-                        __stcs(reinterpret_cast<uint4*>(p.out + rb + c0), lds128(xaddr(RPI * i + sr, ch)));
+                        c_store(reinterpret_cast<uint4*>(p.out + rb + c0), lds128(xaddr(RPI * i + sr, ch)));
                 }
                 if (!vec) edge_store(m, n, h);
                 __syncwarp();
@@ -1209,6 +1248,8 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiPrologue] = epi_pro;
         p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiTail] = epi_tail;
         p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiLdWait] = epi_ldw;
+        p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiIssue] = epi_issue;
+        p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiLand] = epi_land;
     }
 }
 
