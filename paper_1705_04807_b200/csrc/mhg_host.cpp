@@ -233,6 +233,9 @@ mhg::GemmParams gemm_params(const Buffers& b, const mhg_view& out, const Checked
     p.bias32 = (uint32_t)(((uint64_t(1) << 31) / q) * q);
     p.w16 = (uint32_t)((uint64_t(1) << 16) % q);
     p.w16_small = p.w16 < 256;
+    // single-reduction fold when every exact chunk is short enough (TU regime)
+    p.fold_short = g.L == 2 && mhg::fold_short_ok(q, (uint64_t)std::min(g.Kt, g.KC) * mhg::kBK);
+    if (const char* fs = std::getenv("MHG_FOLD_SHORT")) p.fold_short = p.fold_short && std::atoi(fs) != 0;
     p.group = 8;  // measured best at the power cap (profiles/r01_raster_groups.txt)
     p.serpentine = 1;
     p.ring = 0;

@@ -67,6 +67,7 @@ struct GemmParams {
     uint32_t bias32;             // q * floor(2^31 / q): a_c + bias32 in [0, 2^32)
     uint32_t w16;                // 2^16 mod q
     int w16_small;               // w16 < 256: fold the top class without a mulmod
+    int fold_short;              // L = 2, w16_small: one reduction per element (chunk K bound, host)
     int mode;                    // 0: out += prod, 2: out = prod (first chunk)
     int vec_ok;                  // t % 4 == 0: 16-byte epilogue accesses allowed
     uint32_t group;              // raster: row tiles per group sharing rhs panels in L2

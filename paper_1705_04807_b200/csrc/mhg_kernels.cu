@@ -790,7 +790,7 @@ __device__ __forceinline__ void tmem_wait_st() {
 // geometry (no table loads).  Otherwise (narrow tiles, CTA pair) the row's
 // C_old is prefetched into registers at tile start, addressed through smem
 // column offsets.
-template <int L, int W, int EPI_WARPS, bool PAIR, bool XPOSE = false>
+template <int L, int W, int EPI_WARPS, bool PAIR, bool XPOSE = false, bool FOLD_SHORT = false>
 __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t first_tile,
                                               uint32_t tile_stride, uint32_t num_tiles,
                                               uint32_t row_groups, uint32_t rank, uint32_t nchunks,
@@ -832,6 +832,37 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
 #ifndef MHG_DRAIN_PIPE
 #define MHG_DRAIN_PIPE 0
 #endif
+    // Per-element folds of the two class groups.  Default (any chunk size):
+    // reduce each class before combining (three reductions per element).
+    // fold_short (planner, GemmParams::fold_short): with a1 = 256 a1h + a1l
+    // (a1l the low byte), 256 a1 == 256 a1l + w16 a1h (mod q), so
+    //   S == a0 + 256 a1l + w16 (a1h + a2)   (mod q)
+    // stays within +-(2^31 - 2^17) for the chunk's K (host-checked bound) and
+    // one reduction per element suffices.
+    auto fold_g1 = [&](int32_t x, int32_t y, uint32_t layout) -> uint32_t {
+        if constexpr (FOLD_SHORT) {
+            // layout 0: x = a1, y = a2; layout 1: x = a0, y = a1
+            if (layout == 0)
+                return (((uint32_t)x & 0xffu) << 8) + p.w16 * (uint32_t)((x >> 8) + y);
+            return (uint32_t)x + (((uint32_t)y & 0xffu) << 8) + p.w16 * (uint32_t)(y >> 8);
+        }
+        const uint32_t r1 = red32((uint32_t)(layout ? y : x) + p.bias32, p);
+        if (layout == 0) {
+            const uint32_t r2 = red32((uint32_t)y + p.bias32, p);
+            return (r1 << 8) + p.w16 * r2;
+        }
+        return (uint32_t)x + p.bias32 + (r1 << 8);
+    };
+    auto fold_g2 = [&](uint32_t c, int32_t z, uint32_t layout) -> uint32_t {
+        // layout 0: z = a0; layout 1: z = a2
+        if constexpr (FOLD_SHORT) {
+            if (layout == 0) return red32(c + (uint32_t)z + p.bias32, p);
+            return red32(c + p.w16 * (uint32_t)z + p.bias32, p);
+        }
+        if (layout == 0) return red32(c + (uint32_t)z + p.bias32, p);
+        const uint32_t r2 = red32((uint32_t)z + p.bias32, p);
+        return red32(c + p.w16 * r2, p);
+    };
     auto drain_l2_small = [&](uint32_t tbase, uint32_t n_tile, uint32_t* cur_, uint32_t layout) {
         const int lo_cls = layout ? 0 : 1;  // first group: {lo_cls, lo_cls + 1}
         if constexpr (MHG_DRAIN_PIPE != 0) {
@@ -851,17 +882,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
                     tmem_ld<CW>(tbase + (lo_cls + 1) * W + (t + 1) * CW, a[(t + 1) & 1][1]);
                 }
 #pragma unroll
-                for (int j = 0; j < CW; ++j) {
-                    const int32_t* x = a[t & 1][0];
-                    const int32_t* y = a[t & 1][1];
-                    const uint32_t r1 = red32((uint32_t)(layout ? y[j] : x[j]) + p.bias32, p);
-                    if (layout == 0) {
-                        const uint32_t r2 = red32((uint32_t)y[j] + p.bias32, p);
-                        cur_[t * CW + j] += (r1 << 8) + p.w16 * r2;
-                    } else {
-                        cur_[t * CW + j] += (uint32_t)x[j] + p.bias32 + (r1 << 8);
-                    }
-                }
+                for (int j = 0; j < CW; ++j) cur_[t * CW + j] += fold_g1(a[t & 1][0][j], a[t & 1][1][j], layout);
                 if (t + 1 < NS) {
                     tmem_wait_ld();
                     reg_fence(a[(t + 1) & 1][0]);
@@ -877,15 +898,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
             for (int t = 0; t < NS; ++t) {
                 if (t + 1 < NS) tmem_ld<CW>(tbase + (layout ? 2 : 0) * W + (t + 1) * CW, b[(t + 1) & 1]);
 #pragma unroll
-                for (int j = 0; j < CW; ++j) {
-                    const int32_t v = b[t & 1][j];
-                    if (layout == 0) {
-                        cur_[t * CW + j] = red32(cur_[t * CW + j] + (uint32_t)v + p.bias32, p);
-                    } else {
-                        const uint32_t r2 = red32((uint32_t)v + p.bias32, p);
-                        cur_[t * CW + j] = red32(cur_[t * CW + j] + p.w16 * r2, p);
-                    }
-                }
+                for (int j = 0; j < CW; ++j) cur_[t * CW + j] = fold_g2(cur_[t * CW + j], b[t & 1][j], layout);
                 if (t + 1 < NS) {
                     tmem_wait_ld();
                     reg_fence(b[(t + 1) & 1]);
@@ -903,15 +916,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
             tmem_wait_ld();
             epi_ldw += clock64() - l0;
 #pragma unroll
-            for (int j = 0; j < CW; ++j) {
-                const uint32_t r1 = red32((uint32_t)a[layout ? 1 : 0][j] + p.bias32, p);
-                if (layout == 0) {
-                    const uint32_t r2 = red32((uint32_t)a[1][j] + p.bias32, p);
-                    cur_[j0 + j] += (r1 << 8) + p.w16 * r2;
-                } else {
-                    cur_[j0 + j] += (uint32_t)a[0][j] + p.bias32 + (r1 << 8);
-                }
-            }
+            for (int j = 0; j < CW; ++j) cur_[j0 + j] += fold_g1(a[0][j], a[1][j], layout);
         }
         release();
 #pragma unroll
@@ -923,14 +928,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
             tmem_wait_ld();
             epi_ldw += clock64() - l0;
 #pragma unroll
-            for (int j = 0; j < CW; ++j) {
-                if (layout == 0) {
-                    cur_[j0 + j] = red32(cur_[j0 + j] + (uint32_t)a[0][j] + p.bias32, p);
-                } else {
-                    const uint32_t r2 = red32((uint32_t)a[0][j] + p.bias32, p);
-                    cur_[j0 + j] = red32(cur_[j0 + j] + p.w16 * r2, p);
-                }
-            }
+            for (int j = 0; j < CW; ++j) cur_[j0 + j] = fold_g2(cur_[j0 + j], a[0][j], layout);
         }
     };
     // drain weight classes [C0, C1) of this warp's columns and fold them into cur
@@ -1253,7 +1251,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     }
 }
 
-template <int L>
+template <int L, bool FOLD_SHORT = false>
 __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParams p) {
     using Cfg = GemmCfg<L>;
     constexpr int W = Cfg::W;
@@ -1406,7 +1404,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
             }
         }
     } else {
-        epilogue_role<L, W, Cfg::EPI_WARPS, false, Cfg::XPOSE>(p, blockIdx.x, gridDim.x, num_tiles,
+        epilogue_role<L, W, Cfg::EPI_WARPS, false, Cfg::XPOSE, FOLD_SHORT>(p, blockIdx.x, gridDim.x, num_tiles,
                                                                p.Mt, 0, nchunks, tmem, s_col, tmem_full,
                                                                tmem_empty, warp, lane, xbuf);
     }
@@ -1633,6 +1631,11 @@ template <int L>
 int configure_gemm_t() {
     int e = (int)cudaFuncSetAttribute(k_gemm<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       GemmCfg<L>::SMEM);
+    if constexpr (L == 2) {
+        if (!e)
+            e = (int)cudaFuncSetAttribute(k_gemm<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          GemmCfg<L>::SMEM);
+    }
     return e;
 }
 
@@ -1650,6 +1653,12 @@ int launch_gemm_t(const GemmParams& p, int num_sms, cudaStream_t s) {
     using Cfg = GemmCfg<L>;
     const uint32_t tiles = p.Mt * p.Nt;
     const int grid = (int)(tiles < (uint32_t)num_sms ? tiles : (uint32_t)num_sms);
+    if constexpr (L == 2) {
+        if (p.fold_short) {
+            k_gemm<L, true><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p);
+            return (int)cudaGetLastError();
+        }
+    }
     k_gemm<L><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p);
     return (int)cudaGetLastError();
 }

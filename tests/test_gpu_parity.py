@@ -184,6 +184,32 @@ def test_adversarial_extreme_digits(gpu, mh):
                     _constant_case(mh, 1024, 64, q, a, b, q - 1, 1024, op)
 
 
+def _extremes(q):
+    """Residues whose signed representatives have extreme limb digits."""
+    H = min((q - 1) // 2, 127 * 257)
+    return (H, q - H, q - 1, 1, (q + 1) // 2)
+
+
+@pytest.mark.parametrize("q,k", [(65287, 512), (65287, 640), (65519, 1024), (257, 1024)])
+def test_single_reduction_fold_bound(gpu, mh, q, k):
+    """The single-reduction L=2 fold (fold_short) at the edge of its K bound:
+    q = 65287 has 2^16 mod q = 249, so K = 512 is the largest chunk the host
+    admits (K = 640 falls back to the per-class fold); extreme digits, all ops."""
+    ex = _extremes(q)
+    for a in ex:
+        for b in ex[:2]:
+            for op in (OP_ADD, OP_SUB, OP_SET):
+                _constant_case(mh, 1024, 64, q, a, b, q - 1, k, op)
+
+
+@pytest.mark.slow
+def test_single_reduction_fold_at_k8064(gpu, mh):
+    """p = 65521: the largest single-chunk K on the fold_short path (63 k-tiles)."""
+    ex = _extremes(P16)
+    for a, b in [(ex[0], ex[0]), (ex[1], ex[0]), (ex[0], ex[1])]:
+        _constant_case(mh, 8192, 64, P16, a, b, P16 - 1, 8064, OP_SUB)
+
+
 @pytest.mark.slow
 def test_adversarial_int32_headroom(gpu, mh):
     """K = 32768 (cfg5's inner length) with extreme digits: the int32 class
