@@ -127,11 +127,14 @@ def lib():
         "mhg_plan_info": ([vp, P(u64), P(u64), P(u32), P(u32), P(u64)], C.c_int),
         "mhg_plan_destroy": ([vp], C.c_int),
         "mhg_limb_params": ([u32, P(u32), P(u32), P(u64)], C.c_int),
+        "mhg_fold_level": ([u32, u64, P(u32)], C.c_int),
         "mhg_plan_time_gemm": ([vp, C.c_int, vp, P(C.c_float)], C.c_int),
         "mhg_plan_set_profiling": ([vp, C.c_int], C.c_int),
         "mhg_plan_gemm_time": ([vp, P(C.c_float), P(u64)], C.c_int),
     }
     for name, (args, res) in sigs.items():
+        if os.environ.get("MHG_LIB") and not hasattr(L, name):
+            continue  # an older A/B build without this (diagnostic) entry point
         f = getattr(L, name)
         f.argtypes = args
         f.restype = res
@@ -206,6 +209,13 @@ def limb_params(q: int):
     L, H, K = C.c_uint32(), C.c_uint32(), C.c_uint64()
     _check(lib().mhg_limb_params(q, C.byref(L), C.byref(H), C.byref(K)))
     return L.value, H.value, K.value
+
+
+def fold_level(q: int, k_chunk: int) -> int:
+    """Reductions per output the 2-limb epilogue uses for chunks of k_chunk."""
+    lv = C.c_uint32()
+    _check(lib().mhg_fold_level(q, k_chunk, C.byref(lv)))
+    return lv.value
 
 
 def _stream_ptr(stream) -> Optional[int]:

@@ -233,17 +233,21 @@ mhg::GemmParams gemm_params(const Buffers& b, const mhg_view& out, const Checked
     p.bias32 = (uint32_t)(((uint64_t(1) << 31) / q) * q);
     p.w16 = (uint32_t)((uint64_t(1) << 16) % q);
     p.w16_small = p.w16 < 256;
-    // single-reduction fold when every exact chunk is short enough (TU regime)
-    p.fold_short = g.L == 2 && mhg::fold_short_ok(q, (uint64_t)std::min(g.Kt, g.KC) * mhg::kBK);
-    if (const char* fs = std::getenv("MHG_FOLD_SHORT")) p.fold_short = p.fold_short && std::atoi(fs) != 0;
+    // cheapest exact fold for the longest chunk (MHG_FOLD raises the level, A/B only)
+    p.fold = g.L == 2 ? mhg::fold_level(q, (uint64_t)std::min(g.Kt, g.KC) * mhg::kBK) : 3;
+    if (const char* fl = std::getenv("MHG_FOLD")) p.fold = std::max(p.fold, std::min(3, std::atoi(fl)));
     p.group = 8;  // measured best at the power cap (profiles/r01_raster_groups.txt)
     p.serpentine = 1;
     p.ring = 0;
     if (const char* rg = std::getenv("MHG_RING")) p.ring = std::atoi(rg);
     p.early_release = 1;
     if (const char* er = std::getenv("MHG_EARLY_RELEASE")) p.early_release = std::atoi(er) != 0;
-    p.wait_hint = 0;
+    // suspend (instead of re-polling) in mbarrier waits: -1% at n = 16384 / 8192 under the
+    // power cap (profiles/r01_wait_hint.txt); the thread wakes when the phase completes
+    p.wait_hint = 100000;
     if (const char* wh = std::getenv("MHG_WAIT_HINT")) p.wait_hint = (uint32_t)std::atoi(wh);
+    p.wait_roles = 7;
+    if (const char* wr = std::getenv("MHG_WAIT_ROLES")) p.wait_roles = (uint32_t)std::atoi(wr);
     p.l2_hints = 1;  // measured: -1.3% (n=16384), -2% (n=32768)
     if (const char* lh = std::getenv("MHG_L2HINTS")) p.l2_hints = std::atoi(lh) != 0;
     if (const char* sp = std::getenv("MHG_SERPENTINE")) p.serpentine = std::atoi(sp) != 0;
@@ -486,6 +490,15 @@ mhg_status mhg_limb_params(uint32_t q, uint32_t* limbs, uint32_t* threshold, uin
     if (threshold) *threshold = lp.H;
     if (k_max) *k_max = lp.k_max;
     return MHG_OK;
+}
+
+mhg_status mhg_fold_level(uint32_t q, uint64_t k_chunk, uint32_t* level) {
+    mhg_status s = mhg_modulus_check(q);
+    if (s) return s;
+    return guarded([&] {
+        if (!level) fail(MHG_ERR_INVALID_ARGUMENT, "fold_level: null output");
+        *level = mhg::limb_params(q).L == 2 ? (uint32_t)mhg::fold_level(q, k_chunk) : 3u;
+    });
 }
 
 // ------------------------------------------------------------- containers

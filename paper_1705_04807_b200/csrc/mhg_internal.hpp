@@ -67,7 +67,7 @@ struct GemmParams {
     uint32_t bias32;             // q * floor(2^31 / q): a_c + bias32 in [0, 2^32)
     uint32_t w16;                // 2^16 mod q
     int w16_small;               // w16 < 256: fold the top class without a mulmod
-    int fold_short;              // L = 2, w16_small: one reduction per element (chunk K bound, host)
+    int fold;                    // lean L = 2 fold level 3 / 2 / 1 (reductions per element; host)
     int mode;                    // 0: out += prod, 2: out = prod (first chunk)
     int vec_ok;                  // t % 4 == 0: 16-byte epilogue accesses allowed
     uint32_t group;              // raster: row tiles per group sharing rhs panels in L2
@@ -76,6 +76,7 @@ struct GemmParams {
     int ring;                    // pipeline stages in use (0 = all); diagnostics
     int early_release;           // alternate TMEM bases and release before the last class group
     uint32_t wait_hint;          // mbarrier try_wait suspend-time hint, ns (k_gemm roles)
+    uint32_t wait_roles;         // roles using the hint: 1 producer, 2 MMA issuer, 4 epilogue
     unsigned long long* stats;   // optional per-CTA wait-cycle counters (diagnostics), or null
 };
 

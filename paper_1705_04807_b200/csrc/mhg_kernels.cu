@@ -790,7 +790,7 @@ __device__ __forceinline__ void tmem_wait_st() {
 // geometry (no table loads).  Otherwise (narrow tiles, CTA pair) the row's
 // C_old is prefetched into registers at tile start, addressed through smem
 // column offsets.
-template <int L, int W, int EPI_WARPS, bool PAIR, bool XPOSE = false, bool FOLD_SHORT = false>
+template <int L, int W, int EPI_WARPS, bool PAIR, bool XPOSE = false, int FOLD = 3>
 __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t first_tile,
                                               uint32_t tile_stride, uint32_t num_tiles,
                                               uint32_t row_groups, uint32_t rank, uint32_t nchunks,
@@ -832,18 +832,21 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
 #ifndef MHG_DRAIN_PIPE
 #define MHG_DRAIN_PIPE 0
 #endif
-    // Per-element folds of the two class groups.  Default (any chunk size):
-    // reduce each class before combining (three reductions per element).
-    // fold_short (planner, GemmParams::fold_short): with a1 = 256 a1h + a1l
-    // (a1l the low byte), 256 a1 == 256 a1l + w16 a1h (mod q), so
-    //   S == a0 + 256 a1l + w16 (a1h + a2)   (mod q)
-    // stays within +-(2^31 - 2^17) for the chunk's K (host-checked bound) and
-    // one reduction per element suffices.
+    // Per-element folds of the two class groups (lean L = 2 path), by FOLD level
+    // (host-chosen, GemmParams::fold; each level exact for the chunk's K):
+    //   3: reduce every class before combining (three reductions per element);
+    //   2: with a1 = 256 a1h + a1l (a1l the low byte), 256 a1 == 256 a1l + w16 a1h
+    //      (mod q): only a2 is reduced first (two reductions);
+    //   1: a0 + 256 a1l + w16 (a1h + a2) itself stays within 2^31 - 2^17 for
+    //      short chunks (one reduction).
     auto fold_g1 = [&](int32_t x, int32_t y, uint32_t layout) -> uint32_t {
-        if constexpr (FOLD_SHORT) {
-            // layout 0: x = a1, y = a2; layout 1: x = a0, y = a1
-            if (layout == 0)
-                return (((uint32_t)x & 0xffu) << 8) + p.w16 * (uint32_t)((x >> 8) + y);
+        // layout 0: x = a1, y = a2; layout 1: x = a0, y = a1
+        if constexpr (FOLD <= 2) {
+            if (layout == 0) {
+                const uint32_t lo = (((uint32_t)x & 0xffu) << 8);
+                if constexpr (FOLD == 1) return lo + p.w16 * (uint32_t)((x >> 8) + y);
+                return lo + p.w16 * ((uint32_t)(x >> 8) + red32((uint32_t)y + p.bias32, p));
+            }
             return (uint32_t)x + (((uint32_t)y & 0xffu) << 8) + p.w16 * (uint32_t)(y >> 8);
         }
         const uint32_t r1 = red32((uint32_t)(layout ? y : x) + p.bias32, p);
@@ -855,12 +858,10 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     };
     auto fold_g2 = [&](uint32_t c, int32_t z, uint32_t layout) -> uint32_t {
         // layout 0: z = a0; layout 1: z = a2
-        if constexpr (FOLD_SHORT) {
-            if (layout == 0) return red32(c + (uint32_t)z + p.bias32, p);
-            return red32(c + p.w16 * (uint32_t)z + p.bias32, p);
-        }
         if (layout == 0) return red32(c + (uint32_t)z + p.bias32, p);
+        if constexpr (FOLD == 1) return red32(c + p.w16 * (uint32_t)z + p.bias32, p);
         const uint32_t r2 = red32((uint32_t)z + p.bias32, p);
+        if constexpr (FOLD == 2) return red32(c + p.w16 * r2 + p.bias32, p);
         return red32(c + p.w16 * r2, p);
     };
     auto drain_l2_small = [&](uint32_t tbase, uint32_t n_tile, uint32_t* cur_, uint32_t layout) {
@@ -1133,7 +1134,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         epi_pro += clock64() - tp0;
         for (uint32_t c = 0; c < nchunks; ++c) {
             const long long w0 = clock64();
-            mbar_wait_hint(tmem_full, acc_ph, p.wait_hint);
+            mbar_wait_hint(tmem_full, acc_ph, (p.wait_roles & 4) ? p.wait_hint : 0u);
             const long long w1 = clock64();
             epi_wait += w1 - w0;
             tc_fence_after();
@@ -1251,7 +1252,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     }
 }
 
-template <int L, bool FOLD_SHORT = false>
+template <int L, int FOLD = 3>
 __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParams p) {
     using Cfg = GemmCfg<L>;
     constexpr int W = Cfg::W;
@@ -1313,7 +1314,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
                 for (uint32_t j = 0; j < p.Kt; ++j) {
                     const uint32_t kt = rev ? p.Kt - 1 - j : j;
                     const long long w0 = clock64();
-                    mbar_wait_hint(&empty[st], ph ^ 1, p.wait_hint);
+                    mbar_wait_hint(&empty[st], ph ^ 1, (p.wait_roles & 1) ? p.wait_hint : 0u);
                     wait_empty += clock64() - w0;
                     mbar_expect_tx(&full[st], Cfg::STAGE);
                     if (p.l2_hints) {
@@ -1353,12 +1354,12 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
                     const uint32_t kb = c * p.KC;
                     const uint32_t ke = (kb + p.KC < p.Kt) ? kb + p.KC : p.Kt;
                     long long w0 = clock64();
-                    mbar_wait_hint(tmem_empty, acc_ph ^ 1, p.wait_hint);
+                    mbar_wait_hint(tmem_empty, acc_ph ^ 1, (p.wait_roles & 2) ? p.wait_hint : 0u);
                     wait_tmem += clock64() - w0;
                     tc_fence_after();
                     for (uint32_t kt = kb; kt < ke; ++kt) {
                         w0 = clock64();
-                        mbar_wait_hint(&full[st], ph, p.wait_hint);
+                        mbar_wait_hint(&full[st], ph, (p.wait_roles & 2) ? p.wait_hint : 0u);
                         wait_full += clock64() - w0;
                         tc_fence_after();
                         const uint32_t a0 = smem_u32(sA + st * Cfg::A_STAGE);
@@ -1404,7 +1405,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
             }
         }
     } else {
-        epilogue_role<L, W, Cfg::EPI_WARPS, false, Cfg::XPOSE, FOLD_SHORT>(p, blockIdx.x, gridDim.x, num_tiles,
+        epilogue_role<L, W, Cfg::EPI_WARPS, false, Cfg::XPOSE, FOLD>(p, blockIdx.x, gridDim.x, num_tiles,
                                                                p.Mt, 0, nchunks, tmem, s_col, tmem_full,
                                                                tmem_empty, warp, lane, xbuf);
     }
@@ -1633,7 +1634,10 @@ int configure_gemm_t() {
                                       GemmCfg<L>::SMEM);
     if constexpr (L == 2) {
         if (!e)
-            e = (int)cudaFuncSetAttribute(k_gemm<L, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            e = (int)cudaFuncSetAttribute(k_gemm<L, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          GemmCfg<L>::SMEM);
+        if (!e)
+            e = (int)cudaFuncSetAttribute(k_gemm<L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           GemmCfg<L>::SMEM);
     }
     return e;
@@ -1654,8 +1658,9 @@ int launch_gemm_t(const GemmParams& p, int num_sms, cudaStream_t s) {
     const uint32_t tiles = p.Mt * p.Nt;
     const int grid = (int)(tiles < (uint32_t)num_sms ? tiles : (uint32_t)num_sms);
     if constexpr (L == 2) {
-        if (p.fold_short) {
-            k_gemm<L, true><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p);
+        if (p.fold == 1 || p.fold == 2) {
+            if (p.fold == 1) k_gemm<L, 1><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p);
+            else k_gemm<L, 2><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p);
             return (int)cudaGetLastError();
         }
     }

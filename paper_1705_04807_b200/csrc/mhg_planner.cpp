@@ -162,14 +162,18 @@ Counters oblivious_counters(uint64_t n, uint64_t t, const Rect& out, const Rect&
 }
 
 // -------------------------------------------------------------- task grid
-bool fold_short_ok(uint32_t q, uint64_t k_chunk) {
-    if (q < 2 || q > 65536) return false;
+int fold_level(uint32_t q, uint64_t k_chunk) {
+    if (q < 2 || q > 65536) return 3;
     const uint64_t w16 = (uint64_t(1) << 16) % q;
-    if (w16 >= 256) return false;
-    // |a0|, |a2| <= 2^14 k; |a1| <= 2^15 k, so |a1 >> 8| <= 2^7 k; 0 <= a1l <= 255
-    const uint64_t bound = (uint64_t)(q - 1) + (uint64_t(1) << 14) * k_chunk + 255 * 256 +
-                           w16 * ((uint64_t(1) << 7) * k_chunk + (uint64_t(1) << 14) * k_chunk);
-    return bound <= (uint64_t(1) << 31) - (uint64_t(1) << 17);
+    if (w16 >= 256) return 3;
+    // |a0|, |a2| <= 2^14 k; |a1| <= 2^15 k, so |a1 >> 8| <= 2^7 k; 0 <= a1l <= 255;
+    // cur < q before the chunk
+    const uint64_t lim = (uint64_t(1) << 31) - (uint64_t(1) << 17);
+    const uint64_t common = (uint64_t)(q - 1) + (uint64_t(1) << 14) * k_chunk + 255 * 256 +
+                            w16 * ((uint64_t(1) << 7) * k_chunk);
+    if (common + w16 * ((uint64_t(1) << 14) * k_chunk) <= lim) return 1;
+    if (common + w16 * (uint64_t)(q - 1) <= lim) return 2;
+    return 3;
 }
 
 GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t cols) {

@@ -59,9 +59,10 @@ struct GemmGeometry {
 
 GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t cols);
 
-// Whether the single-reduction L = 2 fold (GemmParams::fold_short) is exact for
-// chunks of k_chunk inner products: with w16 = 2^16 mod q < 256, every partial
-// sum of  cur + a0 + 256 a1l + w16 (a1h + a2)  stays within 2^31 - 2^17.
-bool fold_short_ok(uint32_t q, uint64_t k_chunk);
+// Cheapest exact fold level of the lean L = 2 epilogue (GemmParams::fold) for
+// chunks of k_chunk inner products (w16 = 2^16 mod q < 256; 3 otherwise):
+//   1 if  cur + a0 + 256 a1l + w16 (a1h + a2)  stays within 2^31 - 2^17,
+//   2 if  cur + a0 + 256 a1l + w16 a1h + w16 (a2 mod q)  does, else 3.
+int fold_level(uint32_t q, uint64_t k_chunk);
 
 }  // namespace mhg

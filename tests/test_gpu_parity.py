@@ -192,7 +192,7 @@ def _extremes(q):
 
 @pytest.mark.parametrize("q,k", [(65287, 512), (65287, 640), (65519, 1024), (257, 1024)])
 def test_single_reduction_fold_bound(gpu, mh, q, k):
-    """The single-reduction L=2 fold (fold_short) at the edge of its K bound:
+    """Fold level 1 (single reduction, L=2) at the edge of its K bound:
     q = 65287 has 2^16 mod q = 249, so K = 512 is the largest chunk the host
     admits (K = 640 falls back to the per-class fold); extreme digits, all ops."""
     ex = _extremes(q)
@@ -202,9 +202,21 @@ def test_single_reduction_fold_bound(gpu, mh, q, k):
                 _constant_case(mh, 1024, 64, q, a, b, q - 1, k, op)
 
 
+@pytest.mark.parametrize("level", ["2", "3"])
+def test_forced_fold_levels(gpu, mh, monkeypatch, level):
+    """Fold levels 2 and 3 forced (MHG_FOLD) where level 1 would be chosen:
+    the same exact results through every lean-fold arithmetic variant."""
+    monkeypatch.setenv("MHG_FOLD", level)
+    for q in (P16, 65287, 257):
+        ex = _extremes(q)
+        for a, b in [(ex[0], ex[0]), (ex[1], ex[0]), (ex[2], ex[4])]:
+            for op in (OP_ADD, OP_SUB):
+                _constant_case(mh, 1024, 64, q, a, b, q - 1, 1024, op)
+
+
 @pytest.mark.slow
 def test_single_reduction_fold_at_k8064(gpu, mh):
-    """p = 65521: the largest single-chunk K on the fold_short path (63 k-tiles)."""
+    """p = 65521: the largest single-chunk K on fold level 1 (63 k-tiles)."""
     ex = _extremes(P16)
     for a, b in [(ex[0], ex[0]), (ex[1], ex[0]), (ex[0], ex[1])]:
         _constant_case(mh, 8192, 64, P16, a, b, P16 - 1, 8064, OP_SUB)

@@ -162,3 +162,93 @@ def test_device_calls_fail_loudly_without_gpu(mh):
     with pytest.raises(mh.DeviceError):
         mh.Matrix(mh.Layout(8, 4), mh.Modulus(2))
     assert mh.lib().mhg_device_check() != 0
+
+
+# ---- fold levels of the 2-limb epilogue (mhg_fold_level; kernel fold_g1 / fold_g2)
+M32 = 0xFFFFFFFF
+
+
+def _emulate_fold(level, layout, a0, a1, a2, cur, q):
+    """Bit-exact emulation of the kernel's lean L=2 fold (uint32 wrap-around,
+    Barrett red32 with m = floor(2^32 / q), csrc/mhg_kernels.cu fold_g1/fold_g2)."""
+    w16 = (1 << 16) % q
+    m32 = (1 << 32) // q
+    bias32 = ((1 << 31) // q) * q
+
+    def red32(u):
+        u &= M32
+        r = (u - ((u * m32) >> 32) * q) & M32
+        return r - q if r >= q else r
+
+    def sra8(v):  # arithmetic shift of an int32
+        return v >> 8
+
+    x, y, z = (a1, a2, a0) if layout == 0 else (a0, a1, a2)
+    if level <= 2:
+        if layout == 0:
+            lo = (x & 0xFF) << 8
+            if level == 1:
+                g1 = lo + w16 * ((sra8(x) + y) & M32)
+            else:
+                g1 = lo + w16 * (((sra8(x) & M32) + red32(y + bias32)) & M32)
+        else:
+            g1 = x + ((y & 0xFF) << 8) + w16 * (sra8(y) & M32)
+    else:
+        r1 = red32((y if layout else x) + bias32)
+        g1 = ((r1 << 8) + w16 * red32(y + bias32)) if layout == 0 else (x + bias32 + (r1 << 8))
+    c = (cur + g1) & M32
+    if layout == 0:
+        return red32(c + z + bias32)
+    if level == 1:
+        return red32(c + w16 * (z & M32) + bias32)
+    r2 = red32(z + bias32)
+    return red32(c + w16 * r2 + bias32) if level == 2 else red32(c + w16 * r2)
+
+
+@pytest.mark.parametrize("q", [65521, 65519, 65287, 257, 3])
+def test_fold_levels_exact_at_their_bounds(mh, q):
+    """For each fold level the host admits, the kernel arithmetic (emulated bit
+    for bit) is exact at the largest admitted chunk with extreme class sums."""
+    L, H, kmax = mh.limb_params(q)
+    if L != 2:
+        assert mh.fold_level(q, 128) == 3
+        return
+    rng = np.random.default_rng(q)
+    # largest |top digit| of any representative (the low digit spans [-128, 127])
+    top = max(abs(_digits(v, q, H, L, neg)[-1]) for v in range(q) for neg in (False, True)) \
+        if q < 70000 else 128
+    for level in (1, 2, 3):
+        lo, hi = 0, kmax  # largest K with fold_level(q, K) <= level
+        while lo < hi:
+            mid = (lo + hi + 1) // 2
+            if mh.fold_level(q, mid) <= level:
+                lo = mid
+            else:
+                hi = mid - 1
+        K = lo
+        if K == 0:
+            continue
+        # class-sum magnitudes reachable with chunk K (products of digits)
+        e0, e1, e2 = 128 * 128 * K, 2 * 128 * top * K, top * top * K
+        cases = [(s0 * e0, s1 * e1, s2 * e2) for s0 in (-1, 1) for s1 in (-1, 1) for s2 in (-1, 1)]
+        cases += [(int(rng.integers(-e0, e0 + 1)), int(rng.integers(-e1, e1 + 1)),
+                   int(rng.integers(-e2, e2 + 1))) for _ in range(300)]
+        for a0, a1, a2 in cases:
+            for cur in (0, q - 1, int(rng.integers(0, q))):
+                want = (cur + a0 + 256 * a1 + 65536 * a2) % q
+                for layout in (0, 1):
+                    got = _emulate_fold(level, layout, a0, a1, a2, cur, q)
+                    assert got == want, (q, level, K, layout, a0, a1, a2, cur)
+
+
+def test_fold_level_choices(mh):
+    """p = 65521: one reduction up to K = 8064 (63 k-tiles), two beyond; a prime
+    with 2^16 mod q >= 256 always takes the per-class fold."""
+    assert mh.fold_level(65521, 1024) == 1
+    assert mh.fold_level(65521, 8064) == 1
+    assert mh.fold_level(65521, 8192) == 2
+    assert mh.fold_level(65521, 65408) == 2
+    assert mh.fold_level(65287, 512) == 1 and mh.fold_level(65287, 640) == 2
+    q = 40009  # 2^16 mod q = 25527
+    assert (1 << 16) % q >= 256 and mh.fold_level(q, 128) == 3
+    assert mh.fold_level(2147483647, 128) == 3
