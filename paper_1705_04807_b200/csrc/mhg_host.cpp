@@ -233,6 +233,7 @@ mhg::GemmParams gemm_params(const Buffers& b, const mhg_view& out, const Checked
     p.bias32 = (uint32_t)(((uint64_t(1) << 31) / q) * q);
     p.w16 = (uint32_t)((uint64_t(1) << 16) % q);
     p.w16_small = p.w16 < 256;
+    p.mc = g.mc ? 1 : 0;
     // cheapest exact fold for the longest chunk (MHG_FOLD raises the level, A/B only)
     p.fold = g.L == 2 ? mhg::fold_level(q, (uint64_t)std::min(g.Kt, g.KC) * mhg::kBK) : 3;
     if (const char* fl = std::getenv("MHG_FOLD")) p.fold = std::max(p.fold, std::min(3, std::atoi(fl)));

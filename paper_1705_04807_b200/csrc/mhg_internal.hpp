@@ -68,6 +68,7 @@ struct GemmParams {
     uint32_t w16;                // 2^16 mod q
     int w16_small;               // w16 < 256: fold the top class without a mulmod
     int fold;                    // lean L = 2 fold level 3 / 2 / 1 (reductions per element; host)
+    int mc;                      // column-pair clusters with lhs multicast (Nt even; planner)
     int mode;                    // 0: out += prod, 2: out = prod (first chunk)
     int vec_ok;                  // t % 4 == 0: 16-byte epilogue accesses allowed
     uint32_t group;              // raster: row tiles per group sharing rhs panels in L2

@@ -442,6 +442,17 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
         : "memory");
 }
 
+// One bulk copy delivered to the same smem offset of every CTA in ctaMask,
+// each completing tx bytes on its own barrier at bar's offset (cluster multicast).
+__device__ __forceinline__ void bulk_g2s_mc_hint(void* dst, const void* src, uint32_t bytes,
+                                                 uint64_t* bar, uint16_t mask, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        ".L2::cache_hint [%0], [%1], %2, [%3], %4, %5;" ::"r"(smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask), "l"(policy)
+        : "memory");
+}
+
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -465,6 +476,15 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                      smem_u32(bar))
                  : "memory");
+}
+
+// MMA completion signalled on the barrier at bar's offset in every CTA of mask
+__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"(mask)
+        : "memory");
 }
 
 // D[tmem] (+)= A[smem] * B[smem]^T, int8 x int8 -> int32
@@ -790,7 +810,7 @@ __device__ __forceinline__ void tmem_wait_st() {
 // geometry (no table loads).  Otherwise (narrow tiles, CTA pair) the row's
 // C_old is prefetched into registers at tile start, addressed through smem
 // column offsets.
-template <int L, int W, int EPI_WARPS, bool PAIR, bool XPOSE = false, int FOLD = 3>
+template <int L, int W, int EPI_WARPS, bool PAIR, bool XPOSE = false, int FOLD = 3, bool NPAIR = false>
 __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t first_tile,
                                               uint32_t tile_stride, uint32_t num_tiles,
                                               uint32_t row_groups, uint32_t rank, uint32_t nchunks,
@@ -1021,7 +1041,10 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     auto load_cold = [&](uint32_t tile) {
         const bool live = tile < num_tiles && p.mode != 2;
         uint32_t lm = 0, ln = 0;
-        if (live) tile_coords(tile, row_groups, p.Nt, p.group, lm, ln);
+        if (live) {
+            tile_coords(tile, row_groups, NPAIR ? p.Nt / 2 : p.Nt, p.group, lm, ln);
+            if (NPAIR) ln = 2 * ln + rank;
+        }
         const uint64_t own = row_at(lm, row);
         uint64_t c0[NH];
         bool vec[NH];
@@ -1055,7 +1078,8 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride) {
         const long long tp0 = clock64();
         uint32_t tm, n;
-        tile_coords(tile, row_groups, p.Nt, p.group, tm, n);
+        tile_coords(tile, row_groups, NPAIR ? p.Nt / 2 : p.Nt, p.group, tm, n);
+        if (NPAIR) n = 2 * n + rank;  // column-pair clusters: rank picks the column tile
         const uint32_t m = PAIR ? 2 * tm + rank : tm;
         uint32_t cur[WH];
         uint64_t rbase = 0;
@@ -1252,7 +1276,13 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     }
 }
 
-template <int L, int FOLD = 3>
+// MC (column-pair clusters, launched with cluster dim 2): the two CTAs of a
+// cluster take column tiles 2nn and 2nn+1 of the same row tile in lock step;
+// each loads half of every lhs stage and multicasts it to both, so per-SM lhs
+// traffic from L2 halves (operand bytes per k-slice 64 KB -> 48 KB at L=2).  A
+// stage is refilled only after both CTAs' MMAs released it (empty barriers
+// count two arrivals; the MMA commit is multicast).
+template <int L, int FOLD = 3, bool MC = false>
 __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParams p) {
     using Cfg = GemmCfg<L>;
     constexpr int W = Cfg::W;
@@ -1271,7 +1301,12 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
     uint8_t* xbuf = reinterpret_cast<uint8_t*>(s_col + W);  // per-warp C transpose buffers
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t num_tiles = p.Mt * p.Nt;
+    // MC: tiles are (row tile, column-tile pair); this CTA takes column 2nn + rank
+    const uint32_t rank = MC ? cluster_rank() : 0u;
+    const uint32_t npairs = MC ? p.Nt / 2 : p.Nt;
+    const uint32_t num_tiles = p.Mt * npairs;
+    const uint32_t first_tile = MC ? blockIdx.x / 2 : blockIdx.x;
+    const uint32_t tile_stride = MC ? gridDim.x / 2 : gridDim.x;
     const uint32_t nchunks = (p.Kt + p.KC - 1) / p.KC;
     const int ring = (p.ring > 0 && p.ring < STAGES) ? p.ring : STAGES;  // tuning hook
 
@@ -1283,7 +1318,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
     } else if (warp == 1 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], MC ? 2 : 1);
         }
         mbar_init(tmem_full, 1);
         mbar_init(tmem_empty, Cfg::EPI_WARPS);  // one arrive per epilogue warp
@@ -1292,6 +1327,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
     }
     tc_fence_before();
     __syncthreads();
+    if constexpr (MC) cluster_sync_all();  // peers' barriers initialised before any multicast
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -1303,9 +1339,10 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
             long long wait_empty = 0;
             uint32_t ord = 0;
             const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
-            for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x, ++ord) {
+            for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride, ++ord) {
                 uint32_t m, n;
-                tile_coords(tile, p.Mt, p.Nt, p.group, m, n);
+                tile_coords(tile, p.Mt, npairs, p.group, m, n);
+                if (MC) n = 2 * n + rank;
                 const int8_t* a_src = p.apack + (uint64_t)m * p.Kt * Cfg::A_STAGE;
                 const int8_t* b_src = p.bpack + (uint64_t)n * p.Kt * Cfg::B_STAGE;
                 // serpentine K: odd tiles of a CTA sweep K backwards, so the next wave
@@ -1317,7 +1354,15 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
                     mbar_wait_hint(&empty[st], ph ^ 1, (p.wait_roles & 1) ? p.wait_hint : 0u);
                     wait_empty += clock64() - w0;
                     mbar_expect_tx(&full[st], Cfg::STAGE);
-                    if (p.l2_hints) {
+                    if constexpr (MC) {
+                        // this CTA's half of the lhs stage, to both CTAs (same offset)
+                        constexpr uint32_t HALF = Cfg::A_STAGE / 2;
+                        bulk_g2s_mc_hint(sA + st * Cfg::A_STAGE + rank * HALF,
+                                         a_src + (uint64_t)kt * Cfg::A_STAGE + rank * HALF, HALF,
+                                         &full[st], (uint16_t)0x3, pol_keep);
+                        bulk_g2s_hint(sB + st * Cfg::B_STAGE, b_src + (uint64_t)kt * Cfg::B_STAGE,
+                                      Cfg::B_STAGE, &full[st], pol_stream);
+                    } else if (p.l2_hints) {
                         // lhs panels of the raster group are re-read by the next waves;
                         // rhs panels only by the current one
                         bulk_g2s_hint(sA + st * Cfg::A_STAGE, a_src + (uint64_t)kt * Cfg::A_STAGE,
@@ -1349,7 +1394,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
             uint32_t ph = 0, acc_ph = 0;
             long long wait_full = 0, wait_tmem = 0;
             const long long t_begin = clock64();
-            for (uint32_t tile = blockIdx.x; tile < num_tiles; tile += gridDim.x) {
+            for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride) {
                 for (uint32_t c = 0; c < nchunks; ++c) {
                     const uint32_t kb = c * p.KC;
                     const uint32_t ke = (kb + p.KC < p.Kt) ? kb + p.KC : p.Kt;
@@ -1387,7 +1432,8 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
                                 }
                             }
                         }
-                        tc_commit(&empty[st]);
+                        if constexpr (MC) tc_commit_mc(&empty[st], (uint16_t)0x3);
+                        else tc_commit(&empty[st]);
                         if (++st == ring) {
                             st = 0;
                             ph ^= 1;
@@ -1405,12 +1451,14 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
             }
         }
     } else {
-        epilogue_role<L, W, Cfg::EPI_WARPS, false, Cfg::XPOSE, FOLD>(p, blockIdx.x, gridDim.x, num_tiles,
-                                                               p.Mt, 0, nchunks, tmem, s_col, tmem_full,
-                                                               tmem_empty, warp, lane, xbuf);
+        epilogue_role<L, W, Cfg::EPI_WARPS, false, Cfg::XPOSE, FOLD, MC>(
+            p, first_tile, tile_stride, num_tiles, p.Mt, rank, nchunks, tmem, s_col, tmem_full,
+            tmem_empty, warp, lane, xbuf);
     }
 
     __syncthreads();
+    // MC: the peer may still multicast into this CTA's smem / arrive on its barriers
+    if constexpr (MC) cluster_sync_all();
     if (warp == 0) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
@@ -1632,12 +1680,21 @@ template <int L>
 int configure_gemm_t() {
     int e = (int)cudaFuncSetAttribute(k_gemm<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       GemmCfg<L>::SMEM);
+    if (!e)
+        e = (int)cudaFuncSetAttribute(k_gemm<L, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      GemmCfg<L>::SMEM);
     if constexpr (L == 2) {
         if (!e)
             e = (int)cudaFuncSetAttribute(k_gemm<L, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           GemmCfg<L>::SMEM);
         if (!e)
             e = (int)cudaFuncSetAttribute(k_gemm<L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          GemmCfg<L>::SMEM);
+        if (!e)
+            e = (int)cudaFuncSetAttribute(k_gemm<L, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          GemmCfg<L>::SMEM);
+        if (!e)
+            e = (int)cudaFuncSetAttribute(k_gemm<L, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           GemmCfg<L>::SMEM);
     }
     return e;
@@ -1652,9 +1709,38 @@ __global__ void k_fill_view(uint32_t* __restrict__ out, const uint64_t* __restri
         out[rowoff[x / cols] + coloff[x % cols]] = value;
 }
 
+template <typename Kernel>
+int launch_cluster2(Kernel k, uint32_t grid, uint32_t threads, uint32_t smem, cudaStream_t s,
+                    const GemmParams& p) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid, 1, 1);
+    cfg.blockDim = dim3(threads, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return (int)cudaLaunchKernelEx(&cfg, k, p);
+}
+
 template <int L>
 int launch_gemm_t(const GemmParams& p, int num_sms, cudaStream_t s) {
     using Cfg = GemmCfg<L>;
+    if (p.mc) {
+        // column-pair clusters: one cluster per 2 SMs, Nt even (planner)
+        const uint32_t pairs = p.Mt * (p.Nt / 2);
+        const uint32_t clusters = pairs < (uint32_t)num_sms / 2 ? pairs : (uint32_t)num_sms / 2;
+        const uint32_t grid = 2 * clusters;
+        if constexpr (L == 2) {
+            if (p.fold == 1) return launch_cluster2(k_gemm<L, 1, true>, grid, Cfg::THREADS, Cfg::SMEM, s, p);
+            if (p.fold == 2) return launch_cluster2(k_gemm<L, 2, true>, grid, Cfg::THREADS, Cfg::SMEM, s, p);
+        }
+        return launch_cluster2(k_gemm<L, 3, true>, grid, Cfg::THREADS, Cfg::SMEM, s, p);
+    }
     const uint32_t tiles = p.Mt * p.Nt;
     const int grid = (int)(tiles < (uint32_t)num_sms ? tiles : (uint32_t)num_sms);
     if constexpr (L == 2) {

@@ -189,6 +189,8 @@ GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t c
     g.pair = sel && std::string(sel) == "2cta";
     if (g.pair) g.Mt += g.Mt & 1u;  // pairs take two row tiles
     g.Nt = (uint32_t)((cols + g.W - 1) / g.W);
+    g.mc = !g.pair && sel && std::string(sel) == "mc";
+    if (g.mc) g.Nt += g.Nt & 1u;  // clusters take two column tiles
     g.Kt = (uint32_t)((inner + kBK - 1) / kBK);
     g.KC = (uint32_t)std::max<uint64_t>(1, lp.k_max / kBK);
     // test hook: a smaller chunk exercises the multi-chunk path on small inputs

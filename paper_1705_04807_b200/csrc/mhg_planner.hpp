@@ -50,6 +50,7 @@ Counters oblivious_counters(uint64_t n, uint64_t t, const Rect& out, const Rect&
 // -------------------------------------------------------------- task grid
 struct GemmGeometry {
     bool pair;            // CTA-pair kernel (k_gemm2); Mt is then even
+    bool mc;              // column-pair clusters with lhs multicast (k_gemm MC); Nt is then even
     uint32_t L, W;        // limbs, output tile width
     uint32_t Mt, Nt, Kt;  // tiles along rows / cols / inner (128-byte K slices)
     uint32_t KC;          // K slices per exact int32 chunk

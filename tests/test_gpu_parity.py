@@ -368,10 +368,11 @@ def test_tu_schur_sweep(gpu, mh, oracle):
     assert macs == sum(((n - k) ** 2) * block for k in range(block, n, block))
 
 
-@pytest.mark.parametrize("kernel", ["1cta", "2cta"])
+@pytest.mark.parametrize("kernel", ["1cta", "2cta", "mc"])
 def test_both_gemm_kernels(gpu, mh, oracle, monkeypatch, kernel):
-    """The single-CTA (default) and CTA-pair (cta_group::2, MHG_GEMM=2cta)
-    kernels on ragged views, every limb count, all ops, forced K-chunking."""
+    """The single-CTA (default), CTA-pair (cta_group::2, MHG_GEMM=2cta) and
+    column-pair multicast-cluster (MHG_GEMM=mc) kernels on ragged views, every
+    limb count, all ops, forced K-chunking."""
     monkeypatch.setenv("MHG_GEMM", kernel)
     rng = np.random.default_rng(5)
     for q in (97, P16, P24, P31):
@@ -435,7 +436,7 @@ def test_plan_graph_replay_matches_direct(gpu, mh, oracle):
     assert plan.info()["launches"] == 3
 
 
-@pytest.mark.parametrize("kernel", ["1cta", "2cta"])
+@pytest.mark.parametrize("kernel", ["1cta", "2cta", "mc"])
 def test_guard_bands(gpu, mh, oracle, monkeypatch, kernel):
     """Out-of-bounds detector (compute-sanitizer is unavailable on this pool):
     each container is wrapped in the middle of a larger device buffer whose
