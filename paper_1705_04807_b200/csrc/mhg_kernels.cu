@@ -360,39 +360,11 @@ __device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity, u
         : "memory");
 }
 
-// global C_old / C accesses of the coalesced epilogue (cache-hint variants:
-// MHG_CHINT 0 = .cs streaming, 1 = default caching, 2 = L1 no-allocate loads)
-#ifndef MHG_CHINT
-#define MHG_CHINT 0
-#endif
-__device__ __forceinline__ uint4 c_load(const uint4* a) {
-    if constexpr (MHG_CHINT == 0) return __ldcs(a);
-    else if constexpr (MHG_CHINT == 1) return *a;
-    else {
-        uint4 v;
-        asm volatile("ld.global.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-                     : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                     : "l"(a));
-        return v;
-    }
-}
+// global C_old / C accesses of the coalesced epilogue: streaming (.cs) -- measured
+// best against default caching and L1::no_allocate (profiles/r01_epilogue_ab.txt)
+__device__ __forceinline__ uint4 c_load(const uint4* a) { return __ldcs(a); }
 
-// Predicated streaming 16-byte load straight into v (left unchanged when
-// !pred).  Written as one predicated PTX load so that no register move -- which
-// would wait for the data -- follows it: all of a tile's C_old loads go out
-// back to back.
-__device__ __forceinline__ void c_load_pred(uint4& v, const uint32_t* a, bool pred) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "@p ld.global.cs.v4.u32 {%0, %1, %2, %3}, [%5];\n\t}"
-        : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w)
-        : "r"((uint32_t)pred), "l"(a));
-}
-
-__device__ __forceinline__ void c_store(uint4* a, uint4 v) {
-    if constexpr (MHG_CHINT == 0) __stcs(a, v);
-    else *a = v;
-}
+__device__ __forceinline__ void c_store(uint4* a, uint4 v) { __stcs(a, v); }
 
 __device__ __forceinline__ void sts128(uint32_t addr, uint4 v) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z),
@@ -561,14 +533,6 @@ __device__ __forceinline__ void tmem_wait_ld() {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// Orders every later use of v after the preceding tcgen05.wait::ld: the empty
-// volatile asms "rewrite" the registers and cannot move above the wait.
-template <int N>
-__device__ __forceinline__ void reg_fence(int32_t (&v)[N]) {
-#pragma unroll
-    for (int i = 0; i < N; ++i) asm volatile("" : "+r"(v[i]));
-}
-
 // x mod q for |x| < 2^62 (bias = multiple of q >= 2^62 makes it non-negative)
 __device__ __forceinline__ uint32_t red_signed(int64_t x, const GemmParams& p) {
     const uint64_t u = (uint64_t)x + p.bias;
@@ -686,11 +650,8 @@ struct GemmCfg {
     // two epilogue warps per SMSP, 64 columns each; W = 128 uses the coalesced
     // C path with a 4 KB per-warp transpose buffer, the narrow-tile primes keep
     // row-per-thread C access (see epilogue_role)
-#ifndef MHG_EPI_WARPS
-#define MHG_EPI_WARPS 8
-#endif
     static constexpr bool XPOSE = (W == 128);
-    static constexpr int EPI_WARPS = XPOSE ? MHG_EPI_WARPS : 8;
+    static constexpr int EPI_WARPS = 8;
     static constexpr int XBUF = XPOSE ? EPI_WARPS * (W * 4 / EPI_WARPS >= 64 ? 4096 : 2048) : 0;
     static constexpr int FIXED = 1024 /*align slack*/ + 256 /*barriers*/ + 8 * W /*column offsets*/ + XBUF;
     static constexpr int STAGES_RAW = (232448 - FIXED) / STAGE;
@@ -820,10 +781,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     constexpr int EPI_THREADS = EPI_WARPS * 32;
     constexpr int WH = W * 4 / EPI_WARPS;  // columns per epilogue warp
     constexpr int CLASSES = 2 * L - 1;
-#ifndef MHG_CW
-#define MHG_CW 16
-#endif
-    constexpr int CW = L <= 2 ? MHG_CW : 8;  // TMEM columns per drain step (register budget)
+    constexpr int CW = L <= 2 ? 16 : 8;  // TMEM columns per drain step (x8 / x32 measured slower)
     constexpr uint64_t kNoCol = ~uint64_t(0);
     const int ew = warp - 2;
     const int quad = warp & 3;
@@ -849,9 +807,6 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     // bias + 256 r1 (unreduced, < 2^32 - 2^24) -- release, then class 2:
     // cur = red(cur + w16 r2).  Every class sum is within 2^31 - 2^17 (class 0
     // and class 2 within 2^30), so no step wraps 32 bits.
-#ifndef MHG_DRAIN_PIPE
-#define MHG_DRAIN_PIPE 0
-#endif
     // Per-element folds of the two class groups (lean L = 2 path), by FOLD level
     // (host-chosen, GemmParams::fold; each level exact for the chunk's K):
     //   3: reduce every class before combining (three reductions per element);
@@ -886,47 +841,6 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     };
     auto drain_l2_small = [&](uint32_t tbase, uint32_t n_tile, uint32_t* cur_, uint32_t layout) {
         const int lo_cls = layout ? 0 : 1;  // first group: {lo_cls, lo_cls + 1}
-        if constexpr (MHG_DRAIN_PIPE != 0) {
-            // software-pipelined: the TMEM loads of step t+1 are in flight while
-            // step t folds (columns past the view are folded too, never stored)
-            constexpr int NS = WH / CW;
-            int32_t a[2][2][CW];
-            tmem_ld<CW>(tbase + lo_cls * W, a[0][0]);
-            tmem_ld<CW>(tbase + (lo_cls + 1) * W, a[0][1]);
-            tmem_wait_ld();
-            reg_fence(a[0][0]);
-            reg_fence(a[0][1]);
-#pragma unroll
-            for (int t = 0; t < NS; ++t) {
-                if (t + 1 < NS) {
-                    tmem_ld<CW>(tbase + lo_cls * W + (t + 1) * CW, a[(t + 1) & 1][0]);
-                    tmem_ld<CW>(tbase + (lo_cls + 1) * W + (t + 1) * CW, a[(t + 1) & 1][1]);
-                }
-#pragma unroll
-                for (int j = 0; j < CW; ++j) cur_[t * CW + j] += fold_g1(a[t & 1][0][j], a[t & 1][1][j], layout);
-                if (t + 1 < NS) {
-                    tmem_wait_ld();
-                    reg_fence(a[(t + 1) & 1][0]);
-                    reg_fence(a[(t + 1) & 1][1]);
-                }
-            }
-            release();
-            int32_t b[2][CW];
-            tmem_ld<CW>(tbase + (layout ? 2 : 0) * W, b[0]);
-            tmem_wait_ld();
-            reg_fence(b[0]);
-#pragma unroll
-            for (int t = 0; t < NS; ++t) {
-                if (t + 1 < NS) tmem_ld<CW>(tbase + (layout ? 2 : 0) * W + (t + 1) * CW, b[(t + 1) & 1]);
-#pragma unroll
-                for (int j = 0; j < CW; ++j) cur_[t * CW + j] = fold_g2(cur_[t * CW + j], b[t & 1][j], layout);
-                if (t + 1 < NS) {
-                    tmem_wait_ld();
-                    reg_fence(b[(t + 1) & 1]);
-                }
-            }
-            return;
-        }
 #pragma unroll
         for (int j0 = 0; j0 < WH; j0 += CW) {
             if ((uint64_t)n_tile * W + jb + j0 >= p.cols) continue;  // warp-uniform
@@ -1068,13 +982,6 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
             }
         }
     };
-#ifndef MHG_COLD_EARLY
-#define MHG_COLD_EARLY 0
-#endif
-    // MHG_COLD_EARLY: 1 = the next tile's C_old is loaded during this tile's
-    // stores; 0 = each tile loads its own C_old at tile start.  Measured
-    // (profiles/r01_epilogue_ab.txt): 0 is 21% faster at K = 1024.
-    if constexpr (XPOSE && MHG_COLD_EARLY) load_cold(first_tile);
     for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride) {
         const long long tp0 = clock64();
         uint32_t tm, n;
@@ -1086,13 +993,13 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         bool row_ok = false;
         const uint64_t* col = s_col + jb;
         if constexpr (XPOSE) {
-            if (!MHG_COLD_EARLY) load_cold(tile);
+            load_cold(tile);
             const long long ta = clock64();
             epi_issue += ta - tp0;
             if (p.mode != 2) {
-                // cold holds this tile's C_old (vector lanes; issued before the
-                // previous tile's stores): per pass stage it in the buffer, fill
-                // the edge lanes, read back in row order
+                // cold holds this tile's C_old (vector lanes, all loads in flight):
+                // per pass stage it in the buffer, fill the edge lanes, read back
+                // in row order
 #pragma unroll
                 for (int h = 0; h < NH; ++h) {
                     bool vec;
@@ -1233,9 +1140,6 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
                     sts128(xaddr(lane, g), make_uint4(cur[PW * h + 4 * g], cur[PW * h + 4 * g + 1],
                                                       cur[PW * h + 4 * g + 2], cur[PW * h + 4 * g + 3]));
                 __syncwarp();
-                // once the first pass is staged, the next tile's C_old loads go
-                // out and land during the remaining stores
-                if (MHG_COLD_EARLY && h == 0) load_cold(tile + tile_stride);
                 bool vec;
                 const uint64_t c0 = col_at(n, PW * h + 4 * ch, vec);
 #pragma unroll
