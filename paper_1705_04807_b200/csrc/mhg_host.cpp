@@ -689,7 +689,8 @@ mhg_status mhg_mm(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, mhg_count
 }
 
 mhg_status mhg_mm_ex(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, uint32_t flags,
-                     mhg_counters* ctr, void* stream) {    return guarded([&] {
+                     mhg_counters* ctr, void* stream) {
+    return guarded([&] {
         if (op != MHG_OP_ADD && op != MHG_OP_SUB && op != MHG_OP_SET)
             fail(MHG_ERR_INVALID_ARGUMENT, "mm: unknown op");
         const Checked c = check_problem(out, lhs, rhs, (flags & MHG_ALLOW_ALIAS) != 0);
