@@ -161,7 +161,9 @@ void put_counters(const mhg::Counters& c, mhg_counters* dst) {
 }
 
 // ---------------------------------------------------------------- execution
-// Device memory of one multiply: six offset tables and the two packed operands.
+// Device memory of one multiply: six offset tables (the coalesced epilogue
+// computes output offsets in-kernel; row-per-thread epilogues, the SET fill and
+// the packs read tables) and the two packed operands.
 struct Buffers {
     uint64_t *out_row = nullptr, *out_col = nullptr, *lhs_row = nullptr, *lhs_col = nullptr,
              *rhs_row = nullptr, *rhs_col = nullptr;
@@ -334,10 +336,11 @@ void launch_multiply(const Buffers& b, const mhg_view& out, const mhg_view& lhs,
         cuda_check(cudaStreamWaitEvent(fork->side, fork->split, 0), "fork");
         rhs_stream = fork->side;
     }
-    cuda_check(mhg::launch_pack((int)g.L, 0, lhs.mat->cells, b.lhs_row, b.lhs_col, c.rl.rows,
+    const int vecok = out.mat->t % 4 == 0;
+    cuda_check(mhg::launch_pack((int)g.L, 0, lhs.mat->cells, b.lhs_row, b.lhs_col, vecok, c.rl.rows,
                                 c.rl.cols, mhg::kBM, g.Mt, g.Kt, b.apack, dl, stream),
                "pack lhs");
-    cuda_check(mhg::launch_pack((int)g.L, 1, rhs.mat->cells, b.rhs_row, b.rhs_col, c.rr.cols,
+    cuda_check(mhg::launch_pack((int)g.L, 1, rhs.mat->cells, b.rhs_row, b.rhs_col, vecok, c.rr.cols,
                                 c.rr.rows, g.W, g.Nt, g.Kt, b.bpack, dr, rhs_stream),
                "pack rhs");
     if (fork) {

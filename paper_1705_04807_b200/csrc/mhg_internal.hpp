@@ -97,7 +97,7 @@ int launch_mh_to_rm(const uint32_t* mh, uint32_t* rm, uint64_t n, TileGeom g, vo
 // view columns (lhs).  trans = 1: pack rows are view columns, K is view rows
 // (rhs, transposed to K-major).  rows_per_tile = 128 (lhs) or W (rhs).
 int launch_pack(int L, int trans, const uint32_t* src, const uint64_t* rowoff,
-                const uint64_t* coloff, uint64_t R, uint64_t K, uint32_t rows_per_tile,
+                const uint64_t* coloff, int vecok, uint64_t R, uint64_t K, uint32_t rows_per_tile,
                 uint32_t Rtiles, uint32_t Kt, int8_t* dst, DigitParams dp, void* stream);
 int launch_gemm(int L, const GemmParams& p, int num_sms, void* stream);
 int gemm_smem_bytes(int L);

@@ -28,6 +28,15 @@ namespace {
 
 // ------------------------------------------------------------ index helpers
 __device__ __forceinline__ uint64_t dilate32(uint64_t x) {
+    if (x <= 0xffffull) {
+        // tile grids up to 2^16 per side (every n <= 65536): 32-bit arithmetic
+        uint32_t y = (uint32_t)x;
+        y = (y | (y << 8)) & 0x00ff00ffu;
+        y = (y | (y << 4)) & 0x0f0f0f0fu;
+        y = (y | (y << 2)) & 0x33333333u;
+        y = (y | (y << 1)) & 0x55555555u;
+        return y;
+    }
     x &= 0xffffffffull;
     x = (x | (x << 16)) & 0x0000ffff0000ffffull;
     x = (x | (x << 8)) & 0x00ff00ff00ff00ffull;
@@ -50,12 +59,14 @@ __device__ __forceinline__ void tdivmod(uint64_t v, const TileGeom& g, uint64_t&
 __device__ __forceinline__ uint64_t rowpart(uint64_t i, const TileGeom& g) {
     uint64_t b, r;
     tdivmod(i, g, b, r);
+    if (g.shift >= 0) return (dilate32(b) << (2 * g.shift + 1)) | (r << g.shift);
     return (dilate32(b) << 1) * g.tt + r * g.t;
 }
 
 __device__ __forceinline__ uint64_t colpart(uint64_t j, const TileGeom& g) {
     uint64_t b, r;
     tdivmod(j, g, b, r);
+    if (g.shift >= 0) return (dilate32(b) << (2 * g.shift)) | r;
     return dilate32(b) * g.tt + r;
 }
 
@@ -184,23 +195,41 @@ __device__ __forceinline__ void digits4(const uint32_t (&v)[4], const DigitParam
     }
 }
 
-// Load 4 consecutive view cells along the source's column direction: one
-// 16-byte load when they are contiguous and aligned (t % 4 == 0 inside a tile
-// row), else per-cell loads; cells outside the view read as 0.
-__device__ __forceinline__ void load4(const uint32_t* __restrict__ src, uint64_t rbase, bool rok,
-                                      const uint64_t* __restrict__ coloff, uint64_t c0,
-                                      uint64_t ncols, uint32_t (&v)[4]) {
-    if (rok && c0 + 3 < ncols) {
-        const uint64_t a = __ldg(coloff + c0), b = __ldg(coloff + c0 + 3);
-        if (b == a + 3 && ((rbase + a) & 3) == 0) {
-            const uint4 x = __ldcs(reinterpret_cast<const uint4*>(src + rbase + a));
-            v[0] = x.x; v[1] = x.y; v[2] = x.z; v[3] = x.w;
-            return;
-        }
-    }
+// Four 16-byte runs of a view: rows ri[a] (view coordinates), columns c0..c0+3,
+// through the view's offset tables (L1-resident: neighbouring threads share
+// entries).  All six table loads go out together, then the four data loads are
+// issued unconditionally -- a dead lane reads cell 0 -- so they are all in
+// flight at once (a predicated load is followed by register moves that wait
+// for it, which serialised this loop before).  Lanes whose run is not one
+// aligned 16-byte run (view edges, t % 4 != 0, runs crossing a tile row) are then
+// refilled element by element; cells outside the view read as 0.
+__device__ __forceinline__ void load4x4(const uint32_t* __restrict__ src,
+                                        const uint64_t* __restrict__ rowoff,
+                                        const uint64_t* __restrict__ coloff, bool vecok,
+                                        const uint64_t (&ri)[4], uint64_t nrows, uint64_t c0,
+                                        uint64_t ncols, uint4 (&v)[4]) {
+    const uint64_t clast = ncols - 1;
+    const uint64_t ca = __ldg(coloff + (c0 < ncols ? c0 : clast));
+    const uint64_t cb = __ldg(coloff + (c0 + 3 < ncols ? c0 + 3 : clast));
+    uint64_t rb[4];
+    bool ok[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e)
-        v[e] = (rok && c0 + e < ncols) ? __ldcs(src + rbase + __ldg(coloff + c0 + e)) : 0u;
+    for (int a = 0; a < 4; ++a) {
+        ok[a] = ri[a] < nrows;
+        rb[a] = __ldg(rowoff + (ok[a] ? ri[a] : 0));
+    }
+    const bool cvec = vecok && c0 + 3 < ncols && cb == ca + 3 && (ca & 3) == 0;
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+        v[a] = __ldcs(reinterpret_cast<const uint4*>(src + ((ok[a] && cvec) ? rb[a] + ca : 0)));
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+        if (ok[a] && cvec) continue;
+        auto cell = [&](uint64_t e) -> uint32_t {
+            return (ok[a] && c0 + e < ncols) ? src[rb[a] + __ldg(coloff + c0 + e)] : 0u;
+        };
+        v[a] = make_uint4(cell(0), cell(1), cell(2), cell(3));
+    }
 }
 
 // Swizzle of the K-major UMMA operand image with BK-byte rows (SWIZZLE_<BK>B):
@@ -227,11 +256,16 @@ __device__ __forceinline__ int8_t* pack_dst(int8_t* dst, uint64_t pr, uint64_t k
 // per row).  Smem holds the digit bytes [L][32][128 (+16 pad)].
 constexpr int kRowsStride = kPackK + 16;
 
+// 8 resident blocks per SM (32 registers): full occupancy keeps 4 x 16 B loads per
+// thread x 2048 threads in flight -- 0.91 of measured HBM (profiles/r01_pack.txt)
+#ifndef MHG_PACK_MINB
+#define MHG_PACK_MINB 8
+#endif
 template <int L>
-__global__ void __launch_bounds__(256) k_pack_rows(const uint32_t* __restrict__ src,
+__global__ void __launch_bounds__(256, MHG_PACK_MINB) k_pack_rows(const uint32_t* __restrict__ src,
                                                    const uint64_t* __restrict__ rowoff,
-                                                   const uint64_t* __restrict__ coloff, uint64_t R,
-                                                   uint64_t K, uint32_t rpt, uint32_t Kt,
+                                                   const uint64_t* __restrict__ coloff, int vecok,
+                                                   uint64_t R, uint64_t K, uint32_t rpt, uint32_t Kt,
                                                    uint64_t Rpad, int8_t* __restrict__ dst,
                                                    DigitParams dp) {
     __shared__ __align__(16) uint8_t sd[L][32][kRowsStride];
@@ -241,14 +275,16 @@ __global__ void __launch_bounds__(256) k_pack_rows(const uint32_t* __restrict__ 
     const uint64_t pr0 = (uint64_t)(blockIdx.x / nkb) * 32;
     const uint64_t k0 = (uint64_t)kb * kPackK;
     const int tk = threadIdx.x & 31, tr = threadIdx.x >> 5;
+    uint64_t ri[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) ri[a] = pr0 + 4 * tr + a;
+    uint4 v4[4];
+    load4x4(src, rowoff, coloff, vecok, ri, R, k0 + 4 * tk, K, v4);
 #pragma unroll
     for (int a = 0; a < 4; ++a) {
         const int r = 4 * tr + a;
-        const uint64_t pr = pr0 + r;
-        const bool rok = pr < R;
-        const uint64_t rb = rok ? __ldg(rowoff + pr) : 0;
-        uint32_t v[4], w[L];
-        load4(src, rb, rok, coloff, k0 + 4 * tk, K, v);
+        const uint32_t v[4] = {v4[a].x, v4[a].y, v4[a].z, v4[a].w};
+        uint32_t w[L];
         digits4<L>(v, dp, w);
 #pragma unroll
         for (int s = 0; s < L; ++s) *reinterpret_cast<uint32_t*>(&sd[s][r][4 * tk]) = w[s];
@@ -271,10 +307,10 @@ __global__ void __launch_bounds__(256) k_pack_rows(const uint32_t* __restrict__ 
 constexpr int kColsStride = 36;  // 32 K bytes + 4 pad
 
 template <int L>
-__global__ void __launch_bounds__(256) k_pack_cols(const uint32_t* __restrict__ src,
+__global__ void __launch_bounds__(256, MHG_PACK_MINB) k_pack_cols(const uint32_t* __restrict__ src,
                                                    const uint64_t* __restrict__ rowoff,
-                                                   const uint64_t* __restrict__ coloff, uint64_t R,
-                                                   uint64_t K, uint32_t rpt, uint32_t Kt,
+                                                   const uint64_t* __restrict__ coloff, int vecok,
+                                                   uint64_t R, uint64_t K, uint32_t rpt, uint32_t Kt,
                                                    uint64_t Rpad, int8_t* __restrict__ dst,
                                                    DigitParams dp) {
     __shared__ __align__(16) uint8_t sd[L][128][kColsStride];
@@ -283,14 +319,15 @@ __global__ void __launch_bounds__(256) k_pack_cols(const uint32_t* __restrict__ 
     const uint64_t pr0 = (uint64_t)(blockIdx.x / nkq) * 128;
     const uint64_t k0 = (uint64_t)kq * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-    uint32_t v[4][4];  // [k][pack row]
+    uint64_t ki[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const uint64_t kk = k0 + 4 * ty + i;
-        const bool kok = kk < K;
-        const uint64_t rb = kok ? __ldg(rowoff + kk) : 0;
-        load4(src, rb, kok, coloff, pr0 + 4 * tx, R, v[i]);
-    }
+    for (int i = 0; i < 4; ++i) ki[i] = k0 + 4 * ty + i;
+    uint4 v4[4];  // [k] x 4 pack rows
+    load4x4(src, rowoff, coloff, vecok, ki, K, pr0 + 4 * tx, R, v4);
+    const uint32_t v[4][4] = {{v4[0].x, v4[0].y, v4[0].z, v4[0].w},
+                              {v4[1].x, v4[1].y, v4[1].z, v4[1].w},
+                              {v4[2].x, v4[2].y, v4[2].z, v4[2].w},
+                              {v4[3].x, v4[3].y, v4[3].z, v4[3].w}};
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         const uint32_t col[4] = {v[0][c], v[1][c], v[2][c], v[3][c]};
@@ -916,7 +953,8 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         uint64_t b, r;
         tdivmod(p.out_j0 + gj, p.out_geom, b, r);
         vec = p.vec_ok && (r & 3) == 0 && r + 3 < p.out_geom.t && gj + 3 < p.cols;
-        return dilate32(b) * p.out_geom.tt + r;
+        return p.out_geom.shift >= 0 ? (dilate32(b) << (2 * p.out_geom.shift)) | r
+                                     : dilate32(b) * p.out_geom.tt + r;
     };
     // edge path (a lane whose 4-column run is not one aligned 16-byte run): the
     // pass's rows element by element, staged through the transpose buffer
@@ -1660,17 +1698,17 @@ int launch_gemm_t(const GemmParams& p, int num_sms, cudaStream_t s) {
 
 template <int L>
 int launch_pack_t(int trans, const uint32_t* src, const uint64_t* rowoff, const uint64_t* coloff,
-                  uint64_t R, uint64_t K, uint32_t rpt, uint32_t Rtiles, uint32_t Kt, int8_t* dst,
-                  DigitParams dp, cudaStream_t s) {
+                  int vecok, uint64_t R, uint64_t K, uint32_t rpt, uint32_t Rtiles, uint32_t Kt,
+                  int8_t* dst, DigitParams dp, cudaStream_t s) {
     const uint64_t Rpad = (uint64_t)Rtiles * rpt;
     if (trans) {
         const uint64_t blocks = ((Rpad + 127) / 128) * Kt * (kBK / 32);
-        k_pack_cols<L><<<(unsigned)blocks, 256, 0, s>>>(src, rowoff, coloff, R, K, rpt, Kt, Rpad,
-                                                        dst, dp);
+        k_pack_cols<L><<<(unsigned)blocks, 256, 0, s>>>(src, rowoff, coloff, vecok, R, K, rpt, Kt,
+                                                        Rpad, dst, dp);
     } else {
         const uint64_t blocks = (Rpad / 32) * (((uint64_t)Kt * kBK + kPackK - 1) / kPackK);
-        k_pack_rows<L><<<(unsigned)blocks, 256, 0, s>>>(src, rowoff, coloff, R, K, rpt, Kt, Rpad,
-                                                        dst, dp);
+        k_pack_rows<L><<<(unsigned)blocks, 256, 0, s>>>(src, rowoff, coloff, vecok, R, K, rpt, Kt,
+                                                        Rpad, dst, dp);
     }
     return (int)cudaGetLastError();
 }
@@ -1714,14 +1752,14 @@ int launch_mh_to_rm(const uint32_t* mh, uint32_t* rm, uint64_t n, TileGeom g, vo
 }
 
 int launch_pack(int L, int trans, const uint32_t* src, const uint64_t* rowoff,
-                const uint64_t* coloff, uint64_t R, uint64_t K, uint32_t rpt, uint32_t Rtiles,
-                uint32_t Kt, int8_t* dst, DigitParams dp, void* stream) {
+                const uint64_t* coloff, int vecok, uint64_t R, uint64_t K, uint32_t rpt,
+                uint32_t Rtiles, uint32_t Kt, int8_t* dst, DigitParams dp, void* stream) {
     cudaStream_t s = (cudaStream_t)stream;
     switch (L) {
-        case 1: return launch_pack_t<1>(trans, src, rowoff, coloff, R, K, rpt, Rtiles, Kt, dst, dp, s);
-        case 2: return launch_pack_t<2>(trans, src, rowoff, coloff, R, K, rpt, Rtiles, Kt, dst, dp, s);
-        case 3: return launch_pack_t<3>(trans, src, rowoff, coloff, R, K, rpt, Rtiles, Kt, dst, dp, s);
-        case 4: return launch_pack_t<4>(trans, src, rowoff, coloff, R, K, rpt, Rtiles, Kt, dst, dp, s);
+        case 1: return launch_pack_t<1>(trans, src, rowoff, coloff, vecok, R, K, rpt, Rtiles, Kt, dst, dp, s);
+        case 2: return launch_pack_t<2>(trans, src, rowoff, coloff, vecok, R, K, rpt, Rtiles, Kt, dst, dp, s);
+        case 3: return launch_pack_t<3>(trans, src, rowoff, coloff, vecok, R, K, rpt, Rtiles, Kt, dst, dp, s);
+        case 4: return launch_pack_t<4>(trans, src, rowoff, coloff, vecok, R, K, rpt, Rtiles, Kt, dst, dp, s);
     }
     return (int)cudaErrorInvalidValue;
 }
