@@ -126,21 +126,34 @@ __global__ void k_conv_z(const uint32_t* __restrict__ src, uint32_t* __restrict_
                          TileGeom g, uint32_t q, int* __restrict__ bad, int to_mh) {
     const uint64_t groups = n * n / 4;
     const int sh = g.shift;
+    const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
     int saw_bad = 0;
-    for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < groups;
-         x += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t z = 4 * x;
-        const uint64_t tile = z >> (2 * sh);
-        const uint64_t rem = z & (g.tt - 1);
-        const uint64_t i = ((uint64_t)compact32(tile >> 1) << sh) + (rem >> sh);
-        const uint64_t j = ((uint64_t)compact32(tile) << sh) + (rem & (g.t - 1));
-        const uint64_t r = i * n + j;
-        if (to_mh) {
-            const uint4 v = __ldcs(reinterpret_cast<const uint4*>(src + r));
-            saw_bad |= (v.x >= q) | (v.y >= q) | (v.z >= q) | (v.w >= q);
-            __stcs(reinterpret_cast<uint4*>(dst) + x, v);
-        } else {
-            __stcs(reinterpret_cast<uint4*>(dst + r), __ldcs(reinterpret_cast<const uint4*>(src) + x));
+    // 4 groups per thread per round: all four loads in flight before any store
+    for (uint64_t x0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x0 < groups; x0 += 4 * stride) {
+        uint64_t r[4];
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint64_t x = x0 + u * stride;
+            const uint64_t z = 4 * (x < groups ? x : 0);
+            const uint64_t tile = z >> (2 * sh);
+            const uint64_t rem = z & (g.tt - 1);
+            const uint64_t i = ((uint64_t)compact32(tile >> 1) << sh) + (rem >> sh);
+            const uint64_t j = ((uint64_t)compact32(tile) << sh) + (rem & (g.t - 1));
+            r[u] = i * n + j;
+            v[u] = to_mh ? __ldcs(reinterpret_cast<const uint4*>(src + r[u]))
+                         : __ldcs(reinterpret_cast<const uint4*>(src) + (x < groups ? x : 0));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint64_t x = x0 + u * stride;
+            if (x >= groups) break;
+            if (to_mh) {
+                saw_bad |= (v[u].x >= q) | (v[u].y >= q) | (v[u].z >= q) | (v[u].w >= q);
+                __stcs(reinterpret_cast<uint4*>(dst) + x, v[u]);
+            } else {
+                __stcs(reinterpret_cast<uint4*>(dst + r[u]), v[u]);
+            }
         }
     }
     if (saw_bad) atomicOr(bad, 1);
@@ -151,11 +164,28 @@ __global__ void k_mh_to_rm(const uint32_t* __restrict__ mh, uint32_t* __restrict
     const uint64_t groups = n * n / 4;
     const bool vec = (g.t % 4 == 0) && (n % 4 == 0);
     if (vec) {
-        for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < groups;
-             x += (uint64_t)gridDim.x * blockDim.x) {
-            const uint64_t i = (4 * x) / n, j = (4 * x) % n;
-            const uint4 v = __ldcs(reinterpret_cast<const uint4*>(mh + rowpart(i, g) + colpart(j, g)));
-            __stcs(reinterpret_cast<uint4*>(rm) + x, v);
+        // 4 groups per thread per round: all four loads in flight before any store;
+        // power-of-two n (power-of-two t) splits the flat index with shifts
+        const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+        const int ns = 63 - __clzll((long long)n);
+        const bool npow2 = (uint64_t(1) << ns) == n;
+        for (uint64_t x0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x0 < groups;
+             x0 += 4 * stride) {
+            uint4 v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint64_t x = x0 + u * stride;
+                const uint64_t f = 4 * (x < groups ? x : 0);
+                const uint64_t i = npow2 ? f >> ns : f / n;
+                const uint64_t j = npow2 ? f & (n - 1) : f - i * n;
+                v[u] = __ldcs(reinterpret_cast<const uint4*>(mh + rowpart(i, g) + colpart(j, g)));
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint64_t x = x0 + u * stride;
+                if (x >= groups) break;
+                __stcs(reinterpret_cast<uint4*>(rm) + x, v[u]);
+            }
         }
     } else {
         for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < n * n;
@@ -1723,17 +1753,13 @@ int launch_offsets(uint64_t* dst, uint64_t start, uint64_t count, TileGeom g, in
     return (int)cudaGetLastError();
 }
 
-// Conversion direction choice (measured, profiles/r01_conversion.txt): the
-// Morton-order kernel for row-major -> Morton (contiguous Morton writes, 0.73
-// of HBM vs 0.68), the row-major-order kernel for Morton -> row-major
-// (contiguous row-major writes, 0.86 vs 0.74).  MHG_CONV: 0 both row-order,
-// 2 both Morton-order (A/B only).
+// Conversion kernel choice (measured, profiles/r01_conversion.txt): Morton-order
+// iteration (k_conv_z, 4 groups in flight per thread) in both directions, 0.84-0.89
+// of measured HBM.  MHG_CONV: 0 row-order kernels both ways, 1 Morton-order for
+// row-major -> Morton only (A/B only).
 static int conv_mode() {
-    static const int mode = [] {
-        const char* e = std::getenv("MHG_CONV");
-        return e ? std::atoi(e) : 1;
-    }();
-    return mode;
+    const char* e = std::getenv("MHG_CONV");
+    return e ? std::atoi(e) : 2;
 }
 
 int launch_rm_to_mh(const uint32_t* rm, uint32_t* mh, uint64_t n, TileGeom g, uint32_t q,
