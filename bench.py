@@ -185,6 +185,39 @@ def run_reference(args, rank, world):
 
 
 # ---------------------------------------------------------------- GPU leg
+def time_conversions(mh, torch, mats, n, q, hbm_gbs, reps=3):
+    """Device row-major -> Morton of the three operands (K1, on-device residue check)
+    and one Morton -> row-major, CUDA events; 8 n^2 algorithmic bytes per conversion."""
+    lib = mh.lib()
+    rm = torch.randint(0, q, (n * n,), dtype=torch.int32, device="cuda")
+    back = torch.empty_like(rm)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    for m in mats:  # warm-up
+        assert lib.mhg_rowmajor_to_mh(m.handle, rm.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    ev[0].record()
+    for _ in range(reps):
+        for m in mats:
+            assert lib.mhg_rowmajor_to_mh(m.handle, rm.data_ptr(), None) == 0
+    ev[1].record()
+    ev[2].record()
+    for _ in range(reps):
+        assert lib.mhg_mh_to_rowmajor(mats[0].handle, back.data_ptr(), None) == 0
+    ev[3].record()
+    torch.cuda.synchronize()
+    ok = bool(torch.equal(rm, back))
+    to_mh = ev[0].elapsed_time(ev[1]) / (reps * len(mats))
+    to_rm = ev[2].elapsed_time(ev[3]) / reps
+    byts = 8 * n * n
+    del rm, back
+    torch.cuda.empty_cache()
+    return {"rm_to_mh_ms": to_mh, "mh_to_rm_ms": to_rm, "three_operands_rm_to_mh_ms": 3 * to_mh,
+            "rm_to_mh_gbs": byts / to_mh / 1e6, "mh_to_rm_gbs": byts / to_rm / 1e6,
+            "frac_of_hbm": [byts / to_mh / 1e6 / hbm_gbs, byts / to_rm / 1e6 / hbm_gbs],
+            "hbm_peak_gbs": hbm_gbs, "round_trip_exact": ok,
+            "kernel": "k_conv_z (Morton-order, 16-B accesses, residue check on the way in)"}
+
+
 def e2e_pipelined(mh, torch, lay, mod, flats, set0, prob0, op, n, steps, macs):
     """End to end through the public C ABI with pinned HOST buffers: every step
     uploads its three inputs (mhg_matrix_upload), runs the plan, and downloads
@@ -421,6 +454,11 @@ def run_gpu(args, rank, world, local_rank):
             "frac_of_spec_4500": achieved_tops / 4500.0,
             "gemm_ms": gemm_ms_max, "gemm_share_of_step": gemm_ms_max / ms,
             "gf_macs_per_s_gemm_only": macs_rank / (gemm_ms_max * 1e-3)}
+    # ---- row-major <-> Morton-hybrid conversion of all three operands,
+    # timed separately after everything else (it overwrites the containers)
+    conversion = None
+    if world == 1:
+        conversion = time_conversions(mh, torch, (A, B, Cm), n, q, hbm)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline_json(args, n, t, q, view)
@@ -436,7 +474,7 @@ def run_gpu(args, rank, world, local_rank):
                                     + (f", {len(plans)} K segments pipelined with NCCL broadcasts"
                                        if world > 1 else ""),
                        "l2": "no flush: operands 3 x %.2f GiB >> 126 MB L2" % (n * n * 4 / 2 ** 30)},
-            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "conversion": conversion,
             "gpu_launches": args.steps * launches_per_step,
             "clocks": clk.summary()}
     print(json.dumps(line), flush=True)

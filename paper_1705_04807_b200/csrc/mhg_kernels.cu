@@ -109,6 +109,15 @@ __global__ void k_rm_to_mh(const uint32_t* __restrict__ rm, uint32_t* __restrict
 
 // Inverse of dilate32 on the even bits: compact(dilate32(x)) == x.
 __device__ __forceinline__ uint32_t compact32(uint64_t x) {
+    if ((x >> 32) == 0) {
+        // tile indices below 2^32 (every n <= 65536 tile grid): 32-bit arithmetic
+        uint32_t y = (uint32_t)x & 0x55555555u;
+        y = (y | (y >> 1)) & 0x33333333u;
+        y = (y | (y >> 2)) & 0x0f0f0f0fu;
+        y = (y | (y >> 4)) & 0x00ff00ffu;
+        y = (y | (y >> 8)) & 0x0000ffffu;
+        return y;
+    }
     x &= 0x5555555555555555ull;
     x = (x | (x >> 1)) & 0x3333333333333333ull;
     x = (x | (x >> 2)) & 0x0f0f0f0f0f0f0f0full;
