@@ -309,7 +309,7 @@ def run_gpu(args, rank, world, local_rank):
     import torch.distributed as dist
 
     import paper_1705_04807_b200 as mh
-    from paper_1705_04807_b200.dist import PanelExchange, slice_range
+    from paper_1705_04807_b200.dist import PanelExchange, rank_update, segment_plans, slice_range
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -356,13 +356,7 @@ def run_gpu(args, rank, world, local_rank):
         # one plan per K segment: C[R_r, C_r] op= A[R_r, seg] B[seg, C_r]; the
         # segment's panels are broadcast while the previous segment computes
         segs = ex.segments()
-        plans = []
-        for j, sg in enumerate(segs):
-            op_j = op if (op != mh.OP_SET or j == 0) else mh.OP_ADD
-            plans.append(mh.Plan(mh.Problem(
-                mh.Sub(A, mh.encode(lay, oi, oj), rr, cc),
-                mh.Sub(B, mh.encode(lay, oi, sg.k0), rr, sg.k1 - sg.k0),
-                mh.Sub(Cm, mh.encode(lay, sg.k0, oj), sg.k1 - sg.k0, cc)), op_j))
+        plans = segment_plans(mh, ex, A, B, Cm, op)
     plan = plans[0]
     info = plan.info()
     launches_per_step = sum(pl.info()["launches"] for pl in plans)
@@ -375,17 +369,9 @@ def run_gpu(args, rank, world, local_rank):
         if world == 1:
             plan.run(stream)
             return
-        pending = ex.exchange_segment(segs[0], lhs_f, rhs_f, async_op=True)
-        for wk in pending:
-            wk.wait()
-        for j, pl in enumerate(plans):
-            # enqueue segment j+1's broadcasts before segment j's GEMM: NCCL waits
-            # for the GEMMs already queued, then overlaps this one
-            nxt = ex.exchange_segment(segs[j + 1], lhs_f, rhs_f, async_op=True) \
-                if j + 1 < len(plans) else []
-            pl.run(stream)
-            for wk in nxt:
-                wk.wait()
+        # segment j+1's broadcasts are enqueued before segment j's GEMM: NCCL waits
+        # for the GEMMs already queued, then overlaps this one
+        rank_update(ex, plans, lhs_f, rhs_f, stream)
 
     W = max(args.warmup, 3)
     for _ in range(W):
@@ -499,11 +485,19 @@ def main():
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
+    # functional check of the N>1 path on ONE GPU (never a measurement): every rank on
+    # cuda:0, collectives over gloo (host-staged).  No kernel waits on another rank.
+    shared = os.environ.get("MHG_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local_rank = 0
     if world > 1:
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
         run_gpu(args, rank, world, local_rank)
     finally:

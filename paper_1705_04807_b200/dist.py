@@ -178,3 +178,33 @@ class PanelExchange:
                 parts.append(flat[b:e])
             mine = parts[members.index(self.rank)]
             dist.all_gather(parts, mine.clone(), group=group)
+
+
+def segment_plans(mh, ex: PanelExchange, A, B, C, op: int):
+    """One planned multiply per K segment of this rank's update
+    C[R_r, C_r] op= A[R_r, seg] * B[seg, C_r] (A = out, B = lhs, C = rhs in the
+    reference's Problem order).  A SET update overwrites only with the first
+    segment; the rest accumulate."""
+    lay = A.layout()
+    blk = ex.block
+    plans = []
+    for j, sg in enumerate(ex.segments()):
+        op_j = op if (op != mh.OP_SET or j == 0) else mh.OP_ADD
+        plans.append(mh.Plan(mh.Problem(
+            mh.Sub(A, mh.encode(lay, blk.i0, blk.j0), blk.rows, blk.cols),
+            mh.Sub(B, mh.encode(lay, blk.i0, sg.k0), blk.rows, sg.k1 - sg.k0),
+            mh.Sub(C, mh.encode(lay, sg.k0, blk.j0), sg.k1 - sg.k0, blk.cols)), op_j))
+    return plans
+
+
+def rank_update(ex: PanelExchange, plans, lhs_flat, rhs_flat, stream=None):
+    """This rank's whole update: segment j+1's panel broadcasts are enqueued before
+    segment j's multiply so the exchange overlaps compute (NCCL on GPUs)."""
+    segs = ex.segments()
+    pending = ex.exchange_segment(segs[0], lhs_flat, rhs_flat, async_op=True)
+    for j, pl in enumerate(plans):
+        for wk in pending:
+            wk.wait()
+        pending = (ex.exchange_segment(segs[j + 1], lhs_flat, rhs_flat, async_op=True)
+                   if j + 1 < len(segs) else [])
+        pl.run(stream)
