@@ -350,11 +350,18 @@ void launch_multiply(const Buffers& b, const mhg_view& out, const mhg_view& lhs,
     mhg::GemmParams p = gemm_params(b, out, c, g, op);
     // diagnostics: MHG_GEMM_STATS=1 prints per-CTA wait-cycle shares (synchronous)
     static const bool stats_on = std::getenv("MHG_GEMM_STATS") != nullptr;
+    struct StatsBuf {  // freed on every path, including a failed launch
+        unsigned long long* ptr = nullptr;
+        ~StatsBuf() {
+            if (ptr) cudaFree(ptr);
+        }
+    } statsbuf;
     unsigned long long* stats = nullptr;
     if (stats_on) {
-        cuda_check(cudaMalloc(&stats, 148 * 8 * mhg::kStatCount * 2), "stats alloc");
-        cuda_check(cudaMemset(stats, 0, 148 * 8 * mhg::kStatCount * 2), "stats zero");
-        p.stats = stats;
+        const size_t bytes = (size_t)device_info().sms * mhg::kStatCount * sizeof(unsigned long long);
+        cuda_check(cudaMalloc(&statsbuf.ptr, bytes), "stats alloc");
+        cuda_check(cudaMemset(statsbuf.ptr, 0, bytes), "stats zero");
+        stats = p.stats = statsbuf.ptr;
     }
     const TensorMaps tm = tensor_maps(b, g);
     if (gemm_begin) cuda_check(cudaEventRecord(gemm_begin, (cudaStream_t)stream), "event");
@@ -365,7 +372,6 @@ void launch_multiply(const Buffers& b, const mhg_view& out, const mhg_view& lhs,
         std::vector<unsigned long long> h((size_t)n * mhg::kStatCount);
         cuda_check(cudaStreamSynchronize((cudaStream_t)stream), "stats sync");
         cuda_check(cudaMemcpy(h.data(), stats, h.size() * 8, cudaMemcpyDeviceToHost), "stats copy");
-        cudaFree(stats);
         // MMA-side counters come from MMA-issuing CTAs only (pair leaders);
         // producer / epilogue counters from every CTA: normalise separately
         double tot = 0, s[mhg::kStatCount] = {0};
