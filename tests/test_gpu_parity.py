@@ -520,3 +520,55 @@ def test_two_exact_chunks_at_scale(gpu, mh, oracle):
     got, ctr = _run_gpu(mh, n, t, q, out, lhs, rhs, v, OP_SUB)
     assert ctr.scalar_macs == n ** 3
     assert oracle.freivalds(n, t, q, out, lhs, rhs, got, v, op=OP_SUB, rounds=1)
+
+
+def test_concurrent_calls_on_streams(gpu, mh, oracle):
+    """Concurrent one-shot multiplies and plans from several host threads on their
+    own streams (disjoint outputs -- the reference's concurrency contract,
+    multiply.hpp:25-29): the shared one-shot workspace is ordered by events, plans
+    own theirs; every result must equal the oracle's."""
+    import threading
+
+    import torch
+
+    n, t, q = 256, 32, P16
+    jobs = []
+    for w in range(3):
+        rng = np.random.default_rng(900 + w)
+        out, lhs, rhs = _fill(oracle, 900 + w, n, q)
+        A, B, Cm = _containers(mh, n, t, q, (out, lhs, rhs))
+        seq = []
+        want = out.copy()
+        for it in range(4):
+            r, k, c, corners = _random_views(rng, n)
+            v = _views_from(oracle, n, t, r, k, c, corners)
+            seq.append(v)
+            oracle.mm_dense(n, t, q, want, lhs, rhs, v, op=OP_SUB)
+        jobs.append((A, B, Cm, seq, want))
+    errors = []
+
+    def worker(job, use_plan):
+        try:
+            A, B, Cm, seq, _ = job
+            s = torch.cuda.Stream()
+            for v in seq:
+                prob = mh.Problem(mh.Sub(A, v.out_origin, v.rows, v.cols),
+                                  mh.Sub(B, v.lhs_origin, v.rows, v.inner),
+                                  mh.Sub(Cm, v.rhs_origin, v.inner, v.cols))
+                if use_plan:
+                    mh.Plan(prob, mh.OP_SUB).run(s)
+                else:
+                    mh.mm(prob, mh.OP_SUB, stream=s)
+            s.synchronize()
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker, args=(j, i == 2)) for i, j in enumerate(jobs)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    torch.cuda.synchronize()
+    assert not errors, errors
+    for A, _, _, _, want in jobs:
+        assert np.array_equal(A.cells(), want)
