@@ -13,6 +13,13 @@ from oracle.binding import OP_ADD, OP_SET, OP_SUB, Views
 
 pytestmark = pytest.mark.gpu
 
+
+def reference_available():
+    import os
+
+    from oracle.binding import REF_SO
+    return os.path.exists(REF_SO)
+
 P16 = 65521
 P31 = 2147483647
 P24 = 16777213  # a 24-bit prime: three limbs
@@ -276,6 +283,20 @@ def test_cfg3_misaligned_schur_update(gpu, mh, oracle):
     assert np.array_equal(got, want)
 
 
+def _reference_tiles(reference, oracle, n, t, q, out, lhs, rhs, got, op, tiles):
+    """Recompute 64 x 64 output tiles with the REFERENCE's own mm_oblivious
+    (oracle/_ref: the reference headers compiled in place) on a copy of the
+    original C -- the tile's row panel of A and column panel of B as views -- and
+    compare those cells with the GPU result (full views only)."""
+    ref_out = out.copy()
+    for (r0, c0) in tiles:
+        tv = Views(oracle.encode(n, t, r0, c0), oracle.encode(n, t, r0, 0),
+                   oracle.encode(n, t, 0, c0), 64, n, 64)
+        reference.mm(2, n, t, q, ref_out, lhs, rhs, tv, op=op)
+        idx = [oracle.encode(n, t, r0 + a, c0 + b) for a in range(64) for b in range(64)]
+        assert np.array_equal(got[idx], ref_out[idx]), (r0, c0)
+
+
 def _sampled_tiles(oracle, n, t, q, out, lhs, rhs, got, v, op, tiles):
     for (r0, c0) in tiles:
         nr, nc = min(64, v.rows - r0), min(64, v.cols - c0)
@@ -297,6 +318,10 @@ def test_cfg4_large_prime(gpu, mh, oracle):
     h = n // 2
     _sampled_tiles(oracle, n, t, q, out, lhs, rhs, got, v, OP_SET,
                    [(0, 0), (0, h), (h, 0), (h, h), (n - 64, n - 64), (h - 32, h - 32)])
+    if reference_available():
+        from oracle.binding import Reference
+        _reference_tiles(Reference(), oracle, n, t, q, out, lhs, rhs, got, OP_SET,
+                         [(0, 64), (h, h - 64)])
     bad = got.copy()
     bad[12345] = (bad[12345] + 1) % q
     assert not oracle.freivalds(n, t, q, out, lhs, rhs, bad, v, op=OP_SET, rounds=1)
@@ -315,6 +340,19 @@ def test_north_star_size(gpu, mh, oracle):
     h = n // 2
     _sampled_tiles(oracle, n, t, q, out, lhs, rhs, got, v, OP_SUB,
                    [(0, 0), (0, h), (h, 0), (h, h), (0, n - 64), (n - 64, 0), (n - 64, n - 64)])
+
+
+@pytest.mark.slow
+def test_north_star_against_reference_tiles(gpu, mh, oracle, reference):
+    """The bench workload checked against the reference implementation itself:
+    tiles in all four top-level Morton quadrants recomputed by the reference's
+    mm_oblivious (C -= A*B through its Sub-view API) equal the GPU result."""
+    n, t, q = 16384, 64, P16
+    out, lhs, rhs = _fill(oracle, 0, n, q)
+    got, _ = _run_gpu(mh, n, t, q, out, lhs, rhs, Views(0, 0, 0, n, n, n), OP_SUB)
+    h = n // 2
+    _reference_tiles(reference, oracle, n, t, q, out, lhs, rhs, got, OP_SUB,
+                     [(0, 0), (64, h + 128), (h, 192), (n - 64, n - 64)])
 
 
 def test_alias_mode_same_parent(gpu, mh, oracle):
