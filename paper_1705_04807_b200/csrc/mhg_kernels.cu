@@ -282,8 +282,10 @@ __host__ __device__ constexpr uint32_t swizzled_chunk(uint32_t row, uint32_t chu
 template <int L>
 __device__ __forceinline__ int8_t* pack_dst(int8_t* dst, uint64_t pr, uint64_t kk, int s,
                                             uint32_t rpt, uint32_t Kt) {
-    const uint64_t tile = pr / rpt;
-    const uint32_t rit = (uint32_t)(pr - tile * rpt);
+    // rows per tile is a power of two (128 for the lhs, W for the rhs): shift, not divide
+    const int rs = __ffs(rpt) - 1;
+    const uint64_t tile = pr >> rs;
+    const uint32_t rit = (uint32_t)(pr & (rpt - 1));
     const uint64_t kt = kk / kBK;
     const uint32_t ch = (uint32_t)(kk % kBK) >> 4;
     return dst + ((tile * Kt + kt) * L + s) * (uint64_t)rpt * kBK + (uint64_t)rit * kBK +
