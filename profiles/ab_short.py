@@ -44,7 +44,7 @@ for K in (1024, 2048, 16384 - 1024):
             plans[name] = mh.Plan(prob, mh.OP_SUB)
             plans[name].run()
     res = {name: [] for name, _ in variants}
-    for r in range(5):
+    for r in range(int(os.environ.get("AB_ROUNDS", "5"))):
         for name, env in variants:
             # the GEMM parameters (and env hooks) are read at every time_gemm call
             with env_set(env):
