@@ -172,7 +172,7 @@ def run_reference(args, rank, world):
     cb = cpu_baseline_json(args, n, t, q, view, steps=args.steps, warmup=W)
     line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": W, "ms_per_step": cb.get("ms_per_step"),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
             "data": "synthetic (uniform residues, splitmix stream)",
             "config": {"workload": args.workload, "description": DESCR[args.workload], "n": n,
                        "t": t, "p": q, "op": op},
@@ -451,7 +451,7 @@ def run_gpu(args, rank, world, local_rank):
         cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": W, "ms_per_step": ms, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "int8",
+            "scaling": "strong", "vs_baseline": None, "dtype": "int8",
             "data": "synthetic: uniform residues in [0,p) drawn on device (torch.Generator)",
             "config": {"workload": args.workload, "description": DESCR[args.workload], "n": n,
                        "t": t, "p": q, "op": opname, "limbs": L,
