@@ -13,7 +13,7 @@ import torch  # noqa: E402
 
 import paper_1705_04807_b200 as mh  # noqa: E402
 
-n, q = 16384, 65521
+n, q = 16384, int(os.environ.get("AB_Q", "65521"))
 lay, mod = mh.Layout(n, 64), mh.Modulus(q)
 fl = [torch.randint(0, q, (n * n,), dtype=torch.int32, device="cuda") for _ in range(3)]
 A, B, C = (mh.Matrix.wrap(lay, mod, f.data_ptr(), owner=f) for f in fl)
