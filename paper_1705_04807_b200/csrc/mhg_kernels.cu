@@ -714,7 +714,15 @@ struct GemmCfg {
     // C path with a 4 KB per-warp transpose buffer, the narrow-tile primes keep
     // row-per-thread C access (see epilogue_role)
     static constexpr bool XPOSE = (W == 128);
-    static constexpr int EPI_WARPS = 8;
+#ifndef MHG_SMR
+#define MHG_SMR 0
+#endif
+    // SMR (setmaxnreg layout, W = 128): warpgroup 0 = producer, MMA issuer, 2 idle warps,
+    // shrunk to 40 registers; warpgroups 1-4 = 16 epilogue warps x 32 columns, grown to 104
+    // (the CTA keeps its launch allocation, 640 x 96: 128 x 40 + 512 x 104 <= 61440)
+    static constexpr bool SMR = XPOSE && MHG_SMR;
+    static constexpr int EPI_WARPS = SMR ? 16 : 8;
+    static constexpr int EPI_W0 = SMR ? 4 : 2;  // first epilogue warp
     static constexpr int XBUF = XPOSE ? EPI_WARPS * (W * 4 / EPI_WARPS >= 64 ? 4096 : 2048) : 0;
     static constexpr int FIXED = 1024 /*align slack*/ + 256 /*barriers*/ + 8 * W /*column offsets*/ + XBUF;
     static constexpr int STAGES_RAW = (232448 - FIXED) / STAGE;
@@ -722,7 +730,7 @@ struct GemmCfg {
     static constexpr int SMEM = FIXED + STAGES * STAGE;
     static_assert(SMEM <= 232448, "227 KB dynamic shared memory limit");
     static constexpr int EPI_THREADS = EPI_WARPS * 32;
-    static constexpr int THREADS = 64 + EPI_THREADS;    // producer, MMA, epilogue warps
+    static constexpr int THREADS = 32 * EPI_W0 + EPI_THREADS;  // producer, MMA, (idle,) epilogue
     static_assert(CLASSES * W <= 512, "TMEM columns");
     static_assert(STAGES >= 2, "pipeline depth");
 };
@@ -834,7 +842,8 @@ __device__ __forceinline__ void tmem_wait_st() {
 // geometry (no table loads).  Otherwise (narrow tiles, CTA pair) the row's
 // C_old is prefetched into registers at tile start, addressed through smem
 // column offsets.
-template <int L, int W, int EPI_WARPS, bool PAIR, bool XPOSE = false, int FOLD = 3, bool NPAIR = false>
+template <int L, int W, int EPI_WARPS, bool PAIR, bool XPOSE = false, int FOLD = 3, bool NPAIR = false,
+          int EPI_W0 = 2>
 __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t first_tile,
                                               uint32_t tile_stride, uint32_t num_tiles,
                                               uint32_t row_groups, uint32_t rank, uint32_t nchunks,
@@ -846,7 +855,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     constexpr int CLASSES = 2 * L - 1;
     constexpr int CW = L <= 2 ? 16 : 8;  // TMEM columns per drain step (x8 / x32 measured slower)
     constexpr uint64_t kNoCol = ~uint64_t(0);
-    const int ew = warp - 2;
+    const int ew = warp - EPI_W0;
     const int quad = warp & 3;
     const int jb = (ew >> 2) * WH;  // first tile column of this warp
     const int row = quad * 32 + lane;
@@ -1299,127 +1308,135 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0) {
-        // ---------------- producer: one bulk copy per operand per stage
-        if (lane == 0) {
-            int st = 0;
-            uint32_t ph = 0;
-            long long wait_empty = 0;
-            uint32_t ord = 0;
-            const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
-            for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride, ++ord) {
-                uint32_t m, n;
-                tile_coords(tile, p.Mt, npairs, p.group, m, n);
-                if (MC) n = 2 * n + rank;
-                const int8_t* a_src = p.apack + (uint64_t)m * p.Kt * Cfg::A_STAGE;
-                const int8_t* b_src = p.bpack + (uint64_t)n * p.Kt * Cfg::B_STAGE;
-                // serpentine K: odd tiles of a CTA sweep K backwards, so the next wave
-                // starts on the panel slices the previous wave just left in L2
-                const bool rev = p.serpentine && (ord & 1);
-                for (uint32_t j = 0; j < p.Kt; ++j) {
-                    const uint32_t kt = rev ? p.Kt - 1 - j : j;
-                    const long long w0 = clock64();
-                    mbar_wait_hint(&empty[st], ph ^ 1, (p.wait_roles & 1) ? p.wait_hint : 0u);
-                    wait_empty += clock64() - w0;
-                    mbar_expect_tx(&full[st], Cfg::STAGE);
-                    if constexpr (MC) {
-                        // this CTA's half of the lhs stage, to both CTAs (same offset)
-                        constexpr uint32_t HALF = Cfg::A_STAGE / 2;
-                        bulk_g2s_mc_hint(sA + st * Cfg::A_STAGE + rank * HALF,
-                                         a_src + (uint64_t)kt * Cfg::A_STAGE + rank * HALF, HALF,
-                                         &full[st], (uint16_t)0x3, pol_keep);
-                        bulk_g2s_hint(sB + st * Cfg::B_STAGE, b_src + (uint64_t)kt * Cfg::B_STAGE,
-                                      Cfg::B_STAGE, &full[st], pol_stream);
-                    } else if (p.l2_hints) {
-                        // lhs panels of the raster group are re-read by the next waves;
-                        // rhs panels only by the current one
-                        bulk_g2s_hint(sA + st * Cfg::A_STAGE, a_src + (uint64_t)kt * Cfg::A_STAGE,
-                                      Cfg::A_STAGE, &full[st], pol_keep);
-                        bulk_g2s_hint(sB + st * Cfg::B_STAGE, b_src + (uint64_t)kt * Cfg::B_STAGE,
-                                      Cfg::B_STAGE, &full[st], pol_stream);
-                    } else {
-                        bulk_g2s(sA + st * Cfg::A_STAGE, a_src + (uint64_t)kt * Cfg::A_STAGE,
-                                 Cfg::A_STAGE, &full[st]);
-                        bulk_g2s(sB + st * Cfg::B_STAGE, b_src + (uint64_t)kt * Cfg::B_STAGE,
-                                 Cfg::B_STAGE, &full[st]);
-                    }
-                    if (++st == ring) {
-                        st = 0;
-                        ph ^= 1;
-                    }
-                }
-            }
-            if (p.stats) p.stats[(uint64_t)blockIdx.x * kStatCount + kStatProdWaitEmpty] = wait_empty;
-        }
-    } else if (warp == 1) {
-        // ---------------- MMA issuer (single thread)
-        if (lane == 0) {
-            constexpr uint32_t id_full = idesc_i8(kBM, Cfg::NB);
-            constexpr uint32_t id_head = idesc_i8(kBM, (L > 1 ? L - 1 : 1) * W);
-            constexpr uint32_t id_one = idesc_i8(kBM, W);
-            const bool alt_layout = early_release<L>(p);
-            int st = 0;
-            uint32_t ph = 0, acc_ph = 0;
-            long long wait_full = 0, wait_tmem = 0;
-            const long long t_begin = clock64();
-            for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride) {
-                for (uint32_t c = 0; c < nchunks; ++c) {
-                    const uint32_t kb = c * p.KC;
-                    const uint32_t ke = (kb + p.KC < p.Kt) ? kb + p.KC : p.Kt;
-                    long long w0 = clock64();
-                    mbar_wait_hint(tmem_empty, acc_ph ^ 1, (p.wait_roles & 2) ? p.wait_hint : 0u);
-                    wait_tmem += clock64() - w0;
-                    tc_fence_after();
-                    for (uint32_t kt = kb; kt < ke; ++kt) {
-                        w0 = clock64();
-                        mbar_wait_hint(&full[st], ph, (p.wait_roles & 2) ? p.wait_hint : 0u);
-                        wait_full += clock64() - w0;
-                        tc_fence_after();
-                        const uint32_t a0 = smem_u32(sA + st * Cfg::A_STAGE);
-                        const uint32_t b0 = smem_u32(sB + st * Cfg::B_STAGE);
-#pragma unroll
-                        for (int kk = 0; kk < kBK / 32; ++kk) {
-                            const bool first = (kt == kb) && (kk == 0);
-                            const uint64_t bd = sdesc(b0 + kk * 32);
-#pragma unroll
-                            for (int s = 0; s < L; ++s) {
-                                const uint64_t ad = sdesc(a0 + s * kBM * kBK + kk * 32);
-                                // accumulation jobs alternate TMEM bases 0 / W where the
-                                // epilogue uses the early release (see epilogue_role)
-                                const uint32_t d = tmem + ((alt_layout && acc_ph) ? W : 0) + s * W;
-                                if (!first) {
-                                    mma_i8(d, ad, bd, id_full, 1u);
-                                } else if (s == 0) {
-                                    mma_i8(d, ad, bd, id_full, 0u);
-                                } else {
-                                    // classes s..s+L-2 already hold a product; class
-                                    // s+L-1 is touched for the first time
-                                    mma_i8(d, ad, bd, id_head, 1u);
-                                    mma_i8(d + (L - 1) * W, ad,
-                                           sdesc(b0 + (L - 1) * W * kBK + kk * 32), id_one, 0u);
-                                }
-                            }
+
+    // roles.  SMR: warpgroup 0 (producer, MMA issuer, 2 idle warps) executes one
+    // setmaxnreg.dec and the epilogue warpgroups one setmaxnreg.inc, each dominating its
+    // role's code so ptxas allocates that region to the new budget.
+    if (warp < Cfg::EPI_W0) {
+        if constexpr (Cfg::SMR) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
+        if (warp == 0) {
+            // ---------------- producer: one bulk copy per operand per stage
+            if (lane == 0) {
+                int st = 0;
+                uint32_t ph = 0;
+                long long wait_empty = 0;
+                uint32_t ord = 0;
+                const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
+                for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride, ++ord) {
+                    uint32_t m, n;
+                    tile_coords(tile, p.Mt, npairs, p.group, m, n);
+                    if (MC) n = 2 * n + rank;
+                    const int8_t* a_src = p.apack + (uint64_t)m * p.Kt * Cfg::A_STAGE;
+                    const int8_t* b_src = p.bpack + (uint64_t)n * p.Kt * Cfg::B_STAGE;
+                    // serpentine K: odd tiles of a CTA sweep K backwards, so the next wave
+                    // starts on the panel slices the previous wave just left in L2
+                    const bool rev = p.serpentine && (ord & 1);
+                    for (uint32_t j = 0; j < p.Kt; ++j) {
+                        const uint32_t kt = rev ? p.Kt - 1 - j : j;
+                        const long long w0 = clock64();
+                        mbar_wait_hint(&empty[st], ph ^ 1, (p.wait_roles & 1) ? p.wait_hint : 0u);
+                        wait_empty += clock64() - w0;
+                        mbar_expect_tx(&full[st], Cfg::STAGE);
+                        if constexpr (MC) {
+                            // this CTA's half of the lhs stage, to both CTAs (same offset)
+                            constexpr uint32_t HALF = Cfg::A_STAGE / 2;
+                            bulk_g2s_mc_hint(sA + st * Cfg::A_STAGE + rank * HALF,
+                                             a_src + (uint64_t)kt * Cfg::A_STAGE + rank * HALF, HALF,
+                                             &full[st], (uint16_t)0x3, pol_keep);
+                            bulk_g2s_hint(sB + st * Cfg::B_STAGE, b_src + (uint64_t)kt * Cfg::B_STAGE,
+                                          Cfg::B_STAGE, &full[st], pol_stream);
+                        } else if (p.l2_hints) {
+                            // lhs panels of the raster group are re-read by the next waves;
+                            // rhs panels only by the current one
+                            bulk_g2s_hint(sA + st * Cfg::A_STAGE, a_src + (uint64_t)kt * Cfg::A_STAGE,
+                                          Cfg::A_STAGE, &full[st], pol_keep);
+                            bulk_g2s_hint(sB + st * Cfg::B_STAGE, b_src + (uint64_t)kt * Cfg::B_STAGE,
+                                          Cfg::B_STAGE, &full[st], pol_stream);
+                        } else {
+                            bulk_g2s(sA + st * Cfg::A_STAGE, a_src + (uint64_t)kt * Cfg::A_STAGE,
+                                     Cfg::A_STAGE, &full[st]);
+                            bulk_g2s(sB + st * Cfg::B_STAGE, b_src + (uint64_t)kt * Cfg::B_STAGE,
+                                     Cfg::B_STAGE, &full[st]);
                         }
-                        if constexpr (MC) tc_commit_mc(&empty[st], (uint16_t)0x3);
-                        else tc_commit(&empty[st]);
                         if (++st == ring) {
                             st = 0;
                             ph ^= 1;
                         }
                     }
-                    tc_commit(tmem_full);
-                    acc_ph ^= 1;
                 }
+                if (p.stats) p.stats[(uint64_t)blockIdx.x * kStatCount + kStatProdWaitEmpty] = wait_empty;
             }
-            if (p.stats) {
-                unsigned long long* o = p.stats + (uint64_t)blockIdx.x * kStatCount;
-                o[kStatTotal] = clock64() - t_begin;
-                o[kStatMmaWaitFull] = wait_full;
-                o[kStatMmaWaitTmem] = wait_tmem;
+        } else if (warp == 1) {
+            // ---------------- MMA issuer (single thread)
+            if (lane == 0) {
+                constexpr uint32_t id_full = idesc_i8(kBM, Cfg::NB);
+                constexpr uint32_t id_head = idesc_i8(kBM, (L > 1 ? L - 1 : 1) * W);
+                constexpr uint32_t id_one = idesc_i8(kBM, W);
+                const bool alt_layout = early_release<L>(p);
+                int st = 0;
+                uint32_t ph = 0, acc_ph = 0;
+                long long wait_full = 0, wait_tmem = 0;
+                const long long t_begin = clock64();
+                for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride) {
+                    for (uint32_t c = 0; c < nchunks; ++c) {
+                        const uint32_t kb = c * p.KC;
+                        const uint32_t ke = (kb + p.KC < p.Kt) ? kb + p.KC : p.Kt;
+                        long long w0 = clock64();
+                        mbar_wait_hint(tmem_empty, acc_ph ^ 1, (p.wait_roles & 2) ? p.wait_hint : 0u);
+                        wait_tmem += clock64() - w0;
+                        tc_fence_after();
+                        for (uint32_t kt = kb; kt < ke; ++kt) {
+                            w0 = clock64();
+                            mbar_wait_hint(&full[st], ph, (p.wait_roles & 2) ? p.wait_hint : 0u);
+                            wait_full += clock64() - w0;
+                            tc_fence_after();
+                            const uint32_t a0 = smem_u32(sA + st * Cfg::A_STAGE);
+                            const uint32_t b0 = smem_u32(sB + st * Cfg::B_STAGE);
+    #pragma unroll
+                            for (int kk = 0; kk < kBK / 32; ++kk) {
+                                const bool first = (kt == kb) && (kk == 0);
+                                const uint64_t bd = sdesc(b0 + kk * 32);
+    #pragma unroll
+                                for (int s = 0; s < L; ++s) {
+                                    const uint64_t ad = sdesc(a0 + s * kBM * kBK + kk * 32);
+                                    // accumulation jobs alternate TMEM bases 0 / W where the
+                                    // epilogue uses the early release (see epilogue_role)
+                                    const uint32_t d = tmem + ((alt_layout && acc_ph) ? W : 0) + s * W;
+                                    if (!first) {
+                                        mma_i8(d, ad, bd, id_full, 1u);
+                                    } else if (s == 0) {
+                                        mma_i8(d, ad, bd, id_full, 0u);
+                                    } else {
+                                        // classes s..s+L-2 already hold a product; class
+                                        // s+L-1 is touched for the first time
+                                        mma_i8(d, ad, bd, id_head, 1u);
+                                        mma_i8(d + (L - 1) * W, ad,
+                                               sdesc(b0 + (L - 1) * W * kBK + kk * 32), id_one, 0u);
+                                    }
+                                }
+                            }
+                            if constexpr (MC) tc_commit_mc(&empty[st], (uint16_t)0x3);
+                            else tc_commit(&empty[st]);
+                            if (++st == ring) {
+                                st = 0;
+                                ph ^= 1;
+                            }
+                        }
+                        tc_commit(tmem_full);
+                        acc_ph ^= 1;
+                    }
+                }
+                if (p.stats) {
+                    unsigned long long* o = p.stats + (uint64_t)blockIdx.x * kStatCount;
+                    o[kStatTotal] = clock64() - t_begin;
+                    o[kStatMmaWaitFull] = wait_full;
+                    o[kStatMmaWaitTmem] = wait_tmem;
+                }
             }
         }
     } else {
-        epilogue_role<L, W, Cfg::EPI_WARPS, false, Cfg::XPOSE, FOLD, MC>(
+        if constexpr (Cfg::SMR) asm volatile("setmaxnreg.inc.sync.aligned.u32 104;\n" ::: "memory");
+        epilogue_role<L, W, Cfg::EPI_WARPS, false, Cfg::XPOSE, FOLD, MC, Cfg::EPI_W0>(
             p, first_tile, tile_stride, num_tiles, p.Mt, rank, nchunks, tmem, s_col, tmem_full,
             tmem_empty, warp, lane, xbuf);
     }
