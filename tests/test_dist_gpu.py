@@ -63,3 +63,26 @@ def test_multi_rank_update_matches_oracle(gpu, mh, oracle, tmp_path, world, op_n
     want = out.copy()
     oracle.mm_dense(n, t, q, want, lhs, rhs, Views(0, 0, 0, n, n, n), op=oop)
     assert np.array_equal(got, want)
+
+
+@pytest.mark.gpu
+@pytest.mark.slow
+def test_bench_two_ranks_runs_end_to_end(gpu, mh, tmp_path):
+    """bench.py --gpus 2 under torch.distributed.run (both ranks on cuda:0, gloo:
+    MHG_BENCH_SHARED_GPU=1) prints one well-formed JSON line from rank 0."""
+    import json
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, MHG_BENCH_SHARED_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py",
+           "--gpus", "2", "--workload", "cfg2", "--steps", "3", "--warmup", "3", "--e2e-steps", "2"]
+    out = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
+    assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
