@@ -300,8 +300,9 @@ def e2e_ranked(torch, dist, flats, out_f, step, stream, b, e, steps, macs, dev, 
     return {"value": macs / (float(t[0]) * 1e-3), "unit": UNIT,
             "h2d_bytes_per_step": 3 * (e - b) * 4, "d2h_bytes_per_step": (e - b) * 4,
             "steps": steps, "ms_per_step": float(t[0]),
-            "path": "per-rank pinned slices -> segmented panel broadcasts (NCCL) overlapped with "
-                    "per-segment mhg_plan_run -> slice read-back"}
+            "path": "per-rank pinned slices -> per segment: owner packs its A / B part "
+                    "(mhg_plan_pack), packed limb planes broadcast (NCCL) overlapped with the "
+                    "previous segment's mhg_plan_gemm -> slice read-back"}
 
 
 def run_gpu(args, rank, world, local_rank):
@@ -309,7 +310,8 @@ def run_gpu(args, rank, world, local_rank):
     import torch.distributed as dist
 
     import paper_1705_04807_b200 as mh
-    from paper_1705_04807_b200.dist import PanelExchange, rank_update, segment_plans, slice_range
+    from paper_1705_04807_b200.dist import (PanelExchange, rank_update, rank_update_packed,
+                                            segment_plans, slice_range)
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -359,7 +361,11 @@ def run_gpu(args, rank, world, local_rank):
         plans = segment_plans(mh, ex, A, B, Cm, op)
     plan = plans[0]
     info = plan.info()
-    launches_per_step = sum(pl.info()["launches"] for pl in plans)
+    if world > 1 and os.environ.get("MHG_EXCHANGE") != "u32":
+        # packed exchange: one GEMM per segment + the packs of the parts this rank owns
+        launches_per_step = sum(1 + (rank == sg.a_owner) + (rank == sg.b_owner) for sg in segs)
+    else:
+        launches_per_step = sum(pl.info()["launches"] for pl in plans)
 
     def barrier():
         if world > 1:
@@ -369,9 +375,13 @@ def run_gpu(args, rank, world, local_rank):
         if world == 1:
             plan.run(stream)
             return
-        # segment j+1's broadcasts are enqueued before segment j's GEMM: NCCL waits
-        # for the GEMMs already queued, then overlaps this one
-        rank_update(ex, plans, lhs_f, rhs_f, stream)
+        # packed limb planes on the wire (each owner packs its part; segment j+1's
+        # pack + broadcasts are enqueued before segment j's GEMM); MHG_EXCHANGE=u32
+        # exchanges the uint32 cells and packs every panel locally instead
+        if os.environ.get("MHG_EXCHANGE") == "u32":
+            rank_update(ex, plans, lhs_f, rhs_f, stream)
+        else:
+            rank_update_packed(ex, plans, stream)
 
     W = max(args.warmup, 3)
     for _ in range(W):
@@ -457,7 +467,8 @@ def run_gpu(args, rank, world, local_rank):
                        "t": t, "p": q, "op": opname, "limbs": L,
                        "tiles": info["tiles"], "k_chunks": info["k_chunks"],
                        "partition": f"C-stationary Morton blocks over {world} GPU(s)"
-                                    + (f", {len(plans)} K segments pipelined with NCCL broadcasts"
+                                    + (f", {len(plans)} K segments pipelined with NCCL broadcasts "
+                                       "of packed limb planes"
                                        if world > 1 else ""),
                        "l2": "no flush: operands 3 x %.2f GiB >> 126 MB L2" % (n * n * 4 / 2 ** 30)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "conversion": conversion,

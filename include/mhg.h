@@ -140,6 +140,17 @@ mhg_status mhg_counters_layout(uint64_t n, uint64_t t, uint64_t out_origin, uint
  * mhg_plan_run.  The views' containers must outlive the plan. */
 mhg_status mhg_plan_create(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, mhg_plan *plan);
 mhg_status mhg_plan_run(mhg_plan plan, void *stream);
+/* Split execution of a plan, for exchanging PACKED operands between ranks
+ * (multi-GPU: 2-byte limb planes instead of uint32 cells):
+ *   mhg_plan_pack        pack one operand of the plan's views (which = 0: lhs, 1: rhs)
+ *                        into the plan's workspace (lhs digits negated for SUB);
+ *   mhg_plan_pack_buffer device pointer and byte size of that packed operand -- plans
+ *                        of equal geometry (same operand shape, q, op) share its layout;
+ *   mhg_plan_gemm        the GEMM + epilogue on the current packs (no packing).
+ * mhg_plan_run == pack(lhs) + pack(rhs) + gemm. */
+mhg_status mhg_plan_pack(mhg_plan plan, int which, void *stream);
+mhg_status mhg_plan_pack_buffer(mhg_plan plan, int which, void **ptr, uint64_t *bytes);
+mhg_status mhg_plan_gemm(mhg_plan plan, void *stream);
 mhg_status mhg_plan_counters(mhg_plan plan, mhg_counters *ctr);
 /* Kernel launches per run and the planner's description (tiles, chunks, limbs). */
 mhg_status mhg_plan_info(mhg_plan plan, uint64_t *launches, uint64_t *tiles, uint32_t *limbs,

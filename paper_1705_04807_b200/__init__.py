@@ -123,6 +123,9 @@ def lib():
         "mhg_counters_layout": ([u64] * 8 + [P(Counters)], C.c_int),
         "mhg_plan_create": ([_View, _View, _View, C.c_int, P(vp)], C.c_int),
         "mhg_plan_run": ([vp, vp], C.c_int),
+        "mhg_plan_pack": ([vp, C.c_int, vp], C.c_int),
+        "mhg_plan_pack_buffer": ([vp, C.c_int, P(vp), P(u64)], C.c_int),
+        "mhg_plan_gemm": ([vp, vp], C.c_int),
         "mhg_plan_counters": ([vp, P(Counters)], C.c_int),
         "mhg_plan_info": ([vp, P(u64), P(u64), P(u32), P(u32), P(u64)], C.c_int),
         "mhg_plan_destroy": ([vp], C.c_int),
@@ -396,6 +399,31 @@ class Plan:
 
     def run(self, stream=None):
         _check(lib().mhg_plan_run(self._h, _stream_ptr(stream)))
+
+    # -- split execution (multi-GPU packed-panel exchange, see dist.rank_update_packed)
+    def pack(self, which: int, stream=None):
+        """Pack the lhs (0) or rhs (1) view into this plan's workspace."""
+        _check(lib().mhg_plan_pack(self._h, which, _stream_ptr(stream)))
+
+    def pack_buffer(self, which: int):
+        """The packed lhs (0) / rhs (1) bytes as a zero-copy uint8 CUDA tensor view of
+        the plan's workspace (valid while the plan lives); plans of equal geometry
+        share its layout, so it can be broadcast between ranks."""
+        import torch
+        ptr, nb = C.c_void_p(), C.c_uint64()
+        _check(lib().mhg_plan_pack_buffer(self._h, which, C.byref(ptr), C.byref(nb)))
+
+        class _Buf:  # __cuda_array_interface__ v3 wrapper for torch.as_tensor
+            def __init__(self, p, n):
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": "|u1",
+                                                 "data": (p, False), "version": 3}
+        if not nb.value:
+            return torch.empty(0, dtype=torch.uint8, device="cuda")
+        return torch.as_tensor(_Buf(ptr.value, nb.value), device="cuda")
+
+    def gemm(self, stream=None):
+        """The GEMM + epilogue on the current packs (no packing)."""
+        _check(lib().mhg_plan_gemm(self._h, _stream_ptr(stream)))
 
     def counters(self) -> Counters:
         c = Counters()

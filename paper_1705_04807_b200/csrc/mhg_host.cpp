@@ -321,13 +321,33 @@ struct Fork {
 };
 
 // Pack both operands and run the GEMM: 2 pack launches + 1 GEMM launch.
+// Pack one operand of a multiply into its stage image (which = 0: lhs, K-major rows;
+// 1: rhs, transposed).  The lhs digits of C -= A.B are negated here.
+void launch_pack_operand(const Buffers& b, const mhg_view& out, const mhg_view& v, const Checked& c,
+                         const mhg::GemmGeometry& g, mhg_op op, int which, void* stream) {
+    const mhg::LimbParams lp = mhg::limb_params(out.mat->q);
+    const int vecok = out.mat->t % 4 == 0;
+    if (which == 0) {
+        const mhg::DigitParams dl{out.mat->q, lp.H, op == MHG_OP_SUB ? 1 : 0};
+        cuda_check(mhg::launch_pack((int)g.L, 0, v.mat->cells, b.lhs_row, b.lhs_col, vecok, c.rl.rows,
+                                    c.rl.cols, mhg::kBM, g.Mt, g.Kt, b.apack, dl, stream),
+                   "pack lhs");
+    } else {
+        const mhg::DigitParams dr{out.mat->q, lp.H, 0};
+        cuda_check(mhg::launch_pack((int)g.L, 1, v.mat->cells, b.rhs_row, b.rhs_col, vecok, c.rr.cols,
+                                    c.rr.rows, g.W, g.Nt, g.Kt, b.bpack, dr, stream),
+                   "pack rhs");
+    }
+}
+
+void launch_gemm_stage(const Buffers& b, const mhg_view& out, const Checked& c,
+                       const mhg::GemmGeometry& g, mhg_op op, void* stream,
+                       cudaEvent_t gemm_begin = nullptr, cudaEvent_t gemm_end = nullptr);
+
 void launch_multiply(const Buffers& b, const mhg_view& out, const mhg_view& lhs,
                      const mhg_view& rhs, const Checked& c, const mhg::GemmGeometry& g,
                      mhg_op op, void* stream, cudaEvent_t gemm_begin = nullptr,
                      cudaEvent_t gemm_end = nullptr, const Fork* fork = nullptr) {
-    const mhg::LimbParams lp = mhg::limb_params(out.mat->q);
-    mhg::DigitParams dl{out.mat->q, lp.H, op == MHG_OP_SUB ? 1 : 0};
-    mhg::DigitParams dr{out.mat->q, lp.H, 0};
     // with a fork (graph capture), the two independent packs become parallel
     // branches joined before the GEMM
     void* rhs_stream = stream;
@@ -336,17 +356,19 @@ void launch_multiply(const Buffers& b, const mhg_view& out, const mhg_view& lhs,
         cuda_check(cudaStreamWaitEvent(fork->side, fork->split, 0), "fork");
         rhs_stream = fork->side;
     }
-    const int vecok = out.mat->t % 4 == 0;
-    cuda_check(mhg::launch_pack((int)g.L, 0, lhs.mat->cells, b.lhs_row, b.lhs_col, vecok, c.rl.rows,
-                                c.rl.cols, mhg::kBM, g.Mt, g.Kt, b.apack, dl, stream),
-               "pack lhs");
-    cuda_check(mhg::launch_pack((int)g.L, 1, rhs.mat->cells, b.rhs_row, b.rhs_col, vecok, c.rr.cols,
-                                c.rr.rows, g.W, g.Nt, g.Kt, b.bpack, dr, rhs_stream),
-               "pack rhs");
+    launch_pack_operand(b, out, lhs, c, g, op, 0, stream);
+    launch_pack_operand(b, out, rhs, c, g, op, 1, rhs_stream);
     if (fork) {
         cuda_check(cudaEventRecord(fork->join, fork->side), "join");
         cuda_check(cudaStreamWaitEvent((cudaStream_t)stream, fork->join, 0), "join");
     }
+    launch_gemm_stage(b, out, c, g, op, stream, gemm_begin, gemm_end);
+}
+
+// The GEMM on the current packs (+ the opt-in MHG_GEMM_STATS report).
+void launch_gemm_stage(const Buffers& b, const mhg_view& out, const Checked& c,
+                       const mhg::GemmGeometry& g, mhg_op op, void* stream, cudaEvent_t gemm_begin,
+                       cudaEvent_t gemm_end) {
     mhg::GemmParams p = gemm_params(b, out, c, g, op);
     // diagnostics: MHG_GEMM_STATS=1 prints per-CTA wait-cycle shares (synchronous)
     static const bool stats_on = std::getenv("MHG_GEMM_STATS") != nullptr;
@@ -768,6 +790,50 @@ mhg_status mhg_plan_create_ex(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op o
             }
         }
         *plan = p;
+    });
+}
+
+// Split execution (multi-GPU panel exchange, paper_1705_04807_b200/dist.py): the owner
+// of a segment's operand packs it into the plan's workspace, the packed bytes are
+// broadcast to the ranks whose plans have the same geometry, each runs the GEMM.
+mhg_status mhg_plan_pack(mhg_plan p, int which, void* stream) {
+    return guarded([&] {
+        if (!p || (which != 0 && which != 1)) fail(MHG_ERR_INVALID_ARGUMENT, "plan_pack: bad args");
+        if (p->empty) return;
+        launch_pack_operand(p->buf, p->out, which == 0 ? p->lhs : p->rhs, p->chk, p->geo, p->op, which,
+                            stream);
+    });
+}
+
+mhg_status mhg_plan_pack_buffer(mhg_plan p, int which, void** ptr, uint64_t* bytes) {
+    return guarded([&] {
+        if (!p || !ptr || !bytes || (which != 0 && which != 1))
+            fail(MHG_ERR_INVALID_ARGUMENT, "plan_pack_buffer: bad args");
+        *ptr = p->empty ? nullptr : (which == 0 ? (void*)p->buf.apack : (void*)p->buf.bpack);
+        *bytes = p->empty ? 0 : (which == 0 ? p->geo.apack_bytes : p->geo.bpack_bytes);
+    });
+}
+
+mhg_status mhg_plan_gemm(mhg_plan p, void* stream) {
+    return guarded([&] {
+        if (!p) fail(MHG_ERR_INVALID_ARGUMENT, "plan_gemm: null plan");
+        if (p->empty) return;
+        if (p->chk.rl.cols == 0) fail(MHG_ERR_INVALID_ARGUMENT, "plan_gemm: empty inner dimension");
+        cudaEvent_t b = nullptr, e = nullptr;
+        if (p->profiling) {
+            if (p->ev_used + 2 > p->ev.size()) {
+                const size_t grow = p->ev.size() ? p->ev.size() : 64;
+                for (size_t i = 0; i < grow; ++i) {
+                    cudaEvent_t ev;
+                    cuda_check(cudaEventCreate(&ev), "event");
+                    p->ev.push_back(ev);
+                }
+            }
+            b = p->ev[p->ev_used];
+            e = p->ev[p->ev_used + 1];
+            p->ev_used += 2;
+        }
+        launch_gemm_stage(p->buf, p->out, p->chk, p->geo, p->op, stream, b, e);
     });
 }
 

@@ -208,3 +208,34 @@ def rank_update(ex: PanelExchange, plans, lhs_flat, rhs_flat, stream=None):
         pending = (ex.exchange_segment(segs[j + 1], lhs_flat, rhs_flat, async_op=True)
                    if j + 1 < len(segs) else [])
         pl.run(stream)
+
+
+def rank_update_packed(ex: PanelExchange, plans, stream=None):
+    """This rank's update with PACKED panels on the wire (2-byte limb
+    planes for p < 2^16 instead of uint32 cells): for every K segment, the owner
+    of the A part packs it into its segment plan's workspace and broadcasts the
+    packed bytes inside the row group (all members hold plans of the same lhs
+    geometry), the B part likewise inside the column group; every rank then runs
+    the segment's GEMM on the received packs.  Each rank packs only its own data.
+    Segment j+1's pack + broadcasts are enqueued before segment j's GEMM."""
+    import torch.distributed as dist
+
+    segs = ex.segments()
+
+    def issue(j):
+        sg, pl, works = segs[j], plans[j], []
+        for which, owner, members, group in ((0, sg.a_owner, ex.row_members, ex.row_group),
+                                             (1, sg.b_owner, ex.col_members, ex.col_group)):
+            if ex.rank == owner:
+                pl.pack(which, stream)
+            if len(members) > 1:
+                works.append(dist.broadcast(pl.pack_buffer(which), src=owner, group=group,
+                                            async_op=True))
+        return works
+
+    pending = issue(0)
+    for j, pl in enumerate(plans):
+        for wk in pending:
+            wk.wait()
+        pending = issue(j + 1) if j + 1 < len(plans) else []
+        pl.gemm(stream)

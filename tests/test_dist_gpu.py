@@ -19,13 +19,14 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, t, q, op, outdir):
+def _worker(rank, world, port, n, t, q, op, outdir, packed=False):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
     import torch.distributed as dist
 
     import paper_1705_04807_b200 as mh
-    from paper_1705_04807_b200.dist import PanelExchange, rank_update, segment_plans, slice_range
+    from paper_1705_04807_b200.dist import (PanelExchange, rank_update, rank_update_packed,
+                                            segment_plans, slice_range)
 
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -42,7 +43,10 @@ def _worker(rank, world, port, n, t, q, op, outdir):
         A, B, C = (mh.Matrix.wrap(lay, mod, f.data_ptr(), owner=f) for f in flats)
         ex = PanelExchange(world, rank, n, t)
         plans = segment_plans(mh, ex, A, B, C, op)
-        rank_update(ex, plans, flats[1], flats[2])
+        if packed:
+            rank_update_packed(ex, plans)
+        else:
+            rank_update(ex, plans, flats[1], flats[2])
         torch.cuda.synchronize()
         np.save(os.path.join(outdir, f"slice{rank}.npy"), flats[0][lo:hi].cpu().numpy().view(np.uint32))
     finally:
@@ -50,13 +54,19 @@ def _worker(rank, world, port, n, t, q, op, outdir):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,op_name", [(2, "sub"), (4, "set")])
-def test_multi_rank_update_matches_oracle(gpu, mh, oracle, tmp_path, world, op_name):
+@pytest.mark.parametrize("world,op_name,packed", [(2, "sub", False), (4, "set", False),
+                                                  (2, "sub", True), (4, "sub", True),
+                                                  (4, "set", True)])
+def test_multi_rank_update_matches_oracle(gpu, mh, oracle, tmp_path, world, op_name, packed):
+    """Both exchange modes: uint32 cells (rank_update) and packed limb planes
+    (rank_update_packed: owners pack, packed bytes are broadcast, every rank runs
+    only the GEMM)."""
     n, t, q = 256, 32, 65521
     from oracle.binding import OP_SET, OP_SUB, Views
     op = {"sub": mh.OP_SUB, "set": mh.OP_SET}[op_name]
     oop = {"sub": OP_SUB, "set": OP_SET}[op_name]
-    mp.spawn(_worker, args=(world, _free_port(), n, t, q, op, str(tmp_path)), nprocs=world, join=True)
+    mp.spawn(_worker, args=(world, _free_port(), n, t, q, op, str(tmp_path), packed), nprocs=world,
+             join=True)
     got = np.concatenate([np.load(tmp_path / f"slice{r}.npy") for r in range(world)])
     rng = np.random.default_rng(77)
     out, lhs, rhs = [rng.integers(0, q, n * n, dtype=np.uint32) for _ in range(3)]
