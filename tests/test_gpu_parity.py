@@ -610,3 +610,39 @@ def test_concurrent_calls_on_streams(gpu, mh, oracle):
     assert not errors, errors
     for A, _, _, _, want in jobs:
         assert np.array_equal(A.cells(), want)
+
+
+def test_split_plan_execution(gpu, mh, oracle):
+    """mhg_plan_pack / pack_buffer / gemm (the packed multi-GPU exchange): packing
+    both operands then running the GEMM equals the oracle; a packed operand copied
+    into another plan of the same geometry is consumed as-is; bad arguments raise."""
+    import torch
+
+    n, t, q = 256, 32, P16
+    out, lhs, rhs = _fill(oracle, 1700, n, q)
+    A, B, Cm = _containers(mh, n, t, q, (out, lhs, rhs))
+    v = _views_from(oracle, n, t, 200, 150, 170, [30, 40, 20, 60, 50, 70])
+    prob = mh.Problem(mh.Sub(A, v.out_origin, v.rows, v.cols), mh.Sub(B, v.lhs_origin, v.rows, v.inner),
+                      mh.Sub(Cm, v.rhs_origin, v.inner, v.cols))
+    pl = mh.Plan(prob, mh.OP_SUB)
+    pl.pack(0)
+    pl.pack(1)
+    pl.gemm()
+    torch.cuda.synchronize()
+    want = out.copy()
+    oracle.mm_dense(n, t, q, want, lhs, rhs, v, op=OP_SUB)
+    assert np.array_equal(A.cells(), want)
+    # a second plan over the same shapes on other containers, fed the first plan's packs
+    A2, B2, C2 = _containers(mh, n, t, q, (out, np.zeros_like(lhs), np.zeros_like(rhs)))
+    pl2 = mh.Plan(mh.Problem(mh.Sub(A2, v.out_origin, v.rows, v.cols),
+                             mh.Sub(B2, v.lhs_origin, v.rows, v.inner),
+                             mh.Sub(C2, v.rhs_origin, v.inner, v.cols)), mh.OP_SUB)
+    for which in (0, 1):
+        dst, src = pl2.pack_buffer(which), pl.pack_buffer(which)
+        assert dst.numel() == src.numel() > 0
+        dst.copy_(src)
+    pl2.gemm()
+    torch.cuda.synchronize()
+    assert np.array_equal(A2.cells(), want)
+    with pytest.raises(mh.InvalidArgument):
+        pl.pack(2)
