@@ -301,8 +301,8 @@ def e2e_ranked(torch, dist, flats, out_f, step, stream, b, e, steps, macs, dev, 
             "h2d_bytes_per_step": 3 * (e - b) * 4, "d2h_bytes_per_step": (e - b) * 4,
             "steps": steps, "ms_per_step": float(t[0]),
             "path": "per-rank pinned slices -> per segment: owner packs its A / B part "
-                    "(mhg_plan_pack), packed limb planes broadcast (NCCL) overlapped with the "
-                    "previous segment's mhg_plan_gemm -> slice read-back"}
+                    "(mhg_plan_pack), packed limb planes exchanged (config.exchange) overlapped "
+                    "with the segments' mhg_plan_gemm -> slice read-back"}
 
 
 def run_gpu(args, rank, world, local_rank):
@@ -310,8 +310,8 @@ def run_gpu(args, rank, world, local_rank):
     import torch.distributed as dist
 
     import paper_1705_04807_b200 as mh
-    from paper_1705_04807_b200.dist import (PanelExchange, rank_update, rank_update_packed,
-                                            segment_plans, slice_range)
+    from paper_1705_04807_b200.dist import (PanelExchange, PeerPanels, rank_update,
+                                            rank_update_packed, segment_plans, slice_range)
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -361,7 +361,19 @@ def run_gpu(args, rank, world, local_rank):
         plans = segment_plans(mh, ex, A, B, Cm, op)
     plan = plans[0]
     info = plan.info()
-    if world > 1 and os.environ.get("MHG_EXCHANGE") != "u32":
+    # N > 1 panel exchange: "p2p" (default) = packed limb planes pulled from the owners'
+    # workspaces over CUDA IPC peer memory by the copy engines (no SMs taken from the
+    # GEMM); "nccl" = the same bytes as NCCL broadcasts; "u32" = uint32 cells broadcast,
+    # every rank packs its whole panels
+    exchange = os.environ.get("MHG_EXCHANGE", "p2p") if world > 1 else "none"
+    if exchange not in ("none", "p2p", "nccl", "u32"):
+        raise SystemExit(f"MHG_EXCHANGE must be p2p, nccl or u32, got {exchange!r}")
+    peer = None
+    if exchange == "p2p":
+        # CPU-only barriers for the IPC event ordering (never wait for the GPU)
+        host_group = dist.new_group(backend="gloo") if dist.get_backend() != "gloo" else None
+        peer = PeerPanels(mh, ex, plans, host_group=host_group)
+    if exchange in ("p2p", "nccl"):
         # packed exchange: one GEMM per segment + the packs of the parts this rank owns
         launches_per_step = sum(1 + (rank == sg.a_owner) + (rank == sg.b_owner) for sg in segs)
     else:
@@ -378,7 +390,9 @@ def run_gpu(args, rank, world, local_rank):
         # packed limb planes on the wire (each owner packs its part; segment j+1's
         # pack + broadcasts are enqueued before segment j's GEMM); MHG_EXCHANGE=u32
         # exchanges the uint32 cells and packs every panel locally instead
-        if os.environ.get("MHG_EXCHANGE") == "u32":
+        if exchange == "p2p":
+            peer.update(stream)
+        elif exchange == "u32":
             rank_update(ex, plans, lhs_f, rhs_f, stream)
         else:
             rank_update_packed(ex, plans, stream)
@@ -425,6 +439,10 @@ def run_gpu(args, rank, world, local_rank):
         else:
             e2e = e2e_ranked(torch, dist, flats, out_f, step, stream, b, e, e2e_steps, macs_total,
                              dev, barrier)
+    if peer is not None:
+        torch.cuda.synchronize()
+        barrier()
+        peer.close()
 
     if rank != 0:
         return
@@ -467,9 +485,14 @@ def run_gpu(args, rank, world, local_rank):
                        "t": t, "p": q, "op": opname, "limbs": L,
                        "tiles": info["tiles"], "k_chunks": info["k_chunks"],
                        "partition": f"C-stationary Morton blocks over {world} GPU(s)"
-                                    + (f", {len(plans)} K segments pipelined with NCCL broadcasts "
-                                       "of packed limb planes"
-                                       if world > 1 else ""),
+                                    + ({"p2p": f", {len(plans)} K segments, packed limb planes "
+                                               "pulled over CUDA IPC peer memory by the copy "
+                                               "engines, overlapped with the per-segment GEMMs",
+                                        "nccl": f", {len(plans)} K segments pipelined with NCCL "
+                                                "broadcasts of packed limb planes",
+                                        "u32": f", {len(plans)} K segments pipelined with NCCL "
+                                               "broadcasts of uint32 cells"}.get(exchange, "")),
+                       "exchange": exchange,
                        "l2": "no flush: operands 3 x %.2f GiB >> 126 MB L2" % (n * n * 4 / 2 ** 30)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "conversion": conversion,
             "gpu_launches": args.steps * launches_per_step,

@@ -152,6 +152,24 @@ mhg_status mhg_plan_pack(mhg_plan plan, int which, void *stream);
 mhg_status mhg_plan_pack_buffer(mhg_plan plan, int which, void **ptr, uint64_t *bytes);
 mhg_status mhg_plan_gemm(mhg_plan plan, void *stream);
 mhg_status mhg_plan_counters(mhg_plan plan, mhg_counters *ctr);
+
+/* Peer memory for the copy-engine panel exchange (multi-GPU, no reference
+ * counterpart: the reference is single-process, multiply.hpp:25-29).  An owner
+ * exports the device allocation holding a packed operand (mhg_plan_pack_buffer);
+ * the other ranks of its row / column group map it once (same node, NVLink peer
+ * access enabled lazily) and pull the bytes with mhg_copy_async, which runs on
+ * the copy engines and leaves every SM to the GEMM.
+ *   mhg_ipc_export  IPC handle of the allocation containing ptr, and ptr's offset in it
+ *   mhg_ipc_open    map a peer's handle in this process; *base = the allocation's start
+ *   mhg_ipc_close   unmap a base returned by mhg_ipc_open
+ *   mhg_copy_async  cudaMemcpyAsync(dst, src, bytes, default direction) on stream */
+typedef struct {
+    unsigned char bytes[64];
+} mhg_ipc_handle;
+mhg_status mhg_ipc_export(const void *ptr, mhg_ipc_handle *handle, uint64_t *offset);
+mhg_status mhg_ipc_open(const mhg_ipc_handle *handle, void **base);
+mhg_status mhg_ipc_close(void *base);
+mhg_status mhg_copy_async(void *dst, const void *src, uint64_t bytes, void *stream);
 /* Kernel launches per run and the planner's description (tiles, chunks, limbs). */
 mhg_status mhg_plan_info(mhg_plan plan, uint64_t *launches, uint64_t *tiles, uint32_t *limbs,
                          uint32_t *k_chunks, uint64_t *workspace_bytes);

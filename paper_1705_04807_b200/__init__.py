@@ -72,6 +72,12 @@ class _View(C.Structure):
                 ("cols", C.c_uint64)]
 
 
+class IpcHandle(C.Structure):
+    """mhg_ipc_handle (include/mhg.h): a cudaIpcMemHandle_t as 64 opaque bytes."""
+
+    _fields_ = [("bytes", C.c_ubyte * 64)]
+
+
 class Counters(C.Structure):
     """multiply.hpp:39-45"""
 
@@ -126,6 +132,10 @@ def lib():
         "mhg_plan_pack": ([vp, C.c_int, vp], C.c_int),
         "mhg_plan_pack_buffer": ([vp, C.c_int, P(vp), P(u64)], C.c_int),
         "mhg_plan_gemm": ([vp, vp], C.c_int),
+        "mhg_ipc_export": ([vp, P(IpcHandle), P(u64)], C.c_int),
+        "mhg_ipc_open": ([P(IpcHandle), P(vp)], C.c_int),
+        "mhg_ipc_close": ([vp], C.c_int),
+        "mhg_copy_async": ([vp, vp, u64, vp], C.c_int),
         "mhg_plan_counters": ([vp, P(Counters)], C.c_int),
         "mhg_plan_info": ([vp, P(u64), P(u64), P(u32), P(u32), P(u64)], C.c_int),
         "mhg_plan_destroy": ([vp], C.c_int),
@@ -219,6 +229,32 @@ def fold_level(q: int, k_chunk: int) -> int:
     lv = C.c_uint32()
     _check(lib().mhg_fold_level(q, k_chunk, C.byref(lv)))
     return lv.value
+
+
+def ipc_export(ptr: int):
+    """(64-byte IPC handle of the device allocation containing ptr, ptr's offset in it)."""
+    h, off = IpcHandle(), C.c_uint64()
+    _check(lib().mhg_ipc_export(C.c_void_p(ptr), C.byref(h), C.byref(off)))
+    return bytes(h.bytes), off.value
+
+
+def ipc_open(handle: bytes) -> int:
+    """Map a peer rank's allocation (handle from ipc_export) here; returns its base."""
+    if len(handle) != 64:
+        raise InvalidArgument("ipc_open: handle must be 64 bytes")
+    h, base = IpcHandle(), C.c_void_p()
+    C.memmove(h.bytes, handle, 64)
+    _check(lib().mhg_ipc_open(C.byref(h), C.byref(base)))
+    return base.value
+
+
+def ipc_close(base: int):
+    _check(lib().mhg_ipc_close(C.c_void_p(base)))
+
+
+def copy_async(dst: int, src: int, nbytes: int, stream=None):
+    """Device-to-device (or peer) copy on the copy engines, ordered on stream."""
+    _check(lib().mhg_copy_async(C.c_void_p(dst), C.c_void_p(src), nbytes, _stream_ptr(stream)))
 
 
 def _stream_ptr(stream) -> Optional[int]:
@@ -404,6 +440,12 @@ class Plan:
     def pack(self, which: int, stream=None):
         """Pack the lhs (0) or rhs (1) view into this plan's workspace."""
         _check(lib().mhg_plan_pack(self._h, which, _stream_ptr(stream)))
+
+    def pack_region(self, which: int):
+        """(device pointer, bytes) of the packed lhs (0) / rhs (1) in the workspace."""
+        ptr, nb = C.c_void_p(), C.c_uint64()
+        _check(lib().mhg_plan_pack_buffer(self._h, which, C.byref(ptr), C.byref(nb)))
+        return (ptr.value or 0), nb.value
 
     def pack_buffer(self, which: int):
         """The packed lhs (0) / rhs (1) bytes as a zero-copy uint8 CUDA tensor view of

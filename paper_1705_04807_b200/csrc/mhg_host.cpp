@@ -890,6 +890,64 @@ mhg_status mhg_plan_run(mhg_plan p, void* stream) {
     });
 }
 
+// Peer memory for the copy-engine panel exchange (paper_1705_04807_b200/dist.py,
+// rank_update_p2p): an owner exports the allocation holding a plan's packed operand,
+// the ranks of its row / column group map it once and pull the packed bytes with
+// cudaMemcpyAsync, which runs on the copy engines over NVLink and leaves every SM
+// to the persistent GEMM (an NCCL broadcast kernel would take SMs from it).
+static_assert(sizeof(cudaIpcMemHandle_t) == sizeof(mhg_ipc_handle), "IPC handle size");
+
+mhg_status mhg_ipc_export(const void* ptr, mhg_ipc_handle* handle, uint64_t* offset) {
+    return guarded([&] {
+        if (!ptr || !handle || !offset) fail(MHG_ERR_INVALID_ARGUMENT, "ipc_export: bad args");
+        using Range = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
+        static Range range = nullptr;
+        if (!range) {
+            void* fn = nullptr;
+            cudaDriverEntryPointQueryResult q{};
+            cuda_check(cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q),
+                       "cuMemGetAddressRange lookup");
+            if (!fn || q != cudaDriverEntryPointSuccess)
+                fail(MHG_ERR_DEVICE, "cuMemGetAddressRange unavailable");
+            range = reinterpret_cast<Range>(fn);
+        }
+        CUdeviceptr base = 0;
+        size_t size = 0;
+        if (range(&base, &size, (CUdeviceptr)ptr) != CUDA_SUCCESS)
+            fail(MHG_ERR_INVALID_ARGUMENT, "ipc_export: not a device allocation");
+        cudaIpcMemHandle_t h;
+        cuda_check(cudaIpcGetMemHandle(&h, (void*)base), "cudaIpcGetMemHandle");
+        std::memcpy(handle->bytes, &h, sizeof h);
+        *offset = (uint64_t)((CUdeviceptr)ptr - base);
+    });
+}
+
+mhg_status mhg_ipc_open(const mhg_ipc_handle* handle, void** base) {
+    return guarded([&] {
+        if (!handle || !base) fail(MHG_ERR_INVALID_ARGUMENT, "ipc_open: bad args");
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle->bytes, sizeof h);
+        cuda_check(cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess),
+                   "cudaIpcOpenMemHandle");
+    });
+}
+
+mhg_status mhg_ipc_close(void* base) {
+    return guarded([&] {
+        if (!base) fail(MHG_ERR_INVALID_ARGUMENT, "ipc_close: null");
+        cuda_check(cudaIpcCloseMemHandle(base), "cudaIpcCloseMemHandle");
+    });
+}
+
+mhg_status mhg_copy_async(void* dst, const void* src, uint64_t bytes, void* stream) {
+    return guarded([&] {
+        if ((!dst || !src) && bytes) fail(MHG_ERR_INVALID_ARGUMENT, "copy_async: null pointer");
+        if (bytes)
+            cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream),
+                       "copy_async");
+    });
+}
+
 mhg_status mhg_plan_counters(mhg_plan p, mhg_counters* ctr) {
     return guarded([&] {
         if (!p) fail(MHG_ERR_INVALID_ARGUMENT, "plan_counters: null plan");

@@ -239,3 +239,153 @@ def rank_update_packed(ex: PanelExchange, plans, stream=None):
             wk.wait()
         pending = issue(j + 1) if j + 1 < len(plans) else []
         pl.gemm(stream)
+
+
+def pull_lists(ex: PanelExchange):
+    """Which packed parts this rank pulls, and which ranks pull from it.
+
+    Returns (pulls, pullers): pulls[j] = [(which, owner)] for segment j (which =
+    0: the A part, 1: the B part), pullers = the ranks that pull any part from
+    this one.  An owner packs segment j's part into ITS OWN segment-j plan, so
+    the pull reads the owner's plan j: every member of a row group sees the same
+    A owner for segment j, and every member of a column group the same B owner
+    (tests/test_dist_gloo.py checks this for P up to 16)."""
+    pulls, pullers = [], set()
+    for sg in ex.segments():
+        row = []
+        for which, owner, members in ((0, sg.a_owner, ex.row_members),
+                                      (1, sg.b_owner, ex.col_members)):
+            if owner == ex.rank:
+                pullers.update(m for m in members if m != ex.rank)
+            else:
+                row.append((which, owner))
+        pulls.append(row)
+    return pulls, pullers
+
+
+class PeerPanels:
+    """Copy-engine exchange of the PACKED panels over NVLink peer memory.
+
+    Same data movement as rank_update_packed (each owner packs its part of every
+    segment once; the members of its row / column group need those bytes), but
+    the bytes move as cudaMemcpyAsync pulls from the owner's workspace, mapped
+    once through CUDA IPC, instead of NCCL broadcasts.  Copies run on the copy
+    engines, so the persistent GEMM keeps all SMs (an NCCL kernel would hold
+    some of them while it runs beside the GEMM), and every segment's pulls are
+    enqueued at once, one copy stream per owner, each GEMM waiting only for its
+    own segment.
+
+    Ordering is by CUDA IPC events, so no stream ever blocks the host:
+      pack_done[j]  recorded by an owner after packing its parts of segment j;
+                    pullers' copy streams wait on it before pulling segment j;
+      copy_done     recorded by a puller after its last pull; an owner's next
+                    pack waits on it before overwriting the workspace.
+    Each cross-process wait is enqueued after a host barrier that follows the
+    matching record (the IPC event contract), on `host_group` (gloo: a CPU-only
+    barrier that never waits for the GPU).  No kernel waits on another rank's
+    kernel: the waits are stream-level dependencies, so the path is exercised
+    safely with all ranks on one GPU (tests/test_dist_gpu.py)."""
+
+    def __init__(self, mh, ex: PanelExchange, plans, host_group=None, device=None):
+        import torch
+        import torch.distributed as dist
+
+        self.mh, self.ex, self.plans = mh, ex, plans
+        self.group = host_group
+        self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+        self.segs = ex.segments()
+        rank, P = ex.rank, ex.P
+        ev = lambda: torch.cuda.Event(enable_timing=False, blocking=False, interprocess=True)
+        self.pack_done = [ev() for _ in self.segs]
+        self.copy_done = ev()
+        exports = {}
+        for j, (sg, pl) in enumerate(zip(self.segs, plans)):
+            for which, owner in ((0, sg.a_owner), (1, sg.b_owner)):
+                ptr, nb = pl.pack_region(which)
+                if owner == rank and nb:
+                    h, off = mh.ipc_export(ptr)
+                    exports[(j, which)] = (h, off, nb)
+        mine = {"exports": exports, "pack_done": [e.ipc_handle() for e in self.pack_done],
+                "copy_done": self.copy_done.ipc_handle()}
+        infos = [None] * P
+        dist.all_gather_object(infos, mine, group=host_group)
+        # pulls[j] = [(owner, dst, src, bytes)]; one mapping per owner allocation
+        self.bases = {}
+        self.pulls = [[] for _ in self.segs]
+        owners = set()
+        lists, pullers = pull_lists(ex)
+        for j, pl in enumerate(plans):
+            for which, owner in lists[j]:
+                dst, nb = pl.pack_region(which)
+                if not nb:
+                    continue
+                h, off, onb = infos[owner]["exports"][(j, which)]
+                if onb != nb:
+                    raise RuntimeError(f"segment {j}: packed sizes differ ({onb} vs {nb})")
+                if h not in self.bases:
+                    self.bases[h] = mh.ipc_open(h)
+                self.pulls[j].append((owner, dst, self.bases[h] + off, nb))
+                owners.add(owner)
+        self.peer_pack_done = {o: [torch.cuda.Event.from_ipc_handle(self.device, hnd)
+                                   for hnd in infos[o]["pack_done"]] for o in sorted(owners)}
+        self.peer_copy_done = [torch.cuda.Event.from_ipc_handle(self.device, infos[p]["copy_done"])
+                               for p in sorted(pullers)]
+        self.copy_streams = {o: torch.cuda.Stream(device=self.device) for o in sorted(owners)}
+        self.join = torch.cuda.Stream(device=self.device)
+        # per (segment, owner): "this owner's pulls of the segment have landed"
+        self.landed = [{o: torch.cuda.Event() for o in {pull[0] for pull in pulls}}
+                       for pulls in self.pulls]
+        self.dst_free = torch.cuda.Event()
+        self.steps = 0
+
+    def _barrier(self):
+        import torch.distributed as dist
+        dist.barrier(group=self.group)
+
+    def close(self):
+        for base in self.bases.values():
+            self.mh.ipc_close(base)
+        self.bases = {}
+
+    def update(self, stream=None):
+        """One whole update of this rank's C block (all K segments)."""
+        import torch
+
+        stream = torch.cuda.current_stream(self.device) if stream is None else stream
+        rank = self.ex.rank
+        self._barrier()  # every puller recorded copy_done of the previous step
+        if self.steps:
+            for e in self.peer_copy_done:
+                stream.wait_event(e)
+        for j, (sg, pl) in enumerate(zip(self.segs, self.plans)):
+            if sg.a_owner == rank:
+                pl.pack(0, stream)
+            if sg.b_owner == rank:
+                pl.pack(1, stream)
+            self.pack_done[j].record(stream)
+        # this rank's pulls overwrite workspaces its previous GEMMs read
+        self.dst_free.record(stream)
+        self._barrier()  # every owner recorded pack_done of this step
+        for cs in self.copy_streams.values():
+            cs.wait_event(self.dst_free)
+        for j, pulls in enumerate(self.pulls):
+            used = []
+            for owner, dst, src, nb in pulls:
+                cs = self.copy_streams[owner]
+                if owner not in used:
+                    cs.wait_event(self.peer_pack_done[owner][j])
+                    used.append(owner)
+                self.mh.copy_async(dst, src, nb, cs)
+            for owner in used:
+                ev = self.landed[j][owner]
+                ev.record(self.copy_streams[owner])
+                stream.wait_event(ev)
+                self.join.wait_event(ev)
+            self.plans[j].gemm(stream)
+        self.copy_done.record(self.join)
+        self.steps += 1
+
+
+def rank_update_p2p(peer: PeerPanels, stream=None):
+    """This rank's update with packed panels pulled over peer memory (PeerPanels)."""
+    peer.update(stream)

@@ -118,3 +118,46 @@ def _worker(rank, world, port, n, t, q):
 @pytest.mark.parametrize("world", [2, 4])
 def test_panel_exchange_gloo(world):
     mp.spawn(_worker, args=(world, _free_port(), 32, 4, 97), nprocs=world, join=True)
+
+
+def test_peer_pull_lists_read_the_owners_own_segment_plan():
+    """PeerPanels pulls segment j's packed part from the owner's segment-j plan:
+    that plan must pack exactly the same part (same K range, same flat range, same
+    panel height / width), and the puller / owner relations must be symmetric."""
+    from types import SimpleNamespace
+
+    from paper_1705_04807_b200.dist import pull_lists, segments
+
+    n, t = 256, 8
+    for P in (1, 2, 4, 8, 16):
+        rows, cols = groups(P, n, t)
+        exs = []
+        for r in range(P):
+            b = morton_block(r, P, n, t)
+            exs.append(SimpleNamespace(rank=r, P=P, block=b, row_members=rows[b.row_band],
+                                       col_members=cols[b.col_band],
+                                       segments=lambda r=r: segments(r, P, n, t)))
+        lists = [pull_lists(ex) for ex in exs]
+        pulled_from = {r: set() for r in range(P)}
+        for r, ex in enumerate(exs):
+            pulls, _ = lists[r]
+            mine = ex.segments()
+            assert len(pulls) == len(mine)
+            for j, row in enumerate(pulls):
+                got = {w for w, _ in row}
+                # every part is either this rank's own or pulled, never both
+                assert got == {w for w, o in ((0, mine[j].a_owner), (1, mine[j].b_owner)) if o != r}
+                for which, owner in row:
+                    pulled_from[owner].add(r)
+                    theirs = exs[owner].segments()[j]
+                    assert (theirs.k0, theirs.k1) == (mine[j].k0, mine[j].k1)
+                    if which == 0:
+                        assert theirs.a_owner == owner and theirs.a_range == mine[j].a_range
+                        assert exs[owner].block.rows == ex.block.rows
+                    else:
+                        assert theirs.b_owner == owner and theirs.b_range == mine[j].b_range
+                        assert exs[owner].block.cols == ex.block.cols
+        for r in range(P):
+            assert lists[r][1] == pulled_from[r]
+        if P == 1:
+            assert lists[0] == ([[]], set())

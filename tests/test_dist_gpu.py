@@ -19,14 +19,14 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def _worker(rank, world, port, n, t, q, op, outdir, packed=False):
+def _worker(rank, world, port, n, t, q, op, outdir, mode="u32", steps=1):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
     import torch.distributed as dist
 
     import paper_1705_04807_b200 as mh
-    from paper_1705_04807_b200.dist import (PanelExchange, rank_update, rank_update_packed,
-                                            segment_plans, slice_range)
+    from paper_1705_04807_b200.dist import (PanelExchange, PeerPanels, rank_update,
+                                            rank_update_packed, segment_plans, slice_range)
 
     torch.cuda.set_device(0)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -43,35 +43,47 @@ def _worker(rank, world, port, n, t, q, op, outdir, packed=False):
         A, B, C = (mh.Matrix.wrap(lay, mod, f.data_ptr(), owner=f) for f in flats)
         ex = PanelExchange(world, rank, n, t)
         plans = segment_plans(mh, ex, A, B, C, op)
-        if packed:
-            rank_update_packed(ex, plans)
-        else:
-            rank_update(ex, plans, flats[1], flats[2])
+        peer = PeerPanels(mh, ex, plans) if mode == "p2p" else None
+        for _ in range(steps):
+            if mode == "p2p":
+                peer.update()
+            elif mode == "packed":
+                rank_update_packed(ex, plans)
+            else:
+                rank_update(ex, plans, flats[1], flats[2])
         torch.cuda.synchronize()
+        dist.barrier()  # peers' pulls from this rank's workspaces are done
+        if peer is not None:
+            peer.close()
         np.save(os.path.join(outdir, f"slice{rank}.npy"), flats[0][lo:hi].cpu().numpy().view(np.uint32))
     finally:
         dist.destroy_process_group()
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("world,op_name,packed", [(2, "sub", False), (4, "set", False),
-                                                  (2, "sub", True), (4, "sub", True),
-                                                  (4, "set", True)])
-def test_multi_rank_update_matches_oracle(gpu, mh, oracle, tmp_path, world, op_name, packed):
-    """Both exchange modes: uint32 cells (rank_update) and packed limb planes
-    (rank_update_packed: owners pack, packed bytes are broadcast, every rank runs
-    only the GEMM)."""
+@pytest.mark.parametrize("world,op_name,mode,steps", [
+    (2, "sub", "u32", 1), (4, "set", "u32", 1),
+    (2, "sub", "packed", 1), (4, "sub", "packed", 1), (4, "set", "packed", 1),
+    (2, "sub", "p2p", 1), (4, "sub", "p2p", 3), (4, "set", "p2p", 2), (8, "add", "p2p", 2)])
+def test_multi_rank_update_matches_oracle(gpu, mh, oracle, tmp_path, world, op_name, mode, steps):
+    """Every exchange mode: uint32 cells (rank_update), packed limb planes broadcast
+    (rank_update_packed: owners pack, every rank runs only the GEMM) and packed
+    planes pulled over CUDA IPC peer memory by the copy engines (PeerPanels);
+    repeated steps check the cross-process event ordering (an owner's repack must
+    wait for its pullers, a pull for the owner's pack)."""
     n, t, q = 256, 32, 65521
     from oracle.binding import OP_SET, OP_SUB, Views
-    op = {"sub": mh.OP_SUB, "set": mh.OP_SET}[op_name]
-    oop = {"sub": OP_SUB, "set": OP_SET}[op_name]
-    mp.spawn(_worker, args=(world, _free_port(), n, t, q, op, str(tmp_path), packed), nprocs=world,
-             join=True)
+    from oracle.binding import OP_ADD
+    op = {"sub": mh.OP_SUB, "set": mh.OP_SET, "add": mh.OP_ADD}[op_name]
+    oop = {"sub": OP_SUB, "set": OP_SET, "add": OP_ADD}[op_name]
+    mp.spawn(_worker, args=(world, _free_port(), n, t, q, op, str(tmp_path), mode, steps),
+             nprocs=world, join=True)
     got = np.concatenate([np.load(tmp_path / f"slice{r}.npy") for r in range(world)])
     rng = np.random.default_rng(77)
     out, lhs, rhs = [rng.integers(0, q, n * n, dtype=np.uint32) for _ in range(3)]
     want = out.copy()
-    oracle.mm_dense(n, t, q, want, lhs, rhs, Views(0, 0, 0, n, n, n), op=oop)
+    for _ in range(steps):
+        oracle.mm_dense(n, t, q, want, lhs, rhs, Views(0, 0, 0, n, n, n), op=oop)
     assert np.array_equal(got, want)
 
 
