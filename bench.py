@@ -268,10 +268,14 @@ def e2e_pipelined(mh, torch, lay, mod, flats, set0, prob0, op, n, steps, macs):
     t1.record(s_dn)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / steps
-    return {"value": macs / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 3 * n * n * 4,
+    h2d = sum(m_.upload_bytes for m_ in sets[(steps - 1) % 2][:3])  # PCIe bytes of the last step
+    return {"value": macs / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": n * n * 4, "steps": steps, "ms_per_step": ms,
-            "path": "pinned host -> mhg_matrix_upload x3 -> mhg_plan_run -> mhg_matrix_download "
-                    "-> pinned host; 2 container sets, H2D / compute / D2H streams overlapped"}
+            "upload_wire": "uint16" if h2d == 3 * n * n * 2 else "uint32",
+            "path": "pinned host -> mhg_matrix_upload x3 (uint16 wire for q <= 2^16: host-threaded "
+                    "narrowing into pinned staging, device widening) -> mhg_plan_run -> "
+                    "mhg_matrix_download -> pinned host; 2 container sets, H2D / compute / D2H "
+                    "streams overlapped"}
 
 
 def e2e_ranked(torch, dist, flats, out_f, step, stream, b, e, steps, macs, dev, barrier):

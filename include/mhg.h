@@ -92,7 +92,16 @@ mhg_status mhg_matrix_wrap(uint64_t n, uint64_t t, uint32_t q, void *device_cell
 mhg_status mhg_matrix_destroy(mhg_matrix m);
 mhg_status mhg_matrix_info(mhg_matrix m, uint64_t *n, uint64_t *t, uint32_t *q, void **device_cells);
 /* Flat Morton-hybrid order copies (Matrix::cells(), matrix.hpp:27-28). */
+/* Upload: asynchronous on `stream` (the host buffer must stay valid until the
+ * stream reaches the copy).  For q <= 2^16 and >= 4M cells the cells travel as
+ * uint16 (half the PCIe bytes): host threads narrow them into pinned staging
+ * while earlier chunks are in flight, and the device widens them; the call then
+ * returns once the host buffer has been read.  Any cell >= 2^16 switches the
+ * rest of the upload to 4-byte copies, so the container always equals a plain
+ * copy of the buffer.  MHG_UPLOAD_WIRE=32 disables the 16-bit wire. */
 mhg_status mhg_matrix_upload(mhg_matrix m, const uint32_t *host_cells, void *stream);
+/* PCIe bytes moved by the last mhg_matrix_upload of `m`. */
+mhg_status mhg_matrix_upload_bytes(mhg_matrix m, uint64_t *bytes);
 mhg_status mhg_matrix_download(mhg_matrix m, uint32_t *host_cells, void *stream);
 /* from_row_major / to_row_major (matrix.hpp:44-67) on DEVICE buffers of n*n
  * row-major uint32 (K1 conversion kernels).  from_row_major's residue check

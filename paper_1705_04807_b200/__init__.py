@@ -119,6 +119,7 @@ def lib():
         "mhg_matrix_destroy": ([vp], C.c_int),
         "mhg_matrix_info": ([vp, P(u64), P(u64), P(u32), P(vp)], C.c_int),
         "mhg_matrix_upload": ([vp, vp, vp], C.c_int),
+        "mhg_matrix_upload_bytes": ([vp, P(u64)], C.c_int),
         "mhg_matrix_download": ([vp, vp, vp], C.c_int),
         "mhg_rowmajor_to_mh": ([vp, vp, vp], C.c_int),
         "mhg_mh_to_rowmajor": ([vp, vp, vp], C.c_int),
@@ -319,6 +320,13 @@ class Matrix:
             import torch
             torch.cuda.synchronize()
         return self
+
+    @property
+    def upload_bytes(self) -> int:
+        """PCIe bytes moved by the last upload (2 per cell on the 16-bit wire)."""
+        b = C.c_uint64()
+        _check(lib().mhg_matrix_upload_bytes(self._h, C.byref(b)))
+        return int(b.value)
 
     def at(self, i: int, j: int) -> int:
         return int(self.cells()[encode(self._layout, i, j)])

@@ -25,6 +25,8 @@ struct mhg_matrix_s {
     uint32_t* cells = nullptr;  // device, n*n
     bool owned = false;
     int device = 0;
+    uint16_t* wire16 = nullptr;   // device scratch of the 16-bit upload wire (mhg_wire.cpp)
+    uint64_t upload_bytes = 0;    // PCIe bytes of the last mhg_matrix_upload
 };
 
 namespace {
@@ -586,6 +588,7 @@ mhg_status mhg_matrix_destroy(mhg_matrix m) {
     return guarded([&] {
         if (!m) return;
         if (m->owned && m->cells) cudaFree(m->cells);
+        if (m->wire16) cudaFree(m->wire16);
         delete m;
     });
 }
@@ -603,9 +606,25 @@ mhg_status mhg_matrix_info(mhg_matrix m, uint64_t* n, uint64_t* t, uint32_t* q, 
 mhg_status mhg_matrix_upload(mhg_matrix m, const uint32_t* host, void* stream) {
     return guarded([&] {
         if (!m || !host) fail(MHG_ERR_INVALID_ARGUMENT, "matrix_upload: null pointer");
-        cuda_check(cudaMemcpyAsync(m->cells, host, m->n * m->n * 4, cudaMemcpyHostToDevice,
+        const uint64_t count = m->n * m->n;
+        if (mhg::wire16_enabled(m->q, count)) {
+            require_device();
+            cuda_check(mhg::upload_wire16(m->cells, &m->wire16, host, count, device_info().sms,
+                                          stream, &m->upload_bytes),
+                       "upload (16-bit wire)");
+            return;
+        }
+        cuda_check(cudaMemcpyAsync(m->cells, host, count * 4, cudaMemcpyHostToDevice,
                                    (cudaStream_t)stream),
                    "upload");
+        m->upload_bytes = count * 4;
+    });
+}
+
+mhg_status mhg_matrix_upload_bytes(mhg_matrix m, uint64_t* bytes) {
+    return guarded([&] {
+        if (!m || !bytes) fail(MHG_ERR_INVALID_ARGUMENT, "matrix_upload_bytes: null pointer");
+        *bytes = m->upload_bytes;
     });
 }
 

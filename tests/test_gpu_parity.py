@@ -646,3 +646,37 @@ def test_split_plan_execution(gpu, mh, oracle):
     assert np.array_equal(A2.cells(), want)
     with pytest.raises(mh.InvalidArgument):
         pl.pack(2)
+
+
+@pytest.mark.parametrize("n,t,q,bad", [
+    (4096, 64, P16, ()),                   # 4 staging chunks, all cells on the 16-bit wire
+    (6144, 96, P16, ()),                   # non-pow2 tile, partial last chunk
+    (2049, 2049, P16, ()),                 # odd cell count: widen tail
+    (6144, 96, P16, (20_000_000,)),        # a cell >= 2^16 in chunk 4: the rest as 4-byte cells
+    (4096, 64, P16, (5, 16_777_215)),      # ... in the first chunk: all 4-byte cells
+    (2048, 64, 65537, ()),                 # q > 2^16: plain copy
+])
+def test_upload_wire16_equals_plain_copy(gpu, mh, n, t, q, bad):
+    """mhg_matrix_upload's 16-bit wire leaves the container byte-identical to a
+    plain copy of the host buffer (Matrix::cells(), matrix.hpp:27-28); from the
+    first chunk holding a wide cell on, the buffer travels as 4-byte cells."""
+    rng = np.random.default_rng(n + sum(bad))
+    cells = rng.integers(0, min(q, 65536), size=n * n, dtype=np.uint32)
+    for b in bad:
+        cells[b] = 0x12345678 + b
+    m = mh.Matrix(mh.Layout(n, t), mh.Modulus(q))
+    m.upload(cells)
+    assert np.array_equal(m.cells(), cells)
+    chunk, total = 1 << 22, n * n  # default MHG_UPLOAD_CHUNK_LOG2
+    if q > 65536:
+        assert m.upload_bytes == 4 * total
+    else:
+        narrow = min(bad) // chunk * chunk if bad else total
+        assert m.upload_bytes == 2 * narrow + 4 * (total - narrow)
+    # re-upload over stale contents, on a side stream, from pinned memory
+    import torch
+    s = torch.cuda.Stream()
+    h = torch.from_numpy(cells[::-1].copy().view(np.int32)).pin_memory()
+    mh._check(mh.lib().mhg_matrix_upload(m.handle, h.data_ptr(), s.cuda_stream))
+    torch.cuda.synchronize()
+    assert np.array_equal(m.cells(), cells[::-1])
