@@ -278,9 +278,10 @@ def e2e_pipelined(mh, torch, lay, mod, flats, set0, prob0, op, n, steps, macs):
                     "streams overlapped"}
 
 
-def e2e_ranked(torch, dist, flats, out_f, step, stream, b, e, steps, macs, dev, barrier):
+def e2e_ranked(mh, torch, dist, mats, flats, out_f, step, stream, b, e, steps, macs, dev, barrier):
     """Multi-GPU end to end: each rank uploads its own 1/P slices from pinned
-    host memory, exchanges panels, updates its C block, reads its slice back."""
+    host memory (mhg_matrix_upload_range: the 16-bit wire for q <= 2^16),
+    exchanges panels, updates its C block, reads its slice back."""
     hosts = []
     for f in flats:
         h = torch.empty(e - b, dtype=torch.int32, pin_memory=True)
@@ -292,8 +293,9 @@ def e2e_ranked(torch, dist, flats, out_f, step, stream, b, e, steps, macs, dev, 
     x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     x0.record(stream)
     for _ in range(steps):
-        for h_, f in zip(hosts, flats):
-            f[b:e].copy_(h_, non_blocking=True)
+        for h_, m_ in zip(hosts, mats):
+            mh._check(mh.lib().mhg_matrix_upload_range(m_.handle, h_.data_ptr(), b, e - b,
+                                                       stream.cuda_stream))
         step()  # segmented panel broadcasts overlapped with the per-segment GEMMs
         res.copy_(out_f[b:e], non_blocking=True)
     x1.record(stream)
@@ -301,8 +303,9 @@ def e2e_ranked(torch, dist, flats, out_f, step, stream, b, e, steps, macs, dev, 
     barrier()
     t = torch.tensor([x0.elapsed_time(x1) / steps], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    h2d = sum(m_.upload_bytes for m_ in mats)
     return {"value": macs / (float(t[0]) * 1e-3), "unit": UNIT,
-            "h2d_bytes_per_step": 3 * (e - b) * 4, "d2h_bytes_per_step": (e - b) * 4,
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": (e - b) * 4,
             "steps": steps, "ms_per_step": float(t[0]),
             "path": "per-rank pinned slices -> per segment: owner packs its A / B part "
                     "(mhg_plan_pack), packed limb planes exchanged (config.exchange) overlapped "
@@ -441,8 +444,8 @@ def run_gpu(args, rank, world, local_rank):
             e2e = e2e_pipelined(mh, torch, lay, mod, flats, (A, B, Cm, plan), prob, op, n, e2e_steps,
                                 macs_total)
         else:
-            e2e = e2e_ranked(torch, dist, flats, out_f, step, stream, b, e, e2e_steps, macs_total,
-                             dev, barrier)
+            e2e = e2e_ranked(mh, torch, dist, (A, B, Cm), flats, out_f, step, stream, b, e, e2e_steps,
+                             macs_total, dev, barrier)
     if peer is not None:
         torch.cuda.synchronize()
         barrier()

@@ -100,7 +100,11 @@ mhg_status mhg_matrix_info(mhg_matrix m, uint64_t *n, uint64_t *t, uint32_t *q, 
  * rest of the upload to 4-byte copies, so the container always equals a plain
  * copy of the buffer.  MHG_UPLOAD_WIRE=32 disables the 16-bit wire. */
 mhg_status mhg_matrix_upload(mhg_matrix m, const uint32_t *host_cells, void *stream);
-/* PCIe bytes moved by the last mhg_matrix_upload of `m`. */
+/* Upload of the flat cell range [offset, offset + count) from `host_cells` (which
+ * holds exactly those cells), same wire rules; e.g. one rank's Morton slice. */
+mhg_status mhg_matrix_upload_range(mhg_matrix m, const uint32_t *host_cells, uint64_t offset,
+                                   uint64_t count, void *stream);
+/* PCIe bytes moved by the last mhg_matrix_upload / _upload_range of `m`. */
 mhg_status mhg_matrix_upload_bytes(mhg_matrix m, uint64_t *bytes);
 mhg_status mhg_matrix_download(mhg_matrix m, uint32_t *host_cells, void *stream);
 /* from_row_major / to_row_major (matrix.hpp:44-67) on DEVICE buffers of n*n

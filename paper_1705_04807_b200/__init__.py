@@ -120,6 +120,7 @@ def lib():
         "mhg_matrix_info": ([vp, P(u64), P(u64), P(u32), P(vp)], C.c_int),
         "mhg_matrix_upload": ([vp, vp, vp], C.c_int),
         "mhg_matrix_upload_bytes": ([vp, P(u64)], C.c_int),
+        "mhg_matrix_upload_range": ([vp, vp, u64, u64, vp], C.c_int),
         "mhg_matrix_download": ([vp, vp, vp], C.c_int),
         "mhg_rowmajor_to_mh": ([vp, vp, vp], C.c_int),
         "mhg_mh_to_rowmajor": ([vp, vp, vp], C.c_int),

@@ -603,21 +603,36 @@ mhg_status mhg_matrix_info(mhg_matrix m, uint64_t* n, uint64_t* t, uint32_t* q, 
     });
 }
 
+namespace {
+void upload_cells(mhg_matrix m, const uint32_t* host, uint64_t offset, uint64_t count, void* stream) {
+    if (mhg::wire16_enabled(m->q, count)) {
+        require_device();
+        cuda_check(mhg::upload_wire16(m->cells, &m->wire16, m->n * m->n, offset, host, count,
+                                      device_info().sms, stream, &m->upload_bytes),
+                   "upload (16-bit wire)");
+        return;
+    }
+    cuda_check(cudaMemcpyAsync(m->cells + offset, host, count * 4, cudaMemcpyHostToDevice,
+                               (cudaStream_t)stream),
+               "upload");
+    m->upload_bytes = count * 4;
+}
+}  // namespace
+
 mhg_status mhg_matrix_upload(mhg_matrix m, const uint32_t* host, void* stream) {
     return guarded([&] {
         if (!m || !host) fail(MHG_ERR_INVALID_ARGUMENT, "matrix_upload: null pointer");
-        const uint64_t count = m->n * m->n;
-        if (mhg::wire16_enabled(m->q, count)) {
-            require_device();
-            cuda_check(mhg::upload_wire16(m->cells, &m->wire16, host, count, device_info().sms,
-                                          stream, &m->upload_bytes),
-                       "upload (16-bit wire)");
-            return;
-        }
-        cuda_check(cudaMemcpyAsync(m->cells, host, count * 4, cudaMemcpyHostToDevice,
-                                   (cudaStream_t)stream),
-                   "upload");
-        m->upload_bytes = count * 4;
+        upload_cells(m, host, 0, m->n * m->n, stream);
+    });
+}
+
+mhg_status mhg_matrix_upload_range(mhg_matrix m, const uint32_t* host, uint64_t offset,
+                                   uint64_t count, void* stream) {
+    return guarded([&] {
+        if (!m || (!host && count)) fail(MHG_ERR_INVALID_ARGUMENT, "matrix_upload_range: null pointer");
+        if (offset > m->n * m->n || count > m->n * m->n - offset)
+            fail(MHG_ERR_OUT_OF_RANGE, "matrix_upload_range: cells outside the container");
+        if (count) upload_cells(m, host, offset, count, stream);
     });
 }
 

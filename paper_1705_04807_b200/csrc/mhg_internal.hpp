@@ -112,12 +112,13 @@ int launch_widen16(const uint16_t* src, uint32_t* dst, uint64_t count, int num_s
 // 16-bit upload wire (mhg_wire.cpp): true when uploads of this container size
 // and modulus take it (q <= 2^16, >= 4M cells, not disabled by MHG_UPLOAD_WIRE=32).
 bool wire16_enabled(uint32_t q, uint64_t count);
-// Upload `count` host cells into `cells`: uint16 through pinned staging + k_widen16
-// while the cells fit 16 bits, plain 4-byte copies for the rest.  *dev16 is the
-// container's uint16 scratch (allocated here on first use; the caller frees it).
-// Returns a cudaError_t value; *wire_bytes = bytes moved over PCIe.
-int upload_wire16(uint32_t* cells, uint16_t** dev16, const uint32_t* host, uint64_t count,
-                  int num_sms, void* stream, uint64_t* wire_bytes);
+// Upload `count` host cells into cells[offset, offset + count): uint16 through pinned
+// staging + k_widen16 while the cells fit 16 bits, plain 4-byte copies for the rest.
+// *dev16 is the container's uint16 scratch of `total` cells (allocated here on first
+// use; the caller frees it).  Returns a cudaError_t value; *wire_bytes = PCIe bytes.
+int upload_wire16(uint32_t* cells, uint16_t** dev16, uint64_t total, uint64_t offset,
+                  const uint32_t* host, uint64_t count, int num_sms, void* stream,
+                  uint64_t* wire_bytes);
 int launch_fill_view(uint32_t* out, const uint64_t* rowoff, const uint64_t* coloff, uint64_t rows,
                      uint64_t cols, uint32_t value, void* stream);
 

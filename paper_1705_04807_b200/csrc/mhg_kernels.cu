@@ -1851,31 +1851,45 @@ int launch_fill_view(uint32_t* out, const uint64_t* rowoff, const uint64_t* colo
 
 // 16-bit upload wire (mhg_matrix_upload, q <= 2^16): residues arrive as uint16 and
 // are widened into the container.  HBM-bound: 6 B per cell (2 read + 4 written);
-// 16-byte loads of 8 cells, two 16-byte stores, grid-stride.
+// 16-byte loads of 8 cells, two 16-byte stores, grid-stride.  A range upload may
+// start anywhere: `head` cells are widened one by one until both pointers are
+// 16-byte aligned (vec = 0: the whole range element-wise).
 __global__ void k_widen16(const uint16_t* __restrict__ src, uint32_t* __restrict__ dst,
-                          uint64_t count) {
-    const uint64_t groups = count / 8;
+                          uint64_t count, uint32_t head, int vec) {
+    const uint64_t tid = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
-    for (uint64_t g = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; g < groups; g += stride) {
-        const uint4 v = __ldcs(reinterpret_cast<const uint4*>(src) + g);
+    if (!vec) {
+        for (uint64_t i = tid; i < count; i += stride) dst[i] = src[i];
+        return;
+    }
+    if (tid < head) dst[tid] = src[tid];
+    const uint64_t groups = (count - head) / 8;
+    const uint4* s4 = reinterpret_cast<const uint4*>(src + head);
+    uint4* d4 = reinterpret_cast<uint4*>(dst + head);
+    for (uint64_t g = tid; g < groups; g += stride) {
+        const uint4 v = __ldcs(s4 + g);
         uint4 lo, hi;
         lo.x = v.x & 0xffffu; lo.y = v.x >> 16; lo.z = v.y & 0xffffu; lo.w = v.y >> 16;
         hi.x = v.z & 0xffffu; hi.y = v.z >> 16; hi.z = v.w & 0xffffu; hi.w = v.w >> 16;
-        uint4* d = reinterpret_cast<uint4*>(dst) + 2 * g;
-        d[0] = lo;
-        d[1] = hi;
+        d4[2 * g] = lo;
+        d4[2 * g + 1] = hi;
     }
-    const uint64_t tail = groups * 8 + (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const uint64_t tail = head + groups * 8 + tid;
     if (tail < count) dst[tail] = src[tail];
 }
 
 int launch_widen16(const uint16_t* src, uint32_t* dst, uint64_t count, int num_sms, void* stream) {
     if (count == 0) return 0;
+    const uint64_t mis = (reinterpret_cast<uintptr_t>(src) >> 1) & 7;
+    uint32_t head = (uint32_t)((8 - mis) & 7);
+    if (head > count) head = (uint32_t)count;
+    const int vec = ((reinterpret_cast<uintptr_t>(src) & 1) == 0) &&
+                    ((reinterpret_cast<uintptr_t>(dst + head) & 15) == 0);
     const uint64_t groups = (count + 7) / 8;
     uint64_t blocks = (groups + 255) / 256;
     const uint64_t cap = (uint64_t)(num_sms > 0 ? num_sms : 148) * 8;
     if (blocks > cap) blocks = cap;
-    k_widen16<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(src, dst, count);
+    k_widen16<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(src, dst, count, head, vec);
     return (int)cudaGetLastError();
 }
 

@@ -92,6 +92,11 @@ int host_threads() {
     CPU_ZERO(&set);
     int n = 1;
     if (sched_getaffinity(0, sizeof(set), &set) == 0) n = CPU_COUNT(&set);
+    // one process per GPU (torchrun): share the host cores between the local ranks
+    if (const char* lw = std::getenv("LOCAL_WORLD_SIZE")) {
+        const int w = std::atoi(lw);
+        if (w > 1) n /= w;
+    }
     return n < 1 ? 1 : (n > 32 ? 32 : n);
 }
 
@@ -197,15 +202,18 @@ bool wire16_enabled(uint32_t q, uint64_t count) {
     return mode == 16 && q <= 65536 && count >= (uint64_t(1) << 22);
 }
 
-int upload_wire16(uint32_t* cells, uint16_t** dev16, const uint32_t* host, uint64_t count,
-                  int num_sms, void* stream, uint64_t* wire_bytes) {
+int upload_wire16(uint32_t* cells, uint16_t** dev16, uint64_t total, uint64_t offset,
+                  const uint32_t* host, uint64_t count, int num_sms, void* stream,
+                  uint64_t* wire_bytes) {
     cudaStream_t s = (cudaStream_t)stream;
     int dev = 0;
     int e = (int)cudaGetDevice(&dev);
     if (e) return e;
     Staging* st = staging_for(dev, &e);
     if (!st) return e;
-    if (!*dev16 && (e = (int)cudaMalloc((void**)dev16, count * 2))) return e;
+    if (!*dev16 && (e = (int)cudaMalloc((void**)dev16, total * 2))) return e;
+    cells += offset;
+    uint16_t* d16 = *dev16 + offset;
     std::lock_guard<std::mutex> g(st->mu);
     Pool& P = pool();
     const uint64_t chunk = chunk_cells();
@@ -225,13 +233,13 @@ int upload_wire16(uint32_t* cells, uint16_t** dev16, const uint32_t* host, uint6
         bool fits = true;
         for (uint32_t h : hi) fits = fits && h == 0;
         if (!fits) break;
-        e = (int)cudaMemcpyAsync(*dev16 + base, slot, len * 2, cudaMemcpyHostToDevice, s);
+        e = (int)cudaMemcpyAsync(d16 + base, slot, len * 2, cudaMemcpyHostToDevice, s);
         if (!e) e = (int)cudaEventRecord(st->done[k], s);
         if (e) return e;
         st->used[k] = true;
         narrow += len;
     }
-    if ((e = launch_widen16(*dev16, cells, narrow, num_sms, stream))) return e;
+    if ((e = launch_widen16(d16, cells, narrow, num_sms, stream))) return e;
     if (narrow < count &&
         (e = (int)cudaMemcpyAsync(cells + narrow, host + narrow, (count - narrow) * 4,
                                   cudaMemcpyHostToDevice, s)))

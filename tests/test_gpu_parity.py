@@ -680,3 +680,22 @@ def test_upload_wire16_equals_plain_copy(gpu, mh, n, t, q, bad):
     mh._check(mh.lib().mhg_matrix_upload(m.handle, h.data_ptr(), s.cuda_stream))
     torch.cuda.synchronize()
     assert np.array_equal(m.cells(), cells[::-1])
+
+
+def test_upload_range(gpu, mh):
+    """mhg_matrix_upload_range: one flat cell range (a rank's Morton slice) from a
+    host buffer holding exactly those cells, on the 16-bit wire (>= 4M cells) or
+    as a plain copy; the rest of the container is untouched; bounds checked."""
+    n, t, q = 4096, 64, P16
+    rng = np.random.default_rng(3)
+    base = rng.integers(0, q, size=n * n, dtype=np.uint32)
+    m = mh.Matrix(mh.Layout(n, t), mh.Modulus(q)).upload(base)
+    want = base.copy()
+    for off, cnt in [(12345, 5_000_000), (n * n - 4_194_304, 4_194_304), (7, 1000), (0, 0)]:
+        part = rng.integers(0, q, size=cnt, dtype=np.uint32)
+        mh._check(mh.lib().mhg_matrix_upload_range(m.handle, part.ctypes.data, off, cnt, None))
+        want[off:off + cnt] = part
+        assert np.array_equal(m.cells(), want), (off, cnt)
+        assert m.upload_bytes == (2 if cnt >= 1 << 22 else 4) * cnt or cnt == 0
+    with pytest.raises(mh.OutOfRange):
+        mh._check(mh.lib().mhg_matrix_upload_range(m.handle, base.ctypes.data, n * n - 10, 11, None))
