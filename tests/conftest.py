@@ -6,6 +6,9 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
+# the upload wire's on/off default depends on the host's core count: pin it on so the
+# wire tests (and every large upload) take the same path on any box
+os.environ.setdefault("MHG_UPLOAD_WIRE", "16")
 
 
 def pytest_configure(config):
