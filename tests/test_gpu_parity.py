@@ -699,3 +699,47 @@ def test_upload_range(gpu, mh):
         assert m.upload_bytes == (2 if cnt >= 1 << 22 else 4) * cnt or cnt == 0
     with pytest.raises(mh.OutOfRange):
         mh._check(mh.lib().mhg_matrix_upload_range(m.handle, base.ctypes.data, n * n - 10, 11, None))
+
+
+def test_concurrent_uploads_from_threads(gpu, mh):
+    """Uploads on the 16-bit wire from several host threads at once (own streams,
+    distinct containers, pinned and pageable sources, full and range uploads):
+    they share one narrowing pool and staging ring and must each land exactly."""
+    import threading
+
+    import torch
+
+    n, t, q = 4096, 64, P16  # halves of 8M cells: both range uploads on the wire
+    rng = np.random.default_rng(44)
+    srcs = [rng.integers(0, q, size=n * n, dtype=np.uint32) for _ in range(4)]
+    mats = [mh.Matrix(mh.Layout(n, t), mh.Modulus(q)) for _ in range(4)]
+    errors = []
+
+    def worker(i):
+        try:
+            s = torch.cuda.Stream()
+            src = srcs[i]
+            for rep in range(3):
+                if i % 2:
+                    h = torch.from_numpy(src.view(np.int32)).pin_memory()
+                    mh._check(mh.lib().mhg_matrix_upload(mats[i].handle, h.data_ptr(), s.cuda_stream))
+                    s.synchronize()
+                else:
+                    half = n * n // 2 + 8 * rep + 1
+                    mh._check(mh.lib().mhg_matrix_upload_range(mats[i].handle, src.ctypes.data, 0,
+                                                               half, s.cuda_stream))
+                    mh._check(mh.lib().mhg_matrix_upload_range(
+                        mats[i].handle, src[half:].ctypes.data, half, n * n - half, s.cuda_stream))
+                    s.synchronize()
+        except Exception as e:  # noqa: BLE001
+            errors.append(e)
+
+    threads = [threading.Thread(target=worker, args=(i,)) for i in range(4)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    assert not errors, errors
+    for m, src in zip(mats, srcs):
+        assert np.array_equal(m.cells(), src)
+        assert m.upload_bytes <= 2 * n * n  # the last (range or full) upload was narrow
