@@ -101,9 +101,10 @@ int host_threads() {
 }
 
 // Fixed pool of narrowing workers.  run(fn) calls fn(id) once on every worker
-// (id 0 = the caller) and returns when all calls are done.  Workers spin for a
-// while after each task (an upload dispatches one task per chunk, ~100 us
-// apart) before parking on the condition variable.
+// (id 0 = the caller) and returns when all calls are done; calls from several
+// threads (uploads to different devices) take turns.  Workers spin ~1 ms after
+// each task (an upload dispatches one task per chunk, a few hundred us apart)
+// before parking on the condition variable.
 class Pool {
 public:
     explicit Pool(int n) : size_(n) {
@@ -119,6 +120,7 @@ public:
     }
     int size() const { return size_; }
     void run(const std::function<void(int)>& fn) {
+        std::lock_guard<std::mutex> one(run_mu_);
         fn_ = &fn;
         pending_.store(size_ - 1, std::memory_order_relaxed);
         {
@@ -134,7 +136,7 @@ private:
     void loop(int id) {
         uint64_t seen = 0;
         for (;;) {
-            for (int i = 0; i < 200000 && gen_.load(std::memory_order_acquire) == seen; ++i)
+            for (int i = 0; i < 20000 && gen_.load(std::memory_order_acquire) == seen; ++i)
                 _mm_pause();
             if (gen_.load(std::memory_order_acquire) == seen) {
                 std::unique_lock<std::mutex> l(mu_);
@@ -148,7 +150,7 @@ private:
     }
     const int size_;
     std::vector<std::thread> workers_;
-    std::mutex mu_;
+    std::mutex mu_, run_mu_;
     std::condition_variable cv_;
     const std::function<void(int)>* fn_ = nullptr;
     std::atomic<uint64_t> gen_{0};
