@@ -238,6 +238,7 @@ mhg::GemmParams gemm_params(const Buffers& b, const mhg_view& out, const Checked
     p.w16 = (uint32_t)((uint64_t(1) << 16) % q);
     p.w16_small = p.w16 < 256;
     p.mc = g.mc ? 1 : 0;
+    p.two = g.two ? 1 : 0;
     // cheapest exact fold for the longest chunk (MHG_FOLD raises the level, A/B only)
     p.fold = g.L == 2 ? mhg::fold_level(q, (uint64_t)std::min(g.Kt, g.KC) * mhg::kBK) : 3;
     if (const char* fl = std::getenv("MHG_FOLD")) p.fold = std::max(p.fold, std::min(3, std::atoi(fl)));
@@ -303,7 +304,7 @@ TensorMaps tensor_maps(const Buffers& b, const mhg::GemmGeometry& g) {
     TensorMaps t{};
     if (g.pair) {
         make_tmap(&t.a, b.apack, g.apack_bytes, mhg::kBM);
-        make_tmap(&t.b, b.bpack, g.bpack_bytes, (uint32_t)mhg::gemm2_b_box_rows((int)g.L));
+        make_tmap(&t.b, b.bpack, g.bpack_bytes, (uint32_t)mhg::gemm2_b_box_rows((int)g.L, g.two ? 1 : 0));
     }
     return t;
 }
@@ -329,13 +330,14 @@ void launch_pack_operand(const Buffers& b, const mhg_view& out, const mhg_view& 
                          const mhg::GemmGeometry& g, mhg_op op, int which, void* stream) {
     const mhg::LimbParams lp = mhg::limb_params(out.mat->q);
     const int vecok = out.mat->t % 4 == 0;
+    const uint32_t m32 = (uint32_t)((uint64_t(1) << 32) / out.mat->q);
     if (which == 0) {
-        const mhg::DigitParams dl{out.mat->q, lp.H, op == MHG_OP_SUB ? 1 : 0};
+        const mhg::DigitParams dl{out.mat->q, lp.H, op == MHG_OP_SUB ? 1 : 0, 0, m32};
         cuda_check(mhg::launch_pack((int)g.L, 0, v.mat->cells, b.lhs_row, b.lhs_col, vecok, c.rl.rows,
                                     c.rl.cols, mhg::kBM, g.Mt, g.Kt, b.apack, dl, stream),
                    "pack lhs");
     } else {
-        const mhg::DigitParams dr{out.mat->q, lp.H, 0};
+        const mhg::DigitParams dr{out.mat->q, lp.H, 0, g.two ? 1 : 0, m32};
         cuda_check(mhg::launch_pack((int)g.L, 1, v.mat->cells, b.rhs_row, b.rhs_col, vecok, c.rr.cols,
                                     c.rr.rows, g.W, g.Nt, g.Kt, b.bpack, dr, stream),
                    "pack rhs");

@@ -25,6 +25,10 @@ struct DigitParams {
     uint32_t q;
     uint32_t H;
     int negate;  // 1: encode (q - x) mod q (C -= A.B as C += (-A).B)
+    // two-class rhs (L = 2, GemmParams::two): besides the digits (b0, b1) of b, also
+    // those (c0, c1) of c = 256 b mod q, planes ordered [b0, c0, b1, c1]
+    int two;
+    uint32_t m32;  // floor(2^32 / q), for c
 };
 
 struct LimbParams {
@@ -70,6 +74,10 @@ struct GemmParams {
     int fold;                    // lean L = 2 fold level 3 / 2 / 1 (reductions per element; host)
     int mc;                      // column-pair clusters with lhs multicast (Nt even; planner)
     int mode;                    // 0: out += prod, 2: out = prod (first chunk)
+    // two-class accumulation (CTA pair, L = 2): limb s multiplies the digits of
+    // 256^s b mod q, so S = lo + 256 hi has 2 classes (256 TMEM columns per job, two
+    // jobs double-buffered); rhs packed with 4 planes (DigitParams::two)
+    int two;
     int vec_ok;                  // t % 4 == 0: 16-byte epilogue accesses allowed
     uint32_t group;              // raster: row tiles per group sharing rhs panels in L2
     int serpentine;              // alternate the K direction per tile (L2 reuse across waves)
@@ -106,7 +114,7 @@ int configure_kernels();  // one-time kernel attributes (dynamic smem opt-in)
 // 128 rows for A, gemm2_b_box_rows(L) rows for B'); requires p.Mt even.
 int launch_gemm2(int L, const GemmParams& p, const void* tmA, const void* tmB, int num_sms,
                  void* stream);
-int gemm2_b_box_rows(int L);
+int gemm2_b_box_rows(int L, int two = 0);
 int launch_widen16(const uint16_t* src, uint32_t* dst, uint64_t count, int num_sms,
                     void* stream);
 // 16-bit upload wire (mhg_wire.cpp): true when uploads of this container size

@@ -347,14 +347,17 @@ __global__ void __launch_bounds__(256, MHG_PACK_MINB) k_pack_rows(const uint32_t
 // pack rows (one 16-byte load) x 4 K rows, transposed in registers.
 constexpr int kColsStride = 36;  // 32 K bytes + 4 pad
 
-template <int L>
+// P = L planes, or P = 2L for the two-class rhs (L = 2): planes [b0, c0, b1, c1] with
+// c = 256 b mod q, so CTA r of a pair fetches its planes {b_r, c_r} as one box.
+template <int L, int P = L>
 __global__ void __launch_bounds__(256, MHG_PACK_MINB) k_pack_cols(const uint32_t* __restrict__ src,
                                                    const uint64_t* __restrict__ rowoff,
                                                    const uint64_t* __restrict__ coloff, int vecok,
                                                    uint64_t R, uint64_t K, uint32_t rpt, uint32_t Kt,
                                                    uint64_t Rpad, int8_t* __restrict__ dst,
                                                    DigitParams dp) {
-    __shared__ __align__(16) uint8_t sd[L][128][kColsStride];
+    static_assert(P == L || (L == 2 && P == 4), "plane layout");
+    __shared__ __align__(16) uint8_t sd[P][128][kColsStride];
     const uint32_t nkq = Kt * (kBK / 32);         // 32-wide K slices
     const uint32_t kq = blockIdx.x % nkq;
     const uint64_t pr0 = (uint64_t)(blockIdx.x / nkq) * 128;
@@ -374,19 +377,40 @@ __global__ void __launch_bounds__(256, MHG_PACK_MINB) k_pack_cols(const uint32_t
         const uint32_t col[4] = {v[0][c], v[1][c], v[2][c], v[3][c]};
         uint32_t w[L];
         digits4<L>(col, dp, w);
+        if constexpr (P == L) {
 #pragma unroll
-        for (int s = 0; s < L; ++s)
-            *reinterpret_cast<uint32_t*>(&sd[s][4 * tx + c][4 * ty]) = w[s];
+            for (int s = 0; s < L; ++s)
+                *reinterpret_cast<uint32_t*>(&sd[s][4 * tx + c][4 * ty]) = w[s];
+        } else {
+            // c = 256 b mod q (b < q <= 2^16: 256 b < 2^24, one Barrett step)
+            uint32_t cv[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                const uint32_t b = dp.negate ? (col[e] ? dp.q - col[e] : 0u) : col[e];
+                const uint32_t u = b << 8;
+                const uint32_t r = u - __umulhi(u, dp.m32) * dp.q;
+                cv[e] = r >= dp.q ? r - dp.q : r;
+            }
+            DigitParams dc = dp;
+            dc.negate = 0;
+            uint32_t wc[L];
+            digits4<L>(cv, dc, wc);
+#pragma unroll
+            for (int s = 0; s < L; ++s) {
+                *reinterpret_cast<uint32_t*>(&sd[2 * s][4 * tx + c][4 * ty]) = w[s];
+                *reinterpret_cast<uint32_t*>(&sd[2 * s + 1][4 * tx + c][4 * ty]) = wc[s];
+            }
+        }
     }
     __syncthreads();
 #pragma unroll
-    for (int e = 0; e < L; ++e) {
-        const int cid = threadIdx.x + 256 * e;  // L x 128 rows x 2 chunks
+    for (int e = 0; e < P; ++e) {
+        const int cid = threadIdx.x + 256 * e;  // P x 128 rows x 2 chunks
         const int s = cid >> 8, r = (cid >> 1) & 127, h = cid & 1;
         const uint64_t pr = pr0 + r;
         if (pr >= Rpad) continue;
         const uint32_t* w = reinterpret_cast<const uint32_t*>(&sd[s][r][16 * h]);
-        *reinterpret_cast<uint4*>(pack_dst<L>(dst, pr, k0 + 16 * h, s, rpt, Kt)) =
+        *reinterpret_cast<uint4*>(pack_dst<P>(dst, pr, k0 + 16 * h, s, rpt, Kt)) =
             make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
@@ -843,7 +867,7 @@ __device__ __forceinline__ void tmem_wait_st() {
 // C_old is prefetched into registers at tile start, addressed through smem
 // column offsets.
 template <int L, int W, int EPI_WARPS, bool PAIR, bool XPOSE = false, int FOLD = 3, bool NPAIR = false,
-          int EPI_W0 = 2>
+          int EPI_W0 = 2, bool TWO = false>
 __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t first_tile,
                                               uint32_t tile_stride, uint32_t num_tiles,
                                               uint32_t row_groups, uint32_t rank, uint32_t nchunks,
@@ -862,7 +886,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
     const uint32_t release_bar =
         PAIR ? mapa_shared(smem_u32(tmem_empty), 0) : smem_u32(tmem_empty);
-    uint32_t acc_ph = 0;
+    uint32_t acc_ph = 0, job2 = 0;
     long long epi_wait = 0, epi_busy = 0, epi_ldw = 0;
     // hand the accumulator columns back to the MMA issuer (one arrive per warp)
     auto release = [&]() {
@@ -1031,6 +1055,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         if (live) {
             tile_coords(tile, row_groups, NPAIR ? p.Nt / 2 : p.Nt, p.group, lm, ln);
             if (NPAIR) ln = 2 * ln + rank;
+            if (PAIR) lm = 2 * lm + rank;  // this CTA's 128-row half of the pair tile
         }
         const uint64_t own = row_at(lm, row);
         uint64_t c0[NH];
@@ -1138,10 +1163,51 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         epi_pro += clock64() - tp0;
         for (uint32_t c = 0; c < nchunks; ++c) {
             const long long w0 = clock64();
-            mbar_wait_hint(tmem_full, acc_ph, (p.wait_roles & 4) ? p.wait_hint : 0u);
+            if constexpr (TWO) {
+                // two accumulators in TMEM: job j uses buffer j % 2, its (j / 2)-th use
+                mbar_wait_hint(tmem_full + (job2 & 1), (job2 >> 1) & 1,
+                               (p.wait_roles & 4) ? p.wait_hint : 0u);
+            } else {
+                mbar_wait_hint(tmem_full, acc_ph, (p.wait_roles & 4) ? p.wait_hint : 0u);
+            }
             const long long w1 = clock64();
             epi_wait += w1 - w0;
             tc_fence_after();
+            if constexpr (TWO) {
+                // S = lo + 256 hi (limb s multiplied the digits of 256^s b mod q).  Lean
+                // fold (2^16 mod q < 256; the planner bounds K so that |t| <= 2^31 - 2^17):
+                // 256 hi = 256 (hi & 255) + 2^16 (hi >> 8) == 256 (hi & 255) + w16 (hi >> 8).
+                const uint32_t buf = job2 & 1;
+                const uint32_t tb = tmem + lane_base + buf * (uint32_t)(2 * W) + jb;
+#pragma unroll
+                for (int j0 = 0; j0 < WH; j0 += CW) {
+                    const bool live = (uint64_t)n * W + jb + j0 < p.cols;  // warp-uniform
+                    int32_t lo[CW], hi[CW];
+                    tmem_ld<CW>(tb + j0, lo);
+                    tmem_ld<CW>(tb + W + j0, hi);
+                    tmem_wait_ld();
+                    if (live) {
+#pragma unroll
+                        for (int j = 0; j < CW; ++j) {
+                            if (p.w16_small) {
+                                const int32_t t = lo[j] + ((hi[j] & 255) << 8) + (int32_t)p.w16 * (hi[j] >> 8);
+                                cur[j0 + j] = red32((uint32_t)t + cur[j0 + j] + p.bias32, p);
+                            } else {
+                                const uint32_t r = red32((uint32_t)lo[j] + p.bias32, p);
+                                const uint32_t h = red32((uint32_t)hi[j] + p.bias32, p);
+                                const uint32_t x = red32(r + (h << 8), p) + cur[j0 + j];
+                                cur[j0 + j] = x >= p.q ? x - p.q : x;
+                            }
+                        }
+                    }
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(tmem_empty + buf), 0));
+                epi_busy += clock64() - w1;
+                ++job2;
+                continue;
+            }
             if constexpr (PAIR) {
 #pragma unroll
                 for (int j0 = 0; j0 < WH; j0 += CW) {
@@ -1466,18 +1532,24 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
 //   - the upper weight classes [L, 2L-1) are zeroed by the epilogue right
 //     after it drains them, so every MMA but the first of a chunk accumulates.
 // =====================================================================
-template <int L>
+template <int L, bool TWO = false>
 struct Gemm2Cfg {
+    static_assert(!TWO || L == 2, "two-class accumulation is the L = 2 layout");
     static constexpr int W = (L <= 2) ? 128 : 64;
-    static constexpr int NB = L * W;
-    static constexpr int NBH = NB / 2;                  // B' rows per CTA
-    static constexpr int CLASSES = 2 * L - 1;
+    static constexpr int NB = TWO ? 2 * W : L * W;       // UMMA N of one limb MMA
+    static constexpr int NBR = TWO ? 2 * L * W : L * W;  // B' rows per (column tile, k tile)
+    static constexpr int NBH = NBR / 2;                  // B' rows per CTA
+    static constexpr int CLASSES = TWO ? 2 : 2 * L - 1;
+    static constexpr int NBUF = TWO ? 2 : 1;             // accumulation jobs in TMEM
     static constexpr int A_STAGE = L * kBM * kBK;
     static constexpr int B_STAGE = NBH * kBK;
     static constexpr int STAGE = A_STAGE + B_STAGE;
-    static constexpr int STAGES_RAW = (220 * 1024) / STAGE;
+    // TWO: the coalesced (transpose-buffer) epilogue, 4 KB per epilogue warp
+    static constexpr bool XPOSE = TWO;
+    static constexpr int XBUF = XPOSE ? 8 * 4096 : 0;
+    static constexpr int STAGES_RAW = (220 * 1024 - XBUF) / STAGE;
     static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-    static constexpr int SMEM = 1024 + STAGES * STAGE + 512 + 8 * W;
+    static constexpr int SMEM = 1024 + STAGES * STAGE + 512 + 8 * W + XBUF;
     static_assert(SMEM <= 232448, "227 KB dynamic shared memory limit");
     static constexpr int EPI_WARPS = 8;
     static constexpr int EPI_THREADS = EPI_WARPS * 32;
@@ -1488,11 +1560,12 @@ struct Gemm2Cfg {
     static_assert(NBH % 16 == 0 || NBH == 64, "B' half rows");
 };
 
-template <int L>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS, 1)
+template <int L, bool TWO = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L, TWO>::THREADS, 1)
     k_gemm2(const __grid_constant__ GemmParams p, const __grid_constant__ CUtensorMap tmA,
             const __grid_constant__ CUtensorMap tmB) {
-    using Cfg = Gemm2Cfg<L>;
+    using Cfg = Gemm2Cfg<L, TWO>;
+    constexpr int NBUF = Cfg::NBUF;
     constexpr int W = Cfg::W;
     constexpr int WH = Cfg::WH;
     constexpr int STAGES = Cfg::STAGES;
@@ -1503,10 +1576,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS
     uint8_t* sB = smem + STAGES * Cfg::A_STAGE;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE);
     uint64_t* empty = full + STAGES;
-    uint64_t* tmem_full = empty + STAGES;
-    uint64_t* tmem_empty = tmem_full + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
-    uint64_t* s_col = tmem_empty + 2;
+    uint64_t* tmem_full = empty + STAGES;        // [NBUF]
+    uint64_t* tmem_empty = tmem_full + NBUF;     // [NBUF]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + NBUF);
+    uint64_t* s_col = tmem_empty + NBUF + 1;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
@@ -1525,15 +1598,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        mbar_init(tmem_full, 1);
-        mbar_init(tmem_empty, 2 * Cfg::EPI_WARPS);
+        for (int b = 0; b < NBUF; ++b) {
+            mbar_init(tmem_full + b, 1);
+            mbar_init(tmem_empty + b, 2 * Cfg::EPI_WARPS);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    if (warp >= 2) {
+    if (!TWO && warp >= 2) {
         // zero the upper weight classes once; afterwards the epilogue re-zeroes
         // them as it drains them
         const int ew = warp - 2, quad = warp & 3, jb = (ew >> 2) * WH;
@@ -1571,7 +1646,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS
                     for (int l = 0; l < L; ++l)
                         tma2d_pair(smem_u32(sA + st * Cfg::A_STAGE + l * kBM * kBK), &tmA, 0,
                                    arow + l * kBM, lbar);
-                    const int brow = (int)(((uint64_t)n * p.Kt + kt) * Cfg::NB + rank * Cfg::NBH);
+                    const int brow = (int)(((uint64_t)n * p.Kt + kt) * Cfg::NBR + rank * Cfg::NBH);
                     tma2d_pair(smem_u32(sB + st * Cfg::B_STAGE), &tmB, 0, brow, lbar);
                     if (++st == STAGES) {
                         st = 0;
@@ -1585,17 +1660,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS
         if (lane == 0 && rank == 0) {
             constexpr uint32_t id_full = idesc_i8(2 * kBM, Cfg::NB);
             int st = 0;
-            uint32_t ph = 0, acc_ph = 0;
+            uint32_t ph = 0, job = 0;
             long long wait_full = 0, wait_tmem = 0;
             const long long t_begin = clock64();
             for (uint32_t tile = pair; tile < num_tiles; tile += npairs) {
-                for (uint32_t c = 0; c < nchunks; ++c) {
+                for (uint32_t c = 0; c < nchunks; ++c, ++job) {
                     const uint32_t kb = c * p.KC;
                     const uint32_t ke = (kb + p.KC < p.Kt) ? kb + p.KC : p.Kt;
+                    // TWO: jobs alternate the two 256-column accumulators
+                    const uint32_t buf = job % NBUF, use = job / NBUF;
                     long long w0 = clock64();
-                    mbar_wait(tmem_empty, acc_ph ^ 1);
+                    mbar_wait(tmem_empty + buf, (use & 1) ^ 1);
                     wait_tmem += clock64() - w0;
                     tc_fence_after();
+                    const uint32_t dbase = tmem + buf * (uint32_t)(Cfg::CLASSES * W);
                     for (uint32_t kt = kb; kt < ke; ++kt) {
                         w0 = clock64();
                         mbar_wait(&full[st], ph);
@@ -1606,11 +1684,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS
 #pragma unroll
                         for (int kk = 0; kk < kBK / 32; ++kk) {
                             const bool first = (kt == kb) && (kk == 0);
-                            const uint64_t bd = sdesc(b0 + kk * 32);
 #pragma unroll
-                            for (int s = 0; s < L; ++s)
-                                mma_i8_pair(tmem + s * W, sdesc(a0 + s * kBM * kBK + kk * 32), bd,
-                                            id_full, (first && s == 0) ? 0u : 1u);
+                            for (int s = 0; s < L; ++s) {
+                                if constexpr (TWO) {
+                                    // limb s x this CTA pair's planes {b_r, c_r}[s]: both classes
+                                    mma_i8_pair(dbase, sdesc(a0 + s * kBM * kBK + kk * 32),
+                                                sdesc(b0 + s * W * kBK + kk * 32), id_full,
+                                                (first && s == 0) ? 0u : 1u);
+                                } else {
+                                    mma_i8_pair(dbase + s * W, sdesc(a0 + s * kBM * kBK + kk * 32),
+                                                sdesc(b0 + kk * 32), id_full, (first && s == 0) ? 0u : 1u);
+                                }
+                            }
                         }
                         tc_commit_pair(&empty[st]);
                         if (++st == STAGES) {
@@ -1618,8 +1703,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS
                             ph ^= 1;
                         }
                     }
-                    tc_commit_pair(tmem_full);
-                    acc_ph ^= 1;
+                    tc_commit_pair(tmem_full + buf);
                 }
             }
             if (p.stats) {
@@ -1630,8 +1714,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS
             }
         }
     } else {
-        epilogue_role<L, W, Cfg::EPI_WARPS, true>(p, pair, npairs, num_tiles, Mt2, rank, nchunks, tmem,
-                                                  s_col, tmem_full, tmem_empty, warp, lane);
+        epilogue_role<L, W, Cfg::EPI_WARPS, true, Cfg::XPOSE, 3, false, 2, TWO>(
+            p, pair, npairs, num_tiles, Mt2, rank, nchunks, tmem, s_col, tmem_full, tmem_empty, warp,
+            lane, smem + STAGES * Cfg::STAGE + 512 + 8 * W);  // 16-byte aligned transpose buffers
     }
 
     tc_fence_before();
@@ -1643,22 +1728,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS
     }
 }
 
-template <int L>
+template <int L, bool TWO = false>
 int launch_gemm2_t(const GemmParams& p, const void* tmA, const void* tmB, int num_sms,
                    cudaStream_t s) {
-    using Cfg = Gemm2Cfg<L>;
+    if constexpr (L == 2 && !TWO) {
+        if (p.two) return launch_gemm2_t<2, true>(p, tmA, tmB, num_sms, s);
+    }
+    using Cfg = Gemm2Cfg<L, TWO>;
     const uint32_t tiles = (p.Mt / 2) * p.Nt;
     uint32_t grid = 2 * tiles < (uint32_t)num_sms ? 2 * tiles : (uint32_t)num_sms;
     grid &= ~1u;
-    k_gemm2<L><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p, *static_cast<const CUtensorMap*>(tmA),
-                                                      *static_cast<const CUtensorMap*>(tmB));
+    k_gemm2<L, TWO><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p, *static_cast<const CUtensorMap*>(tmA),
+                                                           *static_cast<const CUtensorMap*>(tmB));
     return (int)cudaGetLastError();
 }
 
 template <int L>
 int configure_gemm2_t() {
-    return (int)cudaFuncSetAttribute(k_gemm2<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     Gemm2Cfg<L>::SMEM);
+    int e = (int)cudaFuncSetAttribute(k_gemm2<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      Gemm2Cfg<L>::SMEM);
+    if constexpr (L == 2) {
+        if (!e)
+            e = (int)cudaFuncSetAttribute(k_gemm2<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          Gemm2Cfg<2, true>::SMEM);
+    }
+    return e;
 }
 
 template <int L>
@@ -1746,6 +1840,13 @@ int launch_pack_t(int trans, const uint32_t* src, const uint64_t* rowoff, const 
     const uint64_t Rpad = (uint64_t)Rtiles * rpt;
     if (trans) {
         const uint64_t blocks = ((Rpad + 127) / 128) * Kt * (kBK / 32);
+        if constexpr (L == 2) {
+            if (dp.two) {
+                k_pack_cols<2, 4><<<(unsigned)blocks, 256, 0, s>>>(src, rowoff, coloff, vecok, R, K,
+                                                                  rpt, Kt, Rpad, dst, dp);
+                return (int)cudaGetLastError();
+            }
+        }
         k_pack_cols<L><<<(unsigned)blocks, 256, 0, s>>>(src, rowoff, coloff, vecok, R, K, rpt, Kt,
                                                         Rpad, dst, dp);
     } else {
@@ -1838,7 +1939,9 @@ int launch_gemm2(int L, const GemmParams& p, const void* tmA, const void* tmB, i
     return (int)cudaErrorInvalidValue;
 }
 
-int gemm2_b_box_rows(int L) { return (L <= 2 ? 128 : 64) * L / 2; }
+int gemm2_b_box_rows(int L, int two) {
+    return two && L == 2 ? Gemm2Cfg<2, true>::NBH : (L <= 2 ? 128 : 64) * L / 2;
+}
 
 int launch_fill_view(uint32_t* out, const uint64_t* rowoff, const uint64_t* coloff, uint64_t rows,
                      uint64_t cols, uint32_t value, void* stream) {

@@ -186,7 +186,7 @@ GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t c
     // higher clocks than the CTA-pair kernel for the same work (measured,
     // profiles/ab_gemm.py); MHG_GEMM=2cta selects the pair kernel.
     const char* sel = std::getenv("MHG_GEMM");
-    g.pair = sel && std::string(sel) == "2cta";
+    g.pair = sel && (std::string(sel) == "2cta" || std::string(sel) == "2cta2");
     if (g.pair) g.Mt += g.Mt & 1u;  // pairs take two row tiles
     g.Nt = (uint32_t)((cols + g.W - 1) / g.W);
     g.mc = !g.pair && sel && std::string(sel) == "mc";
@@ -198,9 +198,21 @@ GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t c
         const long v = std::strtol(force, nullptr, 10);
         if (v > 0 && (uint64_t)v < g.KC) g.KC = (uint32_t)v;
     }
+    // two-class accumulation (MHG_GEMM=2cta2): the CTA pair with limb s multiplying the
+    // digits of 256^s b mod q.  Class sums obey the same bound as the widest class of the
+    // 3-class layout (2 * 128 * 128 per k); the lean fold (w16 < 256) additionally needs
+    // (32768 + 128 w16) K + 65280 + w16 <= 2^31 - 2^17.
+    g.two = g.pair && g.L == 2 && sel && std::string(sel) == "2cta2";
+    if (g.two) {
+        const uint64_t w16 = (uint64_t(1) << 16) % q;
+        if (w16 < 256) {
+            const uint64_t kcap = ((uint64_t(1) << 31) - (uint64_t(1) << 17) - 65280 - w16) / (32768 + 128 * w16);
+            g.KC = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(g.KC, kcap / kBK));
+        }
+    }
     g.chunks = g.Kt ? (g.Kt + g.KC - 1) / g.KC : 0;
     g.apack_bytes = (uint64_t)g.Mt * kBM * g.Kt * kBK * g.L;
-    g.bpack_bytes = (uint64_t)g.Nt * g.W * g.Kt * kBK * g.L;
+    g.bpack_bytes = (uint64_t)g.Nt * g.W * g.Kt * kBK * g.L * (g.two ? 2 : 1);
     return g;
 }
 

@@ -51,6 +51,7 @@ Counters oblivious_counters(uint64_t n, uint64_t t, const Rect& out, const Rect&
 struct GemmGeometry {
     bool pair;            // CTA-pair kernel (k_gemm2); Mt is then even
     bool mc;              // column-pair clusters with lhs multicast (k_gemm MC); Nt is then even
+    bool two;             // two-class accumulation on the CTA pair (L = 2; rhs with 4 planes)
     uint32_t L, W;        // limbs, output tile width
     uint32_t Mt, Nt, Kt;  // tiles along rows / cols / inner (128-byte K slices)
     uint32_t KC;          // K slices per exact int32 chunk

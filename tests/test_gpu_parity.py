@@ -406,7 +406,7 @@ def test_tu_schur_sweep(gpu, mh, oracle):
     assert macs == sum(((n - k) ** 2) * block for k in range(block, n, block))
 
 
-@pytest.mark.parametrize("kernel", ["1cta", "2cta", "mc"])
+@pytest.mark.parametrize("kernel", ["1cta", "2cta", "2cta2", "mc"])
 def test_both_gemm_kernels(gpu, mh, oracle, monkeypatch, kernel):
     """The single-CTA (default), CTA-pair (cta_group::2, MHG_GEMM=2cta) and
     column-pair multicast-cluster (MHG_GEMM=mc) kernels on ragged views, every
@@ -474,7 +474,7 @@ def test_plan_graph_replay_matches_direct(gpu, mh, oracle):
     assert plan.info()["launches"] == 3
 
 
-@pytest.mark.parametrize("kernel", ["1cta", "2cta", "mc"])
+@pytest.mark.parametrize("kernel", ["1cta", "2cta", "2cta2", "mc"])
 def test_guard_bands(gpu, mh, oracle, monkeypatch, kernel):
     """Out-of-bounds detector (compute-sanitizer is unavailable on this pool):
     each container is wrapped in the middle of a larger device buffer whose
@@ -743,3 +743,33 @@ def test_concurrent_uploads_from_threads(gpu, mh):
     for m, src in zip(mats, srcs):
         assert np.array_equal(m.cells(), src)
         assert m.upload_bytes <= 2 * n * n  # the last (range or full) upload was narrow
+
+
+@pytest.mark.parametrize("q", [P16, 65287, 40961, 257])
+def test_two_class_accumulation(gpu, mh, oracle, monkeypatch, q):
+    """MHG_GEMM=2cta2: the CTA pair with two-class accumulation (limb s multiplies
+    the digits of 256^s b mod q; S = lo + 256 hi; two TMEM jobs double-buffered).
+    Lean one-reduction fold (2^16 mod q < 256: 65521, 65287, 257) and the general
+    fold (40961); random misaligned views incl. multi-chunk K; extreme digits at a
+    long K (closed form)."""
+    monkeypatch.setenv("MHG_GEMM", "2cta2")
+    rng = np.random.default_rng(q)
+    n, t = 1024, 64
+    for op in (OP_ADD, OP_SUB, OP_SET):
+        for force in (None, "2"):
+            if force:
+                monkeypatch.setenv("MHG_FORCE_KCHUNK", force)
+            else:
+                monkeypatch.delenv("MHG_FORCE_KCHUNK", raising=False)
+            r, k, c, corners = _random_views(rng, n)
+            v = _views_from(oracle, n, t, r, k, c, corners)
+            out, lhs, rhs = _fill(oracle, 70 + op, n, q)
+            got, _ = _run_gpu(mh, n, t, q, out, lhs, rhs, v, op)
+            want = out.copy()
+            oracle.mm_dense(n, t, q, want, lhs, rhs, v, op=op)
+            assert np.array_equal(got, want), (q, op, force, r, k, c)
+    monkeypatch.delenv("MHG_FORCE_KCHUNK", raising=False)
+    ex = _extremes(q)
+    for a, b in [(ex[0], ex[0]), (ex[1], ex[0]), (ex[2], ex[4]), (ex[1], ex[1])]:
+        for op in (OP_ADD, OP_SUB):
+            _constant_case(mh, 8192, 64, q, a, b, q - 1, 8192, op)
