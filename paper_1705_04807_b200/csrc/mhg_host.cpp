@@ -274,7 +274,9 @@ struct TensorMaps {
     CUtensorMap a, b;
 };
 
-void make_tmap(CUtensorMap* tm, const void* base, uint64_t bytes, uint32_t box_rows) {
+// 2D tiled tensor map, no swizzle: dims {d0 (inner), d1}, row pitch `pitch` bytes.
+void encode_2d(CUtensorMap* tm, CUtensorMapDataType dtype, const void* base, uint64_t d0, uint64_t d1,
+               uint64_t pitch, uint32_t b0, uint32_t b1) {
     using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                 const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
                                 const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -289,15 +291,44 @@ void make_tmap(CUtensorMap* tm, const void* base, uint64_t bytes, uint32_t box_r
             fail(MHG_ERR_DEVICE, "cuTensorMapEncodeTiled unavailable");
         encode = reinterpret_cast<Encode>(fn);
     }
-    const cuuint64_t dims[2] = {(cuuint64_t)mhg::kBK, bytes / mhg::kBK};
-    const cuuint64_t strides[1] = {(cuuint64_t)mhg::kBK};
-    const cuuint32_t box[2] = {(cuuint32_t)mhg::kBK, box_rows};
+    const cuuint64_t dims[2] = {(cuuint64_t)d0, (cuuint64_t)d1};
+    const cuuint64_t strides[1] = {(cuuint64_t)pitch};
+    const cuuint32_t box[2] = {b0, b1};
     const cuuint32_t estr[2] = {1, 1};
-    const CUresult r = encode(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims,
-                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                              CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    const CUresult r = encode(tm, dtype, 2, const_cast<void*>(base), dims, strides, box, estr,
+                              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(MHG_ERR_DEVICE, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+}
+
+// Packed operand: rows of kBK bytes, boxes of `box_rows` rows.
+void make_tmap(CUtensorMap* tm, const void* base, uint64_t bytes, uint32_t box_rows) {
+    encode_2d(tm, CU_TENSOR_MAP_DATA_TYPE_UINT8, base, mhg::kBK, bytes / mhg::kBK, mhg::kBK,
+              (uint32_t)mhg::kBK, box_rows);
+}
+
+// K1 conversions: the TMA kernel (default; MHG_CONV=1/2 select the LDG/STG kernels)
+// for power-of-two 4 <= t <= 256 with 16-byte aligned rows, else the LDG/STG kernels.
+void convert(const mhg_matrix_s* m, uint32_t* rows, int to_mh, int* flag, void* stream) {
+    static const int mode = [] {
+        const char* e = std::getenv("MHG_CONV");
+        return e ? std::atoi(e) : 3;
+    }();
+    const mhg::TileGeom g = mhg::tile_geom(m->t);
+    const bool tma = mode >= 3 && g.shift >= 0 && m->t % 4 == 0 && m->t <= 256 && m->n % 4 == 0 &&
+                     m->n < (uint64_t(1) << 31) && ((uintptr_t)rows & 15) == 0;
+    if (tma) {
+        CUtensorMap tm;
+        encode_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, rows, m->n, m->n, m->n * 4, (uint32_t)m->t,
+                  mhg::conv_tma_box_rows(m->t));
+        cuda_check(mhg::launch_conv_tma(&tm, m->cells, m->n, g, m->q, flag, to_mh, device_info().sms,
+                                        stream),
+                   to_mh ? "rowmajor_to_mh" : "mh_to_rowmajor");
+    } else if (to_mh) {
+        cuda_check(mhg::launch_rm_to_mh(rows, m->cells, m->n, g, m->q, flag, stream), "rowmajor_to_mh");
+    } else {
+        cuda_check(mhg::launch_mh_to_rm(m->cells, rows, m->n, g, stream), "mh_to_rowmajor");
+    }
 }
 
 TensorMaps tensor_maps(const Buffers& b, const mhg::GemmGeometry& g) {
@@ -664,9 +695,7 @@ mhg_status mhg_rowmajor_to_mh(mhg_matrix dst, const uint32_t* rows, void* stream
         if (!flag) cuda_check(cudaMalloc(&flag, sizeof(int)), "flag alloc");
         cudaStream_t s = (cudaStream_t)stream;
         cuda_check(cudaMemsetAsync(flag, 0, sizeof(int), s), "flag");
-        cuda_check(mhg::launch_rm_to_mh(rows, dst->cells, dst->n, mhg::tile_geom(dst->t), dst->q,
-                                        flag, stream),
-                   "rowmajor_to_mh");
+        convert(dst, const_cast<uint32_t*>(rows), 1, flag, stream);
         int bad = 0;
         cuda_check(cudaMemcpyAsync(&bad, flag, sizeof(int), cudaMemcpyDeviceToHost, s), "flag");
         cuda_check(cudaStreamSynchronize(s), "rowmajor_to_mh sync");
@@ -678,8 +707,7 @@ mhg_status mhg_mh_to_rowmajor(mhg_matrix src, uint32_t* rows, void* stream) {
     return guarded([&] {
         if (!src || !rows) fail(MHG_ERR_INVALID_ARGUMENT, "mh_to_rowmajor: null pointer");
         require_device();
-        cuda_check(mhg::launch_mh_to_rm(src->cells, rows, src->n, mhg::tile_geom(src->t), stream),
-                   "mh_to_rowmajor");
+        convert(src, rows, 0, nullptr, stream);
     });
 }
 
@@ -714,8 +742,14 @@ mhg_status mhg_mh_to_rowmajor_host(mhg_matrix src, uint32_t* host_rows) {
         uint32_t* tmp = nullptr;
         const uint64_t bytes = src->n * src->n * 4;
         cuda_check(cudaMalloc(&tmp, bytes), "scratch alloc");
-        int err = mhg::launch_mh_to_rm(src->cells, tmp, src->n, mhg::tile_geom(src->t), nullptr);
-        if (!err) err = (int)cudaMemcpy(host_rows, tmp, bytes, cudaMemcpyDeviceToHost);
+        int err = 0;
+        try {
+            convert(src, tmp, 0, nullptr, nullptr);
+        } catch (...) {
+            cudaFree(tmp);
+            throw;
+        }
+        err = (int)cudaMemcpy(host_rows, tmp, bytes, cudaMemcpyDeviceToHost);
         cudaFree(tmp);
         cuda_check(err, "mh_to_rowmajor_host");
     });

@@ -101,6 +101,17 @@ int launch_offsets(uint64_t* dst, uint64_t start, uint64_t count, TileGeom g, in
 int launch_rm_to_mh(const uint32_t* rm, uint32_t* mh, uint64_t n, TileGeom g, uint32_t q,
                     int* bad_flag, void* stream);
 int launch_mh_to_rm(const uint32_t* mh, uint32_t* rm, uint64_t n, TileGeom g, void* stream);
+// K1 through the TMA: `tmap` is a CUtensorMap over the row-major buffer (uint32, n x n,
+// box t columns x R rows with R * t * 4 <= 16 KB; conv_tma_box_rows); power-of-two
+// 4 <= t <= 256.  to_mh = 1 also checks residues < q (*bad).
+int launch_conv_tma(const void* tmap, uint32_t* mh, uint64_t n, TileGeom g, uint32_t q, int* bad,
+                    int to_mh, int num_sms, void* stream);
+int conv_tma_smem();  // dynamic shared memory of the TMA conversion kernel
+inline uint32_t conv_tma_box_rows(uint64_t t) {
+    uint32_t R = (uint32_t)t;
+    while ((uint64_t)R * t * 4 > 16384) R >>= 1;
+    return R;
+}
 // Pack an operand into limb planes.  trans = 0: pack rows are view rows, K is
 // view columns (lhs).  trans = 1: pack rows are view columns, K is view rows
 // (rhs, transposed to K-major).  rows_per_tile = 128 (lhs) or W (rhs).

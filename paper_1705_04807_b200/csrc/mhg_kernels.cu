@@ -85,7 +85,7 @@ __global__ void k_offsets(uint64_t* __restrict__ dst, uint64_t start, uint64_t c
 __global__ void k_rm_to_mh(const uint32_t* __restrict__ rm, uint32_t* __restrict__ mh, uint64_t n,
                            TileGeom g, uint32_t q, int* __restrict__ bad) {
     const uint64_t groups = n * n / 4;
-    const bool vec = (g.t % 4 == 0) && (n % 4 == 0);
+    const bool vec = (g.t % 4 == 0) && (n % 4 == 0) && ((reinterpret_cast<uintptr_t>(rm) & 15) == 0);
     int saw_bad = 0;
     if (vec) {
         for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < groups;
@@ -171,7 +171,7 @@ __global__ void k_conv_z(const uint32_t* __restrict__ src, uint32_t* __restrict_
 __global__ void k_mh_to_rm(const uint32_t* __restrict__ mh, uint32_t* __restrict__ rm, uint64_t n,
                            TileGeom g) {
     const uint64_t groups = n * n / 4;
-    const bool vec = (g.t % 4 == 0) && (n % 4 == 0);
+    const bool vec = (g.t % 4 == 0) && (n % 4 == 0) && ((reinterpret_cast<uintptr_t>(rm) & 15) == 0);
     if (vec) {
         // 4 groups per thread per round: all four loads in flight before any store;
         // power-of-two n (power-of-two t) splits the flat index with shifts
@@ -844,6 +844,115 @@ __device__ __forceinline__ void tmem_zero(uint32_t taddr) {
 
 __device__ __forceinline__ void tmem_wait_st() {
     asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
+
+// K1 through the TMA (power-of-two t, 4 <= t <= 256): the unit is a box of R
+// rows x t columns of one tile (R*t*4 <= 16 KB; a whole tile up to t = 64).  Its
+// Morton image is one contiguous run (rows of a tile are row-major), its
+// row-major image a 2D box of the tensor map `tm` (uint32, n x n).  One thread
+// per CTA keeps kConvBufs units in flight: to_mh = 1: 2D tensor load -> smem ->
+// (residue check by all threads) -> 1D bulk store; to_mh = 0: 1D bulk load ->
+// smem -> 2D tensor store.  No data passes through registers except the check.
+constexpr int kConvUnitBytes = 16384;
+
+__device__ __forceinline__ void tma2d_load(uint32_t dst, const CUtensorMap* tm, int c0, int c1,
+                                           uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__device__ __forceinline__ void tma2d_store(const CUtensorMap* tm, int c0, int c1, uint32_t src) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(
+                     reinterpret_cast<uint64_t>(tm)),
+                 "r"(c0), "r"(c1), "r"(src)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(src),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() {
+    asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+
+template <int kConvBufs>
+__global__ void __launch_bounds__(128) k_conv_tma(const __grid_constant__ CUtensorMap tm,
+                                                  uint32_t* __restrict__ mh, uint64_t n, TileGeom g,
+                                                  uint32_t R, uint32_t q, int* __restrict__ bad,
+                                                  int to_mh) {
+    extern __shared__ uint8_t conv_raw[];
+    uint8_t* buf = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(conv_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t full[kConvBufs];
+    const uint32_t t = (uint32_t)g.t;
+    const uint32_t ubytes = R * t * 4;
+    const uint32_t upt = t / R;  // units per tile
+    const uint64_t units = n * n / ((uint64_t)R * t);
+    const bool issuer = threadIdx.x == 0;
+    if (issuer) {
+        for (int b = 0; b < kConvBufs; ++b) mbar_init(&full[b], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    // unit u: tile z = u / upt (Z order), rows [ (u % upt) R, +R ) of that tile
+    auto coords = [&](uint64_t u, int& c0, int& c1, uint64_t& zoff) {
+        const uint64_t z = u / upt;
+        const uint32_t part = (uint32_t)(u % upt);
+        c0 = (int)((uint64_t)compact32(z) * t);
+        c1 = (int)((uint64_t)compact32(z >> 1) * t + part * R);
+        zoff = z * g.tt + (uint64_t)part * R * t;
+    };
+    auto issue_load = [&](uint64_t u, int b) {
+        int c0, c1;
+        uint64_t zoff;
+        coords(u, c0, c1, zoff);
+        mbar_expect_tx(&full[b], ubytes);
+        if (to_mh) tma2d_load(smem_u32(buf + b * kConvUnitBytes), &tm, c0, c1, &full[b]);
+        else bulk_g2s(buf + b * kConvUnitBytes, mh + zoff, ubytes, &full[b]);
+    };
+    const uint64_t first = blockIdx.x, step = gridDim.x;
+    if (issuer) {
+        uint64_t u = first;
+        for (int b = 0; b < kConvBufs && u < units; ++b, u += step) issue_load(u, b);
+    }
+    int saw_bad = 0;
+    uint32_t k = 0;
+    for (uint64_t u = first; u < units; u += step, ++k) {
+        const int b = (int)(k % kConvBufs);
+        const uint32_t phase = (k / kConvBufs) & 1;
+        if (to_mh) {
+            mbar_wait(&full[b], phase);
+            const uint4* v = reinterpret_cast<const uint4*>(buf + b * kConvUnitBytes);
+            for (uint32_t i = threadIdx.x; i < ubytes / 16; i += blockDim.x) {
+                const uint4 x = v[i];
+                saw_bad |= (x.x >= q) | (x.y >= q) | (x.z >= q) | (x.w >= q);
+            }
+            __syncthreads();  // every thread is done reading buffer b
+        }
+        if (issuer) {
+            if (!to_mh) mbar_wait(&full[b], phase);
+            int c0, c1;
+            uint64_t zoff;
+            coords(u, c0, c1, zoff);
+            const uint32_t src = smem_u32(buf + b * kConvUnitBytes);
+            if (to_mh) bulk_s2g(mh + zoff, src, ubytes);
+            else tma2d_store(&tm, c0, c1, src);
+            bulk_commit();
+            bulk_wait_read0();  // the store has read buffer b
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            const uint64_t nu = u + (uint64_t)kConvBufs * step;
+            if (nu < units) issue_load(nu, b);
+        }
+    }
+    if (issuer) bulk_wait0();
+    if (to_mh && __syncthreads_or(saw_bad) && threadIdx.x == 0) atomicOr(bad, 1);
 }
 
 // Epilogue role of both GEMM kernels (warps 2 .. 2+EPI_WARPS-1).  Per tile:
@@ -1878,14 +1987,17 @@ static int conv_mode() {
 
 int launch_rm_to_mh(const uint32_t* rm, uint32_t* mh, uint64_t n, TileGeom g, uint32_t q,
                     int* bad_flag, void* stream) {
-    const bool z = g.shift >= 0 && g.t % 4 == 0 && conv_mode() >= 1;
+    // row-major buffers that are not 16-byte aligned take the element-wise path
+    const bool aligned = (reinterpret_cast<uintptr_t>(rm) & 15) == 0;
+    const bool z = aligned && g.shift >= 0 && g.t % 4 == 0 && conv_mode() >= 1;
     if (z) k_conv_z<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(rm, mh, n, g, q, bad_flag, 1);
     else k_rm_to_mh<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(rm, mh, n, g, q, bad_flag);
     return (int)cudaGetLastError();
 }
 
 int launch_mh_to_rm(const uint32_t* mh, uint32_t* rm, uint64_t n, TileGeom g, void* stream) {
-    const bool z = g.shift >= 0 && g.t % 4 == 0 && conv_mode() >= 2;
+    const bool z = ((reinterpret_cast<uintptr_t>(rm) & 15) == 0) && g.shift >= 0 && g.t % 4 == 0 &&
+                   conv_mode() >= 2;
     if (z) k_conv_z<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(mh, rm, n, g, 0u, nullptr, 0);
     else k_mh_to_rm<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(mh, rm, n, g);
     return (int)cudaGetLastError();
@@ -1916,6 +2028,23 @@ int launch_gemm(int L, const GemmParams& p, int num_sms, void* stream) {
 }
 
 int configure_kernels() {
+    {
+        int e = (int)cudaFuncSetAttribute(k_conv_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          4 * kConvUnitBytes + 1024);
+        if (!e)
+            e = (int)cudaFuncSetAttribute(k_conv_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          2 * kConvUnitBytes + 1024);
+        if (!e)
+            e = (int)cudaFuncSetAttribute(k_conv_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          3 * kConvUnitBytes + 1024);
+        if (!e)
+            e = (int)cudaFuncSetAttribute(k_conv_tma<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          6 * kConvUnitBytes + 1024);
+        if (!e)
+            e = (int)cudaFuncSetAttribute(k_conv_tma<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          12 * kConvUnitBytes + 1024);
+        if (e) return e;
+    }
     int e = configure_gemm_t<1>();
     if (!e) e = configure_gemm_t<2>();
     if (!e) e = configure_gemm_t<3>();
@@ -1979,6 +2108,36 @@ __global__ void k_widen16(const uint16_t* __restrict__ src, uint32_t* __restrict
     }
     const uint64_t tail = head + groups * 8 + tid;
     if (tail < count) dst[tail] = src[tail];
+}
+
+// units in flight: kConvBufs per CTA x CTAs per SM = 12 (MHG_CONV_NB = 2 / 3 / 4 / 6 / 12
+// picks 6 / 4 / 3 / 2 / 1 CTAs per SM; more independent issuers measured faster)
+static int conv_nb() {
+    static const int nb = [] {
+        const char* e = std::getenv("MHG_CONV_NB");
+        const int v = e ? std::atoi(e) : 4;
+        return (v == 2 || v == 3 || v == 4 || v == 6 || v == 12) ? v : 4;
+    }();
+    return nb;
+}
+
+int conv_tma_smem() { return 12 * kConvUnitBytes + 1024; }
+
+int launch_conv_tma(const void* tmap, uint32_t* mh, uint64_t n, TileGeom g, uint32_t q, int* bad,
+                    int to_mh, int num_sms, void* stream) {
+    uint32_t R = (uint32_t)g.t;
+    while ((uint64_t)R * g.t * 4 > (uint64_t)kConvUnitBytes) R >>= 1;
+    const int nb = conv_nb(), per_sm = 12 / nb;
+    const int grid = per_sm * (num_sms > 0 ? num_sms : 148);
+    const int smem = nb * kConvUnitBytes + 1024;
+    const CUtensorMap& tm = *static_cast<const CUtensorMap*>(tmap);
+    cudaStream_t s = (cudaStream_t)stream;
+    if (nb == 4) k_conv_tma<4><<<grid, 128, smem, s>>>(tm, mh, n, g, R, q, bad, to_mh);
+    else if (nb == 2) k_conv_tma<2><<<grid, 128, smem, s>>>(tm, mh, n, g, R, q, bad, to_mh);
+    else if (nb == 3) k_conv_tma<3><<<grid, 128, smem, s>>>(tm, mh, n, g, R, q, bad, to_mh);
+    else if (nb == 12) k_conv_tma<12><<<grid, 128, smem, s>>>(tm, mh, n, g, R, q, bad, to_mh);
+    else k_conv_tma<6><<<grid, 128, smem, s>>>(tm, mh, n, g, R, q, bad, to_mh);
+    return (int)cudaGetLastError();
 }
 
 int launch_widen16(const uint16_t* src, uint32_t* dst, uint64_t count, int num_sms, void* stream) {

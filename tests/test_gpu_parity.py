@@ -773,3 +773,50 @@ def test_two_class_accumulation(gpu, mh, oracle, monkeypatch, q):
     for a, b in [(ex[0], ex[0]), (ex[1], ex[0]), (ex[2], ex[4]), (ex[1], ex[1])]:
         for op in (OP_ADD, OP_SUB):
             _constant_case(mh, 8192, 64, q, a, b, q - 1, 8192, op)
+
+
+@pytest.mark.parametrize("conv", ["3", "2", "0"])
+def test_conversion_kernel_variants(gpu, mh, oracle, monkeypatch, conv):
+    """K1 on device buffers through the C ABI: the TMA kernel (MHG_CONV=3, default;
+    units of R rows x t columns, R < t from t = 128 on), the Morton-order LDG/STG
+    kernel (2) and the row-order one (0), for t = 4 ... 256 and a non-power-of-two
+    tile (fallback); round trip exact; an out-of-range residue in the last unit
+    is reported; misaligned row buffers fall back."""
+    import subprocess
+    import sys
+    # the conversion mode is read once per process: run the cases in a child
+    code = f"""
+import numpy as np, torch, sys
+sys.path.insert(0, {repr(str(__import__('pathlib').Path(__file__).resolve().parents[1]))})
+import paper_1705_04807_b200 as mh
+from oracle.binding import Oracle
+orc = Oracle()
+lib = mh.lib()
+for (n, t) in [(8, 4), (64, 8), (1024, 32), (2048, 64), (2048, 128), (4096, 256), (96, 6)]:
+    q = 65521
+    rng = np.random.default_rng(n + t)
+    grid = rng.integers(0, q, size=(n, n), dtype=np.uint32)
+    m = mh.Matrix(mh.Layout(n, t), mh.Modulus(q))
+    rm = torch.from_numpy(grid.reshape(-1).view(np.int32)).cuda()
+    assert lib.mhg_rowmajor_to_mh(m.handle, rm.data_ptr(), None) == 0
+    assert np.array_equal(m.cells(), orc.rowmajor_to_mh(n, t, grid)), (n, t)
+    back = torch.zeros_like(rm)
+    assert lib.mhg_mh_to_rowmajor(m.handle, back.data_ptr(), None) == 0
+    torch.cuda.synchronize()
+    assert np.array_equal(back.cpu().numpy().view(np.uint32).reshape(n, n), grid), (n, t)
+    bad = rm.clone()
+    bad[-1] = q
+    assert lib.mhg_rowmajor_to_mh(m.handle, bad.data_ptr(), None) == 1, (n, t)
+# misaligned row-major buffer (4-byte offset): LDG/STG fallback, same result
+n, t = 1024, 64
+grid = np.random.default_rng(1).integers(0, 97, size=(n, n), dtype=np.uint32)
+m = mh.Matrix(mh.Layout(n, t), mh.Modulus(97))
+buf = torch.zeros(n * n + 1, dtype=torch.int32, device="cuda")
+buf[1:] = torch.from_numpy(grid.reshape(-1).view(np.int32)).cuda()
+assert lib.mhg_rowmajor_to_mh(m.handle, buf.data_ptr() + 4, None) == 0
+assert np.array_equal(m.cells(), orc.rowmajor_to_mh(n, t, grid))
+print("ok")
+"""
+    env = dict(__import__("os").environ, MHG_CONV=conv)
+    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
