@@ -218,34 +218,38 @@ def time_conversions(mh, torch, mats, n, q, hbm_gbs, reps=3):
             "kernel": "k_conv_z (Morton-order, 16-B accesses, residue check on the way in)"}
 
 
-def e2e_pipelined(mh, torch, lay, mod, flats, set0, prob0, op, n, steps, macs):
+def e2e_pipelined(mh, torch, lay, mod, flats, set0, prob0, op, n, steps, macs, nsets=3):
     """End to end through the public C ABI with pinned HOST buffers: every step
     uploads its three inputs (mhg_matrix_upload), runs the plan, and downloads
-    the result (mhg_matrix_download).  Two container sets alternate so step i's
-    result download and step i+1's uploads overlap step i's compute: H2D,
-    compute and D2H run on three streams ordered by events."""
+    the result (mhg_matrix_download).  `nsets` container sets rotate so step i's
+    result download (which waits for step i's compute) and the uploads of steps
+    i+1 .. i+nsets-1 overlap: H2D, compute and D2H run on three streams ordered
+    by events.  With 2 sets the uploads of step i+2 wait for step i's compute +
+    download (~12 + ~23 ms at n = 16384); 3 sets keep the H2D stream busy."""
     hosts = []
     for f in flats:
         h = torch.empty(n * n, dtype=torch.int32, pin_memory=True)
         h.copy_(f)
         hosts.append(h)
-    res = [torch.empty(n * n, dtype=torch.int32, pin_memory=True) for _ in range(2)]
-    fl2 = [torch.empty_like(f) for f in flats]
-    A2, B2, C2 = (mh.Matrix.wrap(lay, mod, f.data_ptr(), owner=f) for f in fl2)
-    plan2 = mh.Plan(mh.Problem(mh.Sub(A2, prob0.a.origin, prob0.a.rows, prob0.a.cols),
-                               mh.Sub(B2, prob0.b.origin, prob0.b.rows, prob0.b.cols),
-                               mh.Sub(C2, prob0.c.origin, prob0.c.rows, prob0.c.cols)), op)
-    sets = [set0, (A2, B2, C2, plan2)]
+    res = [torch.empty(n * n, dtype=torch.int32, pin_memory=True) for _ in range(nsets)]
+    sets = [set0]
+    for _ in range(nsets - 1):
+        fl2 = [torch.empty_like(f) for f in flats]
+        A2, B2, C2 = (mh.Matrix.wrap(lay, mod, f.data_ptr(), owner=f) for f in fl2)
+        plan2 = mh.Plan(mh.Problem(mh.Sub(A2, prob0.a.origin, prob0.a.rows, prob0.a.cols),
+                                   mh.Sub(B2, prob0.b.origin, prob0.b.rows, prob0.b.cols),
+                                   mh.Sub(C2, prob0.c.origin, prob0.c.rows, prob0.c.cols)), op)
+        sets.append((A2, B2, C2, plan2))
     s_up, s_cmp, s_dn = torch.cuda.Stream(), torch.cuda.Stream(), torch.cuda.Stream()
-    ev_up = [torch.cuda.Event() for _ in range(2)]
-    ev_cmp = [torch.cuda.Event() for _ in range(2)]
-    ev_dn = [torch.cuda.Event() for _ in range(2)]
+    ev_up = [torch.cuda.Event() for _ in range(nsets)]
+    ev_cmp = [torch.cuda.Event() for _ in range(nsets)]
+    ev_dn = [torch.cuda.Event() for _ in range(nsets)]
     lib = mh.lib()
 
     def one(i):
-        k = i % 2
+        k = i % nsets
         A_, B_, C_, pl = sets[k]
-        if i >= 2:  # container set k is free once its previous step was computed and read back
+        if i >= nsets:  # container set k is free once its previous step was computed and read back
             s_up.wait_event(ev_cmp[k])
             s_up.wait_event(ev_dn[k])
         for h_, m_ in zip(hosts, (A_, B_, C_)):
@@ -258,7 +262,7 @@ def e2e_pipelined(mh, torch, lay, mod, flats, set0, prob0, op, n, steps, macs):
         mh._check(lib.mhg_matrix_download(A_.handle, res[k].data_ptr(), s_dn.cuda_stream))
         ev_dn[k].record(s_dn)
 
-    for i in range(2):  # warm-up of both sets / graphs
+    for i in range(nsets):  # warm-up of every set / graph
         one(i)
     torch.cuda.synchronize()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -268,14 +272,14 @@ def e2e_pipelined(mh, torch, lay, mod, flats, set0, prob0, op, n, steps, macs):
     t1.record(s_dn)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1) / steps
-    h2d = sum(m_.upload_bytes for m_ in sets[(steps - 1) % 2][:3])  # PCIe bytes of the last step
+    h2d = sum(m_.upload_bytes for m_ in sets[(steps - 1) % nsets][:3])  # PCIe bytes of the last step
     return {"value": macs / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": n * n * 4, "steps": steps, "ms_per_step": ms,
-            "upload_wire": "uint16" if h2d == 3 * n * n * 2 else "uint32",
+            "upload_wire": "uint16" if h2d == 3 * n * n * 2 else "uint32", "container_sets": nsets,
             "path": "pinned host -> mhg_matrix_upload x3 (uint16 wire for q <= 2^16: host-threaded "
                     "narrowing into pinned staging, device widening) -> mhg_plan_run -> "
-                    "mhg_matrix_download -> pinned host; 2 container sets, H2D / compute / D2H "
-                    "streams overlapped"}
+                    "mhg_matrix_download -> pinned host; %d container sets, H2D / compute / D2H "
+                    "streams overlapped" % nsets}
 
 
 def e2e_ranked(mh, torch, dist, mats, flats, out_f, step, stream, b, e, steps, macs, dev, barrier):
@@ -442,7 +446,7 @@ def run_gpu(args, rank, world, local_rank):
         e2e_steps = max(1, min(args.steps, args.e2e_steps))
         if world == 1:
             e2e = e2e_pipelined(mh, torch, lay, mod, flats, (A, B, Cm, plan), prob, op, n, e2e_steps,
-                                macs_total)
+                                macs_total, nsets=args.e2e_sets)
         else:
             e2e = e2e_ranked(mh, torch, dist, (A, B, Cm), flats, out_f, step, stream, b, e, e2e_steps,
                              macs_total, dev, barrier)
@@ -517,6 +521,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=30,
                     help="e2e steps (default = the device steps; the pipeline fill and drain are amortised over them)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--e2e-sets", type=int, default=3,
+                    help="container sets rotated by the e2e pipeline (uploads run this many steps ahead)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-threads", type=int, default=0)
     args = ap.parse_args()
