@@ -357,22 +357,44 @@ struct Fork {
 // Pack both operands and run the GEMM: 2 pack launches + 1 GEMM launch.
 // Pack one operand of a multiply into its stage image (which = 0: lhs, K-major rows;
 // 1: rhs, transposed).  The lhs digits of C -= A.B are negated here.
+// Pack job of one operand (which = 0: lhs, K-major rows, digits negated for C -= A.B;
+// 1: rhs, transposed; two-class rhs with 4 planes when g.two).
+mhg::PackArgs pack_args(const Buffers& b, const mhg_view& out, const mhg_view& v, const Checked& c,
+                        const mhg::GemmGeometry& g, mhg_op op, int which) {
+    const mhg::LimbParams lp = mhg::limb_params(out.mat->q);
+    const uint32_t m32 = (uint32_t)((uint64_t(1) << 32) / out.mat->q);
+    mhg::PackArgs a{};
+    a.src = v.mat->cells;
+    a.vecok = out.mat->t % 4 == 0;
+    a.Kt = g.Kt;
+    if (which == 0) {
+        a.rowoff = b.lhs_row;
+        a.coloff = b.lhs_col;
+        a.R = c.rl.rows;
+        a.K = c.rl.cols;
+        a.rpt = mhg::kBM;
+        a.Rtiles = g.Mt;
+        a.dst = b.apack;
+        a.dp = mhg::DigitParams{out.mat->q, lp.H, op == MHG_OP_SUB ? 1 : 0, 0, m32};
+    } else {
+        a.rowoff = b.rhs_row;
+        a.coloff = b.rhs_col;
+        a.R = c.rr.cols;
+        a.K = c.rr.rows;
+        a.rpt = g.W;
+        a.Rtiles = g.Nt;
+        a.dst = b.bpack;
+        a.dp = mhg::DigitParams{out.mat->q, lp.H, 0, g.two ? 1 : 0, m32};
+    }
+    return a;
+}
+
 void launch_pack_operand(const Buffers& b, const mhg_view& out, const mhg_view& v, const Checked& c,
                          const mhg::GemmGeometry& g, mhg_op op, int which, void* stream) {
-    const mhg::LimbParams lp = mhg::limb_params(out.mat->q);
-    const int vecok = out.mat->t % 4 == 0;
-    const uint32_t m32 = (uint32_t)((uint64_t(1) << 32) / out.mat->q);
-    if (which == 0) {
-        const mhg::DigitParams dl{out.mat->q, lp.H, op == MHG_OP_SUB ? 1 : 0, 0, m32};
-        cuda_check(mhg::launch_pack((int)g.L, 0, v.mat->cells, b.lhs_row, b.lhs_col, vecok, c.rl.rows,
-                                    c.rl.cols, mhg::kBM, g.Mt, g.Kt, b.apack, dl, stream),
-                   "pack lhs");
-    } else {
-        const mhg::DigitParams dr{out.mat->q, lp.H, 0, g.two ? 1 : 0, m32};
-        cuda_check(mhg::launch_pack((int)g.L, 1, v.mat->cells, b.rhs_row, b.rhs_col, vecok, c.rr.cols,
-                                    c.rr.rows, g.W, g.Nt, g.Kt, b.bpack, dr, stream),
-                   "pack rhs");
-    }
+    const mhg::PackArgs a = pack_args(b, out, v, c, g, op, which);
+    cuda_check(mhg::launch_pack((int)g.L, which, a.src, a.rowoff, a.coloff, a.vecok, a.R, a.K, a.rpt,
+                                a.Rtiles, a.Kt, a.dst, a.dp, stream),
+               which == 0 ? "pack lhs" : "pack rhs");
 }
 
 void launch_gemm_stage(const Buffers& b, const mhg_view& out, const Checked& c,
@@ -383,8 +405,19 @@ void launch_multiply(const Buffers& b, const mhg_view& out, const mhg_view& lhs,
                      const mhg_view& rhs, const Checked& c, const mhg::GemmGeometry& g,
                      mhg_op op, void* stream, cudaEvent_t gemm_begin = nullptr,
                      cudaEvent_t gemm_end = nullptr, const Fork* fork = nullptr) {
-    // with a fork (graph capture), the two independent packs become parallel
-    // branches joined before the GEMM
+    // default: both packs in one launch (k_pack_pair); MHG_PACK_FUSED=0 launches them
+    // separately -- with a fork (graph capture) as parallel branches joined before the GEMM
+    static const bool fused = [] {
+        const char* e = std::getenv("MHG_PACK_FUSED");
+        return !(e && std::atoi(e) == 0);
+    }();
+    if (fused) {
+        cuda_check(mhg::launch_pack_pair((int)g.L, pack_args(b, out, lhs, c, g, op, 0),
+                                         pack_args(b, out, rhs, c, g, op, 1), stream),
+                   "pack lhs + rhs");
+        launch_gemm_stage(b, out, c, g, op, stream, gemm_begin, gemm_end);
+        return;
+    }
     void* rhs_stream = stream;
     if (fork) {
         cuda_check(cudaEventRecord(fork->split, (cudaStream_t)stream), "fork");

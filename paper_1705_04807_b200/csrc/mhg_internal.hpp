@@ -118,6 +118,20 @@ inline uint32_t conv_tma_box_rows(uint64_t t) {
 int launch_pack(int L, int trans, const uint32_t* src, const uint64_t* rowoff,
                 const uint64_t* coloff, int vecok, uint64_t R, uint64_t K, uint32_t rows_per_tile,
                 uint32_t Rtiles, uint32_t Kt, int8_t* dst, DigitParams dp, void* stream);
+// One operand's pack job (launch_pack's arguments; Rpad is derived).
+struct PackArgs {
+    const uint32_t* src;
+    const uint64_t* rowoff;
+    const uint64_t* coloff;
+    int vecok;
+    uint64_t R, K;
+    uint32_t rpt, Rtiles, Kt;
+    uint64_t Rpad;
+    int8_t* dst;
+    DigitParams dp;
+};
+// lhs (rows, trans = 0) and rhs (cols, trans = 1) packs of one multiply in one launch.
+int launch_pack_pair(int L, const PackArgs& lhs, const PackArgs& rhs, void* stream);
 int launch_gemm(int L, const GemmParams& p, int num_sms, void* stream);
 int gemm_smem_bytes(int L);
 int configure_kernels();  // one-time kernel attributes (dynamic smem opt-in)

@@ -303,17 +303,17 @@ constexpr int kRowsStride = kPackK + 16;
 #define MHG_PACK_MINB 8
 #endif
 template <int L>
-__global__ void __launch_bounds__(256, MHG_PACK_MINB) k_pack_rows(const uint32_t* __restrict__ src,
-                                                   const uint64_t* __restrict__ rowoff,
-                                                   const uint64_t* __restrict__ coloff, int vecok,
-                                                   uint64_t R, uint64_t K, uint32_t rpt, uint32_t Kt,
-                                                   uint64_t Rpad, int8_t* __restrict__ dst,
-                                                   DigitParams dp) {
-    __shared__ __align__(16) uint8_t sd[L][32][kRowsStride];
+__device__ __forceinline__ void pack_rows_block(uint32_t bid, const uint32_t* __restrict__ src,
+                                                const uint64_t* __restrict__ rowoff,
+                                                const uint64_t* __restrict__ coloff, int vecok,
+                                                uint64_t R, uint64_t K, uint32_t rpt, uint32_t Kt,
+                                                uint64_t Rpad, int8_t* __restrict__ dst,
+                                                const DigitParams& dp, uint8_t* smem) {
+    auto& sd = *reinterpret_cast<uint8_t(*)[L][32][kRowsStride]>(smem);
     const uint64_t kpad = (uint64_t)Kt * kBK;
     const uint32_t nkb = (uint32_t)((kpad + kPackK - 1) / kPackK);
-    const uint32_t kb = blockIdx.x % nkb;
-    const uint64_t pr0 = (uint64_t)(blockIdx.x / nkb) * 32;
+    const uint32_t kb = bid % nkb;
+    const uint64_t pr0 = (uint64_t)(bid / nkb) * 32;
     const uint64_t k0 = (uint64_t)kb * kPackK;
     const int tk = threadIdx.x & 31, tr = threadIdx.x >> 5;
     uint64_t ri[4];
@@ -342,6 +342,17 @@ __global__ void __launch_bounds__(256, MHG_PACK_MINB) k_pack_rows(const uint32_t
     }
 }
 
+template <int L>
+__global__ void __launch_bounds__(256, MHG_PACK_MINB) k_pack_rows(const uint32_t* __restrict__ src,
+                                                   const uint64_t* __restrict__ rowoff,
+                                                   const uint64_t* __restrict__ coloff, int vecok,
+                                                   uint64_t R, uint64_t K, uint32_t rpt, uint32_t Kt,
+                                                   uint64_t Rpad, int8_t* __restrict__ dst,
+                                                   DigitParams dp) {
+    __shared__ __align__(16) uint8_t sd[L * 32 * kRowsStride];
+    pack_rows_block<L>(blockIdx.x, src, rowoff, coloff, vecok, R, K, rpt, Kt, Rpad, dst, dp, sd);
+}
+
 // rhs (transposed to K-major): pack rows = view columns (contiguous in the
 // source), K = view rows.  Block: 128 pack rows x 32 K; thread: 4 consecutive
 // pack rows (one 16-byte load) x 4 K rows, transposed in registers.
@@ -350,17 +361,17 @@ constexpr int kColsStride = 36;  // 32 K bytes + 4 pad
 // P = L planes, or P = 2L for the two-class rhs (L = 2): planes [b0, c0, b1, c1] with
 // c = 256 b mod q, so CTA r of a pair fetches its planes {b_r, c_r} as one box.
 template <int L, int P = L>
-__global__ void __launch_bounds__(256, MHG_PACK_MINB) k_pack_cols(const uint32_t* __restrict__ src,
-                                                   const uint64_t* __restrict__ rowoff,
-                                                   const uint64_t* __restrict__ coloff, int vecok,
-                                                   uint64_t R, uint64_t K, uint32_t rpt, uint32_t Kt,
-                                                   uint64_t Rpad, int8_t* __restrict__ dst,
-                                                   DigitParams dp) {
+__device__ __forceinline__ void pack_cols_block(uint32_t bid, const uint32_t* __restrict__ src,
+                                                const uint64_t* __restrict__ rowoff,
+                                                const uint64_t* __restrict__ coloff, int vecok,
+                                                uint64_t R, uint64_t K, uint32_t rpt, uint32_t Kt,
+                                                uint64_t Rpad, int8_t* __restrict__ dst,
+                                                const DigitParams& dp, uint8_t* smem) {
     static_assert(P == L || (L == 2 && P == 4), "plane layout");
-    __shared__ __align__(16) uint8_t sd[P][128][kColsStride];
+    auto& sd = *reinterpret_cast<uint8_t(*)[P][128][kColsStride]>(smem);
     const uint32_t nkq = Kt * (kBK / 32);         // 32-wide K slices
-    const uint32_t kq = blockIdx.x % nkq;
-    const uint64_t pr0 = (uint64_t)(blockIdx.x / nkq) * 128;
+    const uint32_t kq = bid % nkq;
+    const uint64_t pr0 = (uint64_t)(bid / nkq) * 128;
     const uint64_t k0 = (uint64_t)kq * 32;
     const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
     uint64_t ki[4];
@@ -413,6 +424,34 @@ __global__ void __launch_bounds__(256, MHG_PACK_MINB) k_pack_cols(const uint32_t
         *reinterpret_cast<uint4*>(pack_dst<P>(dst, pr, k0 + 16 * h, s, rpt, Kt)) =
             make_uint4(w[0], w[1], w[2], w[3]);
     }
+}
+
+template <int L, int P = L>
+__global__ void __launch_bounds__(256, MHG_PACK_MINB) k_pack_cols(const uint32_t* __restrict__ src,
+                                                   const uint64_t* __restrict__ rowoff,
+                                                   const uint64_t* __restrict__ coloff, int vecok,
+                                                   uint64_t R, uint64_t K, uint32_t rpt, uint32_t Kt,
+                                                   uint64_t Rpad, int8_t* __restrict__ dst,
+                                                   DigitParams dp) {
+    __shared__ __align__(16) uint8_t sd[P * 128 * kColsStride];
+    pack_cols_block<L, P>(blockIdx.x, src, rowoff, coloff, vecok, R, K, rpt, Kt, Rpad, dst, dp, sd);
+}
+
+// Both operands of a multiply in ONE launch: blocks [0, nrows) pack the lhs (rows
+// kernel body), the rest the rhs (cols body).  Two HBM-bound grids of ~2 waves
+// each otherwise pay two ramp-down tails (the second graph branch started ~9 us
+// late at cfg3, profiles/r01_pack_fused.txt).
+template <int L, int P = L>
+__global__ void __launch_bounds__(256, MHG_PACK_MINB) k_pack_pair(PackArgs a, PackArgs b,
+                                                                  uint32_t nrows) {
+    constexpr int ROWS_SMEM = L * 32 * kRowsStride, COLS_SMEM = P * 128 * kColsStride;
+    __shared__ __align__(16) uint8_t sd[ROWS_SMEM > COLS_SMEM ? ROWS_SMEM : COLS_SMEM];
+    if (blockIdx.x < nrows)
+        pack_rows_block<L>(blockIdx.x, a.src, a.rowoff, a.coloff, a.vecok, a.R, a.K, a.rpt, a.Kt,
+                           a.Rpad, a.dst, a.dp, sd);
+    else
+        pack_cols_block<L, P>(blockIdx.x - nrows, b.src, b.rowoff, b.coloff, b.vecok, b.R, b.K, b.rpt,
+                              b.Kt, b.Rpad, b.dst, b.dp, sd);
 }
 
 // ------------------------------------------------------------------- K3
@@ -2001,6 +2040,27 @@ int launch_mh_to_rm(const uint32_t* mh, uint32_t* rm, uint64_t n, TileGeom g, vo
     if (z) k_conv_z<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(mh, rm, n, g, 0u, nullptr, 0);
     else k_mh_to_rm<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(mh, rm, n, g);
     return (int)cudaGetLastError();
+}
+
+template <int L, int P = L>
+int launch_pack_pair_t(PackArgs a, PackArgs b, cudaStream_t s) {
+    a.Rpad = (uint64_t)a.Rtiles * a.rpt;
+    b.Rpad = (uint64_t)b.Rtiles * b.rpt;
+    const uint64_t na = (a.Rpad / 32) * (((uint64_t)a.Kt * kBK + kPackK - 1) / kPackK);
+    const uint64_t nb = ((b.Rpad + 127) / 128) * b.Kt * (kBK / 32);
+    k_pack_pair<L, P><<<(unsigned)(na + nb), 256, 0, s>>>(a, b, (uint32_t)na);
+    return (int)cudaGetLastError();
+}
+
+int launch_pack_pair(int L, const PackArgs& lhs, const PackArgs& rhs, void* stream) {
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (L) {
+        case 1: return launch_pack_pair_t<1>(lhs, rhs, s);
+        case 2: return rhs.dp.two ? launch_pack_pair_t<2, 4>(lhs, rhs, s) : launch_pack_pair_t<2>(lhs, rhs, s);
+        case 3: return launch_pack_pair_t<3>(lhs, rhs, s);
+        case 4: return launch_pack_pair_t<4>(lhs, rhs, s);
+    }
+    return (int)cudaErrorInvalidValue;
 }
 
 int launch_pack(int L, int trans, const uint32_t* src, const uint64_t* rowoff,
