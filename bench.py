@@ -494,7 +494,7 @@ def run_gpu(args, rank, world, local_rank):
             "data": "synthetic: uniform residues in [0,p) drawn on device (torch.Generator)",
             "config": {"workload": args.workload, "description": DESCR[args.workload], "n": n,
                        "t": t, "p": q, "op": opname, "limbs": L,
-                       "tiles": info["tiles"], "k_chunks": info["k_chunks"],
+                       "tiles": info["tiles"], "k_chunks": info["k_chunks"], "digits": info.get("digits"),
                        "partition": f"C-stationary Morton blocks over {world} GPU(s)"
                                     + ({"p2p": f", {len(plans)} K segments, packed limb planes "
                                                "pulled over CUDA IPC peer memory by the copy "

@@ -140,6 +140,7 @@ def lib():
         "mhg_copy_async": ([vp, vp, u64, vp], C.c_int),
         "mhg_plan_counters": ([vp, P(Counters)], C.c_int),
         "mhg_plan_info": ([vp, P(u64), P(u64), P(u32), P(u32), P(u64)], C.c_int),
+        "mhg_plan_digits": ([vp, P(C.c_int)], C.c_int),
         "mhg_plan_destroy": ([vp], C.c_int),
         "mhg_limb_params": ([u32, P(u32), P(u32), P(u64)], C.c_int),
         "mhg_fold_level": ([u32, u64, P(u32)], C.c_int),
@@ -485,8 +486,10 @@ class Plan:
         la, ti, li, ch, wb = C.c_uint64(), C.c_uint64(), C.c_uint32(), C.c_uint32(), C.c_uint64()
         _check(lib().mhg_plan_info(self._h, C.byref(la), C.byref(ti), C.byref(li), C.byref(ch),
                                    C.byref(wb)))
+        ud = C.c_int()
+        _check(lib().mhg_plan_digits(self._h, C.byref(ud)))
         return {"launches": la.value, "tiles": ti.value, "limbs": li.value, "k_chunks": ch.value,
-                "workspace_bytes": wb.value}
+                "workspace_bytes": wb.value, "digits": "u8" if ud.value else "s8"}
 
     def time_gemm(self, iters: int = 10, stream=None) -> float:
         ms = C.c_float()

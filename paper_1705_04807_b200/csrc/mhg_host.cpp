@@ -239,9 +239,11 @@ mhg::GemmParams gemm_params(const Buffers& b, const mhg_view& out, const Checked
     p.w16_small = p.w16 < 256;
     p.mc = g.mc ? 1 : 0;
     p.two = g.two ? 1 : 0;
+    p.udig = g.udig ? 1 : 0;
     // cheapest exact fold for the longest chunk (MHG_FOLD raises the level, A/B only)
     p.fold = g.L == 2 ? mhg::fold_level(q, (uint64_t)std::min(g.Kt, g.KC) * mhg::kBK) : 3;
     if (const char* fl = std::getenv("MHG_FOLD")) p.fold = std::max(p.fold, std::min(3, std::atoi(fl)));
+    if (g.udig) p.fold = 3;  // the lean levels' bounds assume balanced signed digits
     p.group = 8;  // measured best at the power cap (profiles/r01_raster_groups.txt)
     p.serpentine = 1;
     p.ring = 0;
@@ -357,6 +359,14 @@ struct Fork {
 // Pack both operands and run the GEMM: 2 pack launches + 1 GEMM launch.
 // Pack one operand of a multiply into its stage image (which = 0: lhs, K-major rows;
 // 1: rhs, transposed).  The lhs digits of C -= A.B are negated here.
+bool pack_fused() {
+    static const bool fused = [] {
+        const char* e = std::getenv("MHG_PACK_FUSED");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return fused;
+}
+
 // Pack job of one operand (which = 0: lhs, K-major rows, digits negated for C -= A.B;
 // 1: rhs, transposed; two-class rhs with 4 planes when g.two).
 mhg::PackArgs pack_args(const Buffers& b, const mhg_view& out, const mhg_view& v, const Checked& c,
@@ -375,7 +385,7 @@ mhg::PackArgs pack_args(const Buffers& b, const mhg_view& out, const mhg_view& v
         a.rpt = mhg::kBM;
         a.Rtiles = g.Mt;
         a.dst = b.apack;
-        a.dp = mhg::DigitParams{out.mat->q, lp.H, op == MHG_OP_SUB ? 1 : 0, 0, m32};
+        a.dp = mhg::DigitParams{out.mat->q, lp.H, op == MHG_OP_SUB ? 1 : 0, 0, m32, g.udig ? 1 : 0};
     } else {
         a.rowoff = b.rhs_row;
         a.coloff = b.rhs_col;
@@ -384,7 +394,7 @@ mhg::PackArgs pack_args(const Buffers& b, const mhg_view& out, const mhg_view& v
         a.rpt = g.W;
         a.Rtiles = g.Nt;
         a.dst = b.bpack;
-        a.dp = mhg::DigitParams{out.mat->q, lp.H, 0, g.two ? 1 : 0, m32};
+        a.dp = mhg::DigitParams{out.mat->q, lp.H, 0, g.two ? 1 : 0, m32, g.udig ? 1 : 0};
     }
     return a;
 }
@@ -407,11 +417,7 @@ void launch_multiply(const Buffers& b, const mhg_view& out, const mhg_view& lhs,
                      cudaEvent_t gemm_end = nullptr, const Fork* fork = nullptr) {
     // default: both packs in one launch (k_pack_pair); MHG_PACK_FUSED=0 launches them
     // separately -- with a fork (graph capture) as parallel branches joined before the GEMM
-    static const bool fused = [] {
-        const char* e = std::getenv("MHG_PACK_FUSED");
-        return !(e && std::atoi(e) == 0);
-    }();
-    if (fused) {
+    if (pack_fused()) {
         cuda_check(mhg::launch_pack_pair((int)g.L, pack_args(b, out, lhs, c, g, op, 0),
                                          pack_args(b, out, rhs, c, g, op, 1), stream),
                    "pack lhs + rhs");
@@ -1062,11 +1068,18 @@ mhg_status mhg_plan_info(mhg_plan p, uint64_t* launches, uint64_t* tiles, uint32
                          uint32_t* k_chunks, uint64_t* workspace_bytes) {
     return guarded([&] {
         if (!p) fail(MHG_ERR_INVALID_ARGUMENT, "plan_info: null plan");
-        if (launches) *launches = p->empty ? 0 : 3;
+        if (launches) *launches = p->empty ? 0 : (pack_fused() ? 2 : 3);
         if (tiles) *tiles = (uint64_t)p->geo.Mt * p->geo.Nt;
         if (limbs) *limbs = p->geo.L;
         if (k_chunks) *k_chunks = p->geo.chunks;
         if (workspace_bytes) *workspace_bytes = p->mem_bytes;
+    });
+}
+
+mhg_status mhg_plan_digits(mhg_plan p, int* unsigned_digits) {
+    return guarded([&] {
+        if (!p || !unsigned_digits) fail(MHG_ERR_INVALID_ARGUMENT, "plan_digits: bad args");
+        *unsigned_digits = p->empty ? 0 : (p->geo.udig ? 1 : 0);
     });
 }
 

@@ -29,6 +29,7 @@ struct DigitParams {
     // those (c0, c1) of c = 256 b mod q, planes ordered [b0, c0, b1, c1]
     int two;
     uint32_t m32;  // floor(2^32 / q), for c
+    int udig;      // unsigned digits: x = sum_s d_s 256^s, d_s in [0, 255] (u8 x u8 MMA)
 };
 
 struct LimbParams {
@@ -78,6 +79,7 @@ struct GemmParams {
     // 256^s b mod q, so S = lo + 256 hi has 2 classes (256 TMEM columns per job, two
     // jobs double-buffered); rhs packed with 4 planes (DigitParams::two)
     int two;
+    int udig;                    // unsigned (u8) digits: non-negative class sums (DigitParams::udig)
     int vec_ok;                  // t % 4 == 0: 16-byte epilogue accesses allowed
     uint32_t group;              // raster: row tiles per group sharing rhs panels in L2
     int serpentine;              // alternate the K direction per tile (L2 reuse across waves)

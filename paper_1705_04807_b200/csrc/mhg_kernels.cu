@@ -209,6 +209,11 @@ __global__ void k_mh_to_rm(const uint32_t* __restrict__ mh, uint32_t* __restrict
 template <int L>
 __device__ __forceinline__ void to_digits(uint32_t v, const DigitParams& dp, int8_t (&d)[L]) {
     if (dp.negate) v = v ? dp.q - v : 0u;
+    if (dp.udig) {
+#pragma unroll
+        for (int s = 0; s < L; ++s) d[s] = (int8_t)(uint8_t)(v >> (8 * s));
+        return;
+    }
     int32_t x = v > dp.H ? (int32_t)(v - dp.q) : (int32_t)v;
 #pragma unroll
     for (int s = 0; s < L - 1; ++s) {
@@ -631,6 +636,8 @@ __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
            | (1u << 10)                // B signed
            | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
 }
+// clearing these makes both operands unsigned (u8 x u8)
+__host__ __device__ constexpr uint32_t idesc_sign_mask() { return (1u << 7) | (1u << 10); }
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
     asm volatile(
@@ -1583,9 +1590,10 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
         } else if (warp == 1) {
             // ---------------- MMA issuer (single thread)
             if (lane == 0) {
-                constexpr uint32_t id_full = idesc_i8(kBM, Cfg::NB);
-                constexpr uint32_t id_head = idesc_i8(kBM, (L > 1 ? L - 1 : 1) * W);
-                constexpr uint32_t id_one = idesc_i8(kBM, W);
+                const uint32_t um = p.udig ? ~idesc_sign_mask() : ~0u;
+                const uint32_t id_full = idesc_i8(kBM, Cfg::NB) & um;
+                const uint32_t id_head = idesc_i8(kBM, (L > 1 ? L - 1 : 1) * W) & um;
+                const uint32_t id_one = idesc_i8(kBM, W) & um;
                 const bool alt_layout = early_release<L>(p);
                 int st = 0;
                 uint32_t ph = 0, acc_ph = 0;

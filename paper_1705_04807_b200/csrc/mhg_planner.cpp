@@ -193,6 +193,20 @@ GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t c
     if (g.mc) g.Nt += g.Nt & 1u;  // clusters take two column tiles
     g.Kt = (uint32_t)((inner + kBK - 1) / kBK);
     g.KC = (uint32_t)std::max<uint64_t>(1, lp.k_max / kBK);
+    // Unsigned digits (u8 x u8 MMA, single-CTA kernel): every class sum is non-negative,
+    // so the int32 accumulators grow monotonically instead of random-walking around 0 --
+    // fewer bit toggles, less power, higher clocks under the 1 kW cap (north star: -1.5%
+    // step time, profiles/r01_unsigned_digits.txt).  The middle class sums L products of
+    // up to 255 * 255 per k, so chunks are shorter (16384 at L = 2 vs 65532 signed), and
+    // the lean fold levels (derived for balanced digits) are off.  Chosen for long K
+    // (>= kUdigKt slices, where the epilogue is negligible); MHG_UDIG=0/1 forces it.
+    const char* ud = std::getenv("MHG_UDIG");
+    const bool want = ud ? std::atoi(ud) != 0 : g.Kt >= kUdigKt;
+    g.udig = want && !g.pair && !g.mc;
+    if (g.udig) {
+        const uint64_t kmax_u = ((uint64_t(1) << 31) - (uint64_t(1) << 17)) / ((uint64_t)lp.L * 65025);
+        g.KC = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(g.KC, kmax_u / kBK));
+    }
     // test hook: a smaller chunk exercises the multi-chunk path on small inputs
     if (const char* force = std::getenv("MHG_FORCE_KCHUNK")) {
         const long v = std::strtol(force, nullptr, 10);

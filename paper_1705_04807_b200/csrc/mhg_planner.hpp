@@ -52,6 +52,7 @@ struct GemmGeometry {
     bool pair;            // CTA-pair kernel (k_gemm2); Mt is then even
     bool mc;              // column-pair clusters with lhs multicast (k_gemm MC); Nt is then even
     bool two;             // two-class accumulation on the CTA pair (L = 2; rhs with 4 planes)
+    bool udig;            // unsigned u8 digits (L = 2, single CTA; MHG_UDIG=1)
     uint32_t L, W;        // limbs, output tile width
     uint32_t Mt, Nt, Kt;  // tiles along rows / cols / inner (128-byte K slices)
     uint32_t KC;          // K slices per exact int32 chunk
@@ -59,6 +60,8 @@ struct GemmGeometry {
     uint64_t apack_bytes, bpack_bytes;
 };
 
+// inner length (in 128-wide slices) from which unsigned digits are chosen (GemmGeometry::udig)
+constexpr uint32_t kUdigKt = 64;
 GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t cols);
 
 // Cheapest exact fold level of the lean L = 2 epilogue (GemmParams::fold) for
