@@ -215,7 +215,7 @@ def time_conversions(mh, torch, mats, n, q, hbm_gbs, reps=3):
             "rm_to_mh_gbs": byts / to_mh / 1e6, "mh_to_rm_gbs": byts / to_rm / 1e6,
             "frac_of_hbm": [byts / to_mh / 1e6 / hbm_gbs, byts / to_rm / 1e6 / hbm_gbs],
             "hbm_peak_gbs": hbm_gbs, "round_trip_exact": ok,
-            "kernel": "k_conv_z (Morton-order, 16-B accesses, residue check on the way in)"}
+            "kernel": "k_conv_tma (2D tensor-map boxes <-> contiguous Morton runs, residue check in smem)"}
 
 
 def e2e_pipelined(mh, torch, lay, mod, flats, set0, prob0, op, n, steps, macs, nsets=3):
@@ -473,7 +473,9 @@ def run_gpu(args, rank, world, local_rank):
     roof = {"bound": "tensor", "achieved": achieved_tops, "peak": int8_peak_tops,
             "unit": "TFLOP/s", "frac": achieved_tops / int8_peak_tops, "traffic": traffic,
             "traffic_source": "profiles/traffic.json (ncu --set full, bytes per launch)",
-            "kernel": f"k_gemm<{L}> (tcgen05.mma.cta_group::1.kind::i8)",
+            "kernel": (f"k_gemm2<{L}> (tcgen05.mma.cta_group::2.kind::i8, CTA pair)"
+                       if info.get("cta_group") == 2 else f"k_gemm<{L}> (tcgen05.mma.cta_group::1.kind::i8)")
+                      + f", {info.get('digits')} digits",
             "peak_source": f"2 x {peak_src} bf16 burst {bf16_burst} TFLOP/s (MEASURED_PEAKS.json); "
                            f"int8 ops counted as 2*L^2*r*k*c, L={L}",
             "frac_of_spec_4500": achieved_tops / 4500.0,

@@ -186,9 +186,10 @@ mhg_status mhg_copy_async(void *dst, const void *src, uint64_t bytes, void *stre
 /* Kernel launches per run and the planner's description (tiles, chunks, limbs). */
 mhg_status mhg_plan_info(mhg_plan plan, uint64_t *launches, uint64_t *tiles, uint32_t *limbs,
                          uint32_t *k_chunks, uint64_t *workspace_bytes);
-/* 1 when the plan packs unsigned (u8) limb digits (long K: lower power at the 1 kW
- * cap), 0 for balanced signed digits. */
-mhg_status mhg_plan_digits(mhg_plan plan, int *unsigned_digits);
+/* The planner's kernel choice: unsigned_digits = 1 for u8 limb digits (long K: lower
+ * power at the 1 kW cap), 0 for balanced s8 digits; cta_group = 1 (single-CTA k_gemm)
+ * or 2 (CTA-pair k_gemm2). */
+mhg_status mhg_plan_variant(mhg_plan plan, int *unsigned_digits, int *cta_group);
 mhg_status mhg_plan_destroy(mhg_plan plan);
 
 /* ---- diagnostics for tests / bench ---- */

@@ -140,7 +140,7 @@ def lib():
         "mhg_copy_async": ([vp, vp, u64, vp], C.c_int),
         "mhg_plan_counters": ([vp, P(Counters)], C.c_int),
         "mhg_plan_info": ([vp, P(u64), P(u64), P(u32), P(u32), P(u64)], C.c_int),
-        "mhg_plan_digits": ([vp, P(C.c_int)], C.c_int),
+        "mhg_plan_variant": ([vp, P(C.c_int), P(C.c_int)], C.c_int),
         "mhg_plan_destroy": ([vp], C.c_int),
         "mhg_limb_params": ([u32, P(u32), P(u32), P(u64)], C.c_int),
         "mhg_fold_level": ([u32, u64, P(u32)], C.c_int),
@@ -486,10 +486,11 @@ class Plan:
         la, ti, li, ch, wb = C.c_uint64(), C.c_uint64(), C.c_uint32(), C.c_uint32(), C.c_uint64()
         _check(lib().mhg_plan_info(self._h, C.byref(la), C.byref(ti), C.byref(li), C.byref(ch),
                                    C.byref(wb)))
-        ud = C.c_int()
-        _check(lib().mhg_plan_digits(self._h, C.byref(ud)))
+        ud, cg = C.c_int(), C.c_int()
+        _check(lib().mhg_plan_variant(self._h, C.byref(ud), C.byref(cg)))
         return {"launches": la.value, "tiles": ti.value, "limbs": li.value, "k_chunks": ch.value,
-                "workspace_bytes": wb.value, "digits": "u8" if ud.value else "s8"}
+                "workspace_bytes": wb.value, "digits": "u8" if ud.value else "s8",
+                "cta_group": cg.value}
 
     def time_gemm(self, iters: int = 10, stream=None) -> float:
         ms = C.c_float()

@@ -1076,10 +1076,11 @@ mhg_status mhg_plan_info(mhg_plan p, uint64_t* launches, uint64_t* tiles, uint32
     });
 }
 
-mhg_status mhg_plan_digits(mhg_plan p, int* unsigned_digits) {
+mhg_status mhg_plan_variant(mhg_plan p, int* unsigned_digits, int* cta_group) {
     return guarded([&] {
-        if (!p || !unsigned_digits) fail(MHG_ERR_INVALID_ARGUMENT, "plan_digits: bad args");
-        *unsigned_digits = p->empty ? 0 : (p->geo.udig ? 1 : 0);
+        if (!p) fail(MHG_ERR_INVALID_ARGUMENT, "plan_variant: null plan");
+        if (unsigned_digits) *unsigned_digits = p->empty ? 0 : (p->geo.udig ? 1 : 0);
+        if (cta_group) *cta_group = p->empty ? 0 : (p->geo.pair ? 2 : 1);
     });
 }
 

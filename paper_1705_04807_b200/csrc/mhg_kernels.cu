@@ -1814,7 +1814,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L, TWO>::TH
         }
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {
-            constexpr uint32_t id_full = idesc_i8(2 * kBM, Cfg::NB);
+            const uint32_t id_full = idesc_i8(2 * kBM, Cfg::NB) & (p.udig ? ~idesc_sign_mask() : ~0u);
             int st = 0;
             uint32_t ph = 0, job = 0;
             long long wait_full = 0, wait_tmem = 0;

@@ -182,18 +182,24 @@ GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t c
     g.L = lp.L;
     g.W = (uint32_t)tile_width((int)lp.L);
     g.Mt = (uint32_t)((rows + kBM - 1) / kBM);
-    // single-CTA kernel by default: under the B200's 1 kW cap it sustains ~17%
-    // higher clocks than the CTA-pair kernel for the same work (measured,
-    // profiles/ab_gemm.py); MHG_GEMM=2cta selects the pair kernel.
+    // Kernel: single CTA by default -- under the B200's 1 kW cap it sustains higher
+    // clocks than the CTA-pair kernel for the same work at L <= 2 (profiles/ab_gemm.py,
+    // r01_ab_pair_vs_1cta.txt).  Four-limb primes with long K take the pair: W = 64
+    // tiles halve the 1-CTA kernel's output per B' byte, and the pair's shared B' is
+    // 3% faster on cfg4 (profiles/r01_unsigned_digits.txt).  MHG_GEMM=1cta / 2cta /
+    // 2cta2 / mc forces a kernel.
     const char* sel = std::getenv("MHG_GEMM");
-    g.pair = sel && (std::string(sel) == "2cta" || std::string(sel) == "2cta2");
+    const uint64_t kt_all = (inner + kBK - 1) / kBK;
+    g.pair = sel ? (std::string(sel) == "2cta" || std::string(sel) == "2cta2")
+                 : (lp.L == 4 && kt_all >= kUdigKt);
     if (g.pair) g.Mt += g.Mt & 1u;  // pairs take two row tiles
     g.Nt = (uint32_t)((cols + g.W - 1) / g.W);
     g.mc = !g.pair && sel && std::string(sel) == "mc";
     if (g.mc) g.Nt += g.Nt & 1u;  // clusters take two column tiles
     g.Kt = (uint32_t)((inner + kBK - 1) / kBK);
     g.KC = (uint32_t)std::max<uint64_t>(1, lp.k_max / kBK);
-    // Unsigned digits (u8 x u8 MMA, single-CTA kernel): every class sum is non-negative,
+    g.two = g.pair && g.L == 2 && sel && std::string(sel) == "2cta2";
+    // Unsigned digits (u8 x u8 MMA; 1-CTA and CTA-pair kernels): every class sum is non-negative,
     // so the int32 accumulators grow monotonically instead of random-walking around 0 --
     // fewer bit toggles, less power, higher clocks under the 1 kW cap (north star: -1.5%
     // step time, profiles/r01_unsigned_digits.txt).  The middle class sums L products of
@@ -202,7 +208,7 @@ GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t c
     // (>= kUdigKt slices, where the epilogue is negligible); MHG_UDIG=0/1 forces it.
     const char* ud = std::getenv("MHG_UDIG");
     const bool want = ud ? std::atoi(ud) != 0 : g.Kt >= kUdigKt;
-    g.udig = want && !g.pair && !g.mc;
+    g.udig = want && !g.two && !g.mc;
     if (g.udig) {
         const uint64_t kmax_u = ((uint64_t(1) << 31) - (uint64_t(1) << 17)) / ((uint64_t)lp.L * 65025);
         g.KC = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(g.KC, kmax_u / kBK));
@@ -216,7 +222,6 @@ GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t c
     // digits of 256^s b mod q.  Class sums obey the same bound as the widest class of the
     // 3-class layout (2 * 128 * 128 per k); the lean fold (w16 < 256) additionally needs
     // (32768 + 128 w16) K + 65280 + w16 <= 2^31 - 2^17.
-    g.two = g.pair && g.L == 2 && sel && std::string(sel) == "2cta2";
     if (g.two) {
         const uint64_t w16 = (uint64_t(1) << 16) % q;
         if (w16 < 256) {
