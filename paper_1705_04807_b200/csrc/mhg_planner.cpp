@@ -182,16 +182,14 @@ GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t c
     g.L = lp.L;
     g.W = (uint32_t)tile_width((int)lp.L);
     g.Mt = (uint32_t)((rows + kBM - 1) / kBM);
-    // Kernel: single CTA by default -- under the B200's 1 kW cap it sustains higher
-    // clocks than the CTA-pair kernel for the same work at L <= 2 (profiles/ab_gemm.py,
-    // r01_ab_pair_vs_1cta.txt).  Four-limb primes with long K take the pair: W = 64
+    // Kernel: single CTA for L <= 2 -- under the B200's 1 kW cap it sustains higher
+    // clocks than the CTA-pair kernel for the same work (profiles/ab_gemm.py,
+    // r01_ab_pair_vs_1cta.txt).  Three- and four-limb primes take the pair: their W = 64
     // tiles halve the 1-CTA kernel's output per B' byte, and the pair's shared B' is
-    // 3% faster on cfg4 (profiles/r01_unsigned_digits.txt).  MHG_GEMM=1cta / 2cta /
-    // 2cta2 / mc forces a kernel.
+    // faster at every K (L = 3: -7..-13%, L = 4: -2..-4%; profiles/r01_pair_wide_primes.txt).
+    // MHG_GEMM=1cta / 2cta / 2cta2 / mc forces a kernel.
     const char* sel = std::getenv("MHG_GEMM");
-    const uint64_t kt_all = (inner + kBK - 1) / kBK;
-    g.pair = sel ? (std::string(sel) == "2cta" || std::string(sel) == "2cta2")
-                 : (lp.L == 4 && kt_all >= kUdigKt);
+    g.pair = sel ? (std::string(sel) == "2cta" || std::string(sel) == "2cta2") : lp.L >= 3;
     if (g.pair) g.Mt += g.Mt & 1u;  // pairs take two row tiles
     g.Nt = (uint32_t)((cols + g.W - 1) / g.W);
     g.mc = !g.pair && sel && std::string(sel) == "mc";
