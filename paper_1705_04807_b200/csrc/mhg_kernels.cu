@@ -1700,7 +1700,9 @@ struct Gemm2Cfg {
     static constexpr int A_STAGE = L * kBM * kBK;
     static constexpr int B_STAGE = NBH * kBK;
     static constexpr int STAGE = A_STAGE + B_STAGE;
-    // TWO: the coalesced (transpose-buffer) epilogue, 4 KB per epilogue warp
+    // TWO: the coalesced (transpose-buffer) epilogue, 4 KB per epilogue warp (for the
+    // 3- and 4-limb pairs it measured within 1% of the row-per-thread path, A/B in
+    // profiles/r01_pair_wide_primes.txt, so they keep the latter)
     static constexpr bool XPOSE = TWO;
     static constexpr int XBUF = XPOSE ? 8 * 4096 : 0;
     static constexpr int STAGES_RAW = (220 * 1024 - XBUF) / STAGE;
