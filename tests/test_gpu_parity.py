@@ -820,3 +820,33 @@ print("ok")
     env = dict(__import__("os").environ, MHG_CONV=conv)
     out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
+
+
+def test_planner_kernel_policy(gpu, mh, monkeypatch):
+    """mhg_plan_variant: u8 digits from K = 8192 (64 slices) on, s8 below; the CTA
+    pair for 3- and 4-limb primes, the single CTA for 1-2 limbs; MHG_UDIG / MHG_GEMM
+    override.  (The results of every combination are pinned by the parity tests.)"""
+    monkeypatch.delenv("MHG_UDIG", raising=False)
+    monkeypatch.delenv("MHG_GEMM", raising=False)
+
+    def variant(q, k, n=8192):
+        lay, mod = mh.Layout(n, 64), mh.Modulus(q)
+        A, B, C = (mh.Matrix(lay, mod) for _ in range(3))
+        info = mh.Plan(mh.Problem(mh.Sub(A, 0, 256, 256), mh.Sub(B, 0, 256, k),
+                                  mh.Sub(C, 0, k, 256)), mh.OP_SUB).info()
+        return info["digits"], info["cta_group"], info["k_chunks"]
+
+    assert variant(P16, 8192) == ("u8", 1, 1)
+    assert variant(P16, 8064) == ("s8", 1, 1)
+    assert variant(P31, 8192) == ("u8", 2, 1)
+    assert variant(P31, 4096) == ("s8", 2, 1)
+    assert variant(P24, 1024) == ("s8", 2, 1)
+    assert variant(97, 512) == ("s8", 1, 1)
+    # u8 chunks: (2^31 - 2^17) / (L * 255^2) -> 16,384 at L = 2
+    assert variant(P16, 16384, n=16384) == ("u8", 1, 1)
+    monkeypatch.setenv("MHG_UDIG", "0")
+    assert variant(P16, 8192)[0] == "s8"
+    monkeypatch.setenv("MHG_UDIG", "1")
+    assert variant(P16, 1024)[0] == "u8"
+    monkeypatch.setenv("MHG_GEMM", "1cta")
+    assert variant(P31, 1024)[1] == 1
