@@ -200,6 +200,8 @@ mhg_status mhg_limb_params(uint32_t q, uint32_t *limbs, uint32_t *threshold, uin
  * inner products (1, 2 or 3 Barrett reductions per output; 3 when q needs more
  * or fewer than 2 limbs or 2^16 mod q >= 256).  See DESIGN.md "Fold levels". */
 mhg_status mhg_fold_level(uint32_t q, uint64_t k_chunk, uint32_t *level);
+/* The same for plans with unsigned (u8) digits (mhg_plan_variant). */
+mhg_status mhg_fold_level_u8(uint32_t q, uint64_t k_chunk, uint32_t *level);
 /* Times `iters` replays of a plan's GEMM kernel alone (CUDA events on
  * `stream`), returns the mean ms per launch in *ms. */
 mhg_status mhg_plan_time_gemm(mhg_plan plan, int iters, void *stream, float *ms);

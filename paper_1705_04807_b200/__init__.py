@@ -144,6 +144,7 @@ def lib():
         "mhg_plan_destroy": ([vp], C.c_int),
         "mhg_limb_params": ([u32, P(u32), P(u32), P(u64)], C.c_int),
         "mhg_fold_level": ([u32, u64, P(u32)], C.c_int),
+        "mhg_fold_level_u8": ([u32, u64, P(u32)], C.c_int),
         "mhg_plan_time_gemm": ([vp, C.c_int, vp, P(C.c_float)], C.c_int),
         "mhg_plan_set_profiling": ([vp, C.c_int], C.c_int),
         "mhg_plan_gemm_time": ([vp, P(C.c_float), P(u64)], C.c_int),
@@ -227,10 +228,11 @@ def limb_params(q: int):
     return L.value, H.value, K.value
 
 
-def fold_level(q: int, k_chunk: int) -> int:
+def fold_level(q: int, k_chunk: int, unsigned_digits: bool = False) -> int:
     """Reductions per output the 2-limb epilogue uses for chunks of k_chunk."""
     lv = C.c_uint32()
-    _check(lib().mhg_fold_level(q, k_chunk, C.byref(lv)))
+    f = lib().mhg_fold_level_u8 if unsigned_digits else lib().mhg_fold_level
+    _check(f(q, k_chunk, C.byref(lv)))
     return lv.value
 
 

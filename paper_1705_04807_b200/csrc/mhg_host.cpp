@@ -243,7 +243,12 @@ mhg::GemmParams gemm_params(const Buffers& b, const mhg_view& out, const Checked
     // cheapest exact fold for the longest chunk (MHG_FOLD raises the level, A/B only)
     p.fold = g.L == 2 ? mhg::fold_level(q, (uint64_t)std::min(g.Kt, g.KC) * mhg::kBK) : 3;
     if (const char* fl = std::getenv("MHG_FOLD")) p.fold = std::max(p.fold, std::min(3, std::atoi(fl)));
-    if (g.udig) p.fold = 3;  // the lean levels' bounds assume balanced signed digits
+    if (g.udig) {
+        // non-negative class sums: no bias, levels from the u8 bounds (MHG_FOLD still raises)
+        p.bias32 = 0;
+        p.fold = g.L == 2 ? mhg::fold_level_u8(q, (uint64_t)std::min(g.Kt, g.KC) * mhg::kBK) : 3;
+        if (const char* fl = std::getenv("MHG_FOLD")) p.fold = std::max(p.fold, std::min(3, std::atoi(fl)));
+    }
     p.group = 8;  // measured best at the power cap (profiles/r01_raster_groups.txt)
     p.serpentine = 1;
     p.ring = 0;
@@ -596,6 +601,15 @@ mhg_status mhg_limb_params(uint32_t q, uint32_t* limbs, uint32_t* threshold, uin
     if (threshold) *threshold = lp.H;
     if (k_max) *k_max = lp.k_max;
     return MHG_OK;
+}
+
+mhg_status mhg_fold_level_u8(uint32_t q, uint64_t k_chunk, uint32_t* level) {
+    mhg_status s = mhg_modulus_check(q);
+    if (s) return s;
+    return guarded([&] {
+        if (!level) fail(MHG_ERR_INVALID_ARGUMENT, "fold_level_u8: null output");
+        *level = mhg::limb_params(q).L == 2 ? (uint32_t)mhg::fold_level_u8(q, k_chunk) : 3u;
+    });
 }
 
 mhg_status mhg_fold_level(uint32_t q, uint64_t k_chunk, uint32_t* level) {

@@ -176,6 +176,21 @@ int fold_level(uint32_t q, uint64_t k_chunk) {
     return 3;
 }
 
+int fold_level_u8(uint32_t q, uint64_t k_chunk) {
+    if (q < 2 || q > 65536) return 3;
+    const uint64_t w16 = (uint64_t(1) << 16) % q;
+    if (w16 >= 256) return 3;
+    // unsigned digits, no bias (every class sum >= 0): a0, a2 <= 255^2 k, a1 <= 2 * 255^2 k
+    // (< 2^31); both layouts of the partial fold sum cur + a0 + 256 a1l + w16 a1h + w16 t
+    // with t = a2 (level 1) or t = a2 mod q (level 2) in uint32 before one reduction
+    const uint64_t lim = (uint64_t(1) << 32) - (uint64_t(1) << 17);
+    const uint64_t a0 = 65025 * k_chunk, a1h = (130050 * k_chunk) >> 8, a2 = 65025 * k_chunk;
+    const uint64_t common = (uint64_t)(q - 1) + a0 + 255 * 256 + w16 * a1h;
+    if (common + w16 * a2 <= lim) return 1;
+    if (common + w16 * (uint64_t)(q - 1) <= lim) return 2;
+    return 3;
+}
+
 GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t cols) {
     const LimbParams lp = limb_params(q);
     GemmGeometry g{};
@@ -197,15 +212,15 @@ GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t c
     g.Kt = (uint32_t)((inner + kBK - 1) / kBK);
     g.KC = (uint32_t)std::max<uint64_t>(1, lp.k_max / kBK);
     g.two = g.pair && g.L == 2 && sel && std::string(sel) == "2cta2";
-    // Unsigned digits (u8 x u8 MMA; 1-CTA and CTA-pair kernels): every class sum is non-negative,
-    // so the int32 accumulators grow monotonically instead of random-walking around 0 --
-    // fewer bit toggles, less power, higher clocks under the 1 kW cap (north star: -1.5%
-    // step time, profiles/r01_unsigned_digits.txt).  The middle class sums L products of
-    // up to 255 * 255 per k, so chunks are shorter (16384 at L = 2 vs 65532 signed), and
-    // the lean fold levels (derived for balanced digits) are off.  Chosen for long K
-    // (>= kUdigKt slices, where the epilogue is negligible); MHG_UDIG=0/1 forces it.
+    // Unsigned digits (u8 x u8 MMA; 1-CTA and CTA-pair kernels), the default: every class
+    // sum is non-negative, so the int32 accumulators grow monotonically instead of
+    // random-walking around 0 -- fewer bit toggles, less power -- and the epilogue needs no
+    // bias (lean fold levels from fold_level_u8).  Measured faster at every K
+    // (profiles/r01_unsigned_digits.txt).  The middle class sums L products of up to
+    // 255 * 255 per k, so exact chunks are shorter (16,384 at L = 2 vs 65,532 signed).
+    // MHG_UDIG=0 selects balanced signed digits.
     const char* ud = std::getenv("MHG_UDIG");
-    const bool want = ud ? std::atoi(ud) != 0 : g.Kt >= kUdigKt;
+    const bool want = ud ? std::atoi(ud) != 0 : true;
     g.udig = want && !g.two && !g.mc;
     if (g.udig) {
         const uint64_t kmax_u = ((uint64_t(1) << 31) - (uint64_t(1) << 17)) / ((uint64_t)lp.L * 65025);

@@ -60,8 +60,6 @@ struct GemmGeometry {
     uint64_t apack_bytes, bpack_bytes;
 };
 
-// inner length (in 128-wide slices) from which unsigned digits are chosen (GemmGeometry::udig)
-constexpr uint32_t kUdigKt = 64;
 GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t cols);
 
 // Cheapest exact fold level of the lean L = 2 epilogue (GemmParams::fold) for
@@ -69,5 +67,8 @@ GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t c
 //   1 if  cur + a0 + 256 a1l + w16 (a1h + a2)  stays within 2^31 - 2^17,
 //   2 if  cur + a0 + 256 a1l + w16 a1h + w16 (a2 mod q)  does, else 3.
 int fold_level(uint32_t q, uint64_t k_chunk);
+// The same for unsigned (u8) digits: class sums are non-negative, so the kernel runs
+// without the q-multiple bias (GemmParams::bias32 = 0) and the levels test uint32 range.
+int fold_level_u8(uint32_t q, uint64_t k_chunk);
 
 }  // namespace mhg

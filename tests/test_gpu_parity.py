@@ -164,7 +164,7 @@ def test_conversion_kernels_roundtrip(gpu, mh, oracle):
 
 
 # Residues whose signed limb digits are the extremes (+127 / -128 / -113 / +64 ...)
-EXTREMES = {P16: (32639, 32640, P16 - 1, 0x807F, 1),
+EXTREMES = {P16: (32639, 32640, P16 - 1, 0x807F, 1, 0xFEFF),
             P31: (1073741823, 1073741824, P31 - 1, 0x7F7F7F7F, 0x80808080 % P31)}
 
 
@@ -182,8 +182,11 @@ def _constant_case(mh, n, t, q, a, b, c0, k, op):
     assert (got == want).all(), (q, a, b, op, int(got[0]), want)
 
 
-def test_adversarial_extreme_digits(gpu, mh):
-    """Extreme-magnitude signed digits in every limb position, all three ops."""
+@pytest.mark.parametrize("udig", ["0", "1"])
+def test_adversarial_extreme_digits(gpu, mh, monkeypatch, udig):
+    """Extreme-magnitude digits in every limb position (balanced s8 digits with
+    MHG_UDIG=0, u8 digits by default), all three ops."""
+    monkeypatch.setenv("MHG_UDIG", udig)
     for q, vals in EXTREMES.items():
         for a in vals:
             for b in vals[:3]:
@@ -194,26 +197,34 @@ def test_adversarial_extreme_digits(gpu, mh):
 def _extremes(q):
     """Residues whose signed representatives have extreme limb digits."""
     H = min((q - 1) // 2, 127 * 257)
-    return (H, q - H, q - 1, 1, (q + 1) // 2)
+    # (+ 0xFEFF: both u8 digits near 255 where it is a residue)
+    return (H, q - H, q - 1, 1, (q + 1) // 2) + ((0xFEFF,) if q > 0xFEFF else ())
 
 
-@pytest.mark.parametrize("q,k", [(65287, 512), (65287, 640), (65519, 1024), (257, 1024)])
-def test_single_reduction_fold_bound(gpu, mh, q, k):
+@pytest.mark.parametrize("udig", ["0", "1"])
+@pytest.mark.parametrize("q,k", [(65287, 512), (65287, 640), (65519, 1024), (257, 1024), (65521, 4096),
+                                 (65521, 8192)])
+def test_single_reduction_fold_bound(gpu, mh, monkeypatch, q, k, udig):
     """Fold level 1 (single reduction, L=2) at the edge of its K bound:
     q = 65287 has 2^16 mod q = 249, so K = 512 is the largest chunk the host
-    admits (K = 640 falls back to the per-class fold); extreme digits, all ops."""
+    admits for s8 digits (K = 640 falls back to the per-class fold); the u8 levels'
+    edges differ (mhg_fold_level_u8: 65521 on level 1 up to K = 4096); extreme
+    digits, all ops."""
+    monkeypatch.setenv("MHG_UDIG", udig)
     ex = _extremes(q)
     for a in ex:
         for b in ex[:2]:
             for op in (OP_ADD, OP_SUB, OP_SET):
-                _constant_case(mh, 1024, 64, q, a, b, q - 1, k, op)
+                _constant_case(mh, max(1024, k), 64, q, a, b, q - 1, k, op)
 
 
+@pytest.mark.parametrize("udig", ["0", "1"])
 @pytest.mark.parametrize("level", ["2", "3"])
-def test_forced_fold_levels(gpu, mh, monkeypatch, level):
+def test_forced_fold_levels(gpu, mh, monkeypatch, level, udig):
     """Fold levels 2 and 3 forced (MHG_FOLD) where level 1 would be chosen:
     the same exact results through every lean-fold arithmetic variant."""
     monkeypatch.setenv("MHG_FOLD", level)
+    monkeypatch.setenv("MHG_UDIG", udig)
     for q in (P16, 65287, 257):
         ex = _extremes(q)
         for a, b in [(ex[0], ex[0]), (ex[1], ex[0]), (ex[2], ex[4])]:
@@ -222,27 +233,33 @@ def test_forced_fold_levels(gpu, mh, monkeypatch, level):
 
 
 @pytest.mark.slow
-def test_single_reduction_fold_at_k8064(gpu, mh):
-    """p = 65521: the largest single-chunk K on fold level 1 (63 k-tiles)."""
+def test_single_reduction_fold_at_k8064(gpu, mh, monkeypatch):
+    """p = 65521, s8 digits: the largest single-chunk K on fold level 1 (63 k-tiles)."""
+    monkeypatch.setenv("MHG_UDIG", "0")
     ex = _extremes(P16)
     for a, b in [(ex[0], ex[0]), (ex[1], ex[0]), (ex[0], ex[1])]:
         _constant_case(mh, 8192, 64, P16, a, b, P16 - 1, 8064, OP_SUB)
 
 
 @pytest.mark.slow
-def test_adversarial_int32_headroom(gpu, mh):
+@pytest.mark.parametrize("udig", ["0", "1"])
+def test_adversarial_int32_headroom(gpu, mh, monkeypatch, udig):
     """K = 32768 (cfg5's inner length) with extreme digits: the int32 class
-    sums reach ~75% (q = 2^31-1) of the bound the planner sized chunks for."""
+    sums reach ~75% (q = 2^31-1) of the bound the planner sized chunks for (s8; u8
+    digits take 2 / 4 chunks of 16,384 / 8,256)."""
+    monkeypatch.setenv("MHG_UDIG", udig)
     for q in (P16, P31):
         for a, b in [(EXTREMES[q][0], EXTREMES[q][0]), (EXTREMES[q][1], EXTREMES[q][0])]:
             _constant_case(mh, 32768, 64, q, a, b, 1, 32768, OP_SUB)
 
 
-def test_k_chunking(gpu, mh, oracle, monkeypatch):
+@pytest.mark.parametrize("udig", ["0", "1"])
+def test_k_chunking(gpu, mh, oracle, monkeypatch, udig):
     """Multi-chunk accumulation (each exact int32 K-chunk drained and folded into
     the output before the next): forced to 2 K-slices per chunk so small
     problems take the path n >= 65536 would take for q = 2^31-1."""
     monkeypatch.setenv("MHG_FORCE_KCHUNK", "2")
+    monkeypatch.setenv("MHG_UDIG", udig)
     rng = np.random.default_rng(77)
     for q in (P16, P31):
         for op in (OP_ADD, OP_SUB, OP_SET):
@@ -823,9 +840,10 @@ print("ok")
 
 
 def test_planner_kernel_policy(gpu, mh, monkeypatch):
-    """mhg_plan_variant: u8 digits from K = 8192 (64 slices) on, s8 below; the CTA
-    pair for 3- and 4-limb primes, the single CTA for 1-2 limbs; MHG_UDIG / MHG_GEMM
-    override.  (The results of every combination are pinned by the parity tests.)"""
+    """mhg_plan_variant: u8 digits by default (s8 with MHG_UDIG=0); the CTA pair for
+    3- and 4-limb primes, the single CTA for 1-2 limbs (MHG_GEMM overrides); u8 chunks
+    of (2^31 - 2^17) / (L * 255^2).  (Every combination's results are pinned by the
+    parity tests.)"""
     monkeypatch.delenv("MHG_UDIG", raising=False)
     monkeypatch.delenv("MHG_GEMM", raising=False)
 
@@ -837,16 +855,14 @@ def test_planner_kernel_policy(gpu, mh, monkeypatch):
         return info["digits"], info["cta_group"], info["k_chunks"]
 
     assert variant(P16, 8192) == ("u8", 1, 1)
-    assert variant(P16, 8064) == ("s8", 1, 1)
+    assert variant(P16, 1024) == ("u8", 1, 1)
     assert variant(P31, 8192) == ("u8", 2, 1)
-    assert variant(P31, 4096) == ("s8", 2, 1)
-    assert variant(P24, 1024) == ("s8", 2, 1)
-    assert variant(97, 512) == ("s8", 1, 1)
-    # u8 chunks: (2^31 - 2^17) / (L * 255^2) -> 16,384 at L = 2
-    assert variant(P16, 16384, n=16384) == ("u8", 1, 1)
+    assert variant(P24, 1024) == ("u8", 2, 1)
+    assert variant(97, 512) == ("u8", 1, 1)
+    assert variant(P16, 16384, n=16384) == ("u8", 1, 1)   # 16,384 = one u8 chunk at L = 2
+    assert variant(P31, 16384, n=16384) == ("u8", 2, 2)   # 8,256 per chunk at L = 4
     monkeypatch.setenv("MHG_UDIG", "0")
     assert variant(P16, 8192)[0] == "s8"
-    monkeypatch.setenv("MHG_UDIG", "1")
-    assert variant(P16, 1024)[0] == "u8"
+    assert variant(P31, 16384, n=16384) == ("s8", 2, 1)
     monkeypatch.setenv("MHG_GEMM", "1cta")
     assert variant(P31, 1024)[1] == 1

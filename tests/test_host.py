@@ -168,12 +168,14 @@ def test_device_calls_fail_loudly_without_gpu(mh):
 M32 = 0xFFFFFFFF
 
 
-def _emulate_fold(level, layout, a0, a1, a2, cur, q):
+def _emulate_fold(level, layout, a0, a1, a2, cur, q, bias32=None):
     """Bit-exact emulation of the kernel's lean L=2 fold (uint32 wrap-around,
-    Barrett red32 with m = floor(2^32 / q), csrc/mhg_kernels.cu fold_g1/fold_g2)."""
+    Barrett red32 with m = floor(2^32 / q), csrc/mhg_kernels.cu fold_g1/fold_g2).
+    bias32 = GemmParams::bias32 (0 for unsigned-digit plans)."""
     w16 = (1 << 16) % q
     m32 = (1 << 32) // q
-    bias32 = ((1 << 31) // q) * q
+    if bias32 is None:
+        bias32 = ((1 << 31) // q) * q
 
     def red32(u):
         u &= M32
@@ -252,3 +254,39 @@ def test_fold_level_choices(mh):
     q = 40009  # 2^16 mod q = 25527
     assert (1 << 16) % q >= 256 and mh.fold_level(q, 128) == 3
     assert mh.fold_level(2147483647, 128) == 3
+
+
+@pytest.mark.parametrize("q", [65521, 65519, 65287, 257, 40009])
+def test_fold_levels_u8_exact_at_their_bounds(mh, q):
+    """Unsigned (u8) digits: class sums in [0, 255^2 k] / [0, 2 * 255^2 k] / [0, 255^2 k],
+    no bias.  For each level mhg_fold_level_u8 admits, the emulated kernel arithmetic is
+    exact at the largest admitted chunk (up to the u8 chunk bound (2^31 - 2^17) / (2 * 255^2))."""
+    kmax_u = ((1 << 31) - (1 << 17)) // (2 * 65025)
+    rng = np.random.default_rng(q + 1)
+    seen = set()
+    for level in (1, 2, 3):
+        lo, hi = 0, kmax_u
+        while lo < hi:
+            mid = (lo + hi + 1) // 2
+            if mh.fold_level(q, mid, unsigned_digits=True) <= level:
+                lo = mid
+            else:
+                hi = mid - 1
+        K = lo
+        if K == 0:
+            continue
+        seen.add(level)
+        e0, e1, e2 = 65025 * K, 2 * 65025 * K, 65025 * K
+        cases = [(b0 * e0, b1 * e1, b2 * e2) for b0 in (0, 1) for b1 in (0, 1) for b2 in (0, 1)]
+        cases += [(int(rng.integers(0, e0 + 1)), int(rng.integers(0, e1 + 1)),
+                   int(rng.integers(0, e2 + 1))) for _ in range(300)]
+        for a0, a1, a2 in cases:
+            for cur in (0, q - 1, int(rng.integers(0, q))):
+                want = (cur + a0 + 256 * a1 + 65536 * a2) % q
+                for layout in (0, 1):
+                    got = _emulate_fold(level, layout, a0, a1, a2, cur, q, bias32=0)
+                    assert got == want, (q, level, K, layout, a0, a1, a2, cur)
+    if (1 << 16) % q < 256:
+        assert 2 in seen  # every u8 chunk has a lean fold
+    else:
+        assert seen == {3}
