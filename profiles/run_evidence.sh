@@ -1,3 +1,5 @@
+# Full evidence set of a round (run from the repo root under gpurun): bench lines for every
+# workload + the reference arm, the ncu launch list and full captures, the k_widen16 capture.
 set -u
 bash profiles/run_final.sh gpurun_out/final > gpurun_out/final_rc.log 2>&1
 bash profiles/run_ncu.sh r01l > gpurun_out/ncu_rc.log 2>&1
