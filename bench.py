@@ -46,6 +46,32 @@ DESCR = {
 }
 METRIC = "GF(p) mult-adds/s, Morton-hybrid C-=A·B mod p, n=16384; % of TC roofline"
 UNIT = "GF(p) MAC/s"
+DATA = ("synthetic: mh::Rng(0) -- std::mt19937_64, the reference's generator (bench.hpp:44-52) -- "
+        "below(p) per cell in flat Morton order, out then lhs then rhs (gen_problem, bench.hpp:101-103); "
+        "C zeroed for C = A*B workloads")
+
+
+def config_of(workload):
+    """The workload description both arms print (identical keys and values)."""
+    n, t, q, op, view = WORKLOADS[workload]
+    cfg = {"workload": workload, "description": DESCR[workload], "n": n, "t": t, "p": q, "op": op}
+    if view is not None:
+        cfg["view"] = {"row0": view[0], "col0": view[1], "rows": view[2], "inner": view[3], "cols": view[4]}
+    gib = n * n * 4 / 2 ** 30
+    cfg["l2"] = ("no flush: operands 3 x %.2f GiB >> 126 MB L2" % gib if 3 * n * n * 4 > (126 << 20)
+                 else "operands 3 x %.1f MiB fit in the 126 MB L2 (no flush between steps)" % (gib * 1024))
+    return cfg
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def limbs_of(q):
@@ -138,13 +164,14 @@ def reference_sample(n, t, q, threads, rows_per_thread=64, cols=512, view=None):
     return ref, h, (i0, rows, j0, cols, k0, min(inner, n - k0))
 
 
-def cpu_baseline_json(args, n, t, q, view, steps=1, warmup=0):
+def cpu_baseline_json(args, n, t, q, view, steps=1, warmup=0, one_core=True):
     threads = args.cpu_threads or os.cpu_count() or 1
     got = reference_sample(n, t, q, threads, view=view)
     if got is None:
         return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                 "sample": "oracle/_ref/libmhref.so missing"}
     ref, h, (i0, rows, j0, cols, k0, inner) = got
+    single = None
     try:
         for _ in range(warmup):
             ref.bench_run(h, i0, rows, j0, cols, k0, inner, threads)
@@ -153,15 +180,26 @@ def cpu_baseline_json(args, n, t, q, view, steps=1, warmup=0):
             ns, macs = ref.bench_run(h, i0, rows, j0, cols, k0, inner, threads)
             tot_ns += ns
             tot_macs += macs
+        if one_core:
+            # the reference is single-threaded by contract (multiply.hpp:25-29): one call
+            # on one core, a 64-row strip of the same sample
+            ns1, macs1 = ref.bench_run(h, i0, min(64, rows), j0, cols, k0, inner, 1)
+            single = {"value": macs1 / (ns1 * 1e-9), "unit": UNIT, "cores": 1,
+                      "sample": f"one mh::mm_oblivious call on output rows [{i0},{i0 + min(64, rows)}) x "
+                                f"cols [{j0},{j0 + cols}), inner {inner} ({macs1} MACs)"}
     finally:
         ref.bench_free(h)
     val = tot_macs / (tot_ns * 1e-9)
     return {"value": val, "unit": UNIT, "cores": threads, "kind": "reference",
             "sample": f"mh::mm_oblivious (reference headers, -O3 -DNDEBUG) on output rows "
                       f"[{i0},{i0 + rows}) x cols [{j0},{j0 + cols}), inner {inner}, of the n={n} "
-                      f"containers; {threads} disjoint row strips on {threads} std::threads; "
-                      f"{steps} step(s) of {tot_macs // max(steps, 1)} MACs",
+                      f"containers (mh::Rng(0) fill, as the GPU arm); {threads} disjoint row strips on "
+                      f"{threads} std::threads; {steps} step(s) of {tot_macs // max(steps, 1)} MACs",
+            "cpu_model": cpu_model(), "one_core": single,
             "ms_per_step": tot_ns / 1e6 / max(steps, 1)}
+
+
+CPU_KEYS = ("value", "unit", "cores", "kind", "sample", "cpu_model", "one_core")
 
 
 def run_reference(args, rank, world):
@@ -173,11 +211,10 @@ def run_reference(args, rank, world):
     line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": W, "ms_per_step": cb.get("ms_per_step"),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
-            "data": "synthetic (uniform residues, splitmix stream)",
-            "config": {"workload": args.workload, "description": DESCR[args.workload], "n": n,
-                       "t": t, "p": q, "op": op},
+            "data": DATA,
+            "config": config_of(args.workload),
             "impl": "reference",
-            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "cpu_baseline": {k: cb.get(k) for k in CPU_KEYS},
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
             "gpu_launches": 0}
@@ -316,13 +353,37 @@ def e2e_ranked(mh, torch, dist, mats, flats, out_f, step, stream, b, e, steps, m
                     "with the segments' mhg_plan_gemm -> slice read-back"}
 
 
+def seeded_containers(mh, torch, dev, n, q, b, e, zero_out=False, seed=0):
+    """Three n x n device containers whose cells [b, e) hold mh::Rng(seed)'s draws in
+    gen_problem's order (out, lhs, rhs; flat Morton order); the rest is zero."""
+    import numpy as np
+    g = mh.Rng(seed)
+    chunk = 1 << 24
+    host = torch.empty(chunk, dtype=torch.int32, pin_memory=True)
+    hv = host.numpy().view(np.uint32)
+    flats = []
+    for which in range(3):
+        f = torch.zeros(n * n, dtype=torch.int32, device=dev)
+        pos = 0
+        while pos < n * n:
+            m = min(chunk, n * n - pos)
+            g.below(q, m, out=hv[:m])
+            lo, hi = max(pos, b), min(pos + m, e)
+            if lo < hi and not (zero_out and which == 0):
+                f[lo:hi].copy_(host[lo - pos:hi - pos], non_blocking=False)
+            pos += m
+        flats.append(f)
+    torch.cuda.synchronize()
+    return flats
+
+
 def run_gpu(args, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
     import paper_1705_04807_b200 as mh
-    from paper_1705_04807_b200.dist import (PanelExchange, PeerPanels, rank_update,
-                                            rank_update_packed, segment_plans, slice_range)
+    from paper_1705_04807_b200.dist import (PanelExchange, PeerPanels, PeerSetupError, exchange_bytes,
+                                            rank_update, rank_update_packed, segment_plans, slice_range)
 
     torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
@@ -332,15 +393,10 @@ def run_gpu(args, rank, world, local_rank):
     lay, mod = mh.Layout(n, t), mh.Modulus(q)
     stream = torch.cuda.current_stream()
 
-    # containers: full-size on every rank; each rank draws its own 1/P Morton slice
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1234 + rank)
-    flats = []
+    # containers: full-size on every rank; each rank keeps its own 1/P Morton slice of
+    # the reference's seed-0 stream (mh::Rng(0), gen_problem's fill order)
     b, e = slice_range(rank, world, n) if world > 1 else (0, n * n)
-    for _ in range(3):
-        f = torch.zeros(n * n, dtype=torch.int32, device=dev)
-        f[b:e] = torch.randint(0, q, (e - b,), dtype=torch.int32, device=dev, generator=gen)
-        flats.append(f)
+    flats = seeded_containers(mh, torch, dev, n, q, b, e, zero_out=(opname == "set"))
     out_f, lhs_f, rhs_f = flats
     A, B, Cm = (mh.Matrix.wrap(lay, mod, f.data_ptr(), owner=f) for f in flats)
 
@@ -380,10 +436,14 @@ def run_gpu(args, rank, world, local_rank):
     if exchange not in ("none", "p2p", "nccl", "u32"):
         raise SystemExit(f"MHG_EXCHANGE must be p2p, nccl or u32, got {exchange!r}")
     peer = None
+    exchange_note = None
     if exchange == "p2p":
         # CPU-only barriers for the IPC event ordering (never wait for the GPU)
         host_group = dist.new_group(backend="gloo") if dist.get_backend() != "gloo" else None
-        peer = PeerPanels(mh, ex, plans, host_group=host_group)
+        try:
+            peer = PeerPanels(mh, ex, plans, host_group=host_group)
+        except PeerSetupError as exc:  # collective: every rank falls back together
+            exchange, exchange_note = "nccl", f"p2p setup failed, fell back to nccl: {exc}"[:300]
     if exchange in ("p2p", "nccl"):
         # packed exchange: one GEMM per segment + the packs of the parts this rank owns
         launches_per_step = sum(1 + (rank == sg.a_owner) + (rank == sg.b_owner) for sg in segs)
@@ -439,6 +499,16 @@ def run_gpu(args, rank, world, local_rank):
         dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
     ms, gemm_ms_max = float(t_ms[0]), float(t_ms[1])
     value = macs_total / (ms * 1e-3)
+    exchange_info = None
+    if world > 1:
+        # per rank: bytes received per step and the step time not covered by its GEMMs
+        # (packs + exchange not hidden behind compute); max over ranks
+        x = torch.tensor([float(exchange_bytes(ex, plans, exchange)), ms_local - gemm_ms], dtype=torch.float64,
+                         device=dev)
+        dist.all_reduce(x, op=dist.ReduceOp.MAX)
+        exchange_info = {"mode": exchange, "bytes_per_rank_step": int(x[0]),
+                         "exposed_ms_per_step": float(x[1]),
+                         "note": exchange_note}
 
     # ---- end to end through the public API with host buffers (pinned)
     e2e = None
@@ -450,6 +520,16 @@ def run_gpu(args, rank, world, local_rank):
         else:
             e2e = e2e_ranked(mh, torch, dist, (A, B, Cm), flats, out_f, step, stream, b, e, e2e_steps,
                              macs_total, dev, barrier)
+    # ---- one more step, checked on the device (Freivalds, mhg_verify) against a snapshot
+    verified = None
+    if world == 1:
+        old_f = out_f.clone()
+        old = mh.Matrix.wrap(lay, mod, old_f.data_ptr(), owner=old_f)
+        step()
+        verified = mh.verify(prob, mh.Sub(old, prob.a.origin, prob.a.rows, prob.a.cols), op, rounds=2,
+                             stream=stream)
+        del old, old_f
+        torch.cuda.empty_cache()
     if peer is not None:
         torch.cuda.synchronize()
         barrier()
@@ -487,15 +567,17 @@ def run_gpu(args, rank, world, local_rank):
     if world == 1:
         conversion = time_conversions(mh, torch, (A, B, Cm), n, q, hbm)
     cpu = None
-    if world == 1 and not args.no_cpu_baseline:
+    if not args.no_cpu_baseline:
+        # rank 0 only, after every rank finished timing (the other ranks are idle)
         cb = cpu_baseline_json(args, n, t, q, view)
-        cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        cpu = {k: cb.get(k) for k in CPU_KEYS}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": W, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "int8",
-            "data": "synthetic: uniform residues in [0,p) drawn on device (torch.Generator)",
-            "config": {"workload": args.workload, "description": DESCR[args.workload], "n": n,
-                       "t": t, "p": q, "op": opname, "limbs": L,
+            "data": DATA,
+            "config": config_of(args.workload),
+            "verified": verified,
+            "kernel_config": {"limbs": L,
                        "tiles": info["tiles"], "k_chunks": info["k_chunks"], "digits": info.get("digits"),
                        "partition": f"C-stationary Morton blocks over {world} GPU(s)"
                                     + ({"p2p": f", {len(plans)} K segments, packed limb planes "
@@ -505,9 +587,9 @@ def run_gpu(args, rank, world, local_rank):
                                                 "broadcasts of packed limb planes",
                                         "u32": f", {len(plans)} K segments pipelined with NCCL "
                                                "broadcasts of uint32 cells"}.get(exchange, "")),
-                       "exchange": exchange,
-                       "l2": "no flush: operands 3 x %.2f GiB >> 126 MB L2" % (n * n * 4 / 2 ** 30)},
+                       "exchange": exchange},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "conversion": conversion,
+            "exchange": exchange_info,
             "gpu_launches": args.steps * launches_per_step,
             "clocks": clk.summary()}
     print(json.dumps(line), flush=True)

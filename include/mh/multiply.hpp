@@ -6,10 +6,9 @@
 // oblivious recursion.  Calls are synchronous like the reference's.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
-#include <map>
 #include <optional>
-#include <tuple>
 
 #include "mh/submatrix.hpp"
 
@@ -83,12 +82,14 @@ inline Counters to_counters(const mhg_counters& c) {
                     c.max_consecutive_jump};
 }
 
-/// out op= lhs * rhs on the device, synchronous; returns the oblivious Counters.
-inline Counters run(const Problem& p, Op op) {
+/// out op= lhs * rhs on the device, synchronous.  `flags` selects whose validation
+/// and Counters apply: 0 = mm_oblivious, MHG_KERNEL_NAIVE / MHG_KERNEL_DEFAULT = the
+/// reference's other two kernels (the same GPU computation).
+inline Counters run(const Problem& p, Op op, std::uint32_t flags = 0) {
     check_problem(p);
     mhg_counters c{};
-    gpu::check(mhg_mm(view_of(p.a), view_of(p.b), view_of(p.c), static_cast<mhg_op>(op), &c,
-                      nullptr));
+    gpu::check(mhg_mm_ex(view_of(p.a), view_of(p.b), view_of(p.c), static_cast<mhg_op>(op), flags, &c,
+                         nullptr));
     gpu::check(mhg_synchronize(nullptr));
     p.a.mat->device_written();
     return to_counters(c);
@@ -102,62 +103,44 @@ inline Counters mm_oblivious(const Problem& p) { return gpu::run(p, Op::Add); }
 /// Same engine with the TU/TURBO operations: Op::Sub is C -= A*B, Op::Set is C = A*B.
 inline Counters mm_oblivious(const Problem& p, Op op) { return gpu::run(p, op); }
 
-namespace detail {
+/// mm_naive / mm_default (multiply.hpp:269-291): the same results from the same GPU
+/// engine, with the reference's validation for these two (no layout guard: the three
+/// containers may differ in n and t) and their Counters in closed form -- base-case,
+/// recursion and encode tallies and the max_consecutive_jump of their encode-addressed
+/// walks (the planner's naive_counters / default_counters, libmhg.so).
+inline Counters mm_naive(const Problem& p) { return gpu::run(p, Op::Add, MHG_KERNEL_NAIVE); }
 
-// Leaves / nodes of the reference's view-halving recursion (default_rec,
-// multiply.hpp:202-230): every dimension above t is cut at ceil(d/2).
-struct DefaultTally {
-    std::uint64_t t;
-    std::map<std::tuple<std::uint64_t, std::uint64_t, std::uint64_t>,
-             std::pair<std::uint64_t, std::uint64_t>> memo;  // (nodes, leaves)
+inline Counters mm_default(const Problem& p) { return gpu::run(p, Op::Add, MHG_KERNEL_DEFAULT); }
 
-    std::pair<std::uint64_t, std::uint64_t> walk(std::uint64_t r, std::uint64_t k, std::uint64_t c) {
-        if (r <= t && k <= t && c <= t) return {1, 1};
-        const auto key = std::make_tuple(r, k, c);
-        if (auto it = memo.find(key); it != memo.end()) return it->second;
-        auto halves = [&](std::uint64_t d) {
-            return d > t ? std::array<std::uint64_t, 2>{(d + 1) / 2, d / 2}
-                         : std::array<std::uint64_t, 2>{d, 0};
-        };
-        std::pair<std::uint64_t, std::uint64_t> acc{1, 0};
-        for (std::uint64_t rr : halves(r))
-            for (std::uint64_t cc : halves(c))
-                for (std::uint64_t kk : halves(k))
-                    if (rr && cc && kk) {
-                        const auto sub = walk(rr, kk, cc);
-                        acc.first += sub.first;
-                        acc.second += sub.second;
-                    }
-        memo[key] = acc;
-        return acc;
-    }
-};
-
-}  // namespace detail
-
-/// mm_naive / mm_default (multiply.hpp:269-291): same results, computed by the
-/// same GPU engine.  Their Counters reproduce the reference's base_case_calls,
-/// scalar_macs, recursive_calls and encode_calls in closed form;
-/// max_consecutive_jump of the reference's encode-addressed walks is not
-/// reproduced (reported as 0) -- these two are comparison kernels, not the path.
-inline Counters mm_naive(const Problem& p) {
-    gpu::run(p, Op::Add);
-    if (p.a.rows == 0 || p.a.cols == 0 || p.b.cols == 0) return Counters{};
-    const std::uint64_t r = p.a.rows, k = p.b.cols, cc = p.a.cols;
-    return Counters{1, r * k * cc, r * cc * (2 * k + 1), 1, 0};
-}
-
-inline Counters mm_default(const Problem& p) {
-    check_problem(p);
-    if (p.a.rows == 0 || p.a.cols == 0 || p.b.cols == 0) return Counters{};
-    gpu::run(p, Op::Add);
-    const std::uint64_t r = p.a.rows, k = p.b.cols, cc = p.a.cols;
-    detail::DefaultTally tally{p.a.mat->layout().t, {}};
-    const auto nodes_leaves = tally.walk(r, k, cc);
-    detail::DefaultTally kt{p.a.mat->layout().t, {}};
-    const std::uint64_t k_leaves = kt.walk(1, k, 1).second;  // leaves along the inner axis
-    return Counters{nodes_leaves.second, r * k * cc, r * cc * k_leaves + 2 * r * k * cc,
-                    nodes_leaves.first, 0};
+/// base_case_mm (multiply.hpp:136-172): out += lhs * rhs for three views that each sit
+/// inside one tile; anything scattered is rejected with std::logic_error, as are shapes
+/// that do not chain.  The multiply runs on the GPU engine (views of one container are
+/// read before the output is written: snapshot semantics, which equals the reference's
+/// in-place walk whenever the output does not overlap an operand).  Counters: one base
+/// case, r*k*c MACs, no encodes; max_consecutive_jump raised to the largest forward
+/// step of the reference's walks (out: +1 along a row, t - cols + 1 to the next row;
+/// lhs: +1 along a row, t - inner + 1 to the next row; rhs: +t down a column, +1
+/// across columns only when inner == 1).
+inline void base_case_mm(const Sub& out, const Sub& lhs, const Sub& rhs, Counters& ctr) {
+    if (!is_contained(out) || !is_contained(lhs) || !is_contained(rhs))
+        throw std::logic_error("base_case_mm: operand spans more than one tile");
+    if (out.rows != lhs.rows || out.cols != rhs.cols || lhs.cols != rhs.rows)
+        throw std::logic_error("base_case_mm: view shapes do not chain");
+    ++ctr.base_case_calls;
+    const std::uint64_t r = out.rows, c = out.cols, k = lhs.cols;
+    if (r == 0 || c == 0 || k == 0) return;
+    std::uint64_t jump = 0;
+    const std::uint64_t ta = out.mat->layout().t, tb = lhs.mat->layout().t, tc = rhs.mat->layout().t;
+    if (c >= 2 || k >= 2) jump = 1;
+    if (r >= 2) jump = std::max({jump, ta - c + 1, tb - k + 1});
+    if (k >= 2) jump = std::max(jump, tc);
+    ctr.max_consecutive_jump = std::max(ctr.max_consecutive_jump, jump);
+    const bool shared = out.mat == lhs.mat || out.mat == rhs.mat || lhs.mat == rhs.mat;
+    gpu::check(mhg_mm_ex(gpu::view_of(out), gpu::view_of(lhs), gpu::view_of(rhs), MHG_OP_ADD,
+                         MHG_KERNEL_NAIVE | (shared ? MHG_ALLOW_ALIAS : 0u), nullptr, nullptr));
+    gpu::check(mhg_synchronize(nullptr));
+    out.mat->device_written();
+    ctr.scalar_macs += r * c * k;
 }
 
 }  // namespace mh

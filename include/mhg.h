@@ -78,6 +78,31 @@ const char *mhg_last_error(void);
 mhg_status mhg_device_check(void);
 const char *mhg_version(void);
 
+/* ---- options (process-wide; no reference counterpart) ----
+ * The planner's kernel and digit choices and the test hooks.  Every value gives
+ * bit-identical results; only speed differs.  Initial values are read ONCE, at the
+ * first use, from the environment variable named beside each key; afterwards only
+ * mhg_set_option changes them.  Unknown keys / out-of-range values fail with
+ * MHG_ERR_INVALID_ARGUMENT. */
+typedef enum {
+    MHG_OPT_DIGITS = 1,          /* MHG_UDIG: 1 = unsigned u8 limb digits (default), 0 = balanced s8 */
+    MHG_OPT_GEMM_KERNEL = 2,     /* MHG_GEMM: 0 = planner (single CTA for <= 2 limbs, CTA pair for
+                                    3-4), 1 = single-CTA k_gemm, 2 = CTA-pair k_gemm2 */
+    MHG_OPT_MIN_FOLD_LEVEL = 3,  /* MHG_FOLD: lowest lean-fold level of the 2-limb epilogue, 1..3 */
+    MHG_OPT_MAX_KCHUNK = 4,      /* MHG_FORCE_KCHUNK: cap on 128-byte K slices per exact int32
+                                    chunk (0 = the planner's bound; small values force multi-chunk K) */
+    MHG_OPT_UPLOAD_WIRE = 5,     /* MHG_UPLOAD_WIRE: 0 = auto (16-bit wire with >= 8 host workers),
+                                    16 = 16-bit wire where eligible, 32 = plain 4-byte copies */
+    MHG_OPT_CONV_KERNEL = 6,     /* MHG_CONV: 0 = TMA where eligible (default), 1 = Morton-order
+                                    LDG/STG, 2 = row-order LDG/STG */
+    MHG_OPT_GEMM_STATS = 7,      /* MHG_GEMM_STATS: 1 = print per-launch wait-cycle shares to stderr
+                                    (synchronous; diagnostics) */
+    MHG_OPT_UPLOAD_THREADS = 8   /* MHG_UPLOAD_THREADS: host narrowing workers (0 = the affinity
+                                    mask / LOCAL_WORLD_SIZE) */
+} mhg_option;
+mhg_status mhg_set_option(int key, int64_t value);
+mhg_status mhg_get_option(int key, int64_t *value);
+
 /* ---- layout codec (layout.hpp:42-99): host-side, no device needed ---- */
 mhg_status mhg_layout_check(uint64_t n, uint64_t t);                 /* Layout(n,t) ctor :50-62 */
 mhg_status mhg_encode(uint64_t n, uint64_t t, uint64_t i, uint64_t j, uint64_t *z); /* :80-85 */
@@ -133,8 +158,14 @@ mhg_status mhg_mm(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, mhg_count
  * container rule (multiply.hpp:59-60) for the TU/TURBO Schur update, where
  * C, A and B are views of ONE parent: the operands are read (packed) before the
  * output is written, so the result is C_new = C_old op A_old * B_old even when
- * the views overlap.  All other checks are unchanged. */
+ * the views overlap.  All other checks are unchanged.
+ * MHG_KERNEL_NAIVE / MHG_KERNEL_DEFAULT: the same GPU computation behind the
+ * reference's other two entry points, mm_naive (multiply.hpp:269-278) and mm_default
+ * (:283-291): their validation (no layout guard -- the three containers may differ in
+ * n and t) and their Counters (closed form, incl. max_consecutive_jump). */
 #define MHG_ALLOW_ALIAS 1u
+#define MHG_KERNEL_NAIVE 2u
+#define MHG_KERNEL_DEFAULT 4u
 mhg_status mhg_mm_ex(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, uint32_t flags,
                      mhg_counters *ctr, void *stream);
 mhg_status mhg_plan_create_ex(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, uint32_t flags,
@@ -147,6 +178,15 @@ mhg_status mhg_counters_oblivious(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_
 mhg_status mhg_counters_layout(uint64_t n, uint64_t t, uint64_t out_origin, uint64_t lhs_origin,
                                uint64_t rhs_origin, uint64_t rows, uint64_t inner, uint64_t cols,
                                mhg_counters *ctr);
+/* Counters of the reference kernel selected by flags (0: mm_oblivious, MHG_KERNEL_NAIVE,
+ * MHG_KERNEL_DEFAULT), with that kernel's validation; no device work. */
+mhg_status mhg_counters_for(uint32_t flags, mhg_view out, mhg_view lhs, mhg_view rhs, mhg_counters *ctr);
+/* The same from raw geometry: each container's (n, t) and the view's flat origin;
+ * pure host code, usable without a GPU. */
+mhg_status mhg_counters_geometry(uint32_t flags, uint64_t n_out, uint64_t t_out, uint64_t out_origin,
+                                 uint64_t n_lhs, uint64_t t_lhs, uint64_t lhs_origin, uint64_t n_rhs,
+                                 uint64_t t_rhs, uint64_t rhs_origin, uint64_t rows, uint64_t inner,
+                                 uint64_t cols, mhg_counters *ctr);
 
 /* Reusable plan: validation, offset tables, packing workspace and a captured
  * CUDA graph (pack lhs, pack rhs, GEMM + fused epilogue) replayed by
@@ -191,6 +231,24 @@ mhg_status mhg_plan_info(mhg_plan plan, uint64_t *launches, uint64_t *tiles, uin
  * or 2 (CTA-pair k_gemm2). */
 mhg_status mhg_plan_variant(mhg_plan plan, int *unsigned_digits, int *cta_group);
 mhg_status mhg_plan_destroy(mhg_plan plan);
+
+/* ---- verification and seeded inputs ---- */
+/* Freivalds check of a finished multiply on the device: out_new == out_old op lhs*rhs
+ * (views of matching shapes; out_old holds the output's cells from before the call,
+ * in its own container) is tested as  C_new r == C_old r op A (B r)  (mod q) for
+ * `rounds` random vectors r derived from `seed`; a wrong result survives a round with
+ * probability <= 1/q.  *ok = 1 when every round agrees.  The device analogue of the
+ * reference's cross-check (MismatchError, bench.hpp:123-125, 186-193).  Synchronous. */
+mhg_status mhg_verify(mhg_view out_new, mhg_view out_old, mhg_view lhs, mhg_view rhs, mhg_op op,
+                      uint32_t rounds, uint64_t seed, int *ok, void *stream);
+/* mh::Rng (bench.hpp:44-52): std::mt19937_64(seed), below(k) = (next() * k) >> 64.
+ * mhg_rng_below writes `count` consecutive draws of below(k) (k <= 2^32) -- a
+ * container filled in flat Morton order from one stream is the reference's
+ * gen_problem fill (:101-103).  Host only. */
+typedef struct mhg_rng_s *mhg_rng;
+mhg_status mhg_rng_create(uint64_t seed, mhg_rng *out);
+mhg_status mhg_rng_below(mhg_rng rng, uint64_t k, uint32_t *dst, uint64_t count);
+mhg_status mhg_rng_destroy(mhg_rng rng);
 
 /* ---- diagnostics for tests / bench ---- */
 /* Host helper: the limb representation parameters the planner picks for q

@@ -220,6 +220,7 @@ class Reference:
         L.ref_extract.argtypes = [U64, U64, U64, C.POINTER(U64), C.POINTER(U64)]
         L.ref_mm.argtypes = [C.c_int, U64, U64, C.c_uint32, U32P, U64, U64, U64, U32P, U64, U64,
                              U32P, U64, C.c_int, C.POINTER(Counters)]
+        L.ref_counters_mixed.argtypes = [C.c_int] + [U64] * 12 + [C.POINTER(Counters)]
         L.ref_gen_problem.argtypes = [U64, U64, C.c_uint32, U64, C.c_uint32, U32P, U32P, U32P,
                                       np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS")]
         L.ref_run_trials_csv.argtypes = [U64, U64, C.c_uint32, U64, C.c_uint32, C.c_int, C.c_char_p]
@@ -246,6 +247,15 @@ class Reference:
 
     def mm_oblivious(self, *a, **k):
         return self.mm(2, *a, **k)
+
+    def counters_mixed(self, kind, geo_out, geo_lhs, geo_rhs, rows, inner, cols) -> Counters:
+        """Counters of mm_naive (kind 0) / mm_default (1); geo_* = (n, t, origin) per container."""
+        ctr = Counters()
+        st = self.lib.ref_counters_mixed(kind, *geo_out, *geo_lhs, *geo_rhs, rows, inner, cols,
+                                         C.byref(ctr))
+        if st:
+            raise _status_error(st)
+        return ctr
 
     def gen_problem(self, n, t, q, seed, skip=0):
         out = np.empty(n * n, np.uint32)

@@ -112,6 +112,22 @@ int ref_mm(int kind, std::uint64_t n, std::uint64_t t, std::uint32_t q, std::uin
     });
 }
 
+// Counters of mm_naive (kind 0) / mm_default (kind 1) on three containers that may
+// differ in layout (the reference allows it for these two): zero-filled GF(2) stores,
+// only the Counters are reported.
+int ref_counters_mixed(int kind, std::uint64_t na, std::uint64_t ta, std::uint64_t oa,
+                       std::uint64_t nb, std::uint64_t tb, std::uint64_t ob, std::uint64_t nc,
+                       std::uint64_t tc, std::uint64_t oc, std::uint64_t rows, std::uint64_t inner,
+                       std::uint64_t cols, Counters5* ctr) {
+    return guarded([&] {
+        const mh::Modulus two(2);
+        mh::Matrix A(mh::Layout(na, ta), two), B(mh::Layout(nb, tb), two), C(mh::Layout(nc, tc), two);
+        const mh::Problem prob{mh::Sub{&A, oa, rows, cols}, mh::Sub{&B, ob, rows, inner},
+                               mh::Sub{&C, oc, inner, cols}};
+        put(kind == 0 ? mh::mm_naive(prob) : mh::mm_default(prob), ctr);
+    });
+}
+
 // Draw the (skip+1)-th instance of Rng(seed) exactly as gen_problem does.
 int ref_gen_problem(std::uint64_t n, std::uint64_t t, std::uint32_t q, std::uint64_t seed,
                     std::uint32_t skip, std::uint32_t* out, std::uint32_t* lhs,
@@ -157,23 +173,18 @@ struct RefBench {
     std::unique_ptr<mh::Matrix> out, lhs, rhs;
 };
 
-// Three n x n containers; cells drawn from a splitmix stream (timing only --
-// the CPU time of mm_oblivious does not depend on the residue values).
+// Three n x n containers filled exactly as the reference's gen_problem fills them
+// (bench.hpp:101-103): one mh::Rng(seed) stream, below(q) per cell in flat Morton
+// order, out then lhs then rhs -- the same residues bench.py's GPU arm multiplies.
 void* ref_bench_new(std::uint64_t n, std::uint64_t t, std::uint32_t q, std::uint64_t seed) {
     try {
         auto* b = new RefBench{mh::Layout(n, t), mh::Modulus(q), nullptr, nullptr, nullptr};
         b->out = std::make_unique<mh::Matrix>(b->lay, b->mod);
         b->lhs = std::make_unique<mh::Matrix>(b->lay, b->mod);
         b->rhs = std::make_unique<mh::Matrix>(b->lay, b->mod);
-        std::uint64_t s = seed;
+        mh::Rng rng(seed);
         for (mh::Matrix* m : {b->out.get(), b->lhs.get(), b->rhs.get()})
-            for (auto& v : m->cells()) {
-                s += 0x9E3779B97F4A7C15ULL;
-                std::uint64_t z = s;
-                z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
-                z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
-                v.v = std::uint32_t((z ^ (z >> 31)) % q);
-            }
+            for (auto& v : m->cells()) v = mh::Fp{std::uint32_t(rng.below(q))};
         return b;
     } catch (...) {
         return nullptr;

@@ -34,14 +34,21 @@ __all__ = [
     "InvalidArgument", "OutOfRange", "LogicError", "DeviceError", "Unsupported",
     "Layout", "Modulus", "Matrix", "Sub", "Problem", "Counters", "Plan",
     "encode", "extract_i", "extract_j", "from_row_major", "to_row_major",
-    "mm_oblivious", "mm", "counters_oblivious", "counters_layout", "limb_params", "lib", "LIB_PATH",
-    "OP_ADD", "OP_SUB", "OP_SET",
+    "mm_oblivious", "mm_naive", "mm_default", "mm", "counters_oblivious", "counters_layout",
+    "counters_geometry", "limb_params", "lib", "LIB_PATH", "KERNEL_NAIVE", "KERNEL_DEFAULT",
+    "verify", "Rng",
+    "OP_ADD", "OP_SUB", "OP_SET", "set_option", "get_option", "options",
+    "OPT_DIGITS", "OPT_GEMM_KERNEL", "OPT_MIN_FOLD_LEVEL", "OPT_MAX_KCHUNK", "OPT_UPLOAD_WIRE",
+    "OPT_CONV_KERNEL", "OPT_GEMM_STATS", "OPT_UPLOAD_THREADS",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 # MHG_LIB: an alternative build of the same library (kernel A/B diagnostics only)
 LIB_PATH = os.environ.get("MHG_LIB") or os.path.join(HERE, "libmhg.so")
 OP_ADD, OP_SUB, OP_SET = 0, 1, 2
+# mhg_option keys (include/mhg.h)
+(OPT_DIGITS, OPT_GEMM_KERNEL, OPT_MIN_FOLD_LEVEL, OPT_MAX_KCHUNK, OPT_UPLOAD_WIRE, OPT_CONV_KERNEL,
+ OPT_GEMM_STATS, OPT_UPLOAD_THREADS) = range(1, 9)
 
 
 class InvalidArgument(ValueError):
@@ -110,6 +117,8 @@ def lib():
         "mhg_last_error": ([], C.c_char_p),
         "mhg_version": ([], C.c_char_p),
         "mhg_device_check": ([], C.c_int),
+        "mhg_set_option": ([C.c_int, C.c_int64], C.c_int),
+        "mhg_get_option": ([C.c_int, P(C.c_int64)], C.c_int),
         "mhg_layout_check": ([u64, u64], C.c_int),
         "mhg_modulus_check": ([u32], C.c_int),
         "mhg_encode": ([u64, u64, u64, u64, P(u64)], C.c_int),
@@ -129,6 +138,8 @@ def lib():
         "mhg_plan_create_ex": ([_View, _View, _View, C.c_int, u32, P(vp)], C.c_int),
         "mhg_counters_oblivious": ([_View, _View, _View, P(Counters)], C.c_int),
         "mhg_counters_layout": ([u64] * 8 + [P(Counters)], C.c_int),
+        "mhg_counters_for": ([u32, _View, _View, _View, P(Counters)], C.c_int),
+        "mhg_counters_geometry": ([u32] + [u64] * 12 + [P(Counters)], C.c_int),
         "mhg_plan_create": ([_View, _View, _View, C.c_int, P(vp)], C.c_int),
         "mhg_plan_run": ([vp, vp], C.c_int),
         "mhg_plan_pack": ([vp, C.c_int, vp], C.c_int),
@@ -139,6 +150,10 @@ def lib():
         "mhg_ipc_close": ([vp], C.c_int),
         "mhg_copy_async": ([vp, vp, u64, vp], C.c_int),
         "mhg_plan_counters": ([vp, P(Counters)], C.c_int),
+        "mhg_verify": ([_View, _View, _View, _View, C.c_int, u32, u64, P(C.c_int), vp], C.c_int),
+        "mhg_rng_create": ([u64, P(vp)], C.c_int),
+        "mhg_rng_below": ([vp, u64, vp, u64], C.c_int),
+        "mhg_rng_destroy": ([vp], C.c_int),
         "mhg_plan_info": ([vp, P(u64), P(u64), P(u32), P(u32), P(u64)], C.c_int),
         "mhg_plan_variant": ([vp, P(C.c_int), P(C.c_int)], C.c_int),
         "mhg_plan_destroy": ([vp], C.c_int),
@@ -163,6 +178,37 @@ def _check(status: int):
     if status:
         msg = lib().mhg_last_error().decode(errors="replace")
         raise _ERR.get(status, DeviceError)(msg)
+
+
+# ---------------------------------------------------------------- options
+def set_option(key: int, value: int):
+    """mhg_set_option: a planner choice or test hook (results are identical for every value)."""
+    _check(lib().mhg_set_option(key, value))
+
+
+def get_option(key: int) -> int:
+    v = C.c_int64()
+    _check(lib().mhg_get_option(key, C.byref(v)))
+    return v.value
+
+
+class options:
+    """Context manager: `with options({OPT_DIGITS: 0}): ...` sets options, restores on exit."""
+
+    def __init__(self, values: dict):
+        self._values = dict(values)
+        self._saved = {}
+
+    def __enter__(self):
+        for k, v in self._values.items():
+            self._saved[k] = get_option(k)
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self._saved.items():
+            set_option(k, v)
+        return False
 
 
 # ------------------------------------------------------------------ codec
@@ -398,17 +444,22 @@ class Problem:
 
 
 ALLOW_ALIAS = 1
+KERNEL_NAIVE = 2    # MHG_KERNEL_NAIVE: mm_naive's validation + Counters (multiply.hpp:269-278)
+KERNEL_DEFAULT = 4  # MHG_KERNEL_DEFAULT: mm_default's (multiply.hpp:283-291)
 
 
-def mm(problem: Problem, op: int = OP_ADD, stream=None, allow_alias: bool = False) -> Counters:
+def mm(problem: Problem, op: int = OP_ADD, stream=None, allow_alias: bool = False,
+       kernel: int = 0) -> Counters:
     """out op= lhs * rhs on the GPU (asynchronous on `stream`; None = default).
 
     allow_alias=True lifts the reference's distinct-container rule (the TU
     Schur update on views of one parent); snapshot semantics: C_new = C_old op
-    A_old * B_old even when the views overlap."""
+    A_old * B_old even when the views overlap.  kernel = KERNEL_NAIVE /
+    KERNEL_DEFAULT applies that reference kernel's validation and Counters."""
     ctr = Counters()
     _check(lib().mhg_mm_ex(problem.a._c(), problem.b._c(), problem.c._c(), op,
-                           ALLOW_ALIAS if allow_alias else 0, C.byref(ctr), _stream_ptr(stream)))
+                           (ALLOW_ALIAS if allow_alias else 0) | kernel, C.byref(ctr),
+                           _stream_ptr(stream)))
     return ctr
 
 
@@ -419,6 +470,66 @@ def mm_oblivious(problem: Problem, stream=None) -> Counters:
     import torch
     torch.cuda.synchronize()
     return ctr
+
+
+def mm_naive(problem: Problem, stream=None) -> Counters:
+    """mm_naive (multiply.hpp:269-278): same result, its Counters; synchronous."""
+    ctr = mm(problem, OP_ADD, stream, kernel=KERNEL_NAIVE)
+    import torch
+    torch.cuda.synchronize()
+    return ctr
+
+
+def mm_default(problem: Problem, stream=None) -> Counters:
+    """mm_default (multiply.hpp:283-291): same result, its Counters; synchronous."""
+    ctr = mm(problem, OP_ADD, stream, kernel=KERNEL_DEFAULT)
+    import torch
+    torch.cuda.synchronize()
+    return ctr
+
+
+def counters_geometry(kernel: int, geo_out, geo_lhs, geo_rhs, rows, inner, cols) -> Counters:
+    """Counters of mm_oblivious (kernel 0), mm_naive (KERNEL_NAIVE) or mm_default
+    (KERNEL_DEFAULT) from raw geometry, geo_* = (n, t, flat origin) per container
+    (host only, no GPU needed)."""
+    ctr = Counters()
+    _check(lib().mhg_counters_geometry(kernel, *geo_out, *geo_lhs, *geo_rhs, rows, inner, cols,
+                                       C.byref(ctr)))
+    return ctr
+
+
+def verify(problem: Problem, old: Sub, op: int = OP_ADD, rounds: int = 2, seed: int = 0x5EED,
+           stream=None) -> bool:
+    """Freivalds check on the device that problem.a now holds old op b*c (mhg_verify);
+    `old` is a view (own container) of the output's cells before the multiply."""
+    ok = C.c_int()
+    _check(lib().mhg_verify(problem.a._c(), old._c(), problem.b._c(), problem.c._c(), op, rounds, seed,
+                            C.byref(ok), _stream_ptr(stream)))
+    return bool(ok.value)
+
+
+class Rng:
+    """mh::Rng (bench.hpp:44-52): mt19937_64(seed); below(k, count) returns the next
+    `count` draws of below(k) as uint32 (the gen_problem fill order, :101-103)."""
+
+    def __init__(self, seed: int):
+        self._h = C.c_void_p()
+        _check(lib().mhg_rng_create(seed, C.byref(self._h)))
+
+    def below(self, k: int, count: int = 1, out: Optional[np.ndarray] = None) -> np.ndarray:
+        a = np.empty(count, dtype=np.uint32) if out is None else out
+        if a.dtype != np.uint32 or not a.flags.c_contiguous or a.size != count:
+            raise InvalidArgument("Rng.below: out must be a contiguous uint32 array of count cells")
+        _check(lib().mhg_rng_below(self._h, k, a.ctypes.data, count))
+        return a
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().mhg_rng_destroy(self._h)
+                self._h = C.c_void_p()
+        except Exception:
+            pass
 
 
 def counters_oblivious(problem: Problem) -> Counters:

@@ -25,11 +25,7 @@ struct DigitParams {
     uint32_t q;
     uint32_t H;
     int negate;  // 1: encode (q - x) mod q (C -= A.B as C += (-A).B)
-    // two-class rhs (L = 2, GemmParams::two): besides the digits (b0, b1) of b, also
-    // those (c0, c1) of c = 256 b mod q, planes ordered [b0, c0, b1, c1]
-    int two;
-    uint32_t m32;  // floor(2^32 / q), for c
-    int udig;      // unsigned digits: x = sum_s d_s 256^s, d_s in [0, 255] (u8 x u8 MMA)
+    int udig;    // unsigned digits: x = sum_s d_s 256^s, d_s in [0, 255] (u8 x u8 MMA)
 };
 
 struct LimbParams {
@@ -73,21 +69,11 @@ struct GemmParams {
     uint32_t w16;                // 2^16 mod q
     int w16_small;               // w16 < 256: fold the top class without a mulmod
     int fold;                    // lean L = 2 fold level 3 / 2 / 1 (reductions per element; host)
-    int mc;                      // column-pair clusters with lhs multicast (Nt even; planner)
     int mode;                    // 0: out += prod, 2: out = prod (first chunk)
-    // two-class accumulation (CTA pair, L = 2): limb s multiplies the digits of
-    // 256^s b mod q, so S = lo + 256 hi has 2 classes (256 TMEM columns per job, two
-    // jobs double-buffered); rhs packed with 4 planes (DigitParams::two)
-    int two;
     int udig;                    // unsigned (u8) digits: non-negative class sums (DigitParams::udig)
     int vec_ok;                  // t % 4 == 0: 16-byte epilogue accesses allowed
     uint32_t group;              // raster: row tiles per group sharing rhs panels in L2
-    int serpentine;              // alternate the K direction per tile (L2 reuse across waves)
-    int l2_hints;                // evict_last for lhs stages, evict_first for rhs stages
-    int ring;                    // pipeline stages in use (0 = all); diagnostics
-    int early_release;           // alternate TMEM bases and release before the last class group
     uint32_t wait_hint;          // mbarrier try_wait suspend-time hint, ns (k_gemm roles)
-    uint32_t wait_roles;         // roles using the hint: 1 producer, 2 MMA issuer, 4 epilogue
     unsigned long long* stats;   // optional per-CTA wait-cycle counters (diagnostics), or null
 };
 
@@ -100,9 +86,10 @@ enum GemmStat { kStatTotal = 0, kStatMmaWaitFull, kStatMmaWaitTmem, kStatProdWai
 // All asynchronous on `stream`; return a cudaError_t value (0 = success).
 int launch_offsets(uint64_t* dst, uint64_t start, uint64_t count, TileGeom g, int is_row,
                    void* stream);
+// LDG/STG conversions; morton = 1 takes the Morton-order kernel where eligible.
 int launch_rm_to_mh(const uint32_t* rm, uint32_t* mh, uint64_t n, TileGeom g, uint32_t q,
-                    int* bad_flag, void* stream);
-int launch_mh_to_rm(const uint32_t* mh, uint32_t* rm, uint64_t n, TileGeom g, void* stream);
+                    int* bad_flag, int morton, void* stream);
+int launch_mh_to_rm(const uint32_t* mh, uint32_t* rm, uint64_t n, TileGeom g, int morton, void* stream);
 // K1 through the TMA: `tmap` is a CUtensorMap over the row-major buffer (uint32, n x n,
 // box t columns x R rows with R * t * 4 <= 16 KB; conv_tma_box_rows); power-of-two
 // 4 <= t <= 256.  to_mh = 1 also checks residues < q (*bad).
@@ -141,7 +128,7 @@ int configure_kernels();  // one-time kernel attributes (dynamic smem opt-in)
 // 128 rows for A, gemm2_b_box_rows(L) rows for B'); requires p.Mt even.
 int launch_gemm2(int L, const GemmParams& p, const void* tmA, const void* tmB, int num_sms,
                  void* stream);
-int gemm2_b_box_rows(int L, int two = 0);
+int gemm2_b_box_rows(int L);
 int launch_widen16(const uint16_t* src, uint32_t* dst, uint64_t count, int num_sms,
                     void* stream);
 // 16-bit upload wire (mhg_wire.cpp): true when uploads of this container size
@@ -156,5 +143,35 @@ int upload_wire16(uint32_t* cells, uint16_t** dev16, uint64_t total, uint64_t of
                   uint64_t* wire_bytes);
 int launch_fill_view(uint32_t* out, const uint64_t* rowoff, const uint64_t* coloff, uint64_t rows,
                      uint64_t cols, uint32_t value, void* stream);
+// Freivalds verification (mhg_verify): y = M x mod q over a view, a random vector, and
+// the comparison of C_new r with C_old r +/- A (B r) (mode 0 add, 1 sub, 2 set).
+int launch_matvec(const uint32_t* m, const uint64_t* rowoff, const uint64_t* coloff, uint64_t rows,
+                  uint64_t cols, const uint32_t* x, uint32_t* y, uint32_t q, int num_sms, void* stream);
+int launch_random_vec(uint32_t* r, uint64_t n, uint64_t seed, uint32_t q, void* stream);
+int launch_freivalds_cmp(const uint32_t* wn, const uint32_t* wo, const uint32_t* z, uint64_t rows, uint32_t q,
+                         int mode, int* bad, void* stream);
+
+}  // namespace mhg
+
+namespace mhg {
+
+// ------------------------------------------------------------------ options
+// Process-wide switches of the planner and test hooks (mhg_set_option, include/mhg.h).
+// Initial values come from the environment, read once (mhg_options.cpp); after that
+// only mhg_set_option changes them, so a stray variable cannot flip a kernel mid-run.
+enum OptionKey {
+    kOptDigits = 1,       // 1 = unsigned u8 limb digits, 0 = balanced s8
+    kOptGemmKernel = 2,   // 0 = planner, 1 = single CTA, 2 = CTA pair
+    kOptMinFold = 3,      // lowest lean-fold level the L = 2 epilogue may use (1..3)
+    kOptMaxKChunk = 4,    // cap on K slices per exact chunk (0 = planner's bound)
+    kOptUploadWire = 5,   // 0 = auto (by host workers), 16 = uint16 wire, 32 = 4-byte copies
+    kOptConvKernel = 6,   // 0 = TMA where eligible, 1 = Morton-order LDG/STG, 2 = row-order
+    kOptGemmStats = 7,    // 1 = per-launch wait-cycle report (synchronous diagnostics)
+    kOptUploadThreads = 8,  // host narrowing workers (0 = affinity / LOCAL_WORLD_SIZE)
+    kOptCount = 9
+};
+int64_t option(int key);
+bool option_valid(int key, int64_t value);
+void set_option(int key, int64_t value);
 
 }  // namespace mhg

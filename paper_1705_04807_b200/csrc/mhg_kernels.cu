@@ -363,17 +363,14 @@ __global__ void __launch_bounds__(256, MHG_PACK_MINB) k_pack_rows(const uint32_t
 // pack rows (one 16-byte load) x 4 K rows, transposed in registers.
 constexpr int kColsStride = 36;  // 32 K bytes + 4 pad
 
-// P = L planes, or P = 2L for the two-class rhs (L = 2): planes [b0, c0, b1, c1] with
-// c = 256 b mod q, so CTA r of a pair fetches its planes {b_r, c_r} as one box.
-template <int L, int P = L>
+template <int L>
 __device__ __forceinline__ void pack_cols_block(uint32_t bid, const uint32_t* __restrict__ src,
                                                 const uint64_t* __restrict__ rowoff,
                                                 const uint64_t* __restrict__ coloff, int vecok,
                                                 uint64_t R, uint64_t K, uint32_t rpt, uint32_t Kt,
                                                 uint64_t Rpad, int8_t* __restrict__ dst,
                                                 const DigitParams& dp, uint8_t* smem) {
-    static_assert(P == L || (L == 2 && P == 4), "plane layout");
-    auto& sd = *reinterpret_cast<uint8_t(*)[P][128][kColsStride]>(smem);
+    auto& sd = *reinterpret_cast<uint8_t(*)[L][128][kColsStride]>(smem);
     const uint32_t nkq = Kt * (kBK / 32);         // 32-wide K slices
     const uint32_t kq = bid % nkq;
     const uint64_t pr0 = (uint64_t)(bid / nkq) * 128;
@@ -393,69 +390,47 @@ __device__ __forceinline__ void pack_cols_block(uint32_t bid, const uint32_t* __
         const uint32_t col[4] = {v[0][c], v[1][c], v[2][c], v[3][c]};
         uint32_t w[L];
         digits4<L>(col, dp, w);
-        if constexpr (P == L) {
 #pragma unroll
-            for (int s = 0; s < L; ++s)
-                *reinterpret_cast<uint32_t*>(&sd[s][4 * tx + c][4 * ty]) = w[s];
-        } else {
-            // c = 256 b mod q (b < q <= 2^16: 256 b < 2^24, one Barrett step)
-            uint32_t cv[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                const uint32_t b = dp.negate ? (col[e] ? dp.q - col[e] : 0u) : col[e];
-                const uint32_t u = b << 8;
-                const uint32_t r = u - __umulhi(u, dp.m32) * dp.q;
-                cv[e] = r >= dp.q ? r - dp.q : r;
-            }
-            DigitParams dc = dp;
-            dc.negate = 0;
-            uint32_t wc[L];
-            digits4<L>(cv, dc, wc);
-#pragma unroll
-            for (int s = 0; s < L; ++s) {
-                *reinterpret_cast<uint32_t*>(&sd[2 * s][4 * tx + c][4 * ty]) = w[s];
-                *reinterpret_cast<uint32_t*>(&sd[2 * s + 1][4 * tx + c][4 * ty]) = wc[s];
-            }
-        }
+        for (int s = 0; s < L; ++s) *reinterpret_cast<uint32_t*>(&sd[s][4 * tx + c][4 * ty]) = w[s];
     }
     __syncthreads();
 #pragma unroll
-    for (int e = 0; e < P; ++e) {
-        const int cid = threadIdx.x + 256 * e;  // P x 128 rows x 2 chunks
+    for (int e = 0; e < L; ++e) {
+        const int cid = threadIdx.x + 256 * e;  // L x 128 rows x 2 chunks
         const int s = cid >> 8, r = (cid >> 1) & 127, h = cid & 1;
         const uint64_t pr = pr0 + r;
         if (pr >= Rpad) continue;
         const uint32_t* w = reinterpret_cast<const uint32_t*>(&sd[s][r][16 * h]);
-        *reinterpret_cast<uint4*>(pack_dst<P>(dst, pr, k0 + 16 * h, s, rpt, Kt)) =
+        *reinterpret_cast<uint4*>(pack_dst<L>(dst, pr, k0 + 16 * h, s, rpt, Kt)) =
             make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
-template <int L, int P = L>
+template <int L>
 __global__ void __launch_bounds__(256, MHG_PACK_MINB) k_pack_cols(const uint32_t* __restrict__ src,
                                                    const uint64_t* __restrict__ rowoff,
                                                    const uint64_t* __restrict__ coloff, int vecok,
                                                    uint64_t R, uint64_t K, uint32_t rpt, uint32_t Kt,
                                                    uint64_t Rpad, int8_t* __restrict__ dst,
                                                    DigitParams dp) {
-    __shared__ __align__(16) uint8_t sd[P * 128 * kColsStride];
-    pack_cols_block<L, P>(blockIdx.x, src, rowoff, coloff, vecok, R, K, rpt, Kt, Rpad, dst, dp, sd);
+    __shared__ __align__(16) uint8_t sd[L * 128 * kColsStride];
+    pack_cols_block<L>(blockIdx.x, src, rowoff, coloff, vecok, R, K, rpt, Kt, Rpad, dst, dp, sd);
 }
 
 // Both operands of a multiply in ONE launch: blocks [0, nrows) pack the lhs (rows
 // kernel body), the rest the rhs (cols body).  Two HBM-bound grids of ~2 waves
 // each otherwise pay two ramp-down tails (the second graph branch started ~9 us
 // late at cfg3, profiles/r01_pack_fused.txt).
-template <int L, int P = L>
+template <int L>
 __global__ void __launch_bounds__(256, MHG_PACK_MINB) k_pack_pair(PackArgs a, PackArgs b,
                                                                   uint32_t nrows) {
-    constexpr int ROWS_SMEM = L * 32 * kRowsStride, COLS_SMEM = P * 128 * kColsStride;
+    constexpr int ROWS_SMEM = L * 32 * kRowsStride, COLS_SMEM = L * 128 * kColsStride;
     __shared__ __align__(16) uint8_t sd[ROWS_SMEM > COLS_SMEM ? ROWS_SMEM : COLS_SMEM];
     if (blockIdx.x < nrows)
         pack_rows_block<L>(blockIdx.x, a.src, a.rowoff, a.coloff, a.vecok, a.R, a.K, a.rpt, a.Kt,
                            a.Rpad, a.dst, a.dp, sd);
     else
-        pack_cols_block<L, P>(blockIdx.x - nrows, b.src, b.rowoff, b.coloff, b.vecok, b.R, b.K, b.rpt,
+        pack_cols_block<L>(blockIdx.x - nrows, b.src, b.rowoff, b.coloff, b.vecok, b.R, b.K, b.rpt,
                               b.Kt, b.Rpad, b.dst, b.dp, sd);
 }
 
@@ -560,17 +535,6 @@ __device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32
         : "memory");
 }
 
-// One bulk copy delivered to the same smem offset of every CTA in ctaMask,
-// each completing tx bytes on its own barrier at bar's offset (cluster multicast).
-__device__ __forceinline__ void bulk_g2s_mc_hint(void* dst, const void* src, uint32_t bytes,
-                                                 uint64_t* bar, uint16_t mask, uint64_t policy) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
-        ".L2::cache_hint [%0], [%1], %2, [%3], %4, %5;" ::"r"(smem_u32(dst)),
-        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(mask), "l"(policy)
-        : "memory");
-}
-
 __device__ __forceinline__ uint64_t l2_policy_evict_last() {
     uint64_t pol;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
@@ -594,15 +558,6 @@ __device__ __forceinline__ void tc_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
                      smem_u32(bar))
                  : "memory");
-}
-
-// MMA completion signalled on the barrier at bar's offset in every CTA of mask
-__device__ __forceinline__ void tc_commit_mc(uint64_t* bar, uint16_t mask) {
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-        " [%0], %1;" ::"r"(smem_u32(bar)),
-        "h"(mask)
-        : "memory");
 }
 
 // D[tmem] (+)= A[smem] * B[smem]^T, int8 x int8 -> int32
@@ -731,7 +686,7 @@ __device__ __forceinline__ uint32_t fold_classes(const int32_t (&acc)[2 * L - 1]
 // 2^16 mod q < 256; wider primes keep the fused single-phase drain.
 template <int L>
 __device__ __forceinline__ bool early_release(const GemmParams& p) {
-    return p.early_release && (L == 1 || (L == 2 && p.w16_small));
+    return L == 1 || (L == 2 && p.w16_small);
 }
 
 // Partial fold over the weight classes [C0, C1): sum_c acc[c - C0] 256^c mod q
@@ -784,15 +739,8 @@ struct GemmCfg {
     // C path with a 4 KB per-warp transpose buffer, the narrow-tile primes keep
     // row-per-thread C access (see epilogue_role)
     static constexpr bool XPOSE = (W == 128);
-#ifndef MHG_SMR
-#define MHG_SMR 0
-#endif
-    // SMR (setmaxnreg layout, W = 128): warpgroup 0 = producer, MMA issuer, 2 idle warps,
-    // shrunk to 40 registers; warpgroups 1-4 = 16 epilogue warps x 32 columns, grown to 104
-    // (the CTA keeps its launch allocation, 640 x 96: 128 x 40 + 512 x 104 <= 61440)
-    static constexpr bool SMR = XPOSE && MHG_SMR;
-    static constexpr int EPI_WARPS = SMR ? 16 : 8;
-    static constexpr int EPI_W0 = SMR ? 4 : 2;  // first epilogue warp
+    static constexpr int EPI_WARPS = 8;
+    static constexpr int EPI_W0 = 2;  // first epilogue warp
     static constexpr int XBUF = XPOSE ? EPI_WARPS * (W * 4 / EPI_WARPS >= 64 ? 4096 : 2048) : 0;
     static constexpr int FIXED = 1024 /*align slack*/ + 256 /*barriers*/ + 8 * W /*column offsets*/ + XBUF;
     static constexpr int STAGES_RAW = (232448 - FIXED) / STAGE;
@@ -900,6 +848,9 @@ __device__ __forceinline__ void tmem_wait_st() {
 // (residue check by all threads) -> 1D bulk store; to_mh = 0: 1D bulk load ->
 // smem -> 2D tensor store.  No data passes through registers except the check.
 constexpr int kConvUnitBytes = 16384;
+// 4 units in flight per CTA x 3 CTAs per SM (more independent issuers measured faster
+// than fewer, deeper CTAs: profiles/r01_conversion_tma.txt)
+constexpr int kConvUnits = 4, kConvCtasPerSm = 3;
 
 __device__ __forceinline__ void tma2d_load(uint32_t dst, const CUtensorMap* tm, int c0, int c1,
                                            uint64_t* bar) {
@@ -1021,8 +972,7 @@ __global__ void __launch_bounds__(128) k_conv_tma(const __grid_constant__ CUtens
 // geometry (no table loads).  Otherwise (narrow tiles, CTA pair) the row's
 // C_old is prefetched into registers at tile start, addressed through smem
 // column offsets.
-template <int L, int W, int EPI_WARPS, bool PAIR, bool XPOSE = false, int FOLD = 3, bool NPAIR = false,
-          int EPI_W0 = 2, bool TWO = false>
+template <int L, int W, int EPI_WARPS, bool PAIR, bool XPOSE = false, int FOLD = 3>
 __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t first_tile,
                                               uint32_t tile_stride, uint32_t num_tiles,
                                               uint32_t row_groups, uint32_t rank, uint32_t nchunks,
@@ -1034,6 +984,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     constexpr int CLASSES = 2 * L - 1;
     constexpr int CW = L <= 2 ? 16 : 8;  // TMEM columns per drain step (x8 / x32 measured slower)
     constexpr uint64_t kNoCol = ~uint64_t(0);
+    constexpr int EPI_W0 = 2;  // warps 0, 1: producer, MMA issuer
     const int ew = warp - EPI_W0;
     const int quad = warp & 3;
     const int jb = (ew >> 2) * WH;  // first tile column of this warp
@@ -1041,7 +992,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
     const uint32_t release_bar =
         PAIR ? mapa_shared(smem_u32(tmem_empty), 0) : smem_u32(tmem_empty);
-    uint32_t acc_ph = 0, job2 = 0;
+    uint32_t acc_ph = 0;
     long long epi_wait = 0, epi_busy = 0, epi_ldw = 0;
     // hand the accumulator columns back to the MMA issuer (one arrive per warp)
     auto release = [&]() {
@@ -1208,8 +1159,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         const bool live = tile < num_tiles && p.mode != 2;
         uint32_t lm = 0, ln = 0;
         if (live) {
-            tile_coords(tile, row_groups, NPAIR ? p.Nt / 2 : p.Nt, p.group, lm, ln);
-            if (NPAIR) ln = 2 * ln + rank;
+            tile_coords(tile, row_groups, p.Nt, p.group, lm, ln);
             if (PAIR) lm = 2 * lm + rank;  // this CTA's 128-row half of the pair tile
         }
         const uint64_t own = row_at(lm, row);
@@ -1238,8 +1188,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride) {
         const long long tp0 = clock64();
         uint32_t tm, n;
-        tile_coords(tile, row_groups, NPAIR ? p.Nt / 2 : p.Nt, p.group, tm, n);
-        if (NPAIR) n = 2 * n + rank;  // column-pair clusters: rank picks the column tile
+        tile_coords(tile, row_groups, p.Nt, p.group, tm, n);
         const uint32_t m = PAIR ? 2 * tm + rank : tm;
         uint32_t cur[WH];
         uint64_t rbase = 0;
@@ -1318,51 +1267,10 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         epi_pro += clock64() - tp0;
         for (uint32_t c = 0; c < nchunks; ++c) {
             const long long w0 = clock64();
-            if constexpr (TWO) {
-                // two accumulators in TMEM: job j uses buffer j % 2, its (j / 2)-th use
-                mbar_wait_hint(tmem_full + (job2 & 1), (job2 >> 1) & 1,
-                               (p.wait_roles & 4) ? p.wait_hint : 0u);
-            } else {
-                mbar_wait_hint(tmem_full, acc_ph, (p.wait_roles & 4) ? p.wait_hint : 0u);
-            }
+            mbar_wait_hint(tmem_full, acc_ph, p.wait_hint);
             const long long w1 = clock64();
             epi_wait += w1 - w0;
             tc_fence_after();
-            if constexpr (TWO) {
-                // S = lo + 256 hi (limb s multiplied the digits of 256^s b mod q).  Lean
-                // fold (2^16 mod q < 256; the planner bounds K so that |t| <= 2^31 - 2^17):
-                // 256 hi = 256 (hi & 255) + 2^16 (hi >> 8) == 256 (hi & 255) + w16 (hi >> 8).
-                const uint32_t buf = job2 & 1;
-                const uint32_t tb = tmem + lane_base + buf * (uint32_t)(2 * W) + jb;
-#pragma unroll
-                for (int j0 = 0; j0 < WH; j0 += CW) {
-                    const bool live = (uint64_t)n * W + jb + j0 < p.cols;  // warp-uniform
-                    int32_t lo[CW], hi[CW];
-                    tmem_ld<CW>(tb + j0, lo);
-                    tmem_ld<CW>(tb + W + j0, hi);
-                    tmem_wait_ld();
-                    if (live) {
-#pragma unroll
-                        for (int j = 0; j < CW; ++j) {
-                            if (p.w16_small) {
-                                const int32_t t = lo[j] + ((hi[j] & 255) << 8) + (int32_t)p.w16 * (hi[j] >> 8);
-                                cur[j0 + j] = red32((uint32_t)t + cur[j0 + j] + p.bias32, p);
-                            } else {
-                                const uint32_t r = red32((uint32_t)lo[j] + p.bias32, p);
-                                const uint32_t h = red32((uint32_t)hi[j] + p.bias32, p);
-                                const uint32_t x = red32(r + (h << 8), p) + cur[j0 + j];
-                                cur[j0 + j] = x >= p.q ? x - p.q : x;
-                            }
-                        }
-                    }
-                }
-                tc_fence_before();
-                __syncwarp();
-                if (lane == 0) mbar_arrive_remote(mapa_shared(smem_u32(tmem_empty + buf), 0));
-                epi_busy += clock64() - w1;
-                ++job2;
-                continue;
-            }
             if constexpr (PAIR) {
 #pragma unroll
                 for (int j0 = 0; j0 < WH; j0 += CW) {
@@ -1474,13 +1382,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     }
 }
 
-// MC (column-pair clusters, launched with cluster dim 2): the two CTAs of a
-// cluster take column tiles 2nn and 2nn+1 of the same row tile in lock step;
-// each loads half of every lhs stage and multicasts it to both, so per-SM lhs
-// traffic from L2 halves (operand bytes per k-slice 64 KB -> 48 KB at L=2).  A
-// stage is refilled only after both CTAs' MMAs released it (empty barriers
-// count two arrivals; the MMA commit is multicast).
-template <int L, int FOLD = 3, bool MC = false>
+template <int L, int FOLD = 3>
 __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParams p) {
     using Cfg = GemmCfg<L>;
     constexpr int W = Cfg::W;
@@ -1499,14 +1401,10 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
     uint8_t* xbuf = reinterpret_cast<uint8_t*>(s_col + W);  // per-warp C transpose buffers
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    // MC: tiles are (row tile, column-tile pair); this CTA takes column 2nn + rank
-    const uint32_t rank = MC ? cluster_rank() : 0u;
-    const uint32_t npairs = MC ? p.Nt / 2 : p.Nt;
-    const uint32_t num_tiles = p.Mt * npairs;
-    const uint32_t first_tile = MC ? blockIdx.x / 2 : blockIdx.x;
-    const uint32_t tile_stride = MC ? gridDim.x / 2 : gridDim.x;
+    const uint32_t num_tiles = p.Mt * p.Nt;
+    const uint32_t first_tile = blockIdx.x;
+    const uint32_t tile_stride = gridDim.x;
     const uint32_t nchunks = (p.Kt + p.KC - 1) / p.KC;
-    const int ring = (p.ring > 0 && p.ring < STAGES) ? p.ring : STAGES;  // tuning hook
 
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
@@ -1516,7 +1414,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
     } else if (warp == 1 && lane == 0) {
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], MC ? 2 : 1);
+            mbar_init(&empty[s], 1);
         }
         mbar_init(tmem_full, 1);
         mbar_init(tmem_empty, Cfg::EPI_WARPS);  // one arrive per epilogue warp
@@ -1525,147 +1423,120 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
     }
     tc_fence_before();
     __syncthreads();
-    if constexpr (MC) cluster_sync_all();  // peers' barriers initialised before any multicast
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
 
-    // roles.  SMR: warpgroup 0 (producer, MMA issuer, 2 idle warps) executes one
-    // setmaxnreg.dec and the epilogue warpgroups one setmaxnreg.inc, each dominating its
-    // role's code so ptxas allocates that region to the new budget.
-    if (warp < Cfg::EPI_W0) {
-        if constexpr (Cfg::SMR) asm volatile("setmaxnreg.dec.sync.aligned.u32 40;\n" ::: "memory");
-        if (warp == 0) {
-            // ---------------- producer: one bulk copy per operand per stage
-            if (lane == 0) {
-                int st = 0;
-                uint32_t ph = 0;
-                long long wait_empty = 0;
-                uint32_t ord = 0;
-                const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
-                for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride, ++ord) {
-                    uint32_t m, n;
-                    tile_coords(tile, p.Mt, npairs, p.group, m, n);
-                    if (MC) n = 2 * n + rank;
-                    const int8_t* a_src = p.apack + (uint64_t)m * p.Kt * Cfg::A_STAGE;
-                    const int8_t* b_src = p.bpack + (uint64_t)n * p.Kt * Cfg::B_STAGE;
-                    // serpentine K: odd tiles of a CTA sweep K backwards, so the next wave
-                    // starts on the panel slices the previous wave just left in L2
-                    const bool rev = p.serpentine && (ord & 1);
-                    for (uint32_t j = 0; j < p.Kt; ++j) {
-                        const uint32_t kt = rev ? p.Kt - 1 - j : j;
-                        const long long w0 = clock64();
-                        mbar_wait_hint(&empty[st], ph ^ 1, (p.wait_roles & 1) ? p.wait_hint : 0u);
-                        wait_empty += clock64() - w0;
-                        mbar_expect_tx(&full[st], Cfg::STAGE);
-                        if constexpr (MC) {
-                            // this CTA's half of the lhs stage, to both CTAs (same offset)
-                            constexpr uint32_t HALF = Cfg::A_STAGE / 2;
-                            bulk_g2s_mc_hint(sA + st * Cfg::A_STAGE + rank * HALF,
-                                             a_src + (uint64_t)kt * Cfg::A_STAGE + rank * HALF, HALF,
-                                             &full[st], (uint16_t)0x3, pol_keep);
-                            bulk_g2s_hint(sB + st * Cfg::B_STAGE, b_src + (uint64_t)kt * Cfg::B_STAGE,
-                                          Cfg::B_STAGE, &full[st], pol_stream);
-                        } else if (p.l2_hints) {
-                            // lhs panels of the raster group are re-read by the next waves;
-                            // rhs panels only by the current one
-                            bulk_g2s_hint(sA + st * Cfg::A_STAGE, a_src + (uint64_t)kt * Cfg::A_STAGE,
-                                          Cfg::A_STAGE, &full[st], pol_keep);
-                            bulk_g2s_hint(sB + st * Cfg::B_STAGE, b_src + (uint64_t)kt * Cfg::B_STAGE,
-                                          Cfg::B_STAGE, &full[st], pol_stream);
-                        } else {
-                            bulk_g2s(sA + st * Cfg::A_STAGE, a_src + (uint64_t)kt * Cfg::A_STAGE,
-                                     Cfg::A_STAGE, &full[st]);
-                            bulk_g2s(sB + st * Cfg::B_STAGE, b_src + (uint64_t)kt * Cfg::B_STAGE,
-                                     Cfg::B_STAGE, &full[st]);
+    if (warp == 0) {
+        // ---------------- producer: one bulk copy per operand per stage
+        if (lane == 0) {
+            int st = 0;
+            uint32_t ph = 0;
+            long long wait_empty = 0;
+            uint32_t ord = 0;
+            // lhs panels of the raster group are re-read by the next waves (evict_last),
+            // rhs panels only by the current one (evict_first): -1.3% at n = 16384
+            const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
+            for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride, ++ord) {
+                uint32_t m, n;
+                tile_coords(tile, p.Mt, p.Nt, p.group, m, n);
+                const int8_t* a_src = p.apack + (uint64_t)m * p.Kt * Cfg::A_STAGE;
+                const int8_t* b_src = p.bpack + (uint64_t)n * p.Kt * Cfg::B_STAGE;
+                // serpentine K: odd tiles of a CTA sweep K backwards, so the next wave
+                // starts on the panel slices the previous wave just left in L2
+                const bool rev = ord & 1;
+                for (uint32_t j = 0; j < p.Kt; ++j) {
+                    const uint32_t kt = rev ? p.Kt - 1 - j : j;
+                    const long long w0 = clock64();
+                    mbar_wait_hint(&empty[st], ph ^ 1, p.wait_hint);
+                    wait_empty += clock64() - w0;
+                    mbar_expect_tx(&full[st], Cfg::STAGE);
+                    bulk_g2s_hint(sA + st * Cfg::A_STAGE, a_src + (uint64_t)kt * Cfg::A_STAGE,
+                                  Cfg::A_STAGE, &full[st], pol_keep);
+                    bulk_g2s_hint(sB + st * Cfg::B_STAGE, b_src + (uint64_t)kt * Cfg::B_STAGE,
+                                  Cfg::B_STAGE, &full[st], pol_stream);
+                    if (++st == STAGES) {
+                        st = 0;
+                        ph ^= 1;
+                    }
+                }
+            }
+            if (p.stats) p.stats[(uint64_t)blockIdx.x * kStatCount + kStatProdWaitEmpty] = wait_empty;
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer (single thread)
+        if (lane == 0) {
+            const uint32_t um = p.udig ? ~idesc_sign_mask() : ~0u;
+            const uint32_t id_full = idesc_i8(kBM, Cfg::NB) & um;
+            const uint32_t id_head = idesc_i8(kBM, (L > 1 ? L - 1 : 1) * W) & um;
+            const uint32_t id_one = idesc_i8(kBM, W) & um;
+            const bool alt_layout = early_release<L>(p);
+            int st = 0;
+            uint32_t ph = 0, acc_ph = 0;
+            long long wait_full = 0, wait_tmem = 0;
+            const long long t_begin = clock64();
+            for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride) {
+                for (uint32_t c = 0; c < nchunks; ++c) {
+                    const uint32_t kb = c * p.KC;
+                    const uint32_t ke = (kb + p.KC < p.Kt) ? kb + p.KC : p.Kt;
+                    long long w0 = clock64();
+                    mbar_wait_hint(tmem_empty, acc_ph ^ 1, p.wait_hint);
+                    wait_tmem += clock64() - w0;
+                    tc_fence_after();
+                    for (uint32_t kt = kb; kt < ke; ++kt) {
+                        w0 = clock64();
+                        mbar_wait_hint(&full[st], ph, p.wait_hint);
+                        wait_full += clock64() - w0;
+                        tc_fence_after();
+                        const uint32_t a0 = smem_u32(sA + st * Cfg::A_STAGE);
+                        const uint32_t b0 = smem_u32(sB + st * Cfg::B_STAGE);
+#pragma unroll
+                        for (int kk = 0; kk < kBK / 32; ++kk) {
+                            const bool first = (kt == kb) && (kk == 0);
+                            const uint64_t bd = sdesc(b0 + kk * 32);
+#pragma unroll
+                            for (int s = 0; s < L; ++s) {
+                                const uint64_t ad = sdesc(a0 + s * kBM * kBK + kk * 32);
+                                // accumulation jobs alternate TMEM bases 0 / W where the
+                                // epilogue uses the early release (see epilogue_role)
+                                const uint32_t d = tmem + ((alt_layout && acc_ph) ? W : 0) + s * W;
+                                if (!first) {
+                                    mma_i8(d, ad, bd, id_full, 1u);
+                                } else if (s == 0) {
+                                    mma_i8(d, ad, bd, id_full, 0u);
+                                } else {
+                                    // classes s..s+L-2 already hold a product; class
+                                    // s+L-1 is touched for the first time
+                                    mma_i8(d, ad, bd, id_head, 1u);
+                                    mma_i8(d + (L - 1) * W, ad,
+                                           sdesc(b0 + (L - 1) * W * kBK + kk * 32), id_one, 0u);
+                                }
+                            }
                         }
-                        if (++st == ring) {
+                        tc_commit(&empty[st]);
+                        if (++st == STAGES) {
                             st = 0;
                             ph ^= 1;
                         }
                     }
+                    tc_commit(tmem_full);
+                    acc_ph ^= 1;
                 }
-                if (p.stats) p.stats[(uint64_t)blockIdx.x * kStatCount + kStatProdWaitEmpty] = wait_empty;
             }
-        } else if (warp == 1) {
-            // ---------------- MMA issuer (single thread)
-            if (lane == 0) {
-                const uint32_t um = p.udig ? ~idesc_sign_mask() : ~0u;
-                const uint32_t id_full = idesc_i8(kBM, Cfg::NB) & um;
-                const uint32_t id_head = idesc_i8(kBM, (L > 1 ? L - 1 : 1) * W) & um;
-                const uint32_t id_one = idesc_i8(kBM, W) & um;
-                const bool alt_layout = early_release<L>(p);
-                int st = 0;
-                uint32_t ph = 0, acc_ph = 0;
-                long long wait_full = 0, wait_tmem = 0;
-                const long long t_begin = clock64();
-                for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride) {
-                    for (uint32_t c = 0; c < nchunks; ++c) {
-                        const uint32_t kb = c * p.KC;
-                        const uint32_t ke = (kb + p.KC < p.Kt) ? kb + p.KC : p.Kt;
-                        long long w0 = clock64();
-                        mbar_wait_hint(tmem_empty, acc_ph ^ 1, (p.wait_roles & 2) ? p.wait_hint : 0u);
-                        wait_tmem += clock64() - w0;
-                        tc_fence_after();
-                        for (uint32_t kt = kb; kt < ke; ++kt) {
-                            w0 = clock64();
-                            mbar_wait_hint(&full[st], ph, (p.wait_roles & 2) ? p.wait_hint : 0u);
-                            wait_full += clock64() - w0;
-                            tc_fence_after();
-                            const uint32_t a0 = smem_u32(sA + st * Cfg::A_STAGE);
-                            const uint32_t b0 = smem_u32(sB + st * Cfg::B_STAGE);
-    #pragma unroll
-                            for (int kk = 0; kk < kBK / 32; ++kk) {
-                                const bool first = (kt == kb) && (kk == 0);
-                                const uint64_t bd = sdesc(b0 + kk * 32);
-    #pragma unroll
-                                for (int s = 0; s < L; ++s) {
-                                    const uint64_t ad = sdesc(a0 + s * kBM * kBK + kk * 32);
-                                    // accumulation jobs alternate TMEM bases 0 / W where the
-                                    // epilogue uses the early release (see epilogue_role)
-                                    const uint32_t d = tmem + ((alt_layout && acc_ph) ? W : 0) + s * W;
-                                    if (!first) {
-                                        mma_i8(d, ad, bd, id_full, 1u);
-                                    } else if (s == 0) {
-                                        mma_i8(d, ad, bd, id_full, 0u);
-                                    } else {
-                                        // classes s..s+L-2 already hold a product; class
-                                        // s+L-1 is touched for the first time
-                                        mma_i8(d, ad, bd, id_head, 1u);
-                                        mma_i8(d + (L - 1) * W, ad,
-                                               sdesc(b0 + (L - 1) * W * kBK + kk * 32), id_one, 0u);
-                                    }
-                                }
-                            }
-                            if constexpr (MC) tc_commit_mc(&empty[st], (uint16_t)0x3);
-                            else tc_commit(&empty[st]);
-                            if (++st == ring) {
-                                st = 0;
-                                ph ^= 1;
-                            }
-                        }
-                        tc_commit(tmem_full);
-                        acc_ph ^= 1;
-                    }
-                }
-                if (p.stats) {
-                    unsigned long long* o = p.stats + (uint64_t)blockIdx.x * kStatCount;
-                    o[kStatTotal] = clock64() - t_begin;
-                    o[kStatMmaWaitFull] = wait_full;
-                    o[kStatMmaWaitTmem] = wait_tmem;
-                }
+            if (p.stats) {
+                unsigned long long* o = p.stats + (uint64_t)blockIdx.x * kStatCount;
+                o[kStatTotal] = clock64() - t_begin;
+                o[kStatMmaWaitFull] = wait_full;
+                o[kStatMmaWaitTmem] = wait_tmem;
             }
         }
     } else {
-        if constexpr (Cfg::SMR) asm volatile("setmaxnreg.inc.sync.aligned.u32 104;\n" ::: "memory");
-        epilogue_role<L, W, Cfg::EPI_WARPS, false, Cfg::XPOSE, FOLD, MC, Cfg::EPI_W0>(
-            p, first_tile, tile_stride, num_tiles, p.Mt, rank, nchunks, tmem, s_col, tmem_full,
+        epilogue_role<L, W, Cfg::EPI_WARPS, false, Cfg::XPOSE, FOLD>(
+            p, first_tile, tile_stride, num_tiles, p.Mt, 0u, nchunks, tmem, s_col, tmem_full,
             tmem_empty, warp, lane, xbuf);
     }
 
     __syncthreads();
-    // MC: the peer may still multicast into this CTA's smem / arrive on its barriers
-    if constexpr (MC) cluster_sync_all();
     if (warp == 0) {
         tc_fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
@@ -1688,26 +1559,21 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
 //   - the upper weight classes [L, 2L-1) are zeroed by the epilogue right
 //     after it drains them, so every MMA but the first of a chunk accumulates.
 // =====================================================================
-template <int L, bool TWO = false>
+template <int L>
 struct Gemm2Cfg {
-    static_assert(!TWO || L == 2, "two-class accumulation is the L = 2 layout");
     static constexpr int W = (L <= 2) ? 128 : 64;
-    static constexpr int NB = TWO ? 2 * W : L * W;       // UMMA N of one limb MMA
-    static constexpr int NBR = TWO ? 2 * L * W : L * W;  // B' rows per (column tile, k tile)
-    static constexpr int NBH = NBR / 2;                  // B' rows per CTA
-    static constexpr int CLASSES = TWO ? 2 : 2 * L - 1;
-    static constexpr int NBUF = TWO ? 2 : 1;             // accumulation jobs in TMEM
+    static constexpr int NB = L * W;      // UMMA N of one limb MMA (stacked B')
+    static constexpr int NBR = L * W;     // B' rows per (column tile, k tile)
+    static constexpr int NBH = NBR / 2;   // B' rows per CTA
+    static constexpr int CLASSES = 2 * L - 1;
     static constexpr int A_STAGE = L * kBM * kBK;
     static constexpr int B_STAGE = NBH * kBK;
     static constexpr int STAGE = A_STAGE + B_STAGE;
-    // TWO: the coalesced (transpose-buffer) epilogue, 4 KB per epilogue warp (for the
-    // 3- and 4-limb pairs it measured within 1% of the row-per-thread path, A/B in
-    // profiles/r01_pair_wide_primes.txt, so they keep the latter)
-    static constexpr bool XPOSE = TWO;
-    static constexpr int XBUF = XPOSE ? 8 * 4096 : 0;
-    static constexpr int STAGES_RAW = (220 * 1024 - XBUF) / STAGE;
+    // row-per-thread C access (the coalesced transpose-buffer epilogue measured within
+    // 1% for the 3- and 4-limb pairs, profiles/r01_pair_wide_primes.txt)
+    static constexpr int STAGES_RAW = (220 * 1024) / STAGE;
     static constexpr int STAGES = STAGES_RAW > 8 ? 8 : STAGES_RAW;
-    static constexpr int SMEM = 1024 + STAGES * STAGE + 512 + 8 * W + XBUF;
+    static constexpr int SMEM = 1024 + STAGES * STAGE + 512 + 8 * W;
     static_assert(SMEM <= 232448, "227 KB dynamic shared memory limit");
     static constexpr int EPI_WARPS = 8;
     static constexpr int EPI_THREADS = EPI_WARPS * 32;
@@ -1718,12 +1584,11 @@ struct Gemm2Cfg {
     static_assert(NBH % 16 == 0 || NBH == 64, "B' half rows");
 };
 
-template <int L, bool TWO = false>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L, TWO>::THREADS, 1)
+template <int L>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS, 1)
     k_gemm2(const __grid_constant__ GemmParams p, const __grid_constant__ CUtensorMap tmA,
             const __grid_constant__ CUtensorMap tmB) {
-    using Cfg = Gemm2Cfg<L, TWO>;
-    constexpr int NBUF = Cfg::NBUF;
+    using Cfg = Gemm2Cfg<L>;
     constexpr int W = Cfg::W;
     constexpr int WH = Cfg::WH;
     constexpr int STAGES = Cfg::STAGES;
@@ -1734,10 +1599,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L, TWO>::TH
     uint8_t* sB = smem + STAGES * Cfg::A_STAGE;
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * Cfg::STAGE);
     uint64_t* empty = full + STAGES;
-    uint64_t* tmem_full = empty + STAGES;        // [NBUF]
-    uint64_t* tmem_empty = tmem_full + NBUF;     // [NBUF]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + NBUF);
-    uint64_t* s_col = tmem_empty + NBUF + 1;
+    uint64_t* tmem_full = empty + STAGES;
+    uint64_t* tmem_empty = tmem_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_empty + 1);
+    uint64_t* s_col = tmem_empty + 2;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = cluster_rank();
@@ -1756,17 +1621,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L, TWO>::TH
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
-        for (int b = 0; b < NBUF; ++b) {
-            mbar_init(tmem_full + b, 1);
-            mbar_init(tmem_empty + b, 2 * Cfg::EPI_WARPS);
-        }
+        mbar_init(tmem_full, 1);
+        mbar_init(tmem_empty, 2 * Cfg::EPI_WARPS);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    if (!TWO && warp >= 2) {
+    if (warp >= 2) {
         // zero the upper weight classes once; afterwards the epilogue re-zeroes
         // them as it drains them
         const int ew = warp - 2, quad = warp & 3, jb = (ew >> 2) * WH;
@@ -1791,7 +1654,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L, TWO>::TH
                 uint32_t pm, n;
                 tile_coords(tile, Mt2, p.Nt, p.group, pm, n);
                 const uint32_t m = 2 * pm + rank;
-                const bool rev = p.serpentine && (ord & 1);
+                const bool rev = ord & 1;
                 for (uint32_t j = 0; j < p.Kt; ++j) {
                     const uint32_t kt = rev ? p.Kt - 1 - j : j;
                     const long long w0 = clock64();
@@ -1825,13 +1688,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L, TWO>::TH
                 for (uint32_t c = 0; c < nchunks; ++c, ++job) {
                     const uint32_t kb = c * p.KC;
                     const uint32_t ke = (kb + p.KC < p.Kt) ? kb + p.KC : p.Kt;
-                    // TWO: jobs alternate the two 256-column accumulators
-                    const uint32_t buf = job % NBUF, use = job / NBUF;
                     long long w0 = clock64();
-                    mbar_wait(tmem_empty + buf, (use & 1) ^ 1);
+                    mbar_wait(tmem_empty, (job & 1) ^ 1);
                     wait_tmem += clock64() - w0;
                     tc_fence_after();
-                    const uint32_t dbase = tmem + buf * (uint32_t)(Cfg::CLASSES * W);
+                    const uint32_t dbase = tmem;
                     for (uint32_t kt = kb; kt < ke; ++kt) {
                         w0 = clock64();
                         mbar_wait(&full[st], ph);
@@ -1844,15 +1705,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L, TWO>::TH
                             const bool first = (kt == kb) && (kk == 0);
 #pragma unroll
                             for (int s = 0; s < L; ++s) {
-                                if constexpr (TWO) {
-                                    // limb s x this CTA pair's planes {b_r, c_r}[s]: both classes
-                                    mma_i8_pair(dbase, sdesc(a0 + s * kBM * kBK + kk * 32),
-                                                sdesc(b0 + s * W * kBK + kk * 32), id_full,
-                                                (first && s == 0) ? 0u : 1u);
-                                } else {
-                                    mma_i8_pair(dbase + s * W, sdesc(a0 + s * kBM * kBK + kk * 32),
-                                                sdesc(b0 + kk * 32), id_full, (first && s == 0) ? 0u : 1u);
-                                }
+                                mma_i8_pair(dbase + s * W, sdesc(a0 + s * kBM * kBK + kk * 32),
+                                            sdesc(b0 + kk * 32), id_full, (first && s == 0) ? 0u : 1u);
                             }
                         }
                         tc_commit_pair(&empty[st]);
@@ -1861,7 +1715,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L, TWO>::TH
                             ph ^= 1;
                         }
                     }
-                    tc_commit_pair(tmem_full + buf);
+                    tc_commit_pair(tmem_full);
                 }
             }
             if (p.stats) {
@@ -1872,9 +1726,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L, TWO>::TH
             }
         }
     } else {
-        epilogue_role<L, W, Cfg::EPI_WARPS, true, Cfg::XPOSE, 3, false, 2, TWO>(
+        epilogue_role<L, W, Cfg::EPI_WARPS, true, false, 3>(
             p, pair, npairs, num_tiles, Mt2, rank, nchunks, tmem, s_col, tmem_full, tmem_empty, warp,
-            lane, smem + STAGES * Cfg::STAGE + 512 + 8 * W);  // 16-byte aligned transpose buffers
+            lane);
     }
 
     tc_fence_before();
@@ -1886,39 +1740,27 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L, TWO>::TH
     }
 }
 
-template <int L, bool TWO = false>
+template <int L>
 int launch_gemm2_t(const GemmParams& p, const void* tmA, const void* tmB, int num_sms,
                    cudaStream_t s) {
-    if constexpr (L == 2 && !TWO) {
-        if (p.two) return launch_gemm2_t<2, true>(p, tmA, tmB, num_sms, s);
-    }
-    using Cfg = Gemm2Cfg<L, TWO>;
+    using Cfg = Gemm2Cfg<L>;
     const uint32_t tiles = (p.Mt / 2) * p.Nt;
     uint32_t grid = 2 * tiles < (uint32_t)num_sms ? 2 * tiles : (uint32_t)num_sms;
     grid &= ~1u;
-    k_gemm2<L, TWO><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p, *static_cast<const CUtensorMap*>(tmA),
-                                                           *static_cast<const CUtensorMap*>(tmB));
+    k_gemm2<L><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p, *static_cast<const CUtensorMap*>(tmA),
+                                                      *static_cast<const CUtensorMap*>(tmB));
     return (int)cudaGetLastError();
 }
 
 template <int L>
 int configure_gemm2_t() {
-    int e = (int)cudaFuncSetAttribute(k_gemm2<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      Gemm2Cfg<L>::SMEM);
-    if constexpr (L == 2) {
-        if (!e)
-            e = (int)cudaFuncSetAttribute(k_gemm2<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          Gemm2Cfg<2, true>::SMEM);
-    }
-    return e;
+    return (int)cudaFuncSetAttribute(k_gemm2<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     Gemm2Cfg<L>::SMEM);
 }
 
 template <int L>
 int configure_gemm_t() {
     int e = (int)cudaFuncSetAttribute(k_gemm<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      GemmCfg<L>::SMEM);
-    if (!e)
-        e = (int)cudaFuncSetAttribute(k_gemm<L, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       GemmCfg<L>::SMEM);
     if constexpr (L == 2) {
         if (!e)
@@ -1926,12 +1768,6 @@ int configure_gemm_t() {
                                           GemmCfg<L>::SMEM);
         if (!e)
             e = (int)cudaFuncSetAttribute(k_gemm<L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          GemmCfg<L>::SMEM);
-        if (!e)
-            e = (int)cudaFuncSetAttribute(k_gemm<L, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          GemmCfg<L>::SMEM);
-        if (!e)
-            e = (int)cudaFuncSetAttribute(k_gemm<L, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           GemmCfg<L>::SMEM);
     }
     return e;
@@ -1946,38 +1782,9 @@ __global__ void k_fill_view(uint32_t* __restrict__ out, const uint64_t* __restri
         out[rowoff[x / cols] + coloff[x % cols]] = value;
 }
 
-template <typename Kernel>
-int launch_cluster2(Kernel k, uint32_t grid, uint32_t threads, uint32_t smem, cudaStream_t s,
-                    const GemmParams& p) {
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(grid, 1, 1);
-    cfg.blockDim = dim3(threads, 1, 1);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    return (int)cudaLaunchKernelEx(&cfg, k, p);
-}
-
 template <int L>
 int launch_gemm_t(const GemmParams& p, int num_sms, cudaStream_t s) {
     using Cfg = GemmCfg<L>;
-    if (p.mc) {
-        // column-pair clusters: one cluster per 2 SMs, Nt even (planner)
-        const uint32_t pairs = p.Mt * (p.Nt / 2);
-        const uint32_t clusters = pairs < (uint32_t)num_sms / 2 ? pairs : (uint32_t)num_sms / 2;
-        const uint32_t grid = 2 * clusters;
-        if constexpr (L == 2) {
-            if (p.fold == 1) return launch_cluster2(k_gemm<L, 1, true>, grid, Cfg::THREADS, Cfg::SMEM, s, p);
-            if (p.fold == 2) return launch_cluster2(k_gemm<L, 2, true>, grid, Cfg::THREADS, Cfg::SMEM, s, p);
-        }
-        return launch_cluster2(k_gemm<L, 3, true>, grid, Cfg::THREADS, Cfg::SMEM, s, p);
-    }
     const uint32_t tiles = p.Mt * p.Nt;
     const int grid = (int)(tiles < (uint32_t)num_sms ? tiles : (uint32_t)num_sms);
     if constexpr (L == 2) {
@@ -1998,13 +1805,6 @@ int launch_pack_t(int trans, const uint32_t* src, const uint64_t* rowoff, const 
     const uint64_t Rpad = (uint64_t)Rtiles * rpt;
     if (trans) {
         const uint64_t blocks = ((Rpad + 127) / 128) * Kt * (kBK / 32);
-        if constexpr (L == 2) {
-            if (dp.two) {
-                k_pack_cols<2, 4><<<(unsigned)blocks, 256, 0, s>>>(src, rowoff, coloff, vecok, R, K,
-                                                                  rpt, Kt, Rpad, dst, dp);
-                return (int)cudaGetLastError();
-            }
-        }
         k_pack_cols<L><<<(unsigned)blocks, 256, 0, s>>>(src, rowoff, coloff, vecok, R, K, rpt, Kt,
                                                         Rpad, dst, dp);
     } else {
@@ -2025,40 +1825,33 @@ int launch_offsets(uint64_t* dst, uint64_t start, uint64_t count, TileGeom g, in
     return (int)cudaGetLastError();
 }
 
-// Conversion kernel choice (measured, profiles/r01_conversion.txt): Morton-order
-// iteration (k_conv_z, 4 groups in flight per thread) in both directions, 0.84-0.89
-// of measured HBM.  MHG_CONV: 0 row-order kernels both ways, 1 Morton-order for
-// row-major -> Morton only (A/B only).
-static int conv_mode() {
-    const char* e = std::getenv("MHG_CONV");
-    return e ? std::atoi(e) : 2;
-}
-
+// LDG/STG conversion kernels: Morton-order iteration (k_conv_z, 4 groups in flight per
+// thread, 0.84-0.89 of measured HBM, profiles/r01_conversion.txt) where the row-major
+// buffer is 16-byte aligned and t is a power of two with t % 4 == 0 (morton = 1), else
+// the element-wise row-order kernels.
 int launch_rm_to_mh(const uint32_t* rm, uint32_t* mh, uint64_t n, TileGeom g, uint32_t q,
-                    int* bad_flag, void* stream) {
-    // row-major buffers that are not 16-byte aligned take the element-wise path
+                    int* bad_flag, int morton, void* stream) {
     const bool aligned = (reinterpret_cast<uintptr_t>(rm) & 15) == 0;
-    const bool z = aligned && g.shift >= 0 && g.t % 4 == 0 && conv_mode() >= 1;
+    const bool z = morton && aligned && g.shift >= 0 && g.t % 4 == 0;
     if (z) k_conv_z<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(rm, mh, n, g, q, bad_flag, 1);
     else k_rm_to_mh<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(rm, mh, n, g, q, bad_flag);
     return (int)cudaGetLastError();
 }
 
-int launch_mh_to_rm(const uint32_t* mh, uint32_t* rm, uint64_t n, TileGeom g, void* stream) {
-    const bool z = ((reinterpret_cast<uintptr_t>(rm) & 15) == 0) && g.shift >= 0 && g.t % 4 == 0 &&
-                   conv_mode() >= 2;
+int launch_mh_to_rm(const uint32_t* mh, uint32_t* rm, uint64_t n, TileGeom g, int morton, void* stream) {
+    const bool z = morton && ((reinterpret_cast<uintptr_t>(rm) & 15) == 0) && g.shift >= 0 && g.t % 4 == 0;
     if (z) k_conv_z<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(mh, rm, n, g, 0u, nullptr, 0);
     else k_mh_to_rm<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(mh, rm, n, g);
     return (int)cudaGetLastError();
 }
 
-template <int L, int P = L>
+template <int L>
 int launch_pack_pair_t(PackArgs a, PackArgs b, cudaStream_t s) {
     a.Rpad = (uint64_t)a.Rtiles * a.rpt;
     b.Rpad = (uint64_t)b.Rtiles * b.rpt;
     const uint64_t na = (a.Rpad / 32) * (((uint64_t)a.Kt * kBK + kPackK - 1) / kPackK);
     const uint64_t nb = ((b.Rpad + 127) / 128) * b.Kt * (kBK / 32);
-    k_pack_pair<L, P><<<(unsigned)(na + nb), 256, 0, s>>>(a, b, (uint32_t)na);
+    k_pack_pair<L><<<(unsigned)(na + nb), 256, 0, s>>>(a, b, (uint32_t)na);
     return (int)cudaGetLastError();
 }
 
@@ -2066,7 +1859,7 @@ int launch_pack_pair(int L, const PackArgs& lhs, const PackArgs& rhs, void* stre
     cudaStream_t s = (cudaStream_t)stream;
     switch (L) {
         case 1: return launch_pack_pair_t<1>(lhs, rhs, s);
-        case 2: return rhs.dp.two ? launch_pack_pair_t<2, 4>(lhs, rhs, s) : launch_pack_pair_t<2>(lhs, rhs, s);
+        case 2: return launch_pack_pair_t<2>(lhs, rhs, s);
         case 3: return launch_pack_pair_t<3>(lhs, rhs, s);
         case 4: return launch_pack_pair_t<4>(lhs, rhs, s);
     }
@@ -2099,20 +1892,8 @@ int launch_gemm(int L, const GemmParams& p, int num_sms, void* stream) {
 
 int configure_kernels() {
     {
-        int e = (int)cudaFuncSetAttribute(k_conv_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          4 * kConvUnitBytes + 1024);
-        if (!e)
-            e = (int)cudaFuncSetAttribute(k_conv_tma<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          2 * kConvUnitBytes + 1024);
-        if (!e)
-            e = (int)cudaFuncSetAttribute(k_conv_tma<3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          3 * kConvUnitBytes + 1024);
-        if (!e)
-            e = (int)cudaFuncSetAttribute(k_conv_tma<6>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          6 * kConvUnitBytes + 1024);
-        if (!e)
-            e = (int)cudaFuncSetAttribute(k_conv_tma<12>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                          12 * kConvUnitBytes + 1024);
+        const int e = (int)cudaFuncSetAttribute(k_conv_tma<kConvUnits>,
+                                                cudaFuncAttributeMaxDynamicSharedMemorySize, conv_tma_smem());
         if (e) return e;
     }
     int e = configure_gemm_t<1>();
@@ -2138,9 +1919,7 @@ int launch_gemm2(int L, const GemmParams& p, const void* tmA, const void* tmB, i
     return (int)cudaErrorInvalidValue;
 }
 
-int gemm2_b_box_rows(int L, int two) {
-    return two && L == 2 ? Gemm2Cfg<2, true>::NBH : (L <= 2 ? 128 : 64) * L / 2;
-}
+int gemm2_b_box_rows(int L) { return (L <= 2 ? 128 : 64) * L / 2; }
 
 int launch_fill_view(uint32_t* out, const uint64_t* rowoff, const uint64_t* coloff, uint64_t rows,
                      uint64_t cols, uint32_t value, void* stream) {
@@ -2148,6 +1927,86 @@ int launch_fill_view(uint32_t* out, const uint64_t* rowoff, const uint64_t* colo
     const uint64_t total = rows * cols;
     const unsigned blocks = (unsigned)((total + 255) / 256 < 4096 ? (total + 255) / 256 : 4096);
     k_fill_view<<<blocks, 256, 0, (cudaStream_t)stream>>>(out, rowoff, coloff, rows, cols, value);
+    return (int)cudaGetLastError();
+}
+
+// ------------------------------------------------------------ verification
+// Freivalds' check of a finished multiply (mhg_verify): C_new r == C_old r +/- A (B r)
+// (mod q) for random vectors r.  Every step is a row-wise mat-vec over a view, HBM-bound:
+// one warp per view row, lanes striding the columns (coalesced inside Morton tile rows),
+// 64-bit accumulation with a Barrett reduction per term.
+__device__ __forceinline__ uint64_t mod64(uint64_t u, uint32_t q, uint64_t mu) {
+    uint64_t r = u - __umul64hi(u, mu) * q;
+    return r >= q ? r - q : r;
+}
+
+// y[i] = sum_j M[rowoff[i] + coloff[j]] x[j] mod q for i < rows
+__global__ void k_matvec(const uint32_t* __restrict__ m, const uint64_t* __restrict__ rowoff,
+                         const uint64_t* __restrict__ coloff, uint64_t rows, uint64_t cols,
+                         const uint32_t* __restrict__ x, uint32_t* __restrict__ y, uint32_t q, uint64_t mu) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warps = (uint64_t)gridDim.x * (blockDim.x / 32);
+    for (uint64_t i = (uint64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5); i < rows; i += warps) {
+        const uint32_t* row = m + rowoff[i];
+        uint64_t acc = 0;
+        for (uint64_t j = lane; j < cols; j += 32)
+            acc = mod64(acc + (uint64_t)__ldcs(row + coloff[j]) * x[j], q, mu);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) y[i] = (uint32_t)mod64(acc, q, mu);
+    }
+}
+
+// r[j] uniform-ish in [0, q) from (seed, j) (splitmix64)
+__global__ void k_random_vec(uint32_t* __restrict__ r, uint64_t n, uint64_t seed, uint32_t q) {
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        uint64_t z = seed + (j + 1) * 0x9E3779B97F4A7C15ull;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        r[j] = (uint32_t)(((unsigned __int128)z * q) >> 64);
+    }
+}
+
+// mode 0: new == old + z, 1: new == old - z, 2: new == z; any mismatch sets *bad
+__global__ void k_freivalds_cmp(const uint32_t* __restrict__ wn, const uint32_t* __restrict__ wo,
+                                const uint32_t* __restrict__ z, uint64_t rows, uint32_t q, int mode,
+                                int* __restrict__ bad) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < rows;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t want;
+        if (mode == 2) want = z[i];
+        else if (mode == 0) want = (uint32_t)(((uint64_t)wo[i] + z[i]) % q);
+        else want = (uint32_t)(((uint64_t)wo[i] + q - z[i]) % q);
+        if (want != wn[i]) atomicOr(bad, 1);
+    }
+}
+
+int launch_matvec(const uint32_t* m, const uint64_t* rowoff, const uint64_t* coloff, uint64_t rows,
+                  uint64_t cols, const uint32_t* x, uint32_t* y, uint32_t q, int num_sms, void* stream) {
+    if (rows == 0) return 0;
+    const uint64_t mu = ~uint64_t(0) / q;
+    const uint64_t blocks = (rows + 7) / 8;  // 8 warps per block
+    const uint64_t cap = (uint64_t)(num_sms > 0 ? num_sms : 148) * 8;
+    k_matvec<<<(unsigned)(blocks < cap ? blocks : cap), 256, 0, (cudaStream_t)stream>>>(m, rowoff, coloff, rows,
+                                                                                        cols, x, y, q, mu);
+    return (int)cudaGetLastError();
+}
+
+int launch_random_vec(uint32_t* r, uint64_t n, uint64_t seed, uint32_t q, void* stream) {
+    if (n == 0) return 0;
+    const uint64_t blocks = (n + 255) / 256;
+    k_random_vec<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, (cudaStream_t)stream>>>(r, n, seed, q);
+    return (int)cudaGetLastError();
+}
+
+int launch_freivalds_cmp(const uint32_t* wn, const uint32_t* wo, const uint32_t* z, uint64_t rows, uint32_t q,
+                         int mode, int* bad, void* stream) {
+    if (rows == 0) return 0;
+    const uint64_t blocks = (rows + 255) / 256;
+    k_freivalds_cmp<<<(unsigned)(blocks < 4096 ? blocks : 4096), 256, 0, (cudaStream_t)stream>>>(wn, wo, z, rows, q,
+                                                                                                 mode, bad);
     return (int)cudaGetLastError();
 }
 
@@ -2180,33 +2039,16 @@ __global__ void k_widen16(const uint16_t* __restrict__ src, uint32_t* __restrict
     if (tail < count) dst[tail] = src[tail];
 }
 
-// units in flight: kConvBufs per CTA x CTAs per SM = 12 (MHG_CONV_NB = 2 / 3 / 4 / 6 / 12
-// picks 6 / 4 / 3 / 2 / 1 CTAs per SM; more independent issuers measured faster)
-static int conv_nb() {
-    static const int nb = [] {
-        const char* e = std::getenv("MHG_CONV_NB");
-        const int v = e ? std::atoi(e) : 4;
-        return (v == 2 || v == 3 || v == 4 || v == 6 || v == 12) ? v : 4;
-    }();
-    return nb;
-}
-
-int conv_tma_smem() { return 12 * kConvUnitBytes + 1024; }
+int conv_tma_smem() { return kConvUnits * kConvUnitBytes + 1024; }
 
 int launch_conv_tma(const void* tmap, uint32_t* mh, uint64_t n, TileGeom g, uint32_t q, int* bad,
                     int to_mh, int num_sms, void* stream) {
     uint32_t R = (uint32_t)g.t;
     while ((uint64_t)R * g.t * 4 > (uint64_t)kConvUnitBytes) R >>= 1;
-    const int nb = conv_nb(), per_sm = 12 / nb;
-    const int grid = per_sm * (num_sms > 0 ? num_sms : 148);
-    const int smem = nb * kConvUnitBytes + 1024;
+    const int grid = kConvCtasPerSm * (num_sms > 0 ? num_sms : 148);
     const CUtensorMap& tm = *static_cast<const CUtensorMap*>(tmap);
-    cudaStream_t s = (cudaStream_t)stream;
-    if (nb == 4) k_conv_tma<4><<<grid, 128, smem, s>>>(tm, mh, n, g, R, q, bad, to_mh);
-    else if (nb == 2) k_conv_tma<2><<<grid, 128, smem, s>>>(tm, mh, n, g, R, q, bad, to_mh);
-    else if (nb == 3) k_conv_tma<3><<<grid, 128, smem, s>>>(tm, mh, n, g, R, q, bad, to_mh);
-    else if (nb == 12) k_conv_tma<12><<<grid, 128, smem, s>>>(tm, mh, n, g, R, q, bad, to_mh);
-    else k_conv_tma<6><<<grid, 128, smem, s>>>(tm, mh, n, g, R, q, bad, to_mh);
+    k_conv_tma<kConvUnits><<<grid, 128, conv_tma_smem(), (cudaStream_t)stream>>>(tm, mh, n, g, R, q, bad,
+                                                                                 to_mh);
     return (int)cudaGetLastError();
 }
 

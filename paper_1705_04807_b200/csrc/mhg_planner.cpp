@@ -2,8 +2,10 @@
 #include "mhg_planner.hpp"
 
 #include <algorithm>
-#include <cstdlib>
-#include <string>
+#include <array>
+#include <map>
+#include <utility>
+#include <vector>
 
 namespace mhg {
 
@@ -161,6 +163,148 @@ Counters oblivious_counters(uint64_t n, uint64_t t, const Rect& out, const Rect&
     return c;
 }
 
+// ------------------------------------ mm_naive / mm_default Counters (closed form)
+namespace {
+
+using i128 = __int128;
+using Segs = std::vector<std::pair<uint64_t, uint64_t>>;  // (offset in the view, length)
+constexpr i128 kNone = -((i128)1 << 100);
+
+// encode = rowpart(i) + colpart(j) (layout.hpp:80-85; the two parts own disjoint bits)
+i128 rowpart(uint64_t t, uint64_t i) { return (i128)((dilate(i / t) << 1) * t * t + (i % t) * t); }
+i128 colpart(uint64_t t, uint64_t j) { return (i128)(dilate(j / t) * t * t + j % t); }
+
+// dilate(b + 1) - dilate(b) = (2 * 4^m + 1) / 3 for b with m trailing ones: the b in
+// [lo, hi] with the most trailing ones has the largest step.
+uint64_t most_trailing_ones(uint64_t lo, uint64_t hi) {
+    uint64_t best = lo;
+    for (int m = 1; m < 63; ++m) {
+        const uint64_t want = (uint64_t(1) << m) - 1;
+        const uint64_t b = lo + ((want - (lo & want)) & want);  // least b >= lo, b % 2^m == 2^m - 1
+        if (b < lo || b > hi) break;
+        best = b;
+    }
+    return best;
+}
+
+// max over x in [x0, x0 + len - 2] of part(x + 1) - part(x), len >= 2.  A step across a
+// tile boundary (x + 1 == 0 mod t) is never smaller than a step inside a tile (colpart:
+// >= t^2 - t + 1 vs 1; rowpart: >= t^2 + t vs t), so the boundary with the most trailing
+// ones in its tile index wins when the range holds a boundary.
+template <typename Part>
+i128 max_step(uint64_t t, uint64_t x0, uint64_t len, Part part) {
+    const uint64_t x1 = x0 + len - 2;
+    const uint64_t fb = ((x0 + t) / t) * t - 1;  // least x >= x0 with (x + 1) % t == 0
+    if (fb <= x1) {
+        const uint64_t b = most_trailing_ones(fb / t, (x1 + 1) / t - 1);
+        const uint64_t x = b * t + t - 1;
+        return part(x + 1) - part(x);
+    }
+    return part(x0 + 1) - part(x0);  // inside one tile
+}
+
+void halving_segments(uint64_t off, uint64_t d, uint64_t t, Segs& out) {
+    if (d <= t) {
+        out.emplace_back(off, d);
+        return;
+    }
+    const uint64_t d1 = (d + 1) / 2;  // multiply.hpp:212-214
+    halving_segments(off, d1, t, out);
+    halving_segments(off + d1, d - d1, t, out);
+}
+
+void raise(uint64_t& best, i128 gap) {
+    if (gap > 0 && gap > (i128)best) best = (uint64_t)gap;
+}
+
+// The largest forward gap of JumpTracker (multiply.hpp:80-90) over kernel_encoded calls
+// (:104-129) on every leaf (row segment x inner segment x column segment); each call has
+// fresh trackers, one per operand, fed in loop order x, y, z.  Every gap kind is a sum
+// of independent terms of at most two segment lists, so the maximum separates.
+uint64_t encoded_max_jump(const Kernel3& g, const Segs& R, const Segs& K, const Segs& C) {
+    auto rowp = [](uint64_t t) { return [t](uint64_t i) { return rowpart(t, i); }; };
+    auto colp = [](uint64_t t) { return [t](uint64_t j) { return colpart(t, j); }; };
+    // largest step inside any segment of length >= 2 (kNone if none)
+    auto steps = [](const Segs& S, uint64_t base, uint64_t t, auto part) {
+        i128 m = kNone;
+        for (const auto& s : S)
+            if (s.second >= 2) m = std::max(m, max_step(t, base + s.first, s.second, part));
+        return m;
+    };
+    // largest part(first) - part(last) of a segment: the backward jump of a rescan
+    auto spans = [](const Segs& S, uint64_t base, auto part) {
+        i128 m = kNone;
+        for (const auto& s : S) m = std::max(m, part(base + s.first) - part(base + s.first + s.second - 1));
+        return m;
+    };
+    uint64_t best = 0;
+    const Geo &A = g.out, &B = g.lhs, &Cg = g.rhs;
+    // out (ia + x, ja + y): colpart steps along a row; next row: rowpart step + span back
+    raise(best, steps(C, A.j, A.t, colp(A.t)));
+    if (const i128 rs = steps(R, A.i, A.t, rowp(A.t)); rs > kNone) raise(best, rs + spans(C, A.j, colp(A.t)));
+    // lhs (ib + x, jb + z): colpart steps along z; a new y rescans the row (backward);
+    // a new x: rowpart step + span back
+    raise(best, steps(K, B.j, B.t, colp(B.t)));
+    if (const i128 rs = steps(R, B.i, B.t, rowp(B.t)); rs > kNone) raise(best, rs + spans(K, B.j, colp(B.t)));
+    // rhs (ic + z, jc + y): rowpart steps along z; a new y: span back + colpart step; a new
+    // x restarts at (ic, jc) (backward)
+    raise(best, steps(K, Cg.i, Cg.t, rowp(Cg.t)));
+    if (const i128 cs = steps(C, Cg.j, Cg.t, colp(Cg.t)); cs > kNone) raise(best, cs + spans(K, Cg.i, rowp(Cg.t)));
+    return best;
+}
+
+}  // namespace
+
+Counters naive_counters(const Kernel3& g) {
+    Counters c;
+    const uint64_t r = g.rows, k = g.inner, cc = g.cols;
+    if (r == 0 || cc == 0 || k == 0) return c;  // multiply.hpp:272
+    c.recursive_calls = 1;
+    c.base_case_calls = 1;
+    c.scalar_macs = r * k * cc;
+    c.encode_calls = r * cc * (2 * k + 1);
+    c.max_consecutive_jump = encoded_max_jump(g, {{0, r}}, {{0, k}}, {{0, cc}});
+    return c;
+}
+
+Counters default_counters(const Kernel3& g) {
+    Counters c;
+    const uint64_t r = g.rows, k = g.inner, cc = g.cols;
+    if (r == 0 || cc == 0 || k == 0) return c;  // multiply.hpp:286
+    const uint64_t t = g.out.t;                 // the output layout's tile side (:288)
+    Segs R, K, C;
+    halving_segments(0, r, t, R);
+    halving_segments(0, k, t, K);
+    halving_segments(0, cc, t, C);
+    c.base_case_calls = R.size() * K.size() * C.size();
+    c.scalar_macs = r * k * cc;
+    c.encode_calls = r * cc * K.size() + 2 * r * k * cc;
+    // nodes: each dimension above t is halved at every level (multiply.hpp:204-229); the
+    // shapes at one depth take at most two values per dimension, so memoise by shape
+    struct Walk {
+        uint64_t t;
+        std::map<std::array<uint64_t, 3>, uint64_t> memo;
+        uint64_t nodes(uint64_t a, uint64_t b, uint64_t d) {
+            if (a <= t && b <= t && d <= t) return 1;
+            const std::array<uint64_t, 3> key{a, b, d};
+            if (auto it = memo.find(key); it != memo.end()) return it->second;
+            auto halves = [&](uint64_t x) {
+                return x > t ? std::array<uint64_t, 2>{(x + 1) / 2, x / 2} : std::array<uint64_t, 2>{x, 0};
+            };
+            uint64_t acc = 1;
+            for (uint64_t aa : halves(a))
+                for (uint64_t dd : halves(d))
+                    for (uint64_t bb : halves(b))
+                        if (aa && bb && dd) acc += nodes(aa, bb, dd);
+            memo[key] = acc;
+            return acc;
+        }
+    } walk{t, {}};
+    c.recursive_calls = walk.nodes(r, k, cc);
+    c.max_consecutive_jump = encoded_max_jump(g, R, K, C);
+    return c;
+}
+
 // -------------------------------------------------------------- task grid
 int fold_level(uint32_t q, uint64_t k_chunk) {
     if (q < 2 || q > 65536) return 3;
@@ -202,49 +346,32 @@ GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t c
     // r01_ab_pair_vs_1cta.txt).  Three- and four-limb primes take the pair: their W = 64
     // tiles halve the 1-CTA kernel's output per B' byte, and the pair's shared B' is
     // faster at every K (L = 3: -7..-13%, L = 4: -2..-4%; profiles/r01_pair_wide_primes.txt).
-    // MHG_GEMM=1cta / 2cta / 2cta2 / mc forces a kernel.
-    const char* sel = std::getenv("MHG_GEMM");
-    g.pair = sel ? (std::string(sel) == "2cta" || std::string(sel) == "2cta2") : lp.L >= 3;
+    // MHG_OPT_GEMM_KERNEL forces one (both are exact for every q).
+    const int64_t kernel = option(kOptGemmKernel);
+    g.pair = kernel == 0 ? lp.L >= 3 : kernel == 2;
     if (g.pair) g.Mt += g.Mt & 1u;  // pairs take two row tiles
     g.Nt = (uint32_t)((cols + g.W - 1) / g.W);
-    g.mc = !g.pair && sel && std::string(sel) == "mc";
-    if (g.mc) g.Nt += g.Nt & 1u;  // clusters take two column tiles
     g.Kt = (uint32_t)((inner + kBK - 1) / kBK);
     g.KC = (uint32_t)std::max<uint64_t>(1, lp.k_max / kBK);
-    g.two = g.pair && g.L == 2 && sel && std::string(sel) == "2cta2";
     // Unsigned digits (u8 x u8 MMA; 1-CTA and CTA-pair kernels), the default: every class
     // sum is non-negative, so the int32 accumulators grow monotonically instead of
     // random-walking around 0 -- fewer bit toggles, less power -- and the epilogue needs no
     // bias (lean fold levels from fold_level_u8).  Measured faster at every K
     // (profiles/r01_unsigned_digits.txt).  The middle class sums L products of up to
-    // 255 * 255 per k, so exact chunks are shorter (16,384 at L = 2 vs 65,532 signed).
-    // MHG_UDIG=0 selects balanced signed digits.
-    const char* ud = std::getenv("MHG_UDIG");
-    const bool want = ud ? std::atoi(ud) != 0 : true;
-    g.udig = want && !g.two && !g.mc;
+    // 255 * 255 per k, so exact chunks are shorter (16,384 at L = 2 -- the north star's K in one chunk -- vs
+    // 65,532 signed).
+    // MHG_OPT_DIGITS = 0 selects balanced signed digits.
+    g.udig = option(kOptDigits) != 0;
     if (g.udig) {
         const uint64_t kmax_u = ((uint64_t(1) << 31) - (uint64_t(1) << 17)) / ((uint64_t)lp.L * 65025);
         g.KC = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(g.KC, kmax_u / kBK));
     }
     // test hook: a smaller chunk exercises the multi-chunk path on small inputs
-    if (const char* force = std::getenv("MHG_FORCE_KCHUNK")) {
-        const long v = std::strtol(force, nullptr, 10);
-        if (v > 0 && (uint64_t)v < g.KC) g.KC = (uint32_t)v;
-    }
-    // two-class accumulation (MHG_GEMM=2cta2): the CTA pair with limb s multiplying the
-    // digits of 256^s b mod q.  Class sums obey the same bound as the widest class of the
-    // 3-class layout (2 * 128 * 128 per k); the lean fold (w16 < 256) additionally needs
-    // (32768 + 128 w16) K + 65280 + w16 <= 2^31 - 2^17.
-    if (g.two) {
-        const uint64_t w16 = (uint64_t(1) << 16) % q;
-        if (w16 < 256) {
-            const uint64_t kcap = ((uint64_t(1) << 31) - (uint64_t(1) << 17) - 65280 - w16) / (32768 + 128 * w16);
-            g.KC = (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(g.KC, kcap / kBK));
-        }
-    }
+    const int64_t cap = option(kOptMaxKChunk);
+    if (cap > 0 && (uint64_t)cap < g.KC) g.KC = (uint32_t)cap;
     g.chunks = g.Kt ? (g.Kt + g.KC - 1) / g.KC : 0;
     g.apack_bytes = (uint64_t)g.Mt * kBM * g.Kt * kBK * g.L;
-    g.bpack_bytes = (uint64_t)g.Nt * g.W * g.Kt * kBK * g.L * (g.two ? 2 : 1);
+    g.bpack_bytes = (uint64_t)g.Nt * g.W * g.Kt * kBK * g.L;
     return g;
 }
 

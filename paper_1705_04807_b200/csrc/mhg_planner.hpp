@@ -47,12 +47,24 @@ uint64_t axis_segments(uint64_t off1, uint64_t off2, uint64_t len, uint64_t S);
 Counters oblivious_counters(uint64_t n, uint64_t t, const Rect& out, const Rect& lhs,
                             const Rect& rhs);
 
+// Geometry of one view for the encode-addressed kernels, whose three containers may
+// have different layouts: tile side t and the view's first cell (i, j).
+struct Geo {
+    uint64_t n, t, i, j;
+};
+struct Kernel3 {
+    Geo out, lhs, rhs;
+    uint64_t rows, inner, cols;
+};
+// Counters of mm_naive (multiply.hpp:269-278) and mm_default (:283-291), closed form
+// (including max_consecutive_jump of their encode-addressed walks).
+Counters naive_counters(const Kernel3& g);
+Counters default_counters(const Kernel3& g);
+
 // -------------------------------------------------------------- task grid
 struct GemmGeometry {
     bool pair;            // CTA-pair kernel (k_gemm2); Mt is then even
-    bool mc;              // column-pair clusters with lhs multicast (k_gemm MC); Nt is then even
-    bool two;             // two-class accumulation on the CTA pair (L = 2; rhs with 4 planes)
-    bool udig;            // unsigned u8 digits (L = 2, single CTA; MHG_UDIG=1)
+    bool udig;            // unsigned u8 digits (MHG_OPT_DIGITS = 1, the default)
     uint32_t L, W;        // limbs, output tile width
     uint32_t Mt, Nt, Kt;  // tiles along rows / cols / inner (128-byte K slices)
     uint32_t KC;          // K slices per exact int32 chunk

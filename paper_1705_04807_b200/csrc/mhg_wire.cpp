@@ -28,27 +28,13 @@
 
 namespace {
 
-// Staging ring: kSlots slots of chunk() cells (MHG_UPLOAD_CHUNK_LOG2, default
-// 2^22 cells = 8 MiB of uint16 per slot).
-constexpr int kMaxSlots = 8;
+// Staging ring: 4 slots of 2^22 cells (8 MiB of uint16 each): small enough to stay
+// in the host LLC while the copy engine reads it (profiles/r01_upload_wire_sweep.txt).
+constexpr int kMaxSlots = 4;
 
-uint64_t chunk_cells() {
-    static const uint64_t c = [] {
-        const char* e = std::getenv("MHG_UPLOAD_CHUNK_LOG2");
-        const int v = e ? std::atoi(e) : 22;
-        return uint64_t(1) << (v >= 16 && v <= 26 ? v : 22);
-    }();
-    return c;
-}
+uint64_t chunk_cells() { return uint64_t(1) << 22; }
 
-int ring_slots() {
-    static const int n = [] {
-        const char* e = std::getenv("MHG_UPLOAD_SLOTS");
-        const int v = e ? std::atoi(e) : 4;
-        return v >= 2 && v <= kMaxSlots ? v : 4;
-    }();
-    return n;
-}
+int ring_slots() { return kMaxSlots; }
 
 // Narrow `n` cells to uint16; returns nonzero iff some cell needs more than 16 bits.
 uint32_t narrow16_scalar(const uint32_t* __restrict src, uint16_t* __restrict dst, uint64_t n) {
@@ -84,10 +70,7 @@ uint32_t narrow16(const uint32_t* src, uint16_t* dst, uint64_t n) {
 }
 
 int host_threads() {
-    if (const char* e = std::getenv("MHG_UPLOAD_THREADS")) {
-        const int v = std::atoi(e);
-        if (v > 0) return v;
-    }
+    if (const int64_t v = mhg::option(mhg::kOptUploadThreads)) return (int)v;
     cpu_set_t set;
     CPU_ZERO(&set);
     int n = 1;
@@ -200,12 +183,8 @@ bool wire16_enabled(uint32_t q, uint64_t count) {
     // narrowing runs at ~6 GB/s of cells per host thread (measured, 16 threads: 87-100 GB/s),
     // so the wire beats the 4-byte copy at the PCIe rate only with >= 8 workers; fewer
     // (e.g. 8 local ranks sharing 16 cores) keep the plain copy unless MHG_UPLOAD_WIRE=16
-    static const int mode = [] {
-        const char* e = std::getenv("MHG_UPLOAD_WIRE");
-        if (e && std::strcmp(e, "32") == 0) return 32;
-        if (e && std::strcmp(e, "16") == 0) return 16;
-        return host_threads() >= 8 ? 16 : 32;
-    }();
+    int64_t mode = mhg::option(mhg::kOptUploadWire);
+    if (mode == 0) mode = host_threads() >= 8 ? 16 : 32;
     return mode == 16 && q <= 65536 && count >= (uint64_t(1) << 22);
 }
 

@@ -263,6 +263,25 @@ def pull_lists(ex: PanelExchange):
     return pulls, pullers
 
 
+class PeerSetupError(RuntimeError):
+    """Peer-memory setup failed on some rank (every rank raises it)."""
+
+
+def exchange_bytes(ex: PanelExchange, plans, mode: str) -> int:
+    """Bytes this rank receives per step: packed planes of the parts it does not own
+    (p2p, nccl) or the uint32 slices of its row / column group (u32)."""
+    if ex.P == 1:
+        return 0
+    total = 0
+    for sg, pl in zip(ex.segments(), plans):
+        for which, owner, members, rng in ((0, sg.a_owner, ex.row_members, sg.a_range),
+                                           (1, sg.b_owner, ex.col_members, sg.b_range)):
+            if owner == ex.rank or len(members) == 1:
+                continue
+            total += pl.pack_region(which)[1] if mode in ("p2p", "nccl") else 4 * (rng[1] - rng[0])
+    return total
+
+
 class PeerPanels:
     """Copy-engine exchange of the PACKED panels over NVLink peer memory.
 
@@ -284,13 +303,22 @@ class PeerPanels:
     matching record (the IPC event contract), on `host_group` (gloo: a CPU-only
     barrier that never waits for the GPU).  No kernel waits on another rank's
     kernel: the waits are stream-level dependencies, so the path is exercised
-    safely with all ranks on one GPU (tests/test_dist_gpu.py)."""
+    safely with all ranks on one GPU (tests/test_dist_gpu.py).
+
+    The owner's packs run on a high-priority side stream, one event per segment, so
+    its own segment-j GEMM waits only for pack j (and segment j's pulls), not for the
+    packs of later segments.
+
+    Setup is collective: if mapping a peer's memory fails on any rank (no peer access
+    between the devices, IPC unsupported), every rank raises PeerSetupError and the
+    caller can fall back to the NCCL exchange (rank_update_packed)."""
 
     def __init__(self, mh, ex: PanelExchange, plans, host_group=None, device=None):
         import torch
         import torch.distributed as dist
 
         self.mh, self.ex, self.plans = mh, ex, plans
+        self.bases = {}
         self.group = host_group
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
         self.segs = ex.segments()
@@ -310,26 +338,37 @@ class PeerPanels:
         infos = [None] * P
         dist.all_gather_object(infos, mine, group=host_group)
         # pulls[j] = [(owner, dst, src, bytes)]; one mapping per owner allocation
-        self.bases = {}
         self.pulls = [[] for _ in self.segs]
         owners = set()
         lists, pullers = pull_lists(ex)
-        for j, pl in enumerate(plans):
-            for which, owner in lists[j]:
-                dst, nb = pl.pack_region(which)
-                if not nb:
-                    continue
-                h, off, onb = infos[owner]["exports"][(j, which)]
-                if onb != nb:
-                    raise RuntimeError(f"segment {j}: packed sizes differ ({onb} vs {nb})")
-                if h not in self.bases:
-                    self.bases[h] = mh.ipc_open(h)
-                self.pulls[j].append((owner, dst, self.bases[h] + off, nb))
-                owners.add(owner)
-        self.peer_pack_done = {o: [torch.cuda.Event.from_ipc_handle(self.device, hnd)
-                                   for hnd in infos[o]["pack_done"]] for o in sorted(owners)}
-        self.peer_copy_done = [torch.cuda.Event.from_ipc_handle(self.device, infos[p]["copy_done"])
-                               for p in sorted(pullers)]
+        error = None
+        try:
+            for j, pl in enumerate(plans):
+                for which, owner in lists[j]:
+                    dst, nb = pl.pack_region(which)
+                    if not nb:
+                        continue
+                    h, off, onb = infos[owner]["exports"][(j, which)]
+                    if onb != nb:
+                        raise RuntimeError(f"segment {j}: packed sizes differ ({onb} vs {nb})")
+                    if h not in self.bases:
+                        self.bases[h] = mh.ipc_open(h)
+                    self.pulls[j].append((owner, dst, self.bases[h] + off, nb))
+                    owners.add(owner)
+            self.peer_pack_done = {o: [torch.cuda.Event.from_ipc_handle(self.device, hnd)
+                                       for hnd in infos[o]["pack_done"]] for o in sorted(owners)}
+            self.peer_copy_done = [torch.cuda.Event.from_ipc_handle(self.device, infos[p]["copy_done"])
+                                   for p in sorted(pullers)]
+        except Exception as exc:  # noqa: BLE001 -- reported collectively below
+            error = f"rank {rank}: {exc}"
+        errors = [None] * P
+        dist.all_gather_object(errors, error, group=host_group)
+        failed = [e for e in errors if e]
+        if failed:
+            self.close()
+            raise PeerSetupError("; ".join(failed))
+        self.pull_bytes = sum(nb for pulls in self.pulls for (_, _, _, nb) in pulls)
+        self.pack_stream = torch.cuda.Stream(device=self.device, priority=-1)
         self.copy_streams = {o: torch.cuda.Stream(device=self.device) for o in sorted(owners)}
         self.join = torch.cuda.Stream(device=self.device)
         # per (segment, owner): "this owner's pulls of the segment have landed"
@@ -353,16 +392,19 @@ class PeerPanels:
 
         stream = torch.cuda.current_stream(self.device) if stream is None else stream
         rank = self.ex.rank
+        ps = self.pack_stream
         self._barrier()  # every puller recorded copy_done of the previous step
+        # packs overwrite workspaces this rank's previous GEMMs and its pullers read
+        ps.wait_stream(stream)
         if self.steps:
             for e in self.peer_copy_done:
-                stream.wait_event(e)
+                ps.wait_event(e)
         for j, (sg, pl) in enumerate(zip(self.segs, self.plans)):
             if sg.a_owner == rank:
-                pl.pack(0, stream)
+                pl.pack(0, ps)
             if sg.b_owner == rank:
-                pl.pack(1, stream)
-            self.pack_done[j].record(stream)
+                pl.pack(1, ps)
+            self.pack_done[j].record(ps)
         # this rank's pulls overwrite workspaces its previous GEMMs read
         self.dst_free.record(stream)
         self._barrier()  # every owner recorded pack_done of this step
@@ -381,6 +423,7 @@ class PeerPanels:
                 ev.record(self.copy_streams[owner])
                 stream.wait_event(ev)
                 self.join.wait_event(ev)
+            stream.wait_event(self.pack_done[j])  # this rank's own parts of segment j
             self.plans[j].gemm(stream)
         self.copy_done.record(self.join)
         self.steps += 1

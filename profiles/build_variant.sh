@@ -10,4 +10,4 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler
      -Xptxas -v -c $C/mhg_kernels.cu -o /tmp/mhg_variant_$name/k.o 2> /tmp/mhg_variant_$name/ptxas.log
 grep -A2 "k_gemmILi2" /tmp/mhg_variant_$name/ptxas.log | grep -E "spill|registers" | sed "s/^/[$name] /"
 nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $R/variants/libmhg_$name.so /tmp/mhg_variant_$name/k.o \
-     $C/build/mhg_host.o $C/build/mhg_planner.o $C/build/mhg_wire.o -lcudart_static -lrt -lpthread -ldl
+     $C/build/mhg_host.o $C/build/mhg_planner.o $C/build/mhg_wire.o $C/build/mhg_options.o -lcudart_static -lrt -lpthread -ldl

@@ -7,7 +7,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 # the upload wire's on/off default depends on the host's core count: pin it on so the
-# wire tests (and every large upload) take the same path on any box
+# wire tests (and every large upload) take the same path on any box (read once, at the
+# library's first use: MHG_OPT_UPLOAD_WIRE's initial value)
 os.environ.setdefault("MHG_UPLOAD_WIRE", "16")
 
 
@@ -45,3 +46,17 @@ def gpu(mh):
     st = mh.lib().mhg_device_check()
     assert st == 0, mh.lib().mhg_last_error().decode()
     return torch.device("cuda:0")
+
+
+@pytest.fixture
+def opts(mh):
+    """opts(key, value): set an mhg option (mh.OPT_*) for this test only."""
+    saved = {}
+
+    def set_(key, value):
+        if key not in saved:
+            saved[key] = mh.get_option(key)
+        mh.set_option(key, value)
+    yield set_
+    for k, v in saved.items():
+        mh.set_option(k, v)

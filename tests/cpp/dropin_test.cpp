@@ -6,8 +6,11 @@
 #include <cstdio>
 #include <functional>
 #include <memory>
+#include <algorithm>
 #include <random>
+#include <set>
 #include <string>
+#include <vector>
 
 namespace {
 
@@ -209,7 +212,385 @@ void test_host_edits_and_copies() {
     CHECK(!(A0 == A));
     A[5] = mh::Fp{0};
     mh::mm_oblivious({mh::Sub{&A, 0, 8, 8}, mh::Sub{&B, 0, 8, 8}, mh::Sub{&C, 0, 8, 8}});
-    CHECK(A[5].v == C[5].v && A[6].v == (2 * C[6].v) % 97);
+    const mh::Matrix& Ar = A;  // reads through the const overload: no host-newer marking
+    const mh::Matrix& Cr = C;
+    CHECK(Ar[5].v == Cr[5].v && Ar[6].v == (2 * Cr[6].v) % 97);
+}
+
+// ---- re-hosted from proj/tests/unit/multiply_test.cpp:308-437 -------------------------
+void test_compatible_parts() {  // multiply_test.cpp:308-361
+    const mh::Modulus two(2);
+    mh::Matrix A(mh::Layout(8, 4), two), B(mh::Layout(8, 4), two), C(mh::Layout(8, 4), two);
+    const mh::Layout& p = A.layout();
+    {  // disjoint row ranges yield nothing
+        const mh::Framed pa{mh::Sub{&A, mh::encode(p, 0, 0), 3, 2}, 0, 0};
+        const mh::Framed pb{mh::Sub{&B, mh::encode(p, 3, 0), 2, 4}, 3, 0};
+        const mh::Framed pc{mh::Sub{&C, mh::encode(p, 0, 0), 4, 2}, 0, 0};
+        CHECK(!mh::compatible_parts(pa, pb, pc).has_value());
+    }
+    {  // identical full frames come back unchanged
+        const mh::Framed pa{mh::Sub{&A, mh::encode(p, 1, 1), 3, 2}, 0, 0};
+        const mh::Framed pb{mh::Sub{&B, mh::encode(p, 2, 2), 3, 4}, 0, 0};
+        const mh::Framed pc{mh::Sub{&C, mh::encode(p, 3, 3), 4, 2}, 0, 0};
+        const auto got = mh::compatible_parts(pa, pb, pc);
+        CHECK(got.has_value());
+        for (int op = 0; got && op < 3; ++op) {
+            const mh::Framed& in = op == 0 ? pa : op == 1 ? pb : pc;
+            const mh::Framed& out = (*got)[op];
+            CHECK(out.view.origin == in.view.origin && out.view.rows == in.view.rows &&
+                  out.view.cols == in.view.cols && out.row0 == in.row0 && out.col0 == in.col0);
+        }
+    }
+    {  // partial overlaps trim to the intersection box
+        const mh::Framed pa{mh::Sub{&A, mh::encode(p, 0, 0), 3, 2}, 0, 0};
+        const mh::Framed pb{mh::Sub{&B, mh::encode(p, 1, 0), 2, 4}, 1, 0};
+        const mh::Framed pc{mh::Sub{&C, mh::encode(p, 2, 0), 2, 2}, 2, 0};
+        const auto got = mh::compatible_parts(pa, pb, pc);
+        CHECK(got.has_value());
+        if (got) {
+            const auto& [ta, tb, tc] = *got;
+            CHECK(ta.row0 == 1 && ta.view.rows == 2 && ta.col0 == 0 && ta.view.cols == 2);
+            CHECK(ta.view.origin == mh::encode(p, 1, 0));
+            CHECK(tb.row0 == 1 && tb.view.rows == 2 && tb.col0 == 2 && tb.view.cols == 2);
+            CHECK(tb.view.origin == mh::encode(p, 1, 2));
+            CHECK(tc.row0 == 2 && tc.view.rows == 2 && tc.col0 == 0 && tc.view.cols == 2);
+            CHECK(tc.view.origin == mh::encode(p, 2, 0));
+        }
+    }
+}
+
+void test_base_case_mm() {  // multiply_test.cpp:363-407
+    std::mt19937_64 eng(66);
+    const mh::Modulus two(2);
+    const mh::Grid ga = random_grid(8, 2, eng), gb = random_grid(8, 2, eng), gc = random_grid(8, 2, eng);
+    {  // scattered operand is rejected
+        mh::Matrix A = mh::from_row_major(ga, 4, two), B = mh::from_row_major(gb, 4, two),
+                   C = mh::from_row_major(gc, 4, two);
+        mh::Counters ctr;
+        const mh::Sub bad{&B, mh::encode(B.layout(), 2, 2), 4, 4};
+        CHECK(!mh::is_contained(bad));
+        CHECK(throws_as<std::logic_error>(
+            [&] { mh::base_case_mm(mh::Sub{&A, 0, 4, 4}, bad, mh::Sub{&C, 0, 4, 4}, ctr); }));
+        CHECK(throws_as<std::logic_error>(  // shapes do not chain
+            [&] { mh::base_case_mm(mh::Sub{&A, 0, 4, 4}, mh::Sub{&B, 0, 4, 3}, mh::Sub{&C, 0, 4, 4}, ctr); }));
+    }
+    {  // single cell: one MAC, empty jump trace
+        mh::Matrix A = mh::from_row_major(ga, 4, two), B = mh::from_row_major(gb, 4, two),
+                   C = mh::from_row_major(gc, 4, two);
+        mh::Counters ctr;
+        mh::base_case_mm(mh::Sub{&A, 0, 1, 1}, mh::Sub{&B, 0, 1, 1}, mh::Sub{&C, 0, 1, 1}, ctr);
+        CHECK(ctr.base_case_calls == 1 && ctr.scalar_macs == 1);
+        CHECK(ctr.max_consecutive_jump == 0 && ctr.encode_calls == 0);
+    }
+    {  // full tiles: t^3 MACs, jumps within the tile side
+        mh::Matrix A = mh::from_row_major(ga, 4, two), B = mh::from_row_major(gb, 4, two),
+                   C = mh::from_row_major(gc, 4, two);
+        const mh::Layout& p = A.layout();
+        mh::Counters ctr;
+        mh::base_case_mm(mh::Sub{&A, mh::encode(p, 4, 4), 4, 4}, mh::Sub{&B, mh::encode(p, 4, 0), 4, 4},
+                         mh::Sub{&C, mh::encode(p, 0, 4), 4, 4}, ctr);
+        CHECK(ctr.scalar_macs == 64);
+        CHECK(ctr.max_consecutive_jump <= 4 && ctr.max_consecutive_jump >= 1);
+        CHECK(ctr.encode_calls == 0);
+        mh::Grid want = ga;
+        dense_acc(want, gb, gc, 4, 4, 4, 0, 0, 4, 4, 4, 4, 2);
+        CHECK(mh::to_row_major(A) == want);
+    }
+    {  // result agrees with the dense oracle
+        mh::Matrix A = mh::from_row_major(ga, 4, two), B = mh::from_row_major(gb, 4, two),
+                   C = mh::from_row_major(gc, 4, two);
+        const mh::Layout& p = A.layout();
+        mh::Counters ctr;
+        mh::Grid want = ga;
+        dense_acc(want, gb, gc, 1, 1, 1, 0, 0, 1, 3, 3, 2, 2);
+        mh::base_case_mm(mh::Sub{&A, mh::encode(p, 1, 1), 3, 3}, mh::Sub{&B, mh::encode(p, 1, 0), 3, 2},
+                         mh::Sub{&C, mh::encode(p, 0, 1), 2, 3}, ctr);
+        CHECK(mh::to_row_major(A) == want);
+    }
+}
+
+// Reference JumpTracker walks (multiply.hpp:80-90, :104-129, :153-170), restated on the
+// test side as the checker of the library's closed forms.
+struct Walk {
+    std::uint64_t last = 0, best = 0;
+    bool armed = false;
+    void touch(std::uint64_t a) {
+        if (armed && a > last && a - last > best) best = a - last;
+        last = a;
+        armed = true;
+    }
+};
+
+std::uint64_t encoded_walk(const mh::Layout& la, const mh::Layout& lb, const mh::Layout& lc,
+                           std::uint64_t ia, std::uint64_t ja, std::uint64_t ib, std::uint64_t jb,
+                           std::uint64_t ic, std::uint64_t jc, std::uint64_t r, std::uint64_t k,
+                           std::uint64_t c) {
+    Walk ta, tb, tc;
+    for (std::uint64_t x = 0; x < r; ++x)
+        for (std::uint64_t y = 0; y < c; ++y) {
+            ta.touch(mh::encode(la, ia + x, ja + y));
+            for (std::uint64_t z = 0; z < k; ++z) {
+                tb.touch(mh::encode(lb, ib + x, jb + z));
+                tc.touch(mh::encode(lc, ic + z, jc + y));
+            }
+        }
+    return std::max({ta.best, tb.best, tc.best});
+}
+
+void default_walk(const mh::Layout& la, const mh::Layout& lb, const mh::Layout& lc, std::uint64_t ia,
+                  std::uint64_t ja, std::uint64_t ib, std::uint64_t jb, std::uint64_t ic, std::uint64_t jc,
+                  std::uint64_t r, std::uint64_t k, std::uint64_t c, std::uint64_t t, std::uint64_t& best) {
+    if (r <= t && k <= t && c <= t) {
+        best = std::max(best, encoded_walk(la, lb, lc, ia, ja, ib, jb, ic, jc, r, k, c));
+        return;
+    }
+    const std::uint64_t r1 = r > t ? (r + 1) / 2 : r, c1 = c > t ? (c + 1) / 2 : c, k1 = k > t ? (k + 1) / 2 : k;
+    for (int rh = 0; rh < 2; ++rh)
+        for (int ch = 0; ch < 2; ++ch)
+            for (int kh = 0; kh < 2; ++kh) {
+                const std::uint64_t rr = rh ? r - r1 : r1, cc = ch ? c - c1 : c1, kk = kh ? k - k1 : k1;
+                const std::uint64_t ro = rh ? r1 : 0, co = ch ? c1 : 0, ko = kh ? k1 : 0;
+                if (rr && cc && kk)
+                    default_walk(la, lb, lc, ia + ro, ja + co, ib + ro, jb + ko, ic + ko, jc + co, rr, kk, cc, t,
+                                 best);
+            }
+}
+
+void test_naive_default_jumps() {  // multiply.hpp:80-129, 202-230 (mixed layouts allowed)
+    std::mt19937_64 eng(99);
+    const mh::Modulus q(97);
+    for (int it = 0; it < 24; ++it) {
+        const std::uint64_t ts[3] = {std::uint64_t(1) << (eng() % 4), std::uint64_t(1) << (eng() % 4),
+                                     std::uint64_t(it % 3 ? 4 : 3)};
+        std::uint64_t ns[3];
+        for (int a = 0; a < 3; ++a) ns[a] = ts[a] << (2 + eng() % 2);
+        mh::Matrix A(mh::Layout(ns[0], ts[0]), q), B(mh::Layout(ns[1], ts[1]), q), C(mh::Layout(ns[2], ts[2]), q);
+        const std::uint64_t r = 1 + eng() % std::min(ns[0], ns[1]), c = 1 + eng() % std::min(ns[0], ns[2]),
+                            k = 1 + eng() % std::min(ns[1], ns[2]);
+        const std::uint64_t ia = eng() % (ns[0] - r + 1), ja = eng() % (ns[0] - c + 1);
+        const std::uint64_t ib = eng() % (ns[1] - r + 1), jb = eng() % (ns[1] - k + 1);
+        const std::uint64_t ic = eng() % (ns[2] - k + 1), jc = eng() % (ns[2] - c + 1);
+        const mh::Problem prob{mh::Sub{&A, mh::encode(A.layout(), ia, ja), r, c},
+                               mh::Sub{&B, mh::encode(B.layout(), ib, jb), r, k},
+                               mh::Sub{&C, mh::encode(C.layout(), ic, jc), k, c}};
+        const mh::Counters n = mh::mm_naive(prob);
+        CHECK(n.max_consecutive_jump ==
+              encoded_walk(A.layout(), B.layout(), C.layout(), ia, ja, ib, jb, ic, jc, r, k, c));
+        std::uint64_t best = 0;
+        default_walk(A.layout(), B.layout(), C.layout(), ia, ja, ib, jb, ic, jc, r, k, c, ts[0], best);
+        const mh::Counters d = mh::mm_default(prob);
+        CHECK(d.max_consecutive_jump == best);
+        CHECK(n.scalar_macs == r * k * c && d.scalar_macs == r * k * c);
+    }
+}
+
+void test_scattered_default_run() {  // multiply_test.cpp:409-424
+    std::mt19937_64 eng(77);
+    const std::uint64_t n = 64, t = 8;
+    const mh::Modulus two(2);
+    mh::Matrix A = mh::from_row_major(random_grid(n, 2, eng), t, two);
+    mh::Matrix B = mh::from_row_major(random_grid(n, 2, eng), t, two);
+    mh::Matrix C = mh::from_row_major(random_grid(n, 2, eng), t, two);
+    const mh::Index s = mh::encode(A.layout(), t / 2, t / 2);
+    const mh::Counters ctr = mh::mm_default({mh::Sub{&A, s, 2 * t, 2 * t}, mh::Sub{&B, s, 2 * t, 2 * t},
+                                             mh::Sub{&C, s, 2 * t, 2 * t}});
+    CHECK(ctr.max_consecutive_jump > t);
+    CHECK(ctr.encode_calls > 0);
+}
+
+void test_work_is_exact() {  // multiply_test.cpp:426-437
+    std::mt19937_64 eng(88);
+    const mh::Modulus q(97);
+    for (int it = 0; it < 10; ++it) {
+        const std::uint64_t n = 16, t = 4;
+        const std::uint64_t r = 1 + eng() % n, k = 1 + eng() % n, c = 1 + eng() % n;
+        const mh::Grid ga = random_grid(n, 97, eng), gb = random_grid(n, 97, eng), gc = random_grid(n, 97, eng);
+        mh::Matrix B = mh::from_row_major(gb, t, q), C = mh::from_row_major(gc, t, q);
+        std::uint64_t res[3];
+        mh::Grid out[3];
+        for (int kind = 0; kind < 3; ++kind) {
+            mh::Matrix A = mh::from_row_major(ga, t, q);
+            const mh::Problem prob{mh::Sub{&A, 0, r, c}, mh::Sub{&B, 0, r, k}, mh::Sub{&C, 0, k, c}};
+            res[kind] = (kind == 0 ? mh::mm_naive(prob) : kind == 1 ? mh::mm_default(prob)
+                                                                    : mh::mm_oblivious(prob)).scalar_macs;
+            out[kind] = mh::to_row_major(A);
+        }
+        CHECK(res[0] == r * k * c && res[1] == r * k * c && res[2] == r * k * c);
+        CHECK(out[0] == out[1] && out[1] == out[2]);
+    }
+}
+
+// ---- re-hosted from proj/tests/unit/submatrix_test.cpp:40-91, 136-249 ----------------
+mh::Sub sub_at(mh::Matrix& m, std::uint64_t i, std::uint64_t j, std::uint64_t r, std::uint64_t c) {
+    return mh::Sub{&m, mh::encode(m.layout(), i, j), r, c};
+}
+
+bool contained_by_scan(const mh::Matrix& m, const mh::Sub& s) {
+    const mh::Layout& p = m.layout();
+    const auto i0 = mh::extract_i(p, s.origin), j0 = mh::extract_j(p, s.origin);
+    std::set<std::pair<std::uint64_t, std::uint64_t>> tiles;
+    for (std::uint64_t x = 0; x < s.rows; ++x)
+        for (std::uint64_t y = 0; y < s.cols; ++y) tiles.emplace((i0 + x) / p.t, (j0 + y) / p.t);
+    return tiles.size() <= 1;
+}
+
+void test_alignment_and_containment() {  // submatrix_test.cpp:40-69
+    mh::Matrix m16(mh::Layout(16, 4), mh::Modulus(2));
+    CHECK(mh::is_aligned(sub_at(m16, 0, 0, 8, 4)));
+    CHECK(!mh::is_aligned(sub_at(m16, 1, 2, 4, 4)));
+    CHECK(!mh::is_aligned(sub_at(m16, 4, 4, 3, 4)));
+    CHECK(mh::is_aligned(sub_at(m16, 4, 8, 4, 8)));
+    CHECK(!mh::is_aligned(sub_at(m16, 4, 8, 12, 4)));
+    CHECK(!mh::is_aligned(sub_at(m16, 0, 0, 0, 4)));
+    mh::Matrix m(mh::Layout(8, 4), mh::Modulus(2));
+    CHECK(mh::is_contained(sub_at(m, 0, 0, 4, 4)));
+    CHECK(mh::is_contained(sub_at(m, 1, 1, 2, 2)));
+    CHECK(!mh::is_contained(sub_at(m, 2, 2, 4, 4)));
+    bool all = true;
+    for (std::uint64_t i = 0; i < 8; ++i)
+        for (std::uint64_t j = 0; j < 8; ++j)
+            for (std::uint64_t r = 0; i + r <= 8; ++r)
+                for (std::uint64_t c = 0; j + c <= 8; ++c) {
+                    const mh::Sub s = sub_at(m, i, j, r, c);
+                    all = all && mh::is_contained(s) == contained_by_scan(m, s);
+                }
+    CHECK(all);
+    CHECK(throws_as<std::out_of_range>([&] { mh::is_contained(sub_at(m, 6, 0, 4, 4)); }));
+    CHECK(throws_as<std::out_of_range>([&] { mh::is_aligned(mh::Sub{&m, 64, 1, 1}); }));
+}
+
+void test_quadrant_order() {  // submatrix_test.cpp:71-91
+    mh::Matrix m8(mh::Layout(8, 4), mh::Modulus(2));
+    const auto q8 = mh::quadrants(mh::Aligned{&m8, 0, 64});
+    for (int t = 0; t < 4; ++t) CHECK(q8[t].origin == std::uint64_t(t) * 16 && q8[t].elems == 16);
+    mh::Matrix m16(mh::Layout(16, 4), mh::Modulus(2));
+    const auto sh = mh::quadrants(mh::Aligned{&m16, 64, 64});
+    CHECK(sh[0].origin == 64 && sh[1].origin == 80 && sh[2].origin == 96 && sh[3].origin == 112);
+    const auto top = mh::quadrants(mh::Aligned{&m16, 0, 256});
+    CHECK(top[1].origin == 64 && top[2].origin == 128 && top[3].origin == 192 && top[0].elems == 64);
+}
+
+void test_split_edge_cases() {  // submatrix_test.cpp:136-168
+    mh::Matrix m(mh::Layout(8, 4), mh::Modulus(2));
+    const auto sp = mh::split_sub(mh::Aligned{&m, 0, 64}, sub_at(m, 0, 0, 2, 2));
+    CHECK(sp.rows_north == 2 && sp.cols_west == 2 && sp.rows_south == 0 && sp.cols_east == 0);
+    CHECK(sp.part[mh::NW] && !sp.part[mh::NE] && !sp.part[mh::SW] && !sp.part[mh::SE]);
+    const mh::Aligned whole{&m, 0, 64};
+    const auto all = mh::split_sub(whole, sub_at(m, 0, 0, 8, 8));
+    const auto qs = mh::quadrants(whole);
+    for (int t = 0; t < 4; ++t)
+        CHECK(all.part[t] && all.part[t]->origin == qs[t].origin && all.part[t]->rows == 4 &&
+              all.part[t]->cols == 4);
+    mh::Matrix m16(mh::Layout(16, 4), mh::Modulus(2)), other(mh::Layout(16, 4), mh::Modulus(2));
+    CHECK(throws_as<std::logic_error>([&] { mh::split_sub(mh::Aligned{&m16, 0, 64}, sub_at(m16, 6, 6, 4, 4)); }));
+    CHECK(throws_as<std::invalid_argument>(
+        [&] { mh::split_sub(mh::Aligned{&other, 0, 64}, sub_at(m16, 0, 0, 2, 2)); }));
+}
+
+// Every view inside every aligned block: split_sub's parts tile it exactly (no gaps,
+// no overlap, nothing outside).  submatrix_test.cpp:170-214 / acceptance criterion 2.
+bool partition_ok(mh::Matrix& m, const mh::Aligned& a, const mh::Sub& s, std::vector<std::uint32_t>& mark,
+                  std::uint32_t& stamp) {
+    const mh::Layout& p = m.layout();
+    const auto si = mh::extract_i(p, s.origin), sj = mh::extract_j(p, s.origin);
+    const auto sp = mh::split_sub(a, s);
+    if (sp.rows_north + sp.rows_south != s.rows || sp.cols_west + sp.cols_east != s.cols) return false;
+    ++stamp;
+    std::uint64_t covered = 0;
+    for (const auto& part : sp.part) {
+        if (!part) continue;
+        const auto pi = mh::extract_i(p, part->origin), pj = mh::extract_j(p, part->origin);
+        for (std::uint64_t x = 0; x < part->rows; ++x)
+            for (std::uint64_t y = 0; y < part->cols; ++y) {
+                if (pi + x < si || pi + x >= si + s.rows || pj + y < sj || pj + y >= sj + s.cols) return false;
+                auto& cell = mark[(pi + x) * p.n + (pj + y)];
+                if (cell == stamp) return false;
+                cell = stamp;
+                ++covered;
+            }
+    }
+    return covered == s.rows * s.cols;
+}
+
+std::vector<std::uint64_t> tile_sides(std::uint64_t n) {
+    std::vector<std::uint64_t> out;
+    for (std::uint64_t t = n;; t /= 2) {
+        out.push_back(t);
+        if (t % 2 != 0) break;
+    }
+    return out;
+}
+
+void test_acceptance_codec() {  // acceptance_main.cpp:43-60 (criterion 1)
+    bool ok = true;
+    for (std::uint64_t n = 1; n <= 256 && ok; ++n)
+        for (std::uint64_t t : tile_sides(n)) {
+            const mh::Layout p(n, t);
+            std::vector<bool> seen(n * n, false);
+            for (std::uint64_t i = 0; i < n && ok; ++i)
+                for (std::uint64_t j = 0; j < n; ++j) {
+                    std::uint64_t z = 0, ii = 0, jj = 0;
+                    // raw C ABI: the codec without exception plumbing per cell
+                    ok = ok && mhg_encode(n, t, i, j, &z) == MHG_OK && z < n * n && !seen[z];
+                    if (!ok) break;
+                    seen[z] = true;
+                    ok = ok && mhg_extract(n, t, z, &ii, &jj) == MHG_OK && ii == i && jj == j;
+                }
+        }
+    CHECK(ok);
+}
+
+void test_acceptance_partition() {  // acceptance_main.cpp:103-162 (criterion 2), submatrix_test.cpp:170-249
+    bool ok = true;
+    for (std::uint64_t n = 1; n <= 64 && ok; ++n)
+        for (std::uint64_t t : tile_sides(n)) {
+            mh::Matrix m(mh::Layout(n, t), mh::Modulus(2));
+            const mh::Layout& p = m.layout();
+            std::vector<std::uint32_t> mark(n * n, 0);
+            std::uint32_t stamp = 0;
+            std::mt19937_64 sample_eng(n * 1000 + t);
+            for (std::uint64_t elems = p.tile; elems <= p.total && ok; elems *= 4)
+                for (std::uint64_t origin = 0; origin < p.total && ok; origin += elems) {
+                    const mh::Aligned a{&m, origin, elems};
+                    std::vector<mh::Aligned> stack{a};  // recursion ends in whole, contained tiles
+                    while (!stack.empty() && ok) {
+                        const mh::Aligned blk = stack.back();
+                        stack.pop_back();
+                        if (blk.elems == p.tile) {
+                            ok = blk.origin % p.tile == 0 && mh::is_contained(mh::Sub{&m, blk.origin, p.t, p.t});
+                            continue;
+                        }
+                        for (const auto& child : mh::quadrants(blk)) stack.push_back(child);
+                    }
+                    if (elems == p.tile) {  // views inside a tile-level block are contained
+                        const auto bi = mh::extract_i(p, origin), bj = mh::extract_j(p, origin);
+                        if (n <= 8)
+                            for (std::uint64_t di = 0; di < p.t; ++di)
+                                for (std::uint64_t dj = 0; dj < p.t; ++dj)
+                                    for (std::uint64_t r = 1; di + r <= p.t; ++r)
+                                        for (std::uint64_t c = 1; dj + c <= p.t; ++c)
+                                            ok = ok && mh::is_contained(sub_at(m, bi + di, bj + dj, r, c));
+                        continue;
+                    }
+                    const auto side = mh::aligned_side(a);
+                    const auto ai = mh::extract_i(p, origin), aj = mh::extract_j(p, origin);
+                    if (n <= 16) {
+                        for (std::uint64_t si = ai; si < ai + side && ok; ++si)
+                            for (std::uint64_t sj = aj; sj < aj + side && ok; ++sj)
+                                for (std::uint64_t r = 1; si + r <= ai + side && ok; ++r)
+                                    for (std::uint64_t c = 1; sj + c <= aj + side && ok; ++c)
+                                        ok = partition_ok(m, a, sub_at(m, si, sj, r, c), mark, stamp);
+                    } else {
+                        ok = partition_ok(m, a, mh::Sub{&m, origin, side, side}, mark, stamp);
+                        for (int k = 0; k < 8 && ok; ++k) {
+                            const auto r = 1 + sample_eng() % side, c = 1 + sample_eng() % side;
+                            const auto si = ai + sample_eng() % (side - r + 1), sj = aj + sample_eng() % (side - c + 1);
+                            ok = partition_ok(m, a, sub_at(m, si, sj, r, c), mark, stamp);
+                        }
+                    }
+                }
+        }
+    CHECK(ok);
 }
 
 }  // namespace
@@ -223,6 +604,16 @@ int main() {
         {"oblivious_random", test_oblivious_random},
         {"default_leaf_counts", test_default_leaf_counts},
         {"host_edits_and_copies", test_host_edits_and_copies},
+        {"compatible_parts", test_compatible_parts},
+        {"base_case_mm", test_base_case_mm},
+        {"naive_default_jumps", test_naive_default_jumps},
+        {"scattered_default_run", test_scattered_default_run},
+        {"work_is_exact", test_work_is_exact},
+        {"alignment_and_containment", test_alignment_and_containment},
+        {"quadrant_order", test_quadrant_order},
+        {"split_edge_cases", test_split_edge_cases},
+        {"acceptance_codec", test_acceptance_codec},
+        {"acceptance_partition", test_acceptance_partition},
     };
     for (const auto& [name, fn] : tests) {
         const int before = g_fail;

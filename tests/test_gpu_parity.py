@@ -183,10 +183,10 @@ def _constant_case(mh, n, t, q, a, b, c0, k, op):
 
 
 @pytest.mark.parametrize("udig", ["0", "1"])
-def test_adversarial_extreme_digits(gpu, mh, monkeypatch, udig):
+def test_adversarial_extreme_digits(gpu, mh, opts, udig):
     """Extreme-magnitude digits in every limb position (balanced s8 digits with
-    MHG_UDIG=0, u8 digits by default), all three ops."""
-    monkeypatch.setenv("MHG_UDIG", udig)
+    MHG_OPT_DIGITS = 0, u8 digits by default), all three ops."""
+    opts(mh.OPT_DIGITS, int(udig))
     for q, vals in EXTREMES.items():
         for a in vals:
             for b in vals[:3]:
@@ -204,13 +204,13 @@ def _extremes(q):
 @pytest.mark.parametrize("udig", ["0", "1"])
 @pytest.mark.parametrize("q,k", [(65287, 512), (65287, 640), (65519, 1024), (257, 1024), (65521, 4096),
                                  (65521, 8192)])
-def test_single_reduction_fold_bound(gpu, mh, monkeypatch, q, k, udig):
+def test_single_reduction_fold_bound(gpu, mh, opts, q, k, udig):
     """Fold level 1 (single reduction, L=2) at the edge of its K bound:
     q = 65287 has 2^16 mod q = 249, so K = 512 is the largest chunk the host
     admits for s8 digits (K = 640 falls back to the per-class fold); the u8 levels'
     edges differ (mhg_fold_level_u8: 65521 on level 1 up to K = 4096); extreme
     digits, all ops."""
-    monkeypatch.setenv("MHG_UDIG", udig)
+    opts(mh.OPT_DIGITS, int(udig))
     ex = _extremes(q)
     for a in ex:
         for b in ex[:2]:
@@ -220,11 +220,11 @@ def test_single_reduction_fold_bound(gpu, mh, monkeypatch, q, k, udig):
 
 @pytest.mark.parametrize("udig", ["0", "1"])
 @pytest.mark.parametrize("level", ["2", "3"])
-def test_forced_fold_levels(gpu, mh, monkeypatch, level, udig):
-    """Fold levels 2 and 3 forced (MHG_FOLD) where level 1 would be chosen:
+def test_forced_fold_levels(gpu, mh, opts, level, udig):
+    """Fold levels 2 and 3 forced (MHG_OPT_MIN_FOLD_LEVEL) where level 1 would be chosen:
     the same exact results through every lean-fold arithmetic variant."""
-    monkeypatch.setenv("MHG_FOLD", level)
-    monkeypatch.setenv("MHG_UDIG", udig)
+    opts(mh.OPT_MIN_FOLD_LEVEL, int(level))
+    opts(mh.OPT_DIGITS, int(udig))
     for q in (P16, 65287, 257):
         ex = _extremes(q)
         for a, b in [(ex[0], ex[0]), (ex[1], ex[0]), (ex[2], ex[4])]:
@@ -233,9 +233,9 @@ def test_forced_fold_levels(gpu, mh, monkeypatch, level, udig):
 
 
 @pytest.mark.slow
-def test_single_reduction_fold_at_k8064(gpu, mh, monkeypatch):
+def test_single_reduction_fold_at_k8064(gpu, mh, opts):
     """p = 65521, s8 digits: the largest single-chunk K on fold level 1 (63 k-tiles)."""
-    monkeypatch.setenv("MHG_UDIG", "0")
+    opts(mh.OPT_DIGITS, 0)
     ex = _extremes(P16)
     for a, b in [(ex[0], ex[0]), (ex[1], ex[0]), (ex[0], ex[1])]:
         _constant_case(mh, 8192, 64, P16, a, b, P16 - 1, 8064, OP_SUB)
@@ -243,23 +243,137 @@ def test_single_reduction_fold_at_k8064(gpu, mh, monkeypatch):
 
 @pytest.mark.slow
 @pytest.mark.parametrize("udig", ["0", "1"])
-def test_adversarial_int32_headroom(gpu, mh, monkeypatch, udig):
+def test_adversarial_int32_headroom(gpu, mh, opts, udig):
     """K = 32768 (cfg5's inner length) with extreme digits: the int32 class
     sums reach ~75% (q = 2^31-1) of the bound the planner sized chunks for (s8; u8
     digits take 2 / 4 chunks of 16,384 / 8,256)."""
-    monkeypatch.setenv("MHG_UDIG", udig)
+    opts(mh.OPT_DIGITS, int(udig))
     for q in (P16, P31):
         for a, b in [(EXTREMES[q][0], EXTREMES[q][0]), (EXTREMES[q][1], EXTREMES[q][0])]:
             _constant_case(mh, 32768, 64, q, a, b, 1, 32768, OP_SUB)
 
 
+def _u8_chunk_slices(q):
+    """128-byte K slices per exact u8 chunk: (2^31 - 2^17) / (L * 255^2), the planner's
+    bound for unsigned digits (mhg_planner.cpp gemm_geometry)."""
+    L = mh_limbs(q)
+    return ((1 << 31) - (1 << 17)) // (L * 255 * 255) // 128
+
+
+def mh_limbs(q):
+    L = 1
+    while q > 256 ** L:
+        L += 1
+    return L
+
+
+# Residues whose packed u8 digits are the largest the field allows: for p = 65521 the
+# class-1 sum a0 b1 + a1 b0 peaks at 2 * 255 * 254 per k with 0xFEFF x 0xFEFF (99.6% of
+# the 2 * 255^2 the chunk bound assumes); p - 1 = 0xFFF0 has the top digit 255.  For
+# p = 2^31 - 1 the top digit is at most 127, so the widest classes peak at ~75%.
+U8_MAX_DIGITS = {P16: (0xFEFF, P16 - 1, 0xFEFE), P31: (P31 - 1, 0x7EFFFFFF, 0x7FFFFEFF)}
+
+
+def _device_constant_case(mh, n, t, q, a, b, c0, rows, k, cols, op, bufs):
+    """Device-filled version of _constant_case for containers too large to stage on the
+    host: out (rows x cols at the origin, all c0) op= lhs (rows x k, all a) * rhs (k x
+    cols, all b).  The view is an aligned power-of-two block at (0, 0), so it is the flat
+    range [0, rows*cols) of the output container; every view cell must equal
+    c0 +/- k a b mod q and every other cell must still be c0."""
+    import torch
+    fo, fa, fb = bufs
+    fo.fill_(int(c0))
+    fa.fill_(int(a))
+    fb.fill_(int(b))
+    lay, mod = mh.Layout(n, t), mh.Modulus(q)
+    A, B, Cm = (mh.Matrix.wrap(lay, mod, f.data_ptr(), owner=f) for f in bufs)
+    mh.mm(mh.Problem(mh.Sub(A, 0, rows, cols), mh.Sub(B, 0, rows, k), mh.Sub(Cm, 0, k, cols)), op)
+    prod = (k * a * b) % q
+    want = {OP_ADD: (c0 + prod) % q, OP_SUB: (c0 - prod) % q, OP_SET: prod}[op]
+    torch.cuda.synchronize()
+    view = fo[:rows * cols]
+    bad_view = int((view != int(want)).sum())
+    bad_rest = int((fo[rows * cols:] != int(c0)).sum())
+    assert bad_view == 0 and bad_rest == 0, (q, a, b, k, op, bad_view, bad_rest,
+                                             int(view[0]) & 0xFFFFFFFF, want)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("udig", [None, 0])
+def test_u8_headroom_at_exact_chunk(gpu, mh, opts, udig):
+    """SURVEY 8(c) 'adversarial max-limb inputs at the largest K per chunk', for the
+    default u8 digits: K = one full exact chunk (p = 65521: 128 slices = 16,384, the
+    north star's K; p = 2^31-1: 64 slices = 8,192) and one slice past it (two chunks),
+    plus K = 16,384 for p = 2^31-1, with max-digit residues on both operands
+    (for C -= A.B the lhs is p - x so that its packed digits are x's), C_old = p - 1,
+    ADD / SUB / SET; digits as the planner picks them (udig None) and balanced s8."""
+    import torch
+    if udig is not None:
+        opts(mh.OPT_DIGITS, udig)
+    n, t, rows, cols = 32768, 64, 1024, 1024
+    bufs = [torch.empty(n * n, dtype=torch.int32, device="cuda") for _ in range(3)]
+    try:
+        for q in (P16, P31):
+            kc = _u8_chunk_slices(q) * 128
+            ks = sorted({kc, kc + 128, 16384})
+            vals = U8_MAX_DIGITS[q]
+            for k in ks:
+                for x, y in [(vals[0], vals[0]), (vals[0], vals[1]), (vals[1], vals[2])]:
+                    for op in (OP_ADD, OP_SUB, OP_SET):
+                        a = (q - x) % q if op == OP_SUB else x  # packed lhs digits = x's
+                        _device_constant_case(mh, n, t, q, a, y, q - 1, rows, k, cols, op, bufs)
+    finally:
+        del bufs
+        torch.cuda.empty_cache()
+
+
+def test_u8_chunk_bound_is_the_planner_bound(gpu, mh):
+    """The K chunks the headroom test targets are exactly the planner's: one chunk at
+    K = 16,384 (p = 65521) / 8,192 (p = 2^31-1), two one slice later."""
+    def chunks(q, k):
+        lay, mod = mh.Layout(16384 * 2, 64), mh.Modulus(q)
+        A, B, C = (mh.Matrix(lay, mod) for _ in range(3))
+        return mh.Plan(mh.Problem(mh.Sub(A, 0, 128, 128), mh.Sub(B, 0, 128, k),
+                                  mh.Sub(C, 0, k, 128)), mh.OP_SUB).info()["k_chunks"]
+    assert _u8_chunk_slices(P16) == 128 and _u8_chunk_slices(P31) == 64
+    for q in (P16, P31):
+        kc = _u8_chunk_slices(q) * 128
+        assert chunks(q, kc) == 1 and chunks(q, kc + 128) == 2
+
+
+@pytest.mark.slow
+def test_north_star_u8_equals_s8(gpu, mh, opts):
+    """The bench workload (n = 16384, p = 65521, C -= A.B, uniform residues) with u8
+    and with balanced s8 digits: byte-identical output containers."""
+    import torch
+    n, t, q = 16384, 64, P16
+    g = torch.Generator(device="cuda").manual_seed(2024)
+    src = [torch.randint(0, q, (n * n,), dtype=torch.int32, device="cuda", generator=g) for _ in range(3)]
+    outs = []
+    for digits in (1, 0):
+        opts(mh.OPT_DIGITS, digits)
+        fo = src[0].clone()
+        lay, mod = mh.Layout(n, t), mh.Modulus(q)
+        A = mh.Matrix.wrap(lay, mod, fo.data_ptr(), owner=fo)
+        B = mh.Matrix.wrap(lay, mod, src[1].data_ptr(), owner=src[1])
+        C = mh.Matrix.wrap(lay, mod, src[2].data_ptr(), owner=src[2])
+        plan = mh.Plan(mh.Problem(mh.Sub(A, 0, n, n), mh.Sub(B, 0, n, n), mh.Sub(C, 0, n, n)), OP_SUB)
+        assert plan.info()["digits"] == ("u8" if digits else "s8")
+        plan.run()
+        torch.cuda.synchronize()
+        outs.append(fo)
+        del plan
+    assert torch.equal(outs[0], outs[1])
+    assert not torch.equal(outs[0], src[0])
+
+
 @pytest.mark.parametrize("udig", ["0", "1"])
-def test_k_chunking(gpu, mh, oracle, monkeypatch, udig):
+def test_k_chunking(gpu, mh, oracle, opts, udig):
     """Multi-chunk accumulation (each exact int32 K-chunk drained and folded into
     the output before the next): forced to 2 K-slices per chunk so small
     problems take the path n >= 65536 would take for q = 2^31-1."""
-    monkeypatch.setenv("MHG_FORCE_KCHUNK", "2")
-    monkeypatch.setenv("MHG_UDIG", udig)
+    opts(mh.OPT_MAX_KCHUNK, 2)
+    opts(mh.OPT_DIGITS, int(udig))
     rng = np.random.default_rng(77)
     for q in (P16, P31):
         for op in (OP_ADD, OP_SUB, OP_SET):
@@ -423,12 +537,12 @@ def test_tu_schur_sweep(gpu, mh, oracle):
     assert macs == sum(((n - k) ** 2) * block for k in range(block, n, block))
 
 
-@pytest.mark.parametrize("kernel", ["1cta", "2cta", "2cta2", "mc"])
-def test_both_gemm_kernels(gpu, mh, oracle, monkeypatch, kernel):
-    """The single-CTA (default), CTA-pair (cta_group::2, MHG_GEMM=2cta) and
-    column-pair multicast-cluster (MHG_GEMM=mc) kernels on ragged views, every
-    limb count, all ops, forced K-chunking."""
-    monkeypatch.setenv("MHG_GEMM", kernel)
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_both_gemm_kernels(gpu, mh, oracle, opts, kernel):
+    """The single-CTA (k_gemm) and CTA-pair (k_gemm2, cta_group::2) kernels
+    (MHG_OPT_GEMM_KERNEL = 1 / 2) on ragged views, every limb count, all ops, forced
+    K-chunking."""
+    opts(mh.OPT_GEMM_KERNEL, kernel)
     rng = np.random.default_rng(5)
     for q in (97, P16, P24, P31):
         for op in (OP_ADD, OP_SUB, OP_SET):
@@ -438,9 +552,9 @@ def test_both_gemm_kernels(gpu, mh, oracle, monkeypatch, kernel):
             v = _views_from(oracle, n, t, r, k, c, corners)
             out, lhs, rhs = _fill(oracle, 40 + op, n, q)
             if op == OP_SUB:
-                monkeypatch.setenv("MHG_FORCE_KCHUNK", "1")
+                opts(mh.OPT_MAX_KCHUNK, 1)
             got, _ = _run_gpu(mh, n, t, q, out, lhs, rhs, v, op)
-            monkeypatch.delenv("MHG_FORCE_KCHUNK", raising=False)
+            opts(mh.OPT_MAX_KCHUNK, 0)
             want = out.copy()
             oracle.mm_dense(n, t, q, want, lhs, rhs, v, op=op)
             assert np.array_equal(got, want), (kernel, q, op, t, v)
@@ -491,14 +605,14 @@ def test_plan_graph_replay_matches_direct(gpu, mh, oracle):
     assert plan.info()["launches"] == 2  # k_pack_pair + k_gemm
 
 
-@pytest.mark.parametrize("kernel", ["1cta", "2cta", "2cta2", "mc"])
-def test_guard_bands(gpu, mh, oracle, monkeypatch, kernel):
+@pytest.mark.parametrize("kernel", [1, 2])
+def test_guard_bands(gpu, mh, oracle, opts, kernel):
     """Out-of-bounds detector (compute-sanitizer is unavailable on this pool):
     each container is wrapped in the middle of a larger device buffer whose
     guard zones hold a sentinel; after multiplies with ragged views, every
     guard word is intact and the result equals the oracle."""
     import torch
-    monkeypatch.setenv("MHG_GEMM", kernel)
+    opts(mh.OPT_GEMM_KERNEL, kernel)
     n, t, guard = 256, 32, 1 << 16
     sentinel = 0x5A5A5A5A
     for q in (97, P16, P31):
@@ -684,7 +798,7 @@ def test_upload_wire16_equals_plain_copy(gpu, mh, n, t, q, bad):
     m = mh.Matrix(mh.Layout(n, t), mh.Modulus(q))
     m.upload(cells)
     assert np.array_equal(m.cells(), cells)
-    chunk, total = 1 << 22, n * n  # default MHG_UPLOAD_CHUNK_LOG2
+    chunk, total = 1 << 22, n * n  # the wire's staging chunk (mhg_wire.cpp)
     if q > 65536:
         assert m.upload_bytes == 4 * total
     else:
@@ -762,90 +876,48 @@ def test_concurrent_uploads_from_threads(gpu, mh):
         assert m.upload_bytes <= 2 * n * n  # the last (range or full) upload was narrow
 
 
-@pytest.mark.parametrize("q", [P16, 65287, 40961, 257])
-def test_two_class_accumulation(gpu, mh, oracle, monkeypatch, q):
-    """MHG_GEMM=2cta2: the CTA pair with two-class accumulation (limb s multiplies
-    the digits of 256^s b mod q; S = lo + 256 hi; two TMEM jobs double-buffered).
-    Lean one-reduction fold (2^16 mod q < 256: 65521, 65287, 257) and the general
-    fold (40961); random misaligned views incl. multi-chunk K; extreme digits at a
-    long K (closed form)."""
-    monkeypatch.setenv("MHG_GEMM", "2cta2")
-    rng = np.random.default_rng(q)
+@pytest.mark.parametrize("conv", [0, 1, 2])
+def test_conversion_kernel_variants(gpu, mh, oracle, opts, conv):
+    """K1 on device buffers through the C ABI: the TMA kernel (MHG_OPT_CONV_KERNEL = 0,
+    default; units of R rows x t columns, R < t from t = 128 on), the Morton-order
+    LDG/STG kernel (1) and the row-order one (2), for t = 4 ... 256 and a
+    non-power-of-two tile (fallback); round trip exact; an out-of-range residue in the
+    last unit is reported; misaligned row buffers fall back."""
+    import torch
+    opts(mh.OPT_CONV_KERNEL, conv)
+    lib = mh.lib()
+    for (n, t) in [(8, 4), (64, 8), (1024, 32), (2048, 64), (2048, 128), (4096, 256), (96, 6)]:
+        q = 65521
+        rng = np.random.default_rng(n + t)
+        grid = rng.integers(0, q, size=(n, n), dtype=np.uint32)
+        m = mh.Matrix(mh.Layout(n, t), mh.Modulus(q))
+        rm = torch.from_numpy(grid.reshape(-1).view(np.int32)).cuda()
+        assert lib.mhg_rowmajor_to_mh(m.handle, rm.data_ptr(), None) == 0
+        assert np.array_equal(m.cells(), oracle.rowmajor_to_mh(n, t, grid)), (n, t)
+        back = torch.zeros_like(rm)
+        assert lib.mhg_mh_to_rowmajor(m.handle, back.data_ptr(), None) == 0
+        torch.cuda.synchronize()
+        assert np.array_equal(back.cpu().numpy().view(np.uint32).reshape(n, n), grid), (n, t)
+        bad = rm.clone()
+        bad[-1] = q
+        assert lib.mhg_rowmajor_to_mh(m.handle, bad.data_ptr(), None) == 1, (n, t)
+    # misaligned row-major buffer (4-byte offset): LDG/STG fallback, same result
     n, t = 1024, 64
-    for op in (OP_ADD, OP_SUB, OP_SET):
-        for force in (None, "2"):
-            if force:
-                monkeypatch.setenv("MHG_FORCE_KCHUNK", force)
-            else:
-                monkeypatch.delenv("MHG_FORCE_KCHUNK", raising=False)
-            r, k, c, corners = _random_views(rng, n)
-            v = _views_from(oracle, n, t, r, k, c, corners)
-            out, lhs, rhs = _fill(oracle, 70 + op, n, q)
-            got, _ = _run_gpu(mh, n, t, q, out, lhs, rhs, v, op)
-            want = out.copy()
-            oracle.mm_dense(n, t, q, want, lhs, rhs, v, op=op)
-            assert np.array_equal(got, want), (q, op, force, r, k, c)
-    monkeypatch.delenv("MHG_FORCE_KCHUNK", raising=False)
-    ex = _extremes(q)
-    for a, b in [(ex[0], ex[0]), (ex[1], ex[0]), (ex[2], ex[4]), (ex[1], ex[1])]:
-        for op in (OP_ADD, OP_SUB):
-            _constant_case(mh, 8192, 64, q, a, b, q - 1, 8192, op)
+    grid = np.random.default_rng(1).integers(0, 97, size=(n, n), dtype=np.uint32)
+    m = mh.Matrix(mh.Layout(n, t), mh.Modulus(97))
+    buf = torch.zeros(n * n + 1, dtype=torch.int32, device="cuda")
+    buf[1:] = torch.from_numpy(grid.reshape(-1).view(np.int32)).cuda()
+    assert lib.mhg_rowmajor_to_mh(m.handle, buf.data_ptr() + 4, None) == 0
+    assert np.array_equal(m.cells(), oracle.rowmajor_to_mh(n, t, grid))
 
 
-@pytest.mark.parametrize("conv", ["3", "2", "0"])
-def test_conversion_kernel_variants(gpu, mh, oracle, monkeypatch, conv):
-    """K1 on device buffers through the C ABI: the TMA kernel (MHG_CONV=3, default;
-    units of R rows x t columns, R < t from t = 128 on), the Morton-order LDG/STG
-    kernel (2) and the row-order one (0), for t = 4 ... 256 and a non-power-of-two
-    tile (fallback); round trip exact; an out-of-range residue in the last unit
-    is reported; misaligned row buffers fall back."""
-    import subprocess
-    import sys
-    # the conversion mode is read once per process: run the cases in a child
-    code = f"""
-import numpy as np, torch, sys
-sys.path.insert(0, {repr(str(__import__('pathlib').Path(__file__).resolve().parents[1]))})
-import paper_1705_04807_b200 as mh
-from oracle.binding import Oracle
-orc = Oracle()
-lib = mh.lib()
-for (n, t) in [(8, 4), (64, 8), (1024, 32), (2048, 64), (2048, 128), (4096, 256), (96, 6)]:
-    q = 65521
-    rng = np.random.default_rng(n + t)
-    grid = rng.integers(0, q, size=(n, n), dtype=np.uint32)
-    m = mh.Matrix(mh.Layout(n, t), mh.Modulus(q))
-    rm = torch.from_numpy(grid.reshape(-1).view(np.int32)).cuda()
-    assert lib.mhg_rowmajor_to_mh(m.handle, rm.data_ptr(), None) == 0
-    assert np.array_equal(m.cells(), orc.rowmajor_to_mh(n, t, grid)), (n, t)
-    back = torch.zeros_like(rm)
-    assert lib.mhg_mh_to_rowmajor(m.handle, back.data_ptr(), None) == 0
-    torch.cuda.synchronize()
-    assert np.array_equal(back.cpu().numpy().view(np.uint32).reshape(n, n), grid), (n, t)
-    bad = rm.clone()
-    bad[-1] = q
-    assert lib.mhg_rowmajor_to_mh(m.handle, bad.data_ptr(), None) == 1, (n, t)
-# misaligned row-major buffer (4-byte offset): LDG/STG fallback, same result
-n, t = 1024, 64
-grid = np.random.default_rng(1).integers(0, 97, size=(n, n), dtype=np.uint32)
-m = mh.Matrix(mh.Layout(n, t), mh.Modulus(97))
-buf = torch.zeros(n * n + 1, dtype=torch.int32, device="cuda")
-buf[1:] = torch.from_numpy(grid.reshape(-1).view(np.int32)).cuda()
-assert lib.mhg_rowmajor_to_mh(m.handle, buf.data_ptr() + 4, None) == 0
-assert np.array_equal(m.cells(), orc.rowmajor_to_mh(n, t, grid))
-print("ok")
-"""
-    env = dict(__import__("os").environ, MHG_CONV=conv)
-    out = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600)
-    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-3000:]
-
-
-def test_planner_kernel_policy(gpu, mh, monkeypatch):
-    """mhg_plan_variant: u8 digits by default (s8 with MHG_UDIG=0); the CTA pair for
-    3- and 4-limb primes, the single CTA for 1-2 limbs (MHG_GEMM overrides); u8 chunks
+def test_planner_kernel_policy(gpu, mh, opts):
+    """mhg_plan_variant: u8 digits by default (s8 with MHG_OPT_DIGITS = 0); the CTA pair
+    for 3- and 4-limb primes, the single CTA for 1-2 limbs (MHG_OPT_GEMM_KERNEL overrides); u8 chunks
     of (2^31 - 2^17) / (L * 255^2).  (Every combination's results are pinned by the
     parity tests.)"""
-    monkeypatch.delenv("MHG_UDIG", raising=False)
-    monkeypatch.delenv("MHG_GEMM", raising=False)
+    opts(mh.OPT_DIGITS, 1)
+    opts(mh.OPT_GEMM_KERNEL, 0)
 
     def variant(q, k, n=8192):
         lay, mod = mh.Layout(n, 64), mh.Modulus(q)
@@ -861,8 +933,51 @@ def test_planner_kernel_policy(gpu, mh, monkeypatch):
     assert variant(97, 512) == ("u8", 1, 1)
     assert variant(P16, 16384, n=16384) == ("u8", 1, 1)   # 16,384 = one u8 chunk at L = 2
     assert variant(P31, 16384, n=16384) == ("u8", 2, 2)   # 8,256 per chunk at L = 4
-    monkeypatch.setenv("MHG_UDIG", "0")
+    opts(mh.OPT_DIGITS, 0)
     assert variant(P16, 8192)[0] == "s8"
     assert variant(P31, 16384, n=16384) == ("s8", 2, 1)
-    monkeypatch.setenv("MHG_GEMM", "1cta")
+    opts(mh.OPT_GEMM_KERNEL, 1)
     assert variant(P31, 1024)[1] == 1
+
+
+@pytest.mark.parametrize("q", [P16, P31, 97])
+def test_device_verify(gpu, mh, oracle, q):
+    """mhg_verify (Freivalds on the device): accepts every exact result -- ADD / SUB /
+    SET, misaligned views -- and rejects a result with one corrupted view cell."""
+    import torch
+    rng = np.random.default_rng(q)
+    n, t = 512, 32
+    rounds = 2 if q > 1000 else 12
+    for op in (OP_ADD, OP_SUB, OP_SET):
+        r, k, c, corners = _random_views(rng, n)
+        v = _views_from(oracle, n, t, r, k, c, corners)
+        out, lhs, rhs = _fill(oracle, 500 + op, n, q)
+        A, B, Cm, old = _containers(mh, n, t, q, (out, lhs, rhs, out))
+        prob = mh.Problem(mh.Sub(A, v.out_origin, v.rows, v.cols), mh.Sub(B, v.lhs_origin, v.rows, v.inner),
+                          mh.Sub(Cm, v.rhs_origin, v.inner, v.cols))
+        mh.mm(prob, op)
+        old_view = mh.Sub(old, v.out_origin, v.rows, v.cols)
+        assert mh.verify(prob, old_view, op, rounds=rounds)
+        # corrupt one cell inside the view
+        cells = A.cells()
+        z = oracle.encode(n, t, corners[0] + r // 2, corners[1] + c // 2)
+        cells[z] = (int(cells[z]) + 1) % q
+        A.upload(cells)
+        assert not mh.verify(prob, old_view, op, rounds=rounds)
+    torch.cuda.synchronize()
+
+
+def test_device_verify_north_star(gpu, mh):
+    """mhg_verify at the bench size (n = 16384, C -= A.B): exact result accepted."""
+    import torch
+    n, t, q = 16384, 64, P16
+    g = torch.Generator(device="cuda").manual_seed(7)
+    f = [torch.randint(0, q, (n * n,), dtype=torch.int32, device="cuda", generator=g) for _ in range(3)]
+    f0 = f[0].clone()
+    lay, mod = mh.Layout(n, t), mh.Modulus(q)
+    A, B, Cm, old = (mh.Matrix.wrap(lay, mod, x.data_ptr(), owner=x) for x in (f[0], f[1], f[2], f0))
+    prob = mh.Problem(mh.Sub(A, 0, n, n), mh.Sub(B, 0, n, n), mh.Sub(Cm, 0, n, n))
+    mh.mm(prob, OP_SUB)
+    assert mh.verify(prob, mh.Sub(old, 0, n, n), OP_SUB)
+    f[0][12345] = (f[0][12345] + 1) % q
+    assert not mh.verify(prob, mh.Sub(old, 0, n, n), OP_SUB)

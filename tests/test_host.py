@@ -290,3 +290,72 @@ def test_fold_levels_u8_exact_at_their_bounds(mh, q):
         assert 2 in seen  # every u8 chunk has a lean fold
     else:
         assert seen == {3}
+
+
+def test_naive_default_counters_equal_reference(mh, reference):
+    """mm_naive / mm_default Counters (multiply.hpp:269-291) in closed form -- incl.
+    max_consecutive_jump of their encode-addressed walks (:80-129) -- equal the
+    reference's own on random problems whose three containers differ in n and t (the
+    two kernels have no layout guard), power-of-two and other tile sides."""
+    rng = np.random.default_rng(20261020)
+    for _ in range(300):
+        geos = []
+        for _ in range(3):
+            t = int(rng.choice([1, 2, 3, 4, 5, 8, 16]))
+            geos.append((t << int(rng.integers(0, 4)), t))
+        r = int(rng.integers(1, min(geos[0][0], geos[1][0]) + 1))
+        c = int(rng.integers(1, min(geos[0][0], geos[2][0]) + 1))
+        k = int(rng.integers(1, min(geos[1][0], geos[2][0]) + 1))
+
+        def corner(g, rows, cols):
+            n, t = g
+            return (n, t, mh.encode(mh.Layout(n, t), int(rng.integers(0, n - rows + 1)),
+                                    int(rng.integers(0, n - cols + 1))))
+        go, gl, gr = corner(geos[0], r, c), corner(geos[1], r, k), corner(geos[2], k, c)
+        for kind, flag in ((0, mh.KERNEL_NAIVE), (1, mh.KERNEL_DEFAULT)):
+            want = reference.counters_mixed(kind, go, gl, gr, r, k, c).as_tuple()
+            got = mh.counters_geometry(flag, go, gl, gr, r, k, c).as_tuple()
+            assert got == want, (kind, go, gl, gr, r, k, c)
+
+
+def test_naive_default_counters_on_acceptance_draws(mh, oracle, reference):
+    """The same on the reference's acceptance draws (gen_problem, same layouts), and the
+    scattered default run of multiply_test.cpp:409-424 (jump > t, encodes > 0)."""
+    for (n, t, seed, count) in [(64, 8, 11, 30), (128, 16, 12, 10), (96, 3, 13, 20)]:
+        g = oracle.rng(seed)
+        for _ in range(count):
+            _, _, _, _, v = oracle.gen_problem(g, n, t, 2)
+            for kind, flag in ((0, mh.KERNEL_NAIVE), (1, mh.KERNEL_DEFAULT)):
+                want = reference.counters_mixed(kind, (n, t, v.out_origin), (n, t, v.lhs_origin),
+                                                (n, t, v.rhs_origin), v.rows, v.inner, v.cols)
+                got = mh.counters_geometry(flag, (n, t, v.out_origin), (n, t, v.lhs_origin),
+                                           (n, t, v.rhs_origin), v.rows, v.inner, v.cols)
+                assert got.as_tuple() == want.as_tuple()
+    n, t = 64, 8
+    s = mh.encode(mh.Layout(n, t), t // 2, t // 2)
+    c = mh.counters_geometry(mh.KERNEL_DEFAULT, (n, t, s), (n, t, s), (n, t, s), 2 * t, 2 * t, 2 * t)
+    assert c.max_consecutive_jump > t and c.encode_calls > 0
+
+
+def test_product_rng_reproduces_reference_draws(mh, oracle):
+    """mhg_rng (mh::Rng, bench.hpp:44-52) in the product library: the seed-0 first
+    gen_problem draw of bench_test.cpp:56-72 (descriptor triple and the container hash
+    4715125990397575263), and the same stream as the oracle's restatement."""
+    g = mh.Rng(0)
+    n = 64
+    assert int(g.below(8)[0]) != 0  # uniform mode
+    r, k, c = (1 + int(x) for x in g.below(n, 3))
+    ia = int(g.below(n - r + 1)[0]); ja = int(g.below(n - c + 1)[0])
+    ib = int(g.below(n - r + 1)[0]); jb = int(g.below(n - k + 1)[0])
+    ic = int(g.below(n - k + 1)[0]); jc = int(g.below(n - c + 1)[0])
+    lay = mh.Layout(n, 8)
+    assert (mh.encode(lay, ia, ja), r, c) == (1, 64, 39)
+    assert (mh.encode(lay, ib, jb), k) == (322, 3)
+    assert mh.encode(lay, ic, jc) == 2855
+    out = g.below(2, n * n)
+    h = 0
+    for x in out.tolist():
+        h = (h * 31 + x) & (2 ** 64 - 1)
+    assert h == 4715125990397575263
+    a, b = mh.Rng(12345), oracle.rng(12345)
+    assert np.array_equal(a.below(65521, 10000), oracle.fill_below(b, 10000, 65521))
