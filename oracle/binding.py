@@ -221,6 +221,7 @@ class Reference:
         L.ref_mm.argtypes = [C.c_int, U64, U64, C.c_uint32, U32P, U64, U64, U64, U32P, U64, U64,
                              U32P, U64, C.c_int, C.POINTER(Counters)]
         L.ref_counters_mixed.argtypes = [C.c_int] + [U64] * 12 + [C.POINTER(Counters)]
+        L.ref_save_matrix.argtypes = [U64, U64, C.c_uint32, U64, C.c_char_p]
         L.ref_gen_problem.argtypes = [U64, U64, C.c_uint32, U64, C.c_uint32, U32P, U32P, U32P,
                                       np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS")]
         L.ref_run_trials_csv.argtypes = [U64, U64, C.c_uint32, U64, C.c_uint32, C.c_int, C.c_char_p]
@@ -247,6 +248,12 @@ class Reference:
 
     def mm_oblivious(self, *a, **k):
         return self.mm(2, *a, **k)
+
+    def save_matrix(self, n, t, q, seed, path):
+        """The reference's save_matrix_file on an mh::Rng(seed)-filled container."""
+        st = self.lib.ref_save_matrix(n, t, q, seed, path.encode())
+        if st:
+            raise _status_error(st)
 
     def counters_mixed(self, kind, geo_out, geo_lhs, geo_rhs, rows, inner, cols) -> Counters:
         """Counters of mm_naive (kind 0) / mm_default (1); geo_* = (n, t, origin) per container."""

@@ -128,6 +128,17 @@ int ref_counters_mixed(int kind, std::uint64_t na, std::uint64_t ta, std::uint64
     });
 }
 
+// The reference's text writer (io.hpp:16-26, save_matrix_file :52-57) on a container
+// filled from mh::Rng(seed) in flat Morton order.
+int ref_save_matrix(std::uint64_t n, std::uint64_t t, std::uint32_t q, std::uint64_t seed, const char* path) {
+    return guarded([&] {
+        mh::Matrix m(mh::Layout(n, t), mh::Modulus(q));
+        mh::Rng rng(seed);
+        for (auto& v : m.cells()) v = mh::Fp{std::uint32_t(rng.below(q))};
+        mh::save_matrix_file(path, m);
+    });
+}
+
 // Draw the (skip+1)-th instance of Rng(seed) exactly as gen_problem does.
 int ref_gen_problem(std::uint64_t n, std::uint64_t t, std::uint32_t q, std::uint64_t seed,
                     std::uint32_t skip, std::uint32_t* out, std::uint32_t* lhs,

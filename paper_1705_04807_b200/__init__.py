@@ -405,7 +405,8 @@ def from_row_major(grid: np.ndarray, t: int, mod: Modulus) -> Matrix:
     lay = Layout(n, t)
     m = Matrix(lay, mod)
     dev = torch.from_numpy(g.view(np.int32)).cuda()
-    _check(lib().mhg_rowmajor_to_mh(m.handle, dev.data_ptr(), None))
+    # on torch's current stream: the buffer came from its caching allocator
+    _check(lib().mhg_rowmajor_to_mh(m.handle, dev.data_ptr(), torch.cuda.current_stream().cuda_stream))
     return m
 
 
@@ -414,7 +415,8 @@ def to_row_major(m: Matrix) -> np.ndarray:
     import torch
     n = m.layout().n
     dev = torch.empty(n * n, dtype=torch.int32, device="cuda")
-    _check(lib().mhg_mh_to_rowmajor(m.handle, dev.data_ptr(), None))
+    # on torch's current stream, which orders the write after earlier users of the block
+    _check(lib().mhg_mh_to_rowmajor(m.handle, dev.data_ptr(), torch.cuda.current_stream().cuda_stream))
     torch.cuda.synchronize()
     return dev.cpu().numpy().view(np.uint32).reshape(n, n)
 

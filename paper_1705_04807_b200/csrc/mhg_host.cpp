@@ -434,7 +434,7 @@ void launch_gemm_stage(const Buffers& b, const mhg_view& out, const Checked& c,
                        cudaEvent_t gemm_end) {
     mhg::GemmParams p = gemm_params(b, out, c, g, op);
     // diagnostics: MHG_OPT_GEMM_STATS = 1 prints per-CTA wait-cycle shares (synchronous)
-    const bool stats_on = mhg::option(mhg::kOptGemmStats) != 0;
+    const bool stats_on = mhg::option(mhg::kOptGemmStats) != 0 && mhg::diag_build();
     struct StatsBuf {  // freed on every path, including a failed launch
         unsigned long long* ptr = nullptr;
         ~StatsBuf() {
@@ -566,6 +566,9 @@ mhg_status mhg_set_option(int key, int64_t value) {
     return guarded([&] {
         if (!mhg::option_valid(key, value))
             fail(MHG_ERR_INVALID_ARGUMENT, "set_option: unknown key or value out of range");
+        if (key == mhg::kOptGemmStats && value && !mhg::diag_build())
+            fail(MHG_ERR_UNSUPPORTED, "set_option: GEMM wait-cycle counters are compiled only into "
+                                      "diagnostic builds (-DMHG_DIAG=1, profiles/build_variant.sh)");
         mhg::set_option(key, value);
     });
 }

@@ -123,6 +123,7 @@ struct PackArgs {
 int launch_pack_pair(int L, const PackArgs& lhs, const PackArgs& rhs, void* stream);
 int launch_gemm(int L, const GemmParams& p, int num_sms, void* stream);
 int gemm_smem_bytes(int L);
+int diag_build();  // 1 when the kernels carry the wait-cycle counters (-DMHG_DIAG=1)
 int configure_kernels();  // one-time kernel attributes (dynamic smem opt-in)
 // CTA-pair GEMM: tmA / tmB point to CUtensorMap (2D uint8, rows of 128 B; box
 // 128 rows for A, gemm2_b_box_rows(L) rows for B'); requires p.Mt even.

@@ -481,9 +481,33 @@ __device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity, u
         : "memory");
 }
 
+// Wait-cycle counters of the GEMM roles (MHG_OPT_GEMM_STATS, profiles/gemm_stats*.py) are
+// compiled only into diagnostic builds (-DMHG_DIAG=1, profiles/build_variant.sh): in the
+// product build diag_clock() is the constant 0, the counters fold away and take no
+// registers (they cost ~14 in the epilogue, where the 10-warp CTA is capped at 168).
+#ifndef MHG_DIAG
+#define MHG_DIAG 0
+#endif
+__device__ __forceinline__ long long diag_clock() {
+#if MHG_DIAG
+    return clock64();
+#else
+    return 0;
+#endif
+}
+
 // global C_old / C accesses of the coalesced epilogue: streaming (.cs) -- measured
 // best against default caching and L1::no_allocate (profiles/r01_epilogue_ab.txt)
 __device__ __forceinline__ uint4 c_load(const uint4* a) { return __ldcs(a); }
+
+// 16-byte global -> shared copy through the LSU (cp.async, no registers); src_bytes = 0
+// zero-fills the destination
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 
 __device__ __forceinline__ void c_store(uint4* a, uint4 v) { __stcs(a, v); }
 
@@ -1047,11 +1071,11 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         for (int j0 = 0; j0 < WH; j0 += CW) {
             if ((uint64_t)n_tile * W + jb + j0 >= p.cols) continue;  // warp-uniform
             int32_t a[2][CW];
-            const long long l0 = clock64();
+            const long long l0 = diag_clock();
             tmem_ld<CW>(tbase + lo_cls * W + j0, a[0]);
             tmem_ld<CW>(tbase + (lo_cls + 1) * W + j0, a[1]);
             tmem_wait_ld();
-            epi_ldw += clock64() - l0;
+            epi_ldw += diag_clock() - l0;
 #pragma unroll
             for (int j = 0; j < CW; ++j) cur_[j0 + j] += fold_g1(a[0][j], a[1][j], layout);
         }
@@ -1060,10 +1084,10 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         for (int j0 = 0; j0 < WH; j0 += CW) {
             if ((uint64_t)n_tile * W + jb + j0 >= p.cols) continue;
             int32_t a[1][CW];
-            const long long l0 = clock64();
+            const long long l0 = diag_clock();
             tmem_ld<CW>(tbase + (layout ? 2 : 0) * W + j0, a[0]);
             tmem_wait_ld();
-            epi_ldw += clock64() - l0;
+            epi_ldw += diag_clock() - l0;
 #pragma unroll
             for (int j = 0; j < CW; ++j) cur_[j0 + j] = fold_g2(cur_[j0 + j], a[0][j], layout);
         }
@@ -1149,44 +1173,8 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
             }
         }
     };
-    // coalesced C_old loads of `tile` for the vector lanes (no waits; edge
-    // lanes are filled element-wise when the tile is staged)
-    uint4 cold[XPOSE ? NH : 1][XPOSE ? NI : 1];
-    uint32_t cmask = 0;  // bit h*NI+i: cold[h][i] holds real data
-    // (always assigns cold -- past the last tile or for SET it is zeros -- so
-    // cold is dead between the staging and the next load)
-    auto load_cold = [&](uint32_t tile) {
-        const bool live = tile < num_tiles && p.mode != 2;
-        uint32_t lm = 0, ln = 0;
-        if (live) {
-            tile_coords(tile, row_groups, p.Nt, p.group, lm, ln);
-            if (PAIR) lm = 2 * lm + rank;  // this CTA's 128-row half of the pair tile
-        }
-        const uint64_t own = row_at(lm, row);
-        uint64_t c0[NH];
-        bool vec[NH];
-#pragma unroll
-        for (int h = 0; h < NH; ++h) {
-            c0[h] = col_at(ln, PW * h + 4 * ch, vec[h]);
-            vec[h] = vec[h] && live;
-        }
-        cmask = 0;
-#pragma unroll
-        for (int i = 0; i < NI; ++i) {
-            const uint64_t rb = __shfl_sync(0xffffffffu, own, RPI * i + sr);
-#pragma unroll
-            for (int h = 0; h < NH; ++h) {
-                // unconditional load (a dead lane reads cell 0 and is masked when
-                // staged): a predicated load would be followed by register moves
-                // that wait for it, serialising the loads
-                const bool ok = vec[h] && rb != kNoCol;
-                cmask |= (uint32_t)ok << (h * NI + i);
-                cold[h][i] = c_load(reinterpret_cast<const uint4*>(p.out + (ok ? rb + c0[h] : 0)));
-            }
-        }
-    };
     for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride) {
-        const long long tp0 = clock64();
+        const long long tp0 = diag_clock();
         uint32_t tm, n;
         tile_coords(tile, row_groups, p.Nt, p.group, tm, n);
         const uint32_t m = PAIR ? 2 * tm + rank : tm;
@@ -1195,42 +1183,10 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         bool row_ok = false;
         const uint64_t* col = s_col + jb;
         if constexpr (XPOSE) {
-            load_cold(tile);
-            const long long ta = clock64();
-            epi_issue += ta - tp0;
-            if (p.mode != 2) {
-                // cold holds this tile's C_old (vector lanes, all loads in flight):
-                // per pass stage it in the buffer, fill the edge lanes, read back
-                // in row order
+            // the classes are folded from zero; C_old is loaded only after the tile's
+            // (last) TMEM release, so its latency overlaps the next job's MMAs
 #pragma unroll
-                for (int h = 0; h < NH; ++h) {
-                    bool vec;
-                    (void)col_at(n, PW * h + 4 * ch, vec);
-                    if (vec) {
-#pragma unroll
-                        for (int i = 0; i < NI; ++i)
-                            sts128(xaddr(RPI * i + sr, ch), ((cmask >> (h * NI + i)) & 1u)
-                                                                ? cold[h][i]
-                                                                : make_uint4(0u, 0u, 0u, 0u));
-                    } else {
-                        edge_load(m, n, h);
-                    }
-                    if (h == 0) epi_land += clock64() - ta;
-                    __syncwarp();
-#pragma unroll
-                    for (int g = 0; g < CPR; ++g) {
-                        const uint4 v = lds128(xaddr(lane, g));
-                        cur[PW * h + 4 * g] = v.x;
-                        cur[PW * h + 4 * g + 1] = v.y;
-                        cur[PW * h + 4 * g + 2] = v.z;
-                        cur[PW * h + 4 * g + 3] = v.w;
-                    }
-                    __syncwarp();
-                }
-            } else {
-#pragma unroll
-                for (int j = 0; j < WH; ++j) cur[j] = 0u;
-            }
+            for (int j = 0; j < WH; ++j) cur[j] = 0u;
         } else {
             const uint64_t gi = (uint64_t)m * kBM + row;
             row_ok = gi < p.rows;
@@ -1264,11 +1220,11 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
                 for (int j = 0; j < WH; ++j) cur[j] = 0u;
             }
         }
-        epi_pro += clock64() - tp0;
+        epi_pro += diag_clock() - tp0;
         for (uint32_t c = 0; c < nchunks; ++c) {
-            const long long w0 = clock64();
+            const long long w0 = diag_clock();
             mbar_wait_hint(tmem_full, acc_ph, p.wait_hint);
-            const long long w1 = clock64();
+            const long long w1 = diag_clock();
             epi_wait += w1 - w0;
             tc_fence_after();
             if constexpr (PAIR) {
@@ -1293,7 +1249,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
                 }
                 tmem_wait_st();
                 release();
-                epi_busy += clock64() - w1;
+                epi_busy += diag_clock() - w1;
             } else {
                 // Jobs alternate TMEM bases 0 / W.  The next job (other base) needs
                 // this job's classes [1, C) (base 0) or [0, C-1) (base W) plus the
@@ -1306,7 +1262,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
                     // fixed layout: drain and fold every class, then release
                     drain(std::integral_constant<int, 0>{}, std::integral_constant<int, CLASSES>{}, tb, n, cur);
                     release();
-                    epi_busy += clock64() - w1;
+                    epi_busy += diag_clock() - w1;
                     acc_ph ^= 1;
                     continue;
                 }
@@ -1314,43 +1270,98 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
                     // lean split for q = 2^16 - small (e.g. 65521): the first group
                     // leaves cur unreduced (< 2^32 - 2^24); the second group finishes
                     drain_l2_small(tb, n, cur, acc_ph);
-                    epi_busy += clock64() - w1;
+                    epi_busy += diag_clock() - w1;
                     acc_ph ^= 1;
                     continue;
                 }
                 if (acc_ph == 0) {
                     drain(std::integral_constant<int, 1>{}, std::integral_constant<int, CLASSES>{}, tb, n, cur);
                     release();
-                    epi_busy += clock64() - w1;
+                    epi_busy += diag_clock() - w1;
                     drain(std::integral_constant<int, 0>{}, std::integral_constant<int, 1>{}, tb, n, cur);
                 } else {
                     drain(std::integral_constant<int, 0>{}, std::integral_constant<int, CLASSES - 1>{}, tb, n, cur);
                     release();
-                    epi_busy += clock64() - w1;
+                    epi_busy += diag_clock() - w1;
                     drain(std::integral_constant<int, CLASSES - 1>{}, std::integral_constant<int, CLASSES>{}, tb, n, cur);
                 }
             }
             acc_ph ^= 1;
         }
-        const long long tt0 = clock64();
+        const long long tt0 = diag_clock();
         if constexpr (XPOSE) {
+            // out = (folded product + C_old) mod q.  The product is final here (< q <=
+            // 2^16: XPOSE tiles are the <= 2-limb ones), so it is held two per register
+            // while this tile's C_old loads are in flight -- they were issued only now,
+            // after the last TMEM release, so their latency overlaps the next job's
+            // MMAs.  Per pass: C_old staged into the buffer (coalesced order), read back
+            // in row order and added, the sums written back in place, then stored in
+            // the coalesced order.
+            static_assert(NH == 2, "two column passes per epilogue warp");
+            uint32_t c16[WH / 2];
+#pragma unroll
+            for (int j = 0; j < WH / 2; ++j) c16[j] = cur[2 * j] | (cur[2 * j + 1] << 16);
+            const bool addc = p.mode != 2;
             const uint64_t own = row_at(m, row);
+            uint64_t c0[NH];
+            bool vec[NH];
 #pragma unroll
-            for (int h = 0; h < NH; ++h) {
-#pragma unroll
-                for (int g = 0; g < CPR; ++g)
-                    sts128(xaddr(lane, g), make_uint4(cur[PW * h + 4 * g], cur[PW * h + 4 * g + 1],
-                                                      cur[PW * h + 4 * g + 2], cur[PW * h + 4 * g + 3]));
-                __syncwarp();
-                bool vec;
-                const uint64_t c0 = col_at(n, PW * h + 4 * ch, vec);
+            for (int h = 0; h < NH; ++h) c0[h] = col_at(n, PW * h + 4 * ch, vec[h]);
+            uint4 c1[NI];  // pass 1's C_old (vector lanes)
+            uint32_t m1 = 0;
+            if (addc) {
+                // pass 0 straight into the transpose buffer (cp.async: no registers; rows past
+                // the view zero-filled), pass 1 into registers: all loads in flight at once
 #pragma unroll
                 for (int i = 0; i < NI; ++i) {
                     const uint64_t rb = __shfl_sync(0xffffffffu, own, RPI * i + sr);
-                    if (vec && rb != kNoCol)
-                        c_store(reinterpret_cast<uint4*>(p.out + rb + c0), lds128(xaddr(RPI * i + sr, ch)));
+                    const bool live = rb != kNoCol;
+                    if (vec[0]) cp_async16(xaddr(RPI * i + sr, ch), p.out + (live ? rb + c0[0] : 0), live ? 16u : 0u);
+                    const bool ok = vec[1] && live;
+                    m1 |= (uint32_t)ok << i;
+                    c1[i] = c_load(reinterpret_cast<const uint4*>(p.out + (ok ? rb + c0[1] : 0)));
                 }
-                if (!vec) edge_store(m, n, h);
+                cp_async_commit();
+            }
+            const long long ta = diag_clock();
+            epi_issue += ta - tt0;
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+                if (addc) {
+                    if (h == 0) {
+                        if (!vec[0]) edge_load(m, n, 0);
+                        cp_async_wait_all();
+                        epi_land += diag_clock() - ta;
+                    } else if (vec[1]) {
+#pragma unroll
+                        for (int i = 0; i < NI; ++i)
+                            sts128(xaddr(RPI * i + sr, ch), ((m1 >> i) & 1u) ? c1[i] : make_uint4(0u, 0u, 0u, 0u));
+                    } else {
+                        edge_load(m, n, 1);
+                    }
+                    __syncwarp();
+                }
+#pragma unroll
+                for (int g = 0; g < CPR; ++g) {
+                    const uint4 v = addc ? lds128(xaddr(lane, g)) : make_uint4(0u, 0u, 0u, 0u);
+                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                    uint32_t o[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        const int jj = PW * h + 4 * g + e;
+                        const uint32_t x = ((c16[jj >> 1] >> (16 * (jj & 1))) & 0xffffu) + w[e];
+                        o[e] = x >= p.q ? x - p.q : x;
+                    }
+                    sts128(xaddr(lane, g), make_uint4(o[0], o[1], o[2], o[3]));
+                }
+                __syncwarp();
+#pragma unroll
+                for (int i = 0; i < NI; ++i) {
+                    const uint64_t rb = __shfl_sync(0xffffffffu, own, RPI * i + sr);
+                    if (vec[h] && rb != kNoCol)
+                        c_store(reinterpret_cast<uint4*>(p.out + rb + c0[h]), lds128(xaddr(RPI * i + sr, ch)));
+                }
+                if (!vec[h]) edge_store(m, n, h);
                 __syncwarp();
             }
         } else if (row_ok) {
@@ -1369,7 +1380,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
                 }
             }
         }
-        epi_tail += clock64() - tt0;
+        epi_tail += diag_clock() - tt0;
     }
     if (p.stats && warp == 2 && lane == 0) {
         p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiWaitFull] = epi_wait;
@@ -1447,9 +1458,9 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
                 const bool rev = ord & 1;
                 for (uint32_t j = 0; j < p.Kt; ++j) {
                     const uint32_t kt = rev ? p.Kt - 1 - j : j;
-                    const long long w0 = clock64();
+                    const long long w0 = diag_clock();
                     mbar_wait_hint(&empty[st], ph ^ 1, p.wait_hint);
-                    wait_empty += clock64() - w0;
+                    wait_empty += diag_clock() - w0;
                     mbar_expect_tx(&full[st], Cfg::STAGE);
                     bulk_g2s_hint(sA + st * Cfg::A_STAGE, a_src + (uint64_t)kt * Cfg::A_STAGE,
                                   Cfg::A_STAGE, &full[st], pol_keep);
@@ -1474,19 +1485,19 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
             int st = 0;
             uint32_t ph = 0, acc_ph = 0;
             long long wait_full = 0, wait_tmem = 0;
-            const long long t_begin = clock64();
+            const long long t_begin = diag_clock();
             for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride) {
                 for (uint32_t c = 0; c < nchunks; ++c) {
                     const uint32_t kb = c * p.KC;
                     const uint32_t ke = (kb + p.KC < p.Kt) ? kb + p.KC : p.Kt;
-                    long long w0 = clock64();
+                    long long w0 = diag_clock();
                     mbar_wait_hint(tmem_empty, acc_ph ^ 1, p.wait_hint);
-                    wait_tmem += clock64() - w0;
+                    wait_tmem += diag_clock() - w0;
                     tc_fence_after();
                     for (uint32_t kt = kb; kt < ke; ++kt) {
-                        w0 = clock64();
+                        w0 = diag_clock();
                         mbar_wait_hint(&full[st], ph, p.wait_hint);
-                        wait_full += clock64() - w0;
+                        wait_full += diag_clock() - w0;
                         tc_fence_after();
                         const uint32_t a0 = smem_u32(sA + st * Cfg::A_STAGE);
                         const uint32_t b0 = smem_u32(sB + st * Cfg::B_STAGE);
@@ -1525,7 +1536,7 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
             }
             if (p.stats) {
                 unsigned long long* o = p.stats + (uint64_t)blockIdx.x * kStatCount;
-                o[kStatTotal] = clock64() - t_begin;
+                o[kStatTotal] = diag_clock() - t_begin;
                 o[kStatMmaWaitFull] = wait_full;
                 o[kStatMmaWaitTmem] = wait_tmem;
             }
@@ -1657,9 +1668,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS
                 const bool rev = ord & 1;
                 for (uint32_t j = 0; j < p.Kt; ++j) {
                     const uint32_t kt = rev ? p.Kt - 1 - j : j;
-                    const long long w0 = clock64();
+                    const long long w0 = diag_clock();
                     mbar_wait(&empty[st], ph ^ 1);
-                    wait_empty += clock64() - w0;
+                    wait_empty += diag_clock() - w0;
                     if (rank == 0) mbar_expect_tx(&full[st], 2 * Cfg::STAGE);
                     const uint32_t lbar = mapa_shared(smem_u32(&full[st]), 0);
                     const int arow = (int)(((uint64_t)m * p.Kt + kt) * L * kBM);
@@ -1683,20 +1694,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS
             int st = 0;
             uint32_t ph = 0, job = 0;
             long long wait_full = 0, wait_tmem = 0;
-            const long long t_begin = clock64();
+            const long long t_begin = diag_clock();
             for (uint32_t tile = pair; tile < num_tiles; tile += npairs) {
                 for (uint32_t c = 0; c < nchunks; ++c, ++job) {
                     const uint32_t kb = c * p.KC;
                     const uint32_t ke = (kb + p.KC < p.Kt) ? kb + p.KC : p.Kt;
-                    long long w0 = clock64();
+                    long long w0 = diag_clock();
                     mbar_wait(tmem_empty, (job & 1) ^ 1);
-                    wait_tmem += clock64() - w0;
+                    wait_tmem += diag_clock() - w0;
                     tc_fence_after();
                     const uint32_t dbase = tmem;
                     for (uint32_t kt = kb; kt < ke; ++kt) {
-                        w0 = clock64();
+                        w0 = diag_clock();
                         mbar_wait(&full[st], ph);
-                        wait_full += clock64() - w0;
+                        wait_full += diag_clock() - w0;
                         tc_fence_after();
                         const uint32_t a0 = smem_u32(sA + st * Cfg::A_STAGE);
                         const uint32_t b0 = smem_u32(sB + st * Cfg::B_STAGE);
@@ -1720,7 +1731,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS
             }
             if (p.stats) {
                 unsigned long long* o = p.stats + (uint64_t)blockIdx.x * kStatCount;
-                o[kStatTotal] = clock64() - t_begin;
+                o[kStatTotal] = diag_clock() - t_begin;
                 o[kStatMmaWaitFull] = wait_full;
                 o[kStatMmaWaitTmem] = wait_tmem;
             }
@@ -2066,6 +2077,8 @@ int launch_widen16(const uint16_t* src, uint32_t* dst, uint64_t count, int num_s
     k_widen16<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(src, dst, count, head, vec);
     return (int)cudaGetLastError();
 }
+
+int diag_build() { return MHG_DIAG; }
 
 int gemm_smem_bytes(int L) {
     switch (L) {

@@ -29,6 +29,10 @@ for K in [int(k) for k in os.environ.get("AB_KS", "1024,2048,4096,15360").split(
     plan.run()
     out[f"K{K}"] = statistics.median(plan.time_gemm(5) for _ in range(5))
     del plan
+plan = mh.Plan(mh.Problem(mh.Sub(A, 0, n, n), mh.Sub(B, 0, n, n), mh.Sub(C, 0, n, n)), mh.OP_SUB)
+plan.run()
+out["ns16k"] = statistics.median(plan.time_gemm(3) for _ in range(5))
+del plan
 M = A
 plans = schur_plans(M, 1024)
 schur_sweep(M, 1024, plans=plans)

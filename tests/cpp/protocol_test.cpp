@@ -5,7 +5,10 @@
 
 #include <cstdio>
 #include <fstream>
+#include <random>
 #include <sstream>
+#include <string>
+#include <vector>
 
 namespace {
 int g_checks = 0, g_fail = 0;
@@ -37,8 +40,57 @@ std::string strip_two(const std::string& csv) {
 }
 }  // namespace
 
+// layout_test.cpp:147-175: the text format round-trips and is exact; malformed files
+// raise std::invalid_argument
+void io_cases() {
+    std::mt19937_64 eng(11);
+    mh::Grid g(8, std::vector<mh::Fp>(8));
+    for (auto& row : g)
+        for (auto& c : row) c = mh::Fp{std::uint32_t(eng() % 97)};
+    const mh::Matrix m = mh::from_row_major(g, 4, mh::Modulus(97));
+    std::ostringstream os;
+    mh::save_matrix(os, m);
+    const std::string text = os.str();
+    CHECK(text.substr(0, 7) == "8 4 97\n");
+    CHECK(text.back() == '\n');
+    std::istringstream is(text);
+    CHECK(mh::load_matrix(is) == m);
+    auto rejects = [](const std::string& s) {
+        std::istringstream in(s);
+        try {
+            (void)mh::load_matrix(in);
+        } catch (const std::invalid_argument&) {
+            return true;
+        } catch (...) {
+            return false;
+        }
+        return false;
+    };
+    CHECK(rejects(""));
+    CHECK(rejects("2 1\n0 0\n0 0\n"));    // truncated header
+    CHECK(rejects("2 1 4\n0 0\n0 0\n"));  // composite modulus
+    CHECK(rejects("2 1 2\n0 0\n0\n"));    // missing residue
+    CHECK(rejects("2 1 2\n0 0\n0 2\n"));  // residue >= q
+    CHECK(rejects("2 1 2\n0 0\n0 -1\n"));
+    CHECK(rejects("6 3 2\n"));              // 6 / 3 is not a power of two
+}
+
 int main(int argc, char** argv) {
+    // --save n t q seed path: a container filled from mh::Rng(seed) in flat Morton
+    // order, written by save_matrix_file (byte parity with the reference's writer is
+    // checked by tests/test_cpp_dropin.py)
+    if (argc == 7 && std::string(argv[1]) == "--save") {
+        const std::uint64_t n = std::stoull(argv[2]), t = std::stoull(argv[3]);
+        const std::uint32_t q = (std::uint32_t)std::stoul(argv[4]);
+        mh::Rng rng(std::stoull(argv[5]));
+        mh::Matrix m(mh::Layout(n, t), mh::Modulus(q));
+        for (auto& v : m.cells()) v = mh::Fp{std::uint32_t(rng.below(q))};
+        mh::save_matrix_file(argv[6], m);
+        const mh::Matrix back = mh::load_matrix_file(argv[6]);
+        return back == m ? 0 : 1;
+    }
     const std::string golden_path = argc > 1 ? argv[1] : "tests/golden/bench_trials_seed0_n64_t8_q2.csv";
+    io_cases();
     mh::Config cfg;
     cfg.n = 64;
     cfg.t = 8;
