@@ -13,4 +13,9 @@ ncu --set full --clock-control none --import-source on -k regex:k_gemm -s 2 -c 1
     -o gpurun_out/${TAG}_gemm_full $CMD > gpurun_out/${TAG}_ncu_gemm.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_pack -s 4 -c 2 \
     -o gpurun_out/${TAG}_pack_full $CMD > gpurun_out/${TAG}_ncu_pack.log 2>&1
+# tensor-pipe evidence for the GEMM: UTCIMMA sub-pipe active cycles / instructions, TMEM
+# bytes read by LDTM (epilogue drains), elapsed cycles
+TP="sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__inst_executed_pipe_tensor_subpipe_imma.sum,sm__mem_tensor_reads_op_ldt.sum,sm__cycles_elapsed.avg,gpu__time_duration.sum"
+ncu --metrics $TP --clock-control none -k regex:k_gemm -s 2 -c 1 --csv \
+    --log-file gpurun_out/${TAG}_tensor_pipe.csv $CMD > gpurun_out/${TAG}_ncu_tp.log 2>&1
 echo "ncu done"
