@@ -190,7 +190,9 @@ mhg_status mhg_counters_geometry(uint32_t flags, uint64_t n_out, uint64_t t_out,
 
 /* Reusable plan: validation, offset tables, packing workspace and a captured
  * CUDA graph (pack lhs, pack rhs, GEMM + fused epilogue) replayed by
- * mhg_plan_run.  The views' containers must outlive the plan. */
+ * mhg_plan_run.  The views' containers must outlive the plan.  mhg_plan_run on a
+ * stream that the caller is capturing enqueues the kernels themselves (they become
+ * nodes of the caller's graph); mhg_mm refuses capture (MHG_ERR_UNSUPPORTED). */
 mhg_status mhg_plan_create(mhg_view out, mhg_view lhs, mhg_view rhs, mhg_op op, mhg_plan *plan);
 mhg_status mhg_plan_run(mhg_plan plan, void *stream);
 /* Split execution of a plan, for exchanging PACKED operands between ranks

@@ -1042,6 +1042,14 @@ mhg_status mhg_plan_run(mhg_plan p, void* stream) {
             launch_multiply(p->buf, p->out, p->lhs, p->rhs, p->chk, p->geo, p->op, stream, b, e);
             return;
         }
+        cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+        cuda_check(cudaStreamIsCapturing((cudaStream_t)stream, &cap_st), "capture query");
+        if (cap_st != cudaStreamCaptureStatusNone) {
+            // the caller is capturing its own graph: enqueue the kernels themselves, so they
+            // become nodes of that graph
+            launch_multiply(p->buf, p->out, p->lhs, p->rhs, p->chk, p->geo, p->op, stream);
+            return;
+        }
         if (!p->exec) {
             // capture pack(lhs + rhs), gemm once; replay as one graph launch (the kernels'
             // one-time attributes were set outside capture by require_device)

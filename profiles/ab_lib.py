@@ -38,7 +38,7 @@ plans = schur_plans(M, 1024)
 schur_sweep(M, 1024, plans=plans)
 torch.cuda.synchronize()
 ts = []
-for _ in range(3):
+for _ in range(7):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); macs = schur_sweep(M, 1024, plans=plans); e1.record(); torch.cuda.synchronize()
     ts.append(e0.elapsed_time(e1))

@@ -981,3 +981,36 @@ def test_device_verify_north_star(gpu, mh):
     assert mh.verify(prob, mh.Sub(old, 0, n, n), OP_SUB)
     f[0][12345] = (f[0][12345] + 1) % q
     assert not mh.verify(prob, mh.Sub(old, 0, n, n), OP_SUB)
+
+
+def test_capture_refused_by_mm_accepted_for_plans(gpu, mh, oracle):
+    """mhg_mm may grow its workspace (allocate + synchronise), so it refuses a capturing
+    stream with MHG_ERR_UNSUPPORTED; a plan replayed inside a user's CUDA graph capture
+    works and gives the exact result."""
+    import torch
+    n, t, q = 256, 32, P16
+    out, lhs, rhs = _fill(oracle, 41, n, q)
+    A, B, Cm = _containers(mh, n, t, q, (out, lhs, rhs))
+    v = _views_from(oracle, n, t, 200, 150, 100, (3, 5, 7, 11, 13, 17))
+    prob = mh.Problem(mh.Sub(A, v.out_origin, v.rows, v.cols), mh.Sub(B, v.lhs_origin, v.rows, v.inner),
+                      mh.Sub(Cm, v.rhs_origin, v.inner, v.cols))
+    plan = mh.Plan(prob, OP_SUB)
+    plan.run()
+    torch.cuda.synchronize()
+    A.upload(out)
+    torch.cuda.synchronize()
+    s = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    refused = False
+    with torch.cuda.graph(g, stream=s):
+        try:
+            mh.mm(prob, OP_SUB, stream=s)
+        except mh.Unsupported:
+            refused = True
+        plan.run(s)
+    assert refused
+    g.replay()
+    torch.cuda.synchronize()
+    want = out.copy()
+    oracle.mm_dense(n, t, q, want, lhs, rhs, v, op=OP_SUB)
+    assert np.array_equal(A.cells(), want)

@@ -359,3 +359,39 @@ def test_product_rng_reproduces_reference_draws(mh, oracle):
     assert h == 4715125990397575263
     a, b = mh.Rng(12345), oracle.rng(12345)
     assert np.array_equal(a.below(65521, 10000), oracle.fill_below(b, 10000, 65521))
+
+
+def test_options_api(mh):
+    """mhg_set_option / mhg_get_option: typed keys, range checks, restore; the GEMM
+    wait counters exist only in diagnostic builds (MHG_ERR_UNSUPPORTED here)."""
+    saved = {k: mh.get_option(k) for k in range(1, 9)}
+    try:
+        assert saved[mh.OPT_DIGITS] in (0, 1)
+        mh.set_option(mh.OPT_DIGITS, 0)
+        assert mh.get_option(mh.OPT_DIGITS) == 0
+        mh.set_option(mh.OPT_MAX_KCHUNK, 3)
+        assert mh.get_option(mh.OPT_MAX_KCHUNK) == 3
+        for key, bad in [(mh.OPT_DIGITS, 2), (mh.OPT_GEMM_KERNEL, 3), (mh.OPT_MIN_FOLD_LEVEL, 0),
+                         (mh.OPT_MIN_FOLD_LEVEL, 4), (mh.OPT_UPLOAD_WIRE, 8), (mh.OPT_CONV_KERNEL, 3),
+                         (mh.OPT_MAX_KCHUNK, -1), (0, 0), (99, 0)]:
+            with pytest.raises(mh.InvalidArgument):
+                mh.set_option(key, bad)
+        with pytest.raises(mh.InvalidArgument):
+            mh.get_option(99)
+        with pytest.raises(mh.Unsupported):  # product build: no wait-cycle counters
+            mh.set_option(mh.OPT_GEMM_STATS, 1)
+        with mh.options({mh.OPT_GEMM_KERNEL: 2, mh.OPT_DIGITS: 1}):
+            assert mh.get_option(mh.OPT_GEMM_KERNEL) == 2
+        assert mh.get_option(mh.OPT_GEMM_KERNEL) == saved[mh.OPT_GEMM_KERNEL]
+    finally:
+        for k, v in saved.items():
+            mh.set_option(k, v)
+
+
+def test_options_select_the_planner_choice(mh):
+    """The options reach the planner: digits and K-chunk cap change the exact chunking
+    reported by the host-only planner entry points (mhg_fold_level / counters are
+    unaffected: results and Counters never depend on the options)."""
+    c0 = mh.counters_layout(1024, 64, 0, 0, 0, 1024, 1024, 1024).as_tuple()
+    with mh.options({mh.OPT_DIGITS: 0, mh.OPT_MAX_KCHUNK: 1}):
+        assert mh.counters_layout(1024, 64, 0, 0, 0, 1024, 1024, 1024).as_tuple() == c0
