@@ -542,17 +542,19 @@ def run_gpu(args, rank, world, local_rank):
     int8_peak_tops = 2.0 * bf16_burst  # dense int8 = 2x dense bf16 on sm_100
     algo_ops = 2.0 * L * L * macs_rank  # int8 ops per GEMM launch (2 per limb MAC)
     achieved_tops = algo_ops / (gemm_ms_max * 1e-3) / 1e12
-    traffic = None
+    traffic = tensor_pipe = None
     try:
         with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             rec = json.load(f).get(args.workload)
         if rec and world == 1:
             traffic = rec["dram_read"] + rec["dram_write"]
+            tensor_pipe = rec.get("tensor_pipe_imma_active_pct")
     except Exception:
         traffic = None
     roof = {"bound": "tensor", "achieved": achieved_tops, "peak": int8_peak_tops,
             "unit": "TFLOP/s", "frac": achieved_tops / int8_peak_tops, "traffic": traffic,
             "traffic_source": "profiles/traffic.json (ncu --set full, bytes per launch)",
+            "tensor_pipe_active_pct_ncu": tensor_pipe,
             "kernel": (f"k_gemm2<{L}> (tcgen05.mma.cta_group::2.kind::i8, CTA pair)"
                        if info.get("cta_group") == 2 else f"k_gemm<{L}> (tcgen05.mma.cta_group::1.kind::i8)")
                       + f", {info.get('digits')} digits",
