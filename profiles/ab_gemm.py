@@ -5,8 +5,9 @@ seconds of back-to-back GEMM launches, sampling SM clock and board power with
 NVML during each window.  Reports ms/launch, median MHz, mean W and
 cycles/launch (ms x MHz) -- the clock-independent efficiency.
 
-  python profiles/ab_gemm.py [n] [q] [rounds] [secs] variant=ENV ...
-  e.g. python profiles/ab_gemm.py 16384 65521 3 2 pair=MHG_GEMM=2cta 1cta=MHG_GEMM=1cta
+  python profiles/ab_gemm.py [n] [q] [rounds] [secs] variant=OPTION=VALUE ...
+  e.g. python profiles/ab_gemm.py 16384 65521 3 2 pair=GEMM_KERNEL=2 1cta=GEMM_KERNEL=1
+  (OPTION: an mhg option without the MHG_OPT_ prefix, include/mhg.h)
 """
 import os
 import statistics
@@ -27,7 +28,12 @@ q = int(args[1]) if len(args) > 1 else 65521
 rounds = int(args[2]) if len(args) > 2 else 3
 secs = float(args[3]) if len(args) > 3 else 2.0
 if not variants:
-    variants = [["pair", "MHG_GEMM=2cta"], ["1cta", "MHG_GEMM=1cta"]]
+    variants = [["pair", "GEMM_KERNEL=2"], ["1cta", "GEMM_KERNEL=1"]]
+
+
+def opt(spec):
+    k, v = spec.split("=", 1)
+    return mh.options({getattr(mh, "OPT_" + k): int(v)})
 
 pynvml.nvmlInit()
 h = pynvml.nvmlDeviceGetHandleByIndex(0)
@@ -36,16 +42,10 @@ fl = [torch.randint(0, q, (n * n,), dtype=torch.int32, device="cuda") for _ in r
 A, B, C = (mh.Matrix.wrap(lay, mod, f.data_ptr(), owner=f) for f in fl)
 prob = mh.Problem(mh.Sub(A, 0, n, n), mh.Sub(B, 0, n, n), mh.Sub(C, 0, n, n))
 plans = {}
-for name, env in variants:
-    k, v = env.split("=", 1)
-    old = os.environ.get(k)
-    os.environ[k] = v
-    plans[name] = mh.Plan(prob, mh.OP_SUB)
-    plans[name].run()
-    if old is None:
-        del os.environ[k]
-    else:
-        os.environ[k] = old
+for name, spec in variants:
+    with opt(spec):
+        plans[name] = mh.Plan(prob, mh.OP_SUB)
+        plans[name].run()
 torch.cuda.synchronize()
 macs = n ** 3
 
@@ -58,24 +58,9 @@ def sample(stop, clocks, watts):
 
 
 res = {name: [] for name, _ in variants}
-class env_set:
-    def __init__(self, spec):
-        self.k, self.v = spec.split("=", 1)
-
-    def __enter__(self):
-        self.old = os.environ.get(self.k)
-        os.environ[self.k] = self.v
-
-    def __exit__(self, *a):
-        if self.old is None:
-            del os.environ[self.k]
-        else:
-            os.environ[self.k] = self.old
-
-
 for r in range(rounds):
     for name, spec in variants:
-      with env_set(spec):
+      with opt(spec):
         pl = plans[name]
         pl.time_gemm(2)
         ms_one = pl.time_gemm(2)

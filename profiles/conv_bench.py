@@ -16,11 +16,12 @@ import paper_1705_04807_b200 as mh  # noqa: E402
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
 q = 65521
-modes = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("MHG_CONV=")] or [None]
+# CONV=0/1/2: MHG_OPT_CONV_KERNEL (TMA / Morton-order LDG-STG / row-order)
+modes = [a.split("=", 1)[1] for a in sys.argv[1:] if a.startswith("CONV=")] or [None]
 for n in [int(a) for a in sys.argv[1:] if "=" not in a] or [16384, 32768]:
   for mode in modes:
     if mode is not None:
-        os.environ["MHG_CONV"] = mode
+        mh.set_option(mh.OPT_CONV_KERNEL, int(mode))
     lay, mod = mh.Layout(n, 64), mh.Modulus(q)
     rm = torch.randint(0, q, (n * n,), dtype=torch.int32, device="cuda")
     back = torch.empty_like(rm)
