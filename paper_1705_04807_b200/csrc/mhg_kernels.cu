@@ -488,6 +488,9 @@ __device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity, u
 #ifndef MHG_DIAG
 #define MHG_DIAG 0
 #endif
+#ifndef MHG_COLD_MID
+#define MHG_COLD_MID 0
+#endif
 __device__ __forceinline__ long long diag_clock() {
 #if MHG_DIAG
     return clock64();
@@ -1065,7 +1068,8 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         if constexpr (FOLD == 2) return red32(c + p.w16 * r2 + p.bias32, p);
         return red32(c + p.w16 * r2, p);
     };
-    auto drain_l2_small = [&](uint32_t tbase, uint32_t n_tile, uint32_t* cur_, uint32_t layout) {
+    auto drain_l2_small = [&](uint32_t tbase, uint32_t n_tile, uint32_t* cur_, uint32_t layout,
+                              auto&& after_release) {
         const int lo_cls = layout ? 0 : 1;  // first group: {lo_cls, lo_cls + 1}
 #pragma unroll
         for (int j0 = 0; j0 < WH; j0 += CW) {
@@ -1080,6 +1084,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
             for (int j = 0; j < CW; ++j) cur_[j0 + j] += fold_g1(a[0][j], a[1][j], layout);
         }
         release();
+        after_release();
 #pragma unroll
         for (int j0 = 0; j0 < WH; j0 += CW) {
             if ((uint64_t)n_tile * W + jb + j0 >= p.cols) continue;
@@ -1182,6 +1187,35 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         uint64_t rbase = 0;
         bool row_ok = false;
         const uint64_t* col = s_col + jb;
+        // C_old of this tile (XPOSE): pass 0 by cp.async into the transpose buffer, pass 1
+        // into registers; issued once, right after the tile's last TMEM release
+        uint4 c1[XPOSE ? NI : 1];
+        uint32_t m1 = 0;
+        uint64_t own = 0, c0[XPOSE ? NH : 1];
+        bool vec[XPOSE ? NH : 1];
+        bool cold_issued = false;
+        auto issue_cold = [&]() {
+            if constexpr (XPOSE) {
+                if (cold_issued) return;
+                cold_issued = true;
+                own = row_at(m, row);
+#pragma unroll
+                for (int h = 0; h < NH; ++h) c0[h] = col_at(n, PW * h + 4 * ch, vec[h]);
+                if (p.mode != 2) {
+#pragma unroll
+                    for (int i = 0; i < NI; ++i) {
+                        const uint64_t rb = __shfl_sync(0xffffffffu, own, RPI * i + sr);
+                        const bool live = rb != kNoCol;
+                        if (vec[0])
+                            cp_async16(xaddr(RPI * i + sr, ch), p.out + (live ? rb + c0[0] : 0), live ? 16u : 0u);
+                        const bool ok = vec[1] && live;
+                        m1 |= (uint32_t)ok << i;
+                        c1[i] = c_load(reinterpret_cast<const uint4*>(p.out + (ok ? rb + c0[1] : 0)));
+                    }
+                    cp_async_commit();
+                }
+            }
+        };
         if constexpr (XPOSE) {
             // the classes are folded from zero; C_old is loaded only after the tile's
             // (last) TMEM release, so its latency overlaps the next job's MMAs
@@ -1269,7 +1303,11 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
                 if constexpr (L == 2) {
                     // lean split for q = 2^16 - small (e.g. 65521): the first group
                     // leaves cur unreduced (< 2^32 - 2^24); the second group finishes
-                    drain_l2_small(tb, n, cur, acc_ph);
+                    drain_l2_small(tb, n, cur, acc_ph, [&] {
+#if MHG_COLD_MID
+                        if (c + 1 == nchunks) issue_cold();
+#endif
+                    });
                     epi_busy += diag_clock() - w1;
                     acc_ph ^= 1;
                     continue;
@@ -1302,27 +1340,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
 #pragma unroll
             for (int j = 0; j < WH / 2; ++j) c16[j] = cur[2 * j] | (cur[2 * j + 1] << 16);
             const bool addc = p.mode != 2;
-            const uint64_t own = row_at(m, row);
-            uint64_t c0[NH];
-            bool vec[NH];
-#pragma unroll
-            for (int h = 0; h < NH; ++h) c0[h] = col_at(n, PW * h + 4 * ch, vec[h]);
-            uint4 c1[NI];  // pass 1's C_old (vector lanes)
-            uint32_t m1 = 0;
-            if (addc) {
-                // pass 0 straight into the transpose buffer (cp.async: no registers; rows past
-                // the view zero-filled), pass 1 into registers: all loads in flight at once
-#pragma unroll
-                for (int i = 0; i < NI; ++i) {
-                    const uint64_t rb = __shfl_sync(0xffffffffu, own, RPI * i + sr);
-                    const bool live = rb != kNoCol;
-                    if (vec[0]) cp_async16(xaddr(RPI * i + sr, ch), p.out + (live ? rb + c0[0] : 0), live ? 16u : 0u);
-                    const bool ok = vec[1] && live;
-                    m1 |= (uint32_t)ok << i;
-                    c1[i] = c_load(reinterpret_cast<const uint4*>(p.out + (ok ? rb + c0[1] : 0)));
-                }
-                cp_async_commit();
-            }
+            issue_cold();  // (no-op when the drain already issued it)
             const long long ta = diag_clock();
             epi_issue += ta - tt0;
 #pragma unroll
