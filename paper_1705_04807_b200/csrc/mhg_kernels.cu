@@ -488,9 +488,7 @@ __device__ __forceinline__ void mbar_wait_hint(uint64_t* bar, uint32_t parity, u
 #ifndef MHG_DIAG
 #define MHG_DIAG 0
 #endif
-#ifndef MHG_COLD_MID
-#define MHG_COLD_MID 0
-#endif
+
 __device__ __forceinline__ long long diag_clock() {
 #if MHG_DIAG
     return clock64();
@@ -1068,8 +1066,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         if constexpr (FOLD == 2) return red32(c + p.w16 * r2 + p.bias32, p);
         return red32(c + p.w16 * r2, p);
     };
-    auto drain_l2_small = [&](uint32_t tbase, uint32_t n_tile, uint32_t* cur_, uint32_t layout,
-                              auto&& after_release) {
+    auto drain_l2_small = [&](uint32_t tbase, uint32_t n_tile, uint32_t* cur_, uint32_t layout) {
         const int lo_cls = layout ? 0 : 1;  // first group: {lo_cls, lo_cls + 1}
 #pragma unroll
         for (int j0 = 0; j0 < WH; j0 += CW) {
@@ -1084,7 +1081,6 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
             for (int j = 0; j < CW; ++j) cur_[j0 + j] += fold_g1(a[0][j], a[1][j], layout);
         }
         release();
-        after_release();
 #pragma unroll
         for (int j0 = 0; j0 < WH; j0 += CW) {
             if ((uint64_t)n_tile * W + jb + j0 >= p.cols) continue;
@@ -1188,7 +1184,9 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         bool row_ok = false;
         const uint64_t* col = s_col + jb;
         // C_old of this tile (XPOSE): pass 0 by cp.async into the transpose buffer, pass 1
-        // into registers; issued once, right after the tile's last TMEM release
+        // into registers; issued after the tile's last TMEM release and the final fold
+        // (issuing them earlier -- at tile start, or between the two drain phases --
+        // measured slower, profiles/r02_short_k.txt)
         uint4 c1[XPOSE ? NI : 1];
         uint32_t m1 = 0;
         uint64_t own = 0, c0[XPOSE ? NH : 1];
@@ -1303,11 +1301,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
                 if constexpr (L == 2) {
                     // lean split for q = 2^16 - small (e.g. 65521): the first group
                     // leaves cur unreduced (< 2^32 - 2^24); the second group finishes
-                    drain_l2_small(tb, n, cur, acc_ph, [&] {
-#if MHG_COLD_MID
-                        if (c + 1 == nchunks) issue_cold();
-#endif
-                    });
+                    drain_l2_small(tb, n, cur, acc_ph);
                     epi_busy += diag_clock() - w1;
                     acc_ph ^= 1;
                     continue;
@@ -1340,7 +1334,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
 #pragma unroll
             for (int j = 0; j < WH / 2; ++j) c16[j] = cur[2 * j] | (cur[2 * j + 1] << 16);
             const bool addc = p.mode != 2;
-            issue_cold();  // (no-op when the drain already issued it)
+            issue_cold();
             const long long ta = diag_clock();
             epi_issue += ta - tt0;
 #pragma unroll
