@@ -1,14 +1,17 @@
 """Regenerate the committed SASS evidence from the built libmhg.so:
-  profiles/r01_sass_census.txt     opcode census (tcgen05 / TMA / mbarrier) per GEMM kernel
-  profiles/r01_sass_k_gemm_L2.txt  trimmed listing of the headline kernel k_gemm<2, fold 2>
+  profiles/TAG_sass_census.txt     opcode census (tcgen05 / TMA / mbarrier) per GEMM kernel
+  profiles/TAG_sass_k_gemm_L2.txt  trimmed listing of the headline kernel k_gemm<2, fold 2>
+(python profiles/sass_evidence.py [TAG], TAG defaults to r02)
 tcgen05.mma -> UTCIMMA (kind::i8), tcgen05.ld -> LDTM, tcgen05.commit -> UTCBAR,
 cp.async.bulk -> UBLKCP, cp.async.bulk.tensor -> UTMALDG, mbarrier -> SYNCS.*"""
 import collections
 import os
 import re
 import subprocess
+import sys
 
 here = os.path.dirname(os.path.abspath(__file__))
+TAG = sys.argv[1] if len(sys.argv) > 1 else "r02"
 lib = os.path.join(os.path.dirname(here), "paper_1705_04807_b200", "libmhg.so")
 sass = subprocess.run(["cuobjdump", "-sass", lib], capture_output=True, text=True).stdout
 funcs, cur = {}, None
@@ -38,9 +41,9 @@ for name in sorted(funcs):
     out.append(f"== {short.group(1) if short else name[:60]} ({ninstr} instructions) {name}")
     for op, c in cnt.most_common():
         out.append(f"  {c:5d} {op}")
-open(os.path.join(here, "r01_sass_census.txt"), "w").write("\n".join(out) + "\n")
+open(os.path.join(here, f"{TAG}_sass_census.txt"), "w").write("\n".join(out) + "\n")
 
-target = [n for n in funcs if re.search(r"k_gemmILi2ELi2ELb0", n)]
+target = [n for n in funcs if re.search(r"k_gemmILi2ELi2EE", n)]
 lines = funcs[target[0]] if target else []
 keep = set()
 for i, line in enumerate(lines):
@@ -55,5 +58,5 @@ for i in sorted(keep):
         lst.append("        ...")
     lst.append(re.sub(r"\s*/\* 0x[0-9a-f]+ \*/\s*$", "", lines[i]))
     prev = i
-open(os.path.join(here, "r01_sass_k_gemm_L2.txt"), "w").write("\n".join(lst) + "\n")
+open(os.path.join(here, f"{TAG}_sass_k_gemm_L2.txt"), "w").write("\n".join(lst) + "\n")
 print("\n".join(out[:40]))
