@@ -312,7 +312,8 @@ def e2e_pipelined(mh, torch, lay, mod, flats, set0, prob0, op, n, steps, macs, n
     h2d = sum(m_.upload_bytes for m_ in sets[(steps - 1) % nsets][:3])  # PCIe bytes of the last step
     return {"value": macs / (ms * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
             "d2h_bytes_per_step": n * n * 4, "steps": steps, "ms_per_step": ms,
-            "upload_wire": "uint16" if h2d == 3 * n * n * 2 else "uint32", "container_sets": nsets,
+            "upload_wire": ("uint16" if h2d == 3 * n * n * 2 else "uint32" if h2d == 3 * n * n * 4 else "mixed"),
+            "upload_adaptive": bool(mh.get_option(mh.OPT_UPLOAD_ADAPTIVE)), "container_sets": nsets,
             "path": "pinned host -> mhg_matrix_upload x3 (uint16 wire for q <= 2^16: host-threaded "
                     "narrowing into pinned staging, device widening) -> mhg_plan_run -> "
                     "mhg_matrix_download -> pinned host; %d container sets, H2D / compute / D2H "

@@ -97,8 +97,11 @@ typedef enum {
                                     LDG/STG, 2 = row-order LDG/STG */
     MHG_OPT_GEMM_STATS = 7,      /* MHG_GEMM_STATS: 1 = print per-launch wait-cycle shares to stderr
                                     (synchronous; diagnostics) */
-    MHG_OPT_UPLOAD_THREADS = 8   /* MHG_UPLOAD_THREADS: host narrowing workers (0 = the affinity
+    MHG_OPT_UPLOAD_THREADS = 8,  /* MHG_UPLOAD_THREADS: host narrowing workers (0 = the affinity
                                     mask / LOCAL_WORLD_SIZE) */
+    MHG_OPT_UPLOAD_ADAPTIVE = 9  /* MHG_UPLOAD_ADAPTIVE: 1 = while the link idles (the host narrows
+                                    slower than PCIe), chunks from the back of a PINNED source
+                                    travel as 4-byte cells on a second copy stream */
 } mhg_option;
 mhg_status mhg_set_option(int key, int64_t value);
 mhg_status mhg_get_option(int key, int64_t *value);

@@ -39,7 +39,7 @@ __all__ = [
     "verify", "Rng",
     "OP_ADD", "OP_SUB", "OP_SET", "set_option", "get_option", "options",
     "OPT_DIGITS", "OPT_GEMM_KERNEL", "OPT_MIN_FOLD_LEVEL", "OPT_MAX_KCHUNK", "OPT_UPLOAD_WIRE",
-    "OPT_CONV_KERNEL", "OPT_GEMM_STATS", "OPT_UPLOAD_THREADS",
+    "OPT_CONV_KERNEL", "OPT_GEMM_STATS", "OPT_UPLOAD_THREADS", "OPT_UPLOAD_ADAPTIVE",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -48,7 +48,7 @@ LIB_PATH = os.environ.get("MHG_LIB") or os.path.join(HERE, "libmhg.so")
 OP_ADD, OP_SUB, OP_SET = 0, 1, 2
 # mhg_option keys (include/mhg.h)
 (OPT_DIGITS, OPT_GEMM_KERNEL, OPT_MIN_FOLD_LEVEL, OPT_MAX_KCHUNK, OPT_UPLOAD_WIRE, OPT_CONV_KERNEL,
- OPT_GEMM_STATS, OPT_UPLOAD_THREADS) = range(1, 9)
+ OPT_GEMM_STATS, OPT_UPLOAD_THREADS, OPT_UPLOAD_ADAPTIVE) = range(1, 10)
 
 
 class InvalidArgument(ValueError):

@@ -169,7 +169,8 @@ enum OptionKey {
     kOptConvKernel = 6,   // 0 = TMA where eligible, 1 = Morton-order LDG/STG, 2 = row-order
     kOptGemmStats = 7,    // 1 = per-launch wait-cycle report (synchronous diagnostics)
     kOptUploadThreads = 8,  // host narrowing workers (0 = affinity / LOCAL_WORLD_SIZE)
-    kOptCount = 9
+    kOptUploadAdaptive = 9, // 1 = idle-link chunks of a pinned upload travel raw (4-byte)
+    kOptCount = 10
 };
 int64_t option(int key);
 bool option_valid(int key, int64_t value);

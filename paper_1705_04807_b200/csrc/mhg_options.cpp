@@ -43,6 +43,7 @@ void seed() {
     g_opt[kOptGemmStats] = std::getenv("MHG_GEMM_STATS") ? 1 : 0;
     const int64_t th = env_int("MHG_UPLOAD_THREADS", 0);
     g_opt[kOptUploadThreads] = th > 0 && th <= 256 ? th : 0;
+    g_opt[kOptUploadAdaptive] = env_int("MHG_UPLOAD_ADAPTIVE", 0) != 0 ? 1 : 0;
 }
 
 }  // namespace
@@ -57,6 +58,7 @@ bool option_valid(int key, int64_t v) {
         case kOptConvKernel: return v >= 0 && v <= 2;
         case kOptGemmStats: return v == 0 || v == 1;
         case kOptUploadThreads: return v >= 0 && v <= 256;
+        case kOptUploadAdaptive: return v == 0 || v == 1;
     }
     return false;
 }

@@ -152,6 +152,9 @@ struct Staging {
     uint16_t* slot[kMaxSlots] = {};
     cudaEvent_t done[kMaxSlots] = {};
     bool used[kMaxSlots] = {};
+    // adaptive raw tail: a second copy stream for 4-byte chunks taken from the back
+    cudaStream_t raw = nullptr;
+    cudaEvent_t start = nullptr, raw_done = nullptr;
     std::mutex mu;
 };
 
@@ -170,6 +173,13 @@ Staging* staging_for(int device, int* err) {
             *err = e;
             return nullptr;  // leaked on purpose: a process-lifetime singleton that failed
         }
+    }
+    int e = (int)cudaStreamCreateWithFlags(&s->raw, cudaStreamNonBlocking);
+    if (!e) e = (int)cudaEventCreateWithFlags(&s->start, cudaEventDisableTiming);
+    if (!e) e = (int)cudaEventCreateWithFlags(&s->raw_done, cudaEventDisableTiming);
+    if (e) {
+        *err = e;
+        return nullptr;
     }
     reg.push_back(s);
     return s;
@@ -205,10 +215,37 @@ int upload_wire16(uint32_t* cells, uint16_t** dev16, uint64_t total, uint64_t of
     const uint64_t chunk = chunk_cells();
     const int slots = ring_slots(), parts = P.size();
     std::vector<uint32_t> hi(parts);
+    // Adaptive raw tail (MHG_OPT_UPLOAD_ADAPTIVE, pinned sources only): whenever the link is
+    // idle when a chunk is about to be narrowed -- the last narrowed chunk has landed and no
+    // raw copy is running, i.e. the host narrows slower than PCIe moves 2-byte cells (a slow
+    // or contended host) -- one chunk from the BACK of the buffer goes as 4-byte cells
+    // straight from the caller's pinned memory on a second copy stream (no host work).
+    cudaPointerAttributes pa{};
+    const bool pinned = cudaPointerGetAttributes(&pa, host) == cudaSuccess && pa.type == cudaMemoryTypeHost;
+    cudaGetLastError();
+    const bool adaptive = pinned && mhg::option(mhg::kOptUploadAdaptive) != 0;
+    uint64_t back = count;  // [back, count) travels raw
+    bool raw_used = false;
+    int last_k = -1;
     uint64_t narrow = 0;  // cells sent as uint16 (a prefix of the container)
-    for (uint64_t c = 0; narrow < count; ++c) {
+    for (uint64_t c = 0; narrow < back; ++c) {
         const int k = (int)(c % slots);
-        const uint64_t base = narrow, len = count - base < chunk ? count - base : chunk;
+        if (adaptive && back - narrow > 2 * chunk &&
+            (last_k < 0 || cudaEventQuery(st->done[last_k]) == cudaSuccess) &&
+            (!raw_used || cudaEventQuery(st->raw_done) == cudaSuccess)) {
+            if (!raw_used) {  // raw copies follow the caller's earlier work on the container
+                if ((e = (int)cudaEventRecord(st->start, s)) ||
+                    (e = (int)cudaStreamWaitEvent(st->raw, st->start, 0)))
+                    return e;
+                raw_used = true;
+            }
+            back -= chunk;
+            if ((e = (int)cudaMemcpyAsync(cells + back, host + back, chunk * 4, cudaMemcpyHostToDevice, st->raw)) ||
+                (e = (int)cudaEventRecord(st->raw_done, st->raw)))
+                return e;
+        }
+        cudaGetLastError();  // cudaEventQuery's cudaErrorNotReady is not an error here
+        const uint64_t base = narrow, len = back - base < chunk ? back - base : chunk;
         if (st->used[k] && (e = (int)cudaEventSynchronize(st->done[k]))) return e;
         const uint64_t per = ((len + parts - 1) / parts + 31) & ~uint64_t(31);  // 64-byte parts
         uint16_t* slot = st->slot[k];
@@ -223,13 +260,15 @@ int upload_wire16(uint32_t* cells, uint16_t** dev16, uint64_t total, uint64_t of
         if (!e) e = (int)cudaEventRecord(st->done[k], s);
         if (e) return e;
         st->used[k] = true;
+        last_k = k;
         narrow += len;
     }
     if ((e = launch_widen16(d16, cells, narrow, num_sms, stream))) return e;
-    if (narrow < count &&
-        (e = (int)cudaMemcpyAsync(cells + narrow, host + narrow, (count - narrow) * 4,
+    if (narrow < back &&
+        (e = (int)cudaMemcpyAsync(cells + narrow, host + narrow, (back - narrow) * 4,
                                   cudaMemcpyHostToDevice, s)))
         return e;
+    if (raw_used && (e = (int)cudaStreamWaitEvent(s, st->raw_done, 0))) return e;
     *wire_bytes = narrow * 2 + (count - narrow) * 4;
     return 0;
 }

@@ -1014,3 +1014,33 @@ def test_capture_refused_by_mm_accepted_for_plans(gpu, mh, oracle):
     want = out.copy()
     oracle.mm_dense(n, t, q, want, lhs, rhs, v, op=OP_SUB)
     assert np.array_equal(A.cells(), want)
+
+
+def test_upload_adaptive_raw_tail(gpu, mh, opts):
+    """MHG_OPT_UPLOAD_ADAPTIVE: chunks of a pinned upload that travel raw (4-byte) while
+    the link idles leave the container byte-identical to a plain copy, also with a wide
+    cell (the rest then goes 4-byte) and for range uploads; PCIe bytes within [2, 4] per
+    cell."""
+    import torch
+    opts(mh.OPT_UPLOAD_ADAPTIVE, 1)
+    n, t, q = 8192, 64, P16
+    rng = np.random.default_rng(91)
+    m = mh.Matrix(mh.Layout(n, t), mh.Modulus(q))
+    for bad in ([], [n * n // 3]):
+        cells = rng.integers(0, q, size=n * n, dtype=np.uint32)
+        for b in bad:
+            cells[b] = 0x12345678
+        h = torch.from_numpy(cells.view(np.int32)).pin_memory()
+        s = torch.cuda.Stream()
+        for _ in range(2):
+            mh._check(mh.lib().mhg_matrix_upload(m.handle, h.data_ptr(), s.cuda_stream))
+        s.synchronize()
+        assert np.array_equal(m.cells(), cells)
+        assert 2 * n * n <= m.upload_bytes <= 4 * n * n
+    off, cnt = 12345, 20_000_000
+    part = rng.integers(0, q, size=cnt, dtype=np.uint32)
+    hp = torch.from_numpy(part.view(np.int32)).pin_memory()
+    want = m.cells()
+    mh._check(mh.lib().mhg_matrix_upload_range(m.handle, hp.data_ptr(), off, cnt, None))
+    want[off:off + cnt] = part
+    assert np.array_equal(m.cells(), want)

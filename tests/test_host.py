@@ -364,7 +364,7 @@ def test_product_rng_reproduces_reference_draws(mh, oracle):
 def test_options_api(mh):
     """mhg_set_option / mhg_get_option: typed keys, range checks, restore; the GEMM
     wait counters exist only in diagnostic builds (MHG_ERR_UNSUPPORTED here)."""
-    saved = {k: mh.get_option(k) for k in range(1, 9)}
+    saved = {k: mh.get_option(k) for k in range(1, 10)}
     try:
         assert saved[mh.OPT_DIGITS] in (0, 1)
         mh.set_option(mh.OPT_DIGITS, 0)
