@@ -729,6 +729,7 @@ namespace {
 void upload_cells(mhg_matrix m, const uint32_t* host, uint64_t offset, uint64_t count, void* stream) {
     if (mhg::wire16_enabled(m->q, count)) {
         require_device();
+        require_resident({m});  // the wire widens on the device with a kernel
         cuda_check(mhg::upload_wire16(m->cells, &m->wire16, m->n * m->n, offset, host, count,
                                       device_info().sms, stream, &m->upload_bytes),
                    "upload (16-bit wire)");
