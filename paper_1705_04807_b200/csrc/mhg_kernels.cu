@@ -1191,11 +1191,8 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         uint32_t m1 = 0;
         uint64_t own = 0, c0[XPOSE ? NH : 1];
         bool vec[XPOSE ? NH : 1];
-        bool cold_issued = false;
         auto issue_cold = [&]() {
             if constexpr (XPOSE) {
-                if (cold_issued) return;
-                cold_issued = true;
                 own = row_at(m, row);
 #pragma unroll
                 for (int h = 0; h < NH; ++h) c0[h] = col_at(n, PW * h + 4 * ch, vec[h]);

@@ -108,3 +108,63 @@ def test_bench_two_ranks_runs_end_to_end(gpu, mh, tmp_path):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
     assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+
+
+def _fallback_worker(rank, world, port, outdir):
+    """Rank 1 cannot map its peers' memory: every rank must raise PeerSetupError (the
+    collective setup decision), after which the packed NCCL-style exchange runs."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch
+    import torch.distributed as dist
+
+    import paper_1705_04807_b200 as mh
+    from paper_1705_04807_b200.dist import (PanelExchange, PeerPanels, PeerSetupError,
+                                            rank_update_packed, segment_plans, slice_range)
+
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        n, t, q = 256, 32, 65521
+        rng = np.random.default_rng(5)
+        full = [rng.integers(0, q, n * n, dtype=np.uint32) for _ in range(3)]
+        lo, hi = slice_range(rank, world, n)
+        flats = []
+        for f in full:
+            d = torch.zeros(n * n, dtype=torch.int32, device="cuda")
+            d[lo:hi] = torch.from_numpy(f[lo:hi].view(np.int32)).cuda()
+            flats.append(d)
+        lay, mod = mh.Layout(n, t), mh.Modulus(q)
+        A, B, C = (mh.Matrix.wrap(lay, mod, f.data_ptr(), owner=f) for f in flats)
+        ex = PanelExchange(world, rank, n, t)
+        plans = segment_plans(mh, ex, A, B, C, mh.OP_SUB)
+        if rank == 1:
+            def refuse(handle):
+                raise mh.DeviceError("simulated: no peer access")
+            mh.ipc_open = refuse
+        raised = False
+        try:
+            PeerPanels(mh, ex, plans)
+        except PeerSetupError:
+            raised = True
+        rank_update_packed(ex, plans)
+        torch.cuda.synchronize()
+        dist.barrier()
+        np.save(os.path.join(outdir, f"slice{rank}.npy"), flats[0][lo:hi].cpu().numpy().view(np.uint32))
+        np.save(os.path.join(outdir, f"raised{rank}.npy"), np.array([raised]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_peer_setup_failure_falls_back_collectively(gpu, mh, oracle, tmp_path):
+    world = 4
+    mp.spawn(_fallback_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    assert all(bool(np.load(tmp_path / f"raised{r}.npy")[0]) for r in range(world))
+    got = np.concatenate([np.load(tmp_path / f"slice{r}.npy") for r in range(world)])
+    from oracle.binding import OP_SUB, Views
+    n, t, q = 256, 32, 65521
+    rng = np.random.default_rng(5)
+    out, lhs, rhs = [rng.integers(0, q, n * n, dtype=np.uint32) for _ in range(3)]
+    want = out.copy()
+    oracle.mm_dense(n, t, q, want, lhs, rhs, Views(0, 0, 0, n, n, n), op=OP_SUB)
+    assert np.array_equal(got, want)
