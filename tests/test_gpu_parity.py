@@ -71,7 +71,10 @@ def test_smoke_cfg1_shape(gpu, mh, oracle, reference):
     assert ctr.as_tuple() == ref_ctr.as_tuple()
 
 
-@pytest.mark.parametrize("q", [2, 97, 257, P16, P24, P31])
+# limb-count boundaries (251 / 257: 1 -> 2 limbs; 65519 / 65537: 2 -> 3; 16777213 /
+# 16777259: 3 -> 4) and a 2-limb prime whose 2^16 mod q >= 256 (40961: the per-class fold
+# instead of the lean one, no early TMEM release)
+@pytest.mark.parametrize("q", [2, 97, 251, 257, 40961, 65519, P16, 65537, P24, 16777259, 1000003, P31])
 @pytest.mark.parametrize("op", [OP_ADD, OP_SUB, OP_SET])
 def test_random_misaligned_views(gpu, mh, oracle, q, op):
     """Random (ragged, misaligned, rectangular) views; whole-container equality."""
@@ -1044,3 +1047,27 @@ def test_upload_adaptive_raw_tail(gpu, mh, opts):
     mh._check(mh.lib().mhg_matrix_upload_range(m.handle, hp.data_ptr(), off, cnt, None))
     want[off:off + cnt] = part
     assert np.array_equal(m.cells(), want)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("udig", [None, 0])
+def test_general_fold_prime_at_chunk_limits(gpu, mh, opts, udig):
+    """A 2-limb prime with 2^16 mod q >= 256 (q = 40961) takes the per-class fold and the
+    fixed TMEM layout (no early release): extreme residues at one full exact chunk, one
+    slice past it and a long K, ADD / SUB / SET, C_old = q - 1, closed form."""
+    import torch
+    if udig is not None:
+        opts(mh.OPT_DIGITS, udig)
+    q = 40961
+    n, t, rows, cols = 32768, 64, 512, 512
+    bufs = [torch.empty(n * n, dtype=torch.int32, device="cuda") for _ in range(3)]
+    try:
+        kc = _u8_chunk_slices(q) * 128
+        for k in sorted({kc, kc + 128, 32768}):
+            for x, y in [(0x9FFF, 0x9FFF), (0x9FFF, q - 1), ((q - 1) // 2, (q + 1) // 2)]:
+                for op in (OP_ADD, OP_SUB, OP_SET):
+                    a = (q - x) % q if op == OP_SUB else x
+                    _device_constant_case(mh, n, t, q, a, y, q - 1, rows, k, cols, op, bufs)
+    finally:
+        del bufs
+        torch.cuda.empty_cache()
