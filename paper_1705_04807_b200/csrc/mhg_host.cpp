@@ -284,7 +284,10 @@ mhg::GemmParams gemm_params(const Buffers& b, const mhg_view& out, const Checked
     if (g.udig) p.bias32 = 0;
     p.fold = g.L != 2 ? 3 : (g.udig ? mhg::fold_level_u8(q, kchunk) : mhg::fold_level(q, kchunk));
     p.fold = std::max<int>(p.fold, (int)mhg::option(mhg::kOptMinFold));
-    p.group = 8;  // measured best at the power cap (profiles/r01_raster_groups.txt)
+    // raster group (row tiles sharing rhs panels in L2): 8 measured best up to n = 16384
+    // (profiles/r01_raster_groups.txt; G = 4 / 6 / 12 within noise or slower), 4 from 256
+    // column tiles on (n = 32768: 95.4 vs 97.0 ms, G = 12 108 ms; profiles/r02_raster_groups.txt)
+    p.group = g.Nt >= 256 ? 4 : 8;
     // suspend (instead of re-polling) in mbarrier waits: -1% at n = 16384 / 8192 under the
     // power cap (profiles/r01_wait_hint.txt); the thread wakes when the phase completes
     p.wait_hint = 100000;
