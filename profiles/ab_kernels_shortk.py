@@ -1,7 +1,7 @@
 """Short-K GEMM kernels A/B in one process: MHG_OPT_GEMM_KERNEL variants on the Schur views
 15360 x K x 15360 at (1024, 1024) of n = 16384 (p = 65521, C -= A.B), GEMM-only median of
 5 x plan.time_gemm(5), plus the TU sweep (panel 1024) per variant.
-  python profiles/ab_kernels_shortk.py [rounds] name=VALUE ...   (e.g. 1cta=1 dual=3)"""
+  python profiles/ab_kernels_shortk.py [rounds] name=VALUE ...   (e.g. 1cta=1 pair=2)"""
 import os
 import statistics
 import sys
@@ -13,7 +13,7 @@ import paper_1705_04807_b200 as mh  # noqa: E402
 from paper_1705_04807_b200.tu import schur_plans, schur_sweep  # noqa: E402
 
 args = [a for a in sys.argv[1:] if "=" not in a]
-variants = [(a.split("=")[0], int(a.split("=")[1])) for a in sys.argv[1:] if "=" in a] or [("1cta", 1), ("dual", 3)]
+variants = [(a.split("=")[0], int(a.split("=")[1])) for a in sys.argv[1:] if "=" in a] or [("1cta", 1), ("pair", 2)]
 rounds = int(args[0]) if args else 2
 Ks = [int(k) for k in os.environ.get("AB_KS", "512,1024,2048,4096,8192").split(",")]
 n, q = 16384, 65521
