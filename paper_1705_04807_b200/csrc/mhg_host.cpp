@@ -274,6 +274,7 @@ mhg::GemmParams gemm_params(const Buffers& b, const mhg_view& out, const Checked
     const uint64_t two62 = uint64_t(1) << 62;
     p.bias = ((two62 + q - 1) / q) * q;
     p.m32 = (uint32_t)((uint64_t(1) << 32) / q);
+    p.nq = (uint32_t)(0u - q);
     p.bias32 = (uint32_t)(((uint64_t(1) << 31) / q) * q);
     p.w16 = (uint32_t)((uint64_t(1) << 16) % q);
     p.w16_small = p.w16 < 256;

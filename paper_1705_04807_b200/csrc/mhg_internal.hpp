@@ -65,6 +65,7 @@ struct GemmParams {
     uint64_t bias;               // multiple of q >= 2^62 (signed -> unsigned shift)
     // 32-bit fold (L <= 2, q <= 2^16): class sums obey |a_c| <= 2^31 - 2^17
     uint32_t m32;                // floor(2^32 / q)
+    uint32_t nq;                 // 2^32 - q (u - t q == u + t nq mod 2^32: one IMAD)
     uint32_t bias32;             // q * floor(2^31 / q): a_c + bias32 in [0, 2^32)
     uint32_t w16;                // 2^16 mod q
     int w16_small;               // w16 < 256: fold the top class without a mulmod

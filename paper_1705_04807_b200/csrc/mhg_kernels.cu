@@ -668,8 +668,8 @@ __device__ __forceinline__ uint32_t mulmod(uint32_t a, uint32_t b, const GemmPar
 // u mod q for u < 2^32, q <= 2^16: Barrett with m = floor(2^32/q) is off by at
 // most one multiple of q.
 __device__ __forceinline__ uint32_t red32(uint32_t u, const GemmParams& p) {
-    const uint32_t r = u - __umulhi(u, p.m32) * p.q;
-    return umin(r, r - p.q);  // r < 2q: r - q wraps above r when r < q
+    const uint32_t r = __umulhi(u, p.m32) * p.nq + u;  // u - floor(u m32 / 2^32) q
+    return umin(r, r + p.nq);  // r < 2q: r - q wraps above r when r < q
 }
 
 // Fold the 2L-1 weight classes of one output element to a canonical residue:
@@ -1068,6 +1068,38 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     };
     auto drain_l2_small = [&](uint32_t tbase, uint32_t n_tile, uint32_t* cur_, uint32_t layout) {
         const int lo_cls = layout ? 0 : 1;  // first group: {lo_cls, lo_cls + 1}
+        if constexpr (FOLD == 1) {
+            // Both layouts in one code path (half the instructions in the I-cache): with
+            // T(a1) = 256 (a1 & 255) + w16 (a1 >> 8), group 1 adds T(a1) + cb * b and group 2
+            // reduces cur + cz * z, where (b, cb, z, cz) = (a2, w16, a0, 1) for layout 0 and
+            // (a0, 1, a2, w16) for layout 1 -- the two formulas of fold_g1 / fold_g2.
+            const uint32_t col_b = layout ? 0u : 2u * W, col_z = layout ? 2u * W : 0u;
+            const uint32_t cb = layout ? 1u : p.w16, cz = layout ? p.w16 : 1u;
+#pragma unroll
+            for (int j0 = 0; j0 < WH; j0 += CW) {
+                if ((uint64_t)n_tile * W + jb + j0 >= p.cols) continue;  // warp-uniform
+                int32_t a[2][CW];
+                tmem_ld<CW>(tbase + W + j0, a[0]);
+                tmem_ld<CW>(tbase + col_b + j0, a[1]);
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < CW; ++j) {
+                    const uint32_t a1 = (uint32_t)a[0][j];
+                    cur_[j0 + j] += ((a1 & 0xffu) << 8) + p.w16 * (uint32_t)(a[0][j] >> 8) + cb * (uint32_t)a[1][j];
+                }
+            }
+            release();
+#pragma unroll
+            for (int j0 = 0; j0 < WH; j0 += CW) {
+                if ((uint64_t)n_tile * W + jb + j0 >= p.cols) continue;
+                int32_t a[1][CW];
+                tmem_ld<CW>(tbase + col_z + j0, a[0]);
+                tmem_wait_ld();
+#pragma unroll
+                for (int j = 0; j < CW; ++j) cur_[j0 + j] = red32(cur_[j0 + j] + cz * (uint32_t)a[0][j] + p.bias32, p);
+            }
+            return;
+        }
 #pragma unroll
         for (int j0 = 0; j0 < WH; j0 += CW) {
             if ((uint64_t)n_tile * W + jb + j0 >= p.cols) continue;  // warp-uniform
@@ -1189,17 +1221,20 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         // measured slower, profiles/r02_short_k.txt)
         uint4 c1[XPOSE ? NI : 1];
         uint32_t m1 = 0;
-        uint64_t own = 0, c0[XPOSE ? NH : 1];
+        uint64_t own = 0, c0[XPOSE ? NH : 1], rbs[XPOSE ? NI : 1];
         bool vec[XPOSE ? NH : 1];
         auto issue_cold = [&]() {
             if constexpr (XPOSE) {
                 own = row_at(m, row);
 #pragma unroll
                 for (int h = 0; h < NH; ++h) c0[h] = col_at(n, PW * h + 4 * ch, vec[h]);
+                // container offsets of the rows this lane moves in the coalesced order
+#pragma unroll
+                for (int i = 0; i < NI; ++i) rbs[i] = __shfl_sync(0xffffffffu, own, RPI * i + sr);
                 if (p.mode != 2) {
 #pragma unroll
                     for (int i = 0; i < NI; ++i) {
-                        const uint64_t rb = __shfl_sync(0xffffffffu, own, RPI * i + sr);
+                        const uint64_t rb = rbs[i];
                         const bool live = rb != kNoCol;
                         if (vec[0])
                             cp_async16(xaddr(RPI * i + sr, ch), p.out + (live ? rb + c0[0] : 0), live ? 16u : 0u);
@@ -1285,7 +1320,8 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
                 // free region, so those are drained and folded first, TMEM is
                 // released, and the remaining class is drained while the next
                 // job's MMAs run.
-                const bool alt = early_release<L>(p);
+                // lean folds (FOLD 1 / 2) exist only for w16 < 256: always the alternating layout
+                const bool alt = (L == 2 && FOLD <= 2) || early_release<L>(p);
                 const uint32_t tb = tmem + lane_base + ((alt && acc_ph) ? W : 0) + jb;
                 if (!alt) {
                     // fixed layout: drain and fold every class, then release
@@ -1336,10 +1372,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
             epi_issue += ta - tt0;
             // The shared-memory loads of a pass are issued as one batch (the asm volatile
             // accesses keep source order, so load / use / store per chunk would expose every
-            // load's latency: K = 1024 -1.3%); the rows' container offsets are fetched once.
-            uint64_t rbs[NI];
-#pragma unroll
-            for (int i = 0; i < NI; ++i) rbs[i] = __shfl_sync(0xffffffffu, own, RPI * i + sr);
+            // load's latency: K = 1024 -1.3%).
 #pragma unroll
             for (int h = 0; h < NH; ++h) {
                 if (addc) {
