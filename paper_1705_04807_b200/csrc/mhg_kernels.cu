@@ -752,6 +752,12 @@ __device__ __forceinline__ uint32_t fold_part(const int32_t (&acc)[C1 - C0][CW],
     }
 }
 
+#ifndef MHG_XADDR_VOLATILE
+#define MHG_XADDR_VOLATILE 1  // transpose-buffer addresses recomputed per use (fewer spills)
+#endif
+#ifndef MHG_COLD_MID
+#define MHG_COLD_MID 0  // pass 0's C_old requested between the two drain groups (A/B)
+#endif
 template <int L>
 struct GemmCfg {
     static constexpr int W = (L <= 2) ? 128 : 64;       // output columns per tile
@@ -1066,7 +1072,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         if constexpr (FOLD == 2) return red32(c + p.w16 * r2 + p.bias32, p);
         return red32(c + p.w16 * r2, p);
     };
-    auto drain_l2_small = [&](uint32_t tbase, uint32_t n_tile, uint32_t* cur_, uint32_t layout) {
+    auto drain_l2_small = [&](uint32_t tbase, uint32_t n_tile, uint32_t* cur_, uint32_t layout, auto&& after_release) {
         const int lo_cls = layout ? 0 : 1;  // first group: {lo_cls, lo_cls + 1}
         if constexpr (FOLD == 1) {
             // Both layouts in one code path (half the instructions in the I-cache): with
@@ -1089,6 +1095,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
                 }
             }
             release();
+            after_release();
 #pragma unroll
             for (int j0 = 0; j0 < WH; j0 += CW) {
                 if ((uint64_t)n_tile * W + jb + j0 >= p.cols) continue;
@@ -1113,6 +1120,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
             for (int j = 0; j < CW; ++j) cur_[j0 + j] += fold_g1(a[0][j], a[1][j], layout);
         }
         release();
+        after_release();
 #pragma unroll
         for (int j0 = 0; j0 < WH; j0 += CW) {
             if ((uint64_t)n_tile * W + jb + j0 >= p.cols) continue;
@@ -1157,7 +1165,13 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     // 8-lane phase of a 16-byte access hits 8 distinct bank groups in both orders)
     auto xaddr = [&](int r, int c) -> uint32_t {
         const int sw = CPR == 8 ? (r & 7) : ((r >> 1) & 3);
-        return xb + r * (PW * 4) + ((c ^ sw) << 4);
+        uint32_t base = xb;
+#if MHG_XADDR_VOLATILE
+        // recomputed at each use: hoisted out of the tile loop, the per-lane addresses
+        // (16+ registers at the 168-register cap) are spilled and reloaded every tile
+        asm volatile("" : "+r"(base));
+#endif
+        return base + r * (PW * 4) + ((c ^ sw) << 4);
     };
     // container offset of output row m*128 + r (kNoCol past the view)
     auto row_at = [&](uint32_t m, int r) -> uint64_t {
@@ -1223,7 +1237,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         uint32_t m1 = 0;
         uint64_t own = 0, c0[XPOSE ? NH : 1], rbs[XPOSE ? NI : 1];
         bool vec[XPOSE ? NH : 1];
-        auto issue_cold = [&]() {
+        auto issue_cold0 = [&]() {
             if constexpr (XPOSE) {
                 own = row_at(m, row);
 #pragma unroll
@@ -1238,13 +1252,27 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
                         const bool live = rb != kNoCol;
                         if (vec[0])
                             cp_async16(xaddr(RPI * i + sr, ch), p.out + (live ? rb + c0[0] : 0), live ? 16u : 0u);
-                        const bool ok = vec[1] && live;
-                        m1 |= (uint32_t)ok << i;
-                        c1[i] = c_load(reinterpret_cast<const uint4*>(p.out + (ok ? rb + c0[1] : 0)));
                     }
                     cp_async_commit();
                 }
             }
+        };
+        auto issue_cold1 = [&]() {
+            if constexpr (XPOSE) {
+                if (p.mode != 2) {
+#pragma unroll
+                    for (int i = 0; i < NI; ++i) {
+                        const bool ok = vec[1] && rbs[i] != kNoCol;
+                        m1 |= (uint32_t)ok << i;
+                        c1[i] = c_load(reinterpret_cast<const uint4*>(p.out + (ok ? rbs[i] + c0[1] : 0)));
+                    }
+                }
+            }
+        };
+        bool cold0_issued = false;
+        auto issue_cold = [&]() {
+            if (!cold0_issued) issue_cold0();
+            issue_cold1();
         };
         if constexpr (XPOSE) {
             // the classes are folded from zero; C_old is loaded only after the tile's
@@ -1334,7 +1362,16 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
                 if constexpr (L == 2) {
                     // lean split for q = 2^16 - small (e.g. 65521): the first group
                     // leaves cur unreduced (< 2^32 - 2^24); the second group finishes
-                    drain_l2_small(tb, n, cur, acc_ph);
+                    drain_l2_small(tb, n, cur, acc_ph, [&]() {
+#if MHG_COLD_MID
+                        if constexpr (XPOSE) {
+                            if (c + 1 == nchunks) {
+                                issue_cold0();
+                                cold0_issued = true;
+                            }
+                        }
+#endif
+                    });
                     epi_busy += diag_clock() - w1;
                     acc_ph ^= 1;
                     continue;
