@@ -12,6 +12,10 @@ with panel width `block` (the panel factorisation / triangular solves of TU are
 outside the hot path and outside this repo):
 
     for k0 = 0, block, 2*block, ...:   A[k1:, k1:] -= A[k1:, k0:k1] * A[k0:k1, k1:]
+
+`SweepGraph` captures a whole sweep (every step's pack + GEMM) into ONE CUDA graph,
+so a repeated sweep is a single launch: no host work between the steps (from Python
+each plan launch costs tens of microseconds, more than the last steps' GPU time).
 """
 from __future__ import annotations
 
@@ -43,11 +47,37 @@ def schur_plans(M: Matrix, block: int, op: int = OP_SUB) -> List[Plan]:
     return [Plan(p, op, allow_alias=True) for p in schur_views(M, block)]
 
 
+def sweep_macs(plans) -> int:
+    """GF(p) multiply-adds of one sweep (the reference's scalar_macs counter, summed)."""
+    return sum(pl.counters().scalar_macs for pl in plans)
+
+
 def schur_sweep(M: Matrix, block: int, op: int = OP_SUB, stream=None, plans=None) -> int:
     """Run the sweep (asynchronously on `stream`); returns GF(p) MACs done."""
     plans = plans if plans is not None else schur_plans(M, block, op)
-    macs = 0
     for pl in plans:
         pl.run(stream)
-        macs += pl.counters().scalar_macs
-    return macs
+    return sweep_macs(plans)
+
+
+class SweepGraph:
+    """A whole sweep captured into one CUDA graph (torch.cuda.CUDAGraph): `replay(stream)`
+    runs every step's pack and GEMM back to back with no host work in between.  The plans
+    (and their workspaces) must outlive the graph; the parent's cells are read and written
+    in place, so a replay is the same in-place update as schur_sweep."""
+
+    def __init__(self, M: Matrix, block: int, op: int = OP_SUB, plans=None):
+        import torch
+        self.plans = plans if plans is not None else schur_plans(M, block, op)
+        self.macs = sweep_macs(self.plans)
+        self._stream = torch.cuda.Stream()
+        self._graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self._graph, stream=self._stream):
+            for pl in self.plans:
+                pl.run(self._stream)
+
+    def replay(self) -> int:
+        """Launch the captured sweep (on the graph's capture stream ordering of the caller's
+        current stream, as torch.cuda.CUDAGraph.replay); returns GF(p) MACs done."""
+        self._graph.replay()
+        return self.macs
