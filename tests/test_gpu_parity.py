@@ -540,6 +540,31 @@ def test_tu_schur_sweep(gpu, mh, oracle):
     assert macs == sum(((n - k) ** 2) * block for k in range(block, n, block))
 
 
+def test_tu_sweep_graph(gpu, mh, oracle):
+    """tu.SweepGraph: the whole aliased sweep captured into one CUDA graph; two replays equal
+    two oracle sweeps (every step reads the previous step's output from the parent)."""
+    import torch
+    from paper_1705_04807_b200.tu import SweepGraph
+    n, t, q, block = 512, 32, P16, 128
+    (cells,) = _fill(oracle, 23, n, q)[:1]
+    lay, mod = mh.Layout(n, t), mh.Modulus(q)
+    M = mh.Matrix(lay, mod).upload(cells)
+    sg = SweepGraph(M, block)
+    want = cells.copy()
+    for rep in range(2):
+        macs = sg.replay()
+        k0 = 0
+        while k0 + block < n:
+            k1, rest = k0 + block, n - k0 - block
+            v = Views(oracle.encode(n, t, k1, k1), oracle.encode(n, t, k1, k0), oracle.encode(n, t, k0, k1),
+                      rest, block, rest)
+            oracle.mm_dense(n, t, q, want, want.copy(), want.copy(), v, op=OP_SUB)
+            k0 = k1
+        torch.cuda.synchronize()
+        assert np.array_equal(M.cells(), want), rep
+    assert macs == sum(((n - k) ** 2) * block for k in range(block, n, block))
+
+
 @pytest.mark.parametrize("kernel", [1, 2])
 def test_both_gemm_kernels(gpu, mh, oracle, opts, kernel):
     """The single-CTA (k_gemm) and CTA-pair (k_gemm2, cta_group::2) kernels
