@@ -453,9 +453,15 @@ void launch_gemm_stage(const Buffers& b, const mhg_view& out, const Checked& c,
         stats = p.stats = statsbuf.ptr;
     }
     const TensorMaps tm = tensor_maps(b, g);
-    if (gemm_begin) cuda_check(cudaEventRecord(gemm_begin, (cudaStream_t)stream), "event");
+    // under stream capture (the plans' profiling graph) the records must become event-record
+    // nodes of the graph (cudaEventRecordExternal); outside capture that flag is refused
+    cudaStreamCaptureStatus cst = cudaStreamCaptureStatusNone;
+    if (gemm_begin || gemm_end)
+        cuda_check(cudaStreamIsCapturing((cudaStream_t)stream, &cst), "capture query");
+    const unsigned rec_flags = cst == cudaStreamCaptureStatusActive ? cudaEventRecordExternal : cudaEventRecordDefault;
+    if (gemm_begin) cuda_check(cudaEventRecordWithFlags(gemm_begin, (cudaStream_t)stream, rec_flags), "event");
     launch_gemm_any(p, g, tm, stream);
-    if (gemm_end) cuda_check(cudaEventRecord(gemm_end, (cudaStream_t)stream), "event");
+    if (gemm_end) cuda_check(cudaEventRecordWithFlags(gemm_end, (cudaStream_t)stream, rec_flags), "event");
     if (stats) {
         const int n = device_info().sms;
         std::vector<unsigned long long> h((size_t)n * mhg::kStatCount);
@@ -558,7 +564,37 @@ struct mhg_plan_s {
     bool profiling = false;
     std::vector<cudaEvent_t> ev;
     size_t ev_used = 0;
+    // profiling graph: the plan's graph with event-record nodes around the GEMM; every run
+    // points the two nodes at the next ring pair, so profiled runs cost one graph launch
+    // (no per-kernel host launches between the steps of a timed loop)
+    cudaGraph_t pgraph = nullptr;
+    cudaGraphExec_t pexec = nullptr;
+    cudaGraphNode_t pnode[2] = {nullptr, nullptr};
+    cudaEvent_t pev[2] = {nullptr, nullptr};
 };
+
+namespace {
+// Capture fn(stream) into a graph on a private capturing stream.
+template <typename F>
+cudaGraph_t capture_graph(F&& fn) {
+    cudaStream_t cap;
+    cuda_check(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking), "capture stream");
+    cuda_check(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal), "capture");
+    try {
+        fn(cap);
+    } catch (...) {
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(cap, &g);
+        if (g) cudaGraphDestroy(g);
+        cudaStreamDestroy(cap);
+        throw;
+    }
+    cudaGraph_t g = nullptr;
+    cuda_check(cudaStreamEndCapture(cap, &g), "end capture");
+    cudaStreamDestroy(cap);
+    return g;
+}
+}  // namespace
 
 extern "C" {
 
@@ -1044,7 +1080,37 @@ mhg_status mhg_plan_run(mhg_plan p, void* stream) {
             }
             cudaEvent_t b = p->ev[p->ev_used], e = p->ev[p->ev_used + 1];
             p->ev_used += 2;
-            launch_multiply(p->buf, p->out, p->lhs, p->rhs, p->chk, p->geo, p->op, stream, b, e);
+            cudaStreamCaptureStatus pst = cudaStreamCaptureStatusNone;
+            cuda_check(cudaStreamIsCapturing((cudaStream_t)stream, &pst), "capture query");
+            if (pst != cudaStreamCaptureStatusNone) {
+                launch_multiply(p->buf, p->out, p->lhs, p->rhs, p->chk, p->geo, p->op, stream, b, e);
+                return;
+            }
+            if (!p->pexec) {
+                for (auto& ev : p->pev) cuda_check(cudaEventCreate(&ev), "event");
+                p->pgraph = capture_graph([&](cudaStream_t cap) {
+                    launch_multiply(p->buf, p->out, p->lhs, p->rhs, p->chk, p->geo, p->op, cap, p->pev[0],
+                                    p->pev[1]);
+                });
+                size_t nn = 0;
+                cuda_check(cudaGraphGetNodes(p->pgraph, nullptr, &nn), "graph nodes");
+                std::vector<cudaGraphNode_t> nodes(nn);
+                cuda_check(cudaGraphGetNodes(p->pgraph, nodes.data(), &nn), "graph nodes");
+                for (cudaGraphNode_t nd : nodes) {
+                    cudaGraphNodeType ty;
+                    cuda_check(cudaGraphNodeGetType(nd, &ty), "node type");
+                    if (ty != cudaGraphNodeTypeEventRecord) continue;
+                    cudaEvent_t ev = nullptr;
+                    cuda_check(cudaGraphEventRecordNodeGetEvent(nd, &ev), "event node");
+                    for (int k = 0; k < 2; ++k)
+                        if (ev == p->pev[k]) p->pnode[k] = nd;
+                }
+                if (!p->pnode[0] || !p->pnode[1]) fail(MHG_ERR_DEVICE, "profiling graph: event nodes not found");
+                cuda_check(cudaGraphInstantiate(&p->pexec, p->pgraph, 0), "graph instantiate");
+            }
+            cuda_check(cudaGraphExecEventRecordNodeSetEvent(p->pexec, p->pnode[0], b), "set event");
+            cuda_check(cudaGraphExecEventRecordNodeSetEvent(p->pexec, p->pnode[1], e), "set event");
+            cuda_check(cudaGraphLaunch(p->pexec, (cudaStream_t)stream), "graph launch");
             return;
         }
         cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
@@ -1319,6 +1385,10 @@ mhg_status mhg_plan_destroy(mhg_plan p) {
     return guarded([&] {
         if (!p) return;
         for (cudaEvent_t e : p->ev) cudaEventDestroy(e);
+        if (p->pexec) cudaGraphExecDestroy(p->pexec);
+        if (p->pgraph) cudaGraphDestroy(p->pgraph);
+        for (cudaEvent_t e : p->pev)
+            if (e) cudaEventDestroy(e);
         if (p->exec) cudaGraphExecDestroy(p->exec);
         if (p->graph) cudaGraphDestroy(p->graph);
         if (p->mem) cudaFree(p->mem);

@@ -629,6 +629,26 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, int32_t (&v)[16]) {
         : "r"(taddr));
 }
 
+// Two x16 loads and the wait in ONE asm statement: the compiler cannot consume the first
+// load's registers (scheduling its arithmetic between the loads) before the second is issued
+// and both have landed -- both loads are in flight together.
+__device__ __forceinline__ void tmem_ld16x2_wait(uint32_t ta, uint32_t tb, int32_t (&a)[16], int32_t (&b)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, [%32];\n\t"
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+        "{%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%33];\n\t"
+        "tcgen05.wait::ld.sync.aligned;"
+        : "=r"(a[0]), "=r"(a[1]), "=r"(a[2]), "=r"(a[3]), "=r"(a[4]), "=r"(a[5]), "=r"(a[6]),
+          "=r"(a[7]), "=r"(a[8]), "=r"(a[9]), "=r"(a[10]), "=r"(a[11]), "=r"(a[12]),
+          "=r"(a[13]), "=r"(a[14]), "=r"(a[15]),
+          "=r"(b[0]), "=r"(b[1]), "=r"(b[2]), "=r"(b[3]), "=r"(b[4]), "=r"(b[5]), "=r"(b[6]),
+          "=r"(b[7]), "=r"(b[8]), "=r"(b[9]), "=r"(b[10]), "=r"(b[11]), "=r"(b[12]),
+          "=r"(b[13]), "=r"(b[14]), "=r"(b[15])
+        : "r"(ta), "r"(tb)
+        : "memory");
+}
+
 __device__ __forceinline__ void tmem_ld8(uint32_t taddr, int32_t (&v)[8]) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
@@ -752,11 +772,19 @@ __device__ __forceinline__ uint32_t fold_part(const int32_t (&acc)[C1 - C0][CW],
     }
 }
 
+#ifndef MHG_SMR
+#define MHG_SMR 1
+#endif
+#define MHG_SMR_CTL_REGS 56   // warpgroup 0 after setmaxnreg.dec
+#define MHG_SMR_EPI_REGS 224  // epilogue warpgroups after setmaxnreg.inc (128*56 + 256*224 <= 64K)
+#ifndef MHG_DRAIN_PIPE
+#define MHG_DRAIN_PIPE MHG_SMR  // all TMEM loads of a drain group in flight at once (needs the registers)
+#endif
 #ifndef MHG_XADDR_VOLATILE
 #define MHG_XADDR_VOLATILE 1  // transpose-buffer addresses recomputed per use (fewer spills)
 #endif
 #ifndef MHG_COLD_MID
-#define MHG_COLD_MID 0  // pass 0's C_old requested between the two drain groups (A/B)
+#define MHG_COLD_MID 1  // pass 0's C_old requested between the two drain groups (A/B)
 #endif
 template <int L>
 struct GemmCfg {
@@ -771,7 +799,10 @@ struct GemmCfg {
     // row-per-thread C access (see epilogue_role)
     static constexpr bool XPOSE = (W == 128);
     static constexpr int EPI_WARPS = 8;
-    static constexpr int EPI_W0 = 2;  // first epilogue warp
+    // MHG_SMR: warpgroup 0 = producer, MMA issuer and two idle warps, which give registers
+    // back (setmaxnreg.dec) so the two epilogue warpgroups run at SMR_EPI_REGS instead of the
+    // 168 a 10-warp CTA is capped at (three warps share SMSPs 0 and 1)
+    static constexpr int EPI_W0 = MHG_SMR ? 4 : 2;  // first epilogue warp
     static constexpr int XBUF = XPOSE ? EPI_WARPS * (W * 4 / EPI_WARPS >= 64 ? 4096 : 2048) : 0;
     static constexpr int FIXED = 1024 /*align slack*/ + 256 /*barriers*/ + 8 * W /*column offsets*/ + XBUF;
     static constexpr int STAGES_RAW = (232448 - FIXED) / STAGE;
@@ -780,6 +811,7 @@ struct GemmCfg {
     static_assert(SMEM <= 232448, "227 KB dynamic shared memory limit");
     static constexpr int EPI_THREADS = EPI_WARPS * 32;
     static constexpr int THREADS = 32 * EPI_W0 + EPI_THREADS;  // producer, MMA, (idle,) epilogue
+    static_assert(!MHG_SMR || (THREADS == 384 && EPI_WARPS == 8), "setmaxnreg layout: 3 warpgroups");
     static_assert(CLASSES * W <= 512, "TMEM columns");
     static_assert(STAGES >= 2, "pipeline depth");
 };
@@ -1003,7 +1035,7 @@ __global__ void __launch_bounds__(128) k_conv_tma(const __grid_constant__ CUtens
 // geometry (no table loads).  Otherwise (narrow tiles, CTA pair) the row's
 // C_old is prefetched into registers at tile start, addressed through smem
 // column offsets.
-template <int L, int W, int EPI_WARPS, bool PAIR, bool XPOSE = false, int FOLD = 3>
+template <int L, int W, int EPI_WARPS, bool PAIR, bool XPOSE = false, int FOLD = 3, int EW0 = 2>
 __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t first_tile,
                                               uint32_t tile_stride, uint32_t num_tiles,
                                               uint32_t row_groups, uint32_t rank, uint32_t nchunks,
@@ -1015,7 +1047,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     constexpr int CLASSES = 2 * L - 1;
     constexpr int CW = L <= 2 ? 16 : 8;  // TMEM columns per drain step (x8 / x32 measured slower)
     constexpr uint64_t kNoCol = ~uint64_t(0);
-    constexpr int EPI_W0 = 2;  // warps 0, 1: producer, MMA issuer
+    constexpr int EPI_W0 = EW0;  // first epilogue warp (warps 0, 1: producer, MMA issuer)
     const int ew = warp - EPI_W0;
     const int quad = warp & 3;
     const int jb = (ew >> 2) * WH;  // first tile column of this warp
@@ -1081,21 +1113,55 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
             // (a0, 1, a2, w16) for layout 1 -- the two formulas of fold_g1 / fold_g2.
             const uint32_t col_b = layout ? 0u : 2u * W, col_z = layout ? 2u * W : 0u;
             const uint32_t cb = layout ? 1u : p.w16, cz = layout ? p.w16 : 1u;
+            static_assert(CW == 16, "x16 drain steps");
+#if MHG_DRAIN_PIPE
+            // every load of the group in flight before the first fold (the epilogue
+            // warpgroups have the registers under MHG_SMR); columns past the view are folded
+            // too (never stored)
+            {
+                int32_t a[WH / CW][2][CW];
+#pragma unroll
+                for (int s = 0; s < WH / CW; ++s) {
+                    tmem_ld16(tbase + W + s * CW, a[s][0]);
+                    tmem_ld16(tbase + col_b + s * CW, a[s][1]);
+                }
+                tmem_wait_ld();
+#pragma unroll
+                for (int s = 0; s < WH / CW; ++s)
+#pragma unroll
+                    for (int j = 0; j < CW; ++j) {
+                        const uint32_t a1 = (uint32_t)a[s][0][j];
+                        cur_[s * CW + j] += ((a1 & 0xffu) << 8) + p.w16 * (uint32_t)(a[s][0][j] >> 8) + cb * (uint32_t)a[s][1][j];
+                    }
+            }
+#else
 #pragma unroll
             for (int j0 = 0; j0 < WH; j0 += CW) {
                 if ((uint64_t)n_tile * W + jb + j0 >= p.cols) continue;  // warp-uniform
                 int32_t a[2][CW];
-                tmem_ld<CW>(tbase + W + j0, a[0]);
-                tmem_ld<CW>(tbase + col_b + j0, a[1]);
-                tmem_wait_ld();
+                tmem_ld16x2_wait(tbase + W + j0, tbase + col_b + j0, a[0], a[1]);
 #pragma unroll
                 for (int j = 0; j < CW; ++j) {
                     const uint32_t a1 = (uint32_t)a[0][j];
                     cur_[j0 + j] += ((a1 & 0xffu) << 8) + p.w16 * (uint32_t)(a[0][j] >> 8) + cb * (uint32_t)a[1][j];
                 }
             }
+#endif
             release();
             after_release();
+#if MHG_DRAIN_PIPE
+            {
+                int32_t a[WH / CW][CW];
+#pragma unroll
+                for (int s = 0; s < WH / CW; ++s) tmem_ld16(tbase + col_z + s * CW, a[s]);
+                tmem_wait_ld();
+#pragma unroll
+                for (int s = 0; s < WH / CW; ++s)
+#pragma unroll
+                    for (int j = 0; j < CW; ++j)
+                        cur_[s * CW + j] = red32(cur_[s * CW + j] + cz * (uint32_t)a[s][j] + p.bias32, p);
+            }
+#else
 #pragma unroll
             for (int j0 = 0; j0 < WH; j0 += CW) {
                 if ((uint64_t)n_tile * W + jb + j0 >= p.cols) continue;
@@ -1105,6 +1171,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
 #pragma unroll
                 for (int j = 0; j < CW; ++j) cur_[j0 + j] = red32(cur_[j0 + j] + cz * (uint32_t)a[0][j] + p.bias32, p);
             }
+#endif
             return;
         }
 #pragma unroll
@@ -1469,7 +1536,7 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
         }
         epi_tail += diag_clock() - tt0;
     }
-    if (p.stats && warp == 2 && lane == 0) {
+    if (p.stats && warp == EW0 && lane == 0) {
         p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiWaitFull] = epi_wait;
         p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiBusy] = epi_busy;
         p.stats[(uint64_t)blockIdx.x * kStatCount + kStatEpiPrologue] = epi_pro;
@@ -1524,7 +1591,10 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-
+    if (warp < Cfg::EPI_W0) {
+#if MHG_SMR
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(MHG_SMR_CTL_REGS));
+#endif
     if (warp == 0) {
         // ---------------- producer: one bulk copy per operand per stage
         if (lane == 0) {
@@ -1628,8 +1698,13 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
                 o[kStatMmaWaitTmem] = wait_tmem;
             }
         }
+    }
     } else {
-        epilogue_role<L, W, Cfg::EPI_WARPS, false, Cfg::XPOSE, FOLD>(
+        // the inc must dominate the epilogue code for ptxas to allocate it the larger budget
+#if MHG_SMR
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(MHG_SMR_EPI_REGS));
+#endif
+        epilogue_role<L, W, Cfg::EPI_WARPS, false, Cfg::XPOSE, FOLD, Cfg::EPI_W0>(
             p, first_tile, tile_stride, num_tiles, p.Mt, 0u, nchunks, tmem, s_col, tmem_full,
             tmem_empty, warp, lane, xbuf);
     }
