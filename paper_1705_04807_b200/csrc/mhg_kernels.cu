@@ -1261,30 +1261,42 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     };
     // edge path (a lane whose 4-column run is not one aligned 16-byte run): the
     // pass's rows element by element, staged through the transpose buffer
+    // The lane's 4 column offsets of pass h are computed once (they do not depend on the
+    // row), and a lane whose run lies wholly past the view (the right-edge tiles of a view
+    // that is not a multiple of 128 wide) skips the rows at once.
+    auto edge_cols = [&](uint32_t n, int h, uint64_t (&cc)[4]) -> bool {
+        bool any = false;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            bool unused;
+            cc[e] = col_at(n, PW * h + 4 * ch + e, unused);
+            any |= cc[e] != kNoCol;
+        }
+        return any;
+    };
     auto edge_load = [&](uint32_t m, uint32_t n, int h) {
+        uint64_t cc[4];
+        const bool any = edge_cols(n, h, cc);
 #pragma unroll 1
         for (int i = 0; i < NI; ++i) {
-            const uint64_t rb = row_at(m, quad * 32 + RPI * i + sr);
+            const uint64_t rb = any ? row_at(m, quad * 32 + RPI * i + sr) : kNoCol;
             const uint32_t dst = xaddr(RPI * i + sr, ch);
-#pragma unroll 1
-            for (int e = 0; e < 4; ++e) {
-                bool unused;
-                const uint64_t cc = col_at(n, PW * h + 4 * ch + e, unused);
-                sts32(dst + 4 * e, (rb != kNoCol && cc != kNoCol) ? p.out[rb + cc] : 0u);
-            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                sts32(dst + 4 * e, (rb != kNoCol && cc[e] != kNoCol) ? p.out[rb + cc[e]] : 0u);
         }
     };
     auto edge_store = [&](uint32_t m, uint32_t n, int h) {
+        uint64_t cc[4];
+        if (!edge_cols(n, h, cc)) return;
 #pragma unroll 1
         for (int i = 0; i < NI; ++i) {
             const uint64_t rb = row_at(m, quad * 32 + RPI * i + sr);
+            if (rb == kNoCol) continue;
             const uint32_t src = xaddr(RPI * i + sr, ch);
-#pragma unroll 1
-            for (int e = 0; e < 4; ++e) {
-                bool unused;
-                const uint64_t cc = col_at(n, PW * h + 4 * ch + e, unused);
-                if (rb != kNoCol && cc != kNoCol) p.out[rb + cc] = lds32(src + 4 * e);
-            }
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+                if (cc[e] != kNoCol) p.out[rb + cc[e]] = lds32(src + 4 * e);
         }
     };
     for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride) {
