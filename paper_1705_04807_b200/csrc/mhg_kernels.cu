@@ -20,6 +20,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <type_traits>
+#include <utility>
 
 #include "mhg_internal.hpp"
 
@@ -426,6 +427,10 @@ __global__ void __launch_bounds__(256, MHG_PACK_MINB) k_pack_pair(PackArgs a, Pa
                                                                   uint32_t nrows) {
     constexpr int ROWS_SMEM = L * 32 * kRowsStride, COLS_SMEM = L * 128 * kColsStride;
     __shared__ __align__(16) uint8_t sd[ROWS_SMEM > COLS_SMEM ? ROWS_SMEM : COLS_SMEM];
+    // programmatic dependent launch: the GEMM that follows may start its prologue (TMEM
+    // allocation, barrier init) while the packs drain; it waits (griddepcontrol.wait) for this
+    // grid's completion before touching the operands
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     if (blockIdx.x < nrows)
         pack_rows_block<L>(blockIdx.x, a.src, a.rowoff, a.coloff, a.vecok, a.R, a.K, a.rpt, a.Kt,
                            a.Rpad, a.dst, a.dp, sd);
@@ -1602,6 +1607,9 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // launched with programmatic stream serialisation: everything above overlapped the
+    // previous kernel (the packs); operands and C may be read only after it completed
+    asm volatile("griddepcontrol.wait;" ::: "memory");
 
     if (warp < Cfg::EPI_W0) {
 #if MHG_SMR
@@ -1814,6 +1822,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // launched with programmatic stream serialisation: everything above overlapped the
+    // previous kernel (the packs); operands and C may be read only after it completed
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (warp >= 2) {
         // zero the upper weight classes once; afterwards the epilogue re-zeroes
         // them as it drains them
@@ -1925,6 +1936,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(Gemm2Cfg<L>::THREADS
     }
 }
 
+// Kernel launch with programmatic stream serialisation (PDL): the kernel may begin before
+// the previous kernel in the stream completes and waits for it with griddepcontrol.wait.
+// Used for GEMMs of at most one wave of tiles (cfg1-class problems: the launch and prologue
+// are a large part of the kernel, -10% per step); multi-wave GEMMs launch plainly (the TU
+// sweep measured 2.7% slower with PDL on every step, profiles/r02b/README.md).
+template <typename... KArgs, typename... Args>
+int launch_pdl(bool pdl, void (*kernel)(KArgs...), unsigned grid, unsigned block, size_t smem, cudaStream_t s,
+               Args&&... args) {
+    if (!pdl) {
+        kernel<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+        return (int)cudaGetLastError();
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return (int)cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 template <int L>
 int launch_gemm2_t(const GemmParams& p, const void* tmA, const void* tmB, int num_sms,
                    cudaStream_t s) {
@@ -1932,9 +1968,8 @@ int launch_gemm2_t(const GemmParams& p, const void* tmA, const void* tmB, int nu
     const uint32_t tiles = (p.Mt / 2) * p.Nt;
     uint32_t grid = 2 * tiles < (uint32_t)num_sms ? 2 * tiles : (uint32_t)num_sms;
     grid &= ~1u;
-    k_gemm2<L><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p, *static_cast<const CUtensorMap*>(tmA),
-                                                      *static_cast<const CUtensorMap*>(tmB));
-    return (int)cudaGetLastError();
+    return launch_pdl(tiles * 2 <= (uint32_t)num_sms, k_gemm2<L>, grid, Cfg::THREADS, Cfg::SMEM, s, p, *static_cast<const CUtensorMap*>(tmA),
+                      *static_cast<const CUtensorMap*>(tmB));
 }
 
 template <int L>
@@ -1972,15 +2007,14 @@ int launch_gemm_t(const GemmParams& p, int num_sms, cudaStream_t s) {
     using Cfg = GemmCfg<L>;
     const uint32_t tiles = p.Mt * p.Nt;
     const int grid = (int)(tiles < (uint32_t)num_sms ? tiles : (uint32_t)num_sms);
+    const bool one_wave = tiles <= (uint32_t)num_sms;
     if constexpr (L == 2) {
         if (p.fold == 1 || p.fold == 2) {
-            if (p.fold == 1) k_gemm<L, 1><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p);
-            else k_gemm<L, 2><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p);
-            return (int)cudaGetLastError();
+            if (p.fold == 1) return launch_pdl(one_wave, k_gemm<L, 1>, grid, Cfg::THREADS, Cfg::SMEM, s, p);
+            return launch_pdl(one_wave, k_gemm<L, 2>, grid, Cfg::THREADS, Cfg::SMEM, s, p);
         }
     }
-    k_gemm<L><<<grid, Cfg::THREADS, Cfg::SMEM, s>>>(p);
-    return (int)cudaGetLastError();
+    return launch_pdl(one_wave, k_gemm<L>, grid, Cfg::THREADS, Cfg::SMEM, s, p);
 }
 
 template <int L>
