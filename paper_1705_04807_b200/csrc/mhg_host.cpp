@@ -289,6 +289,10 @@ mhg::GemmParams gemm_params(const Buffers& b, const mhg_view& out, const Checked
     // (profiles/r01_raster_groups.txt; G = 4 / 6 / 12 within noise or slower), 4 from 256
     // column tiles on (n = 32768: 95.4 vs 97.0 ms, G = 12 108 ms; profiles/r02_raster_groups.txt)
     p.group = g.Nt >= 256 ? 4 : 8;
+    // short K: both packed operands fit in L2 with room to spare, so the rhs stages are kept
+    // too (the C stream is evict-first) instead of streamed (long K: 4 MB rhs panels, each
+    // needed by one raster group only)
+    p.keep_b = g.apack_bytes + g.bpack_bytes <= (uint64_t(80) << 20) ? 1 : 0;
     // suspend (instead of re-polling) in mbarrier waits: -1% at n = 16384 / 8192 under the
     // power cap (profiles/r01_wait_hint.txt); the thread wakes when the phase completes
     p.wait_hint = 100000;

@@ -74,6 +74,7 @@ struct GemmParams {
     int udig;                    // unsigned (u8) digits: non-negative class sums (DigitParams::udig)
     int vec_ok;                  // t % 4 == 0: 16-byte epilogue accesses allowed
     uint32_t group;              // raster: row tiles per group sharing rhs panels in L2
+    int keep_b;                  // rhs stages evict_last too (both packed operands fit in L2)
     uint32_t wait_hint;          // mbarrier try_wait suspend-time hint, ns (k_gemm roles)
     unsigned long long* stats;   // optional per-CTA wait-cycle counters (diagnostics), or null
 };

@@ -1624,7 +1624,8 @@ __global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParam
             uint32_t ord = 0;
             // lhs panels of the raster group are re-read by the next waves (evict_last),
             // rhs panels only by the current one (evict_first): -1.3% at n = 16384
-            const uint64_t pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
+            const uint64_t pol_keep = l2_policy_evict_last();
+            const uint64_t pol_stream = p.keep_b ? pol_keep : l2_policy_evict_first();
             for (uint32_t tile = first_tile; tile < num_tiles; tile += tile_stride, ++ord) {
                 uint32_t m, n;
                 tile_coords(tile, p.Mt, p.Nt, p.group, m, n);
