@@ -293,6 +293,7 @@ mhg::GemmParams gemm_params(const Buffers& b, const mhg_view& out, const Checked
     // too (the C stream is evict-first) instead of streamed (long K: 4 MB rhs panels, each
     // needed by one raster group only)
     p.keep_b = g.apack_bytes + g.bpack_bytes <= (uint64_t(80) << 20) ? 1 : 0;
+    p.narrow = g.narrow ? 1 : 0;
     // suspend (instead of re-polling) in mbarrier waits: -1% at n = 16384 / 8192 under the
     // power cap (profiles/r01_wait_hint.txt); the thread wakes when the phase completes
     p.wait_hint = 100000;

@@ -75,6 +75,7 @@ struct GemmParams {
     int vec_ok;                  // t % 4 == 0: 16-byte epilogue accesses allowed
     uint32_t group;              // raster: row tiles per group sharing rhs panels in L2
     int keep_b;                  // rhs stages evict_last too (both packed operands fit in L2)
+    int narrow;                  // 128 x 64 tiles (GemmGeometry::narrow)
     uint32_t wait_hint;          // mbarrier try_wait suspend-time hint, ns (k_gemm roles)
     unsigned long long* stats;   // optional per-CTA wait-cycle counters (diagnostics), or null
 };

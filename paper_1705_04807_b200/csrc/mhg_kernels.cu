@@ -791,9 +791,13 @@ __device__ __forceinline__ uint32_t fold_part(const int32_t (&acc)[C1 - C0][CW],
 #ifndef MHG_COLD_MID
 #define MHG_COLD_MID 1  // pass 0's C_old requested between the two drain groups (A/B)
 #endif
-template <int L>
+// NARROW: 128 x 64 tiles for 1-2 limb primes (GemmGeometry::narrow), chosen for problems of
+// at most half a wave of 128 x 128 tiles: twice the CTAs, each with half the MMA and epilogue
+// work of the latency chain that bounds such problems (cfg1: 16 -> 32 CTAs).
+template <int L, bool NARROW = false>
 struct GemmCfg {
-    static constexpr int W = (L <= 2) ? 128 : 64;       // output columns per tile
+    static_assert(!NARROW || L <= 2, "narrow tiles are the 1-2 limb case");
+    static constexpr int W = (L <= 2 && !NARROW) ? 128 : 64;  // output columns per tile
     static constexpr int NB = L * W;                    // UMMA N of the stacked B'
     static constexpr int CLASSES = 2 * L - 1;           // weight classes 256^c
     static constexpr int A_STAGE = L * kBM * kBK;       // bytes
@@ -802,7 +806,7 @@ struct GemmCfg {
     // two epilogue warps per SMSP, 64 columns each; W = 128 uses the coalesced
     // C path with a 4 KB per-warp transpose buffer, the narrow-tile primes keep
     // row-per-thread C access (see epilogue_role)
-    static constexpr bool XPOSE = (W == 128);
+    static constexpr bool XPOSE = (W == 128) || NARROW;
     static constexpr int EPI_WARPS = 8;
     // MHG_SMR: warpgroup 0 = producer, MMA issuer and two idle warps, which give registers
     // back (setmaxnreg.dec) so the two epilogue warpgroups run at SMR_EPI_REGS instead of the
@@ -1564,9 +1568,9 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
     }
 }
 
-template <int L, int FOLD = 3>
-__global__ void __launch_bounds__(GemmCfg<L>::THREADS, 1) k_gemm(const GemmParams p) {
-    using Cfg = GemmCfg<L>;
+template <int L, int FOLD = 3, bool NARROW = false>
+__global__ void __launch_bounds__(GemmCfg<L, NARROW>::THREADS, 1) k_gemm(const GemmParams p) {
+    using Cfg = GemmCfg<L, NARROW>;
     constexpr int W = Cfg::W;
     constexpr int STAGES = Cfg::STAGES;
     extern __shared__ uint8_t smem_raw[];
@@ -1983,13 +1987,20 @@ template <int L>
 int configure_gemm_t() {
     int e = (int)cudaFuncSetAttribute(k_gemm<L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       GemmCfg<L>::SMEM);
+    if constexpr (L <= 2) {
+        using N = GemmCfg<L, true>;
+        if (!e) e = (int)cudaFuncSetAttribute(k_gemm<L, 3, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, N::SMEM);
+    }
     if constexpr (L == 2) {
+        using N = GemmCfg<L, true>;
         if (!e)
             e = (int)cudaFuncSetAttribute(k_gemm<L, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           GemmCfg<L>::SMEM);
         if (!e)
             e = (int)cudaFuncSetAttribute(k_gemm<L, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           GemmCfg<L>::SMEM);
+        if (!e) e = (int)cudaFuncSetAttribute(k_gemm<L, 2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, N::SMEM);
+        if (!e) e = (int)cudaFuncSetAttribute(k_gemm<L, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, N::SMEM);
     }
     return e;
 }
@@ -2003,19 +2014,27 @@ __global__ void k_fill_view(uint32_t* __restrict__ out, const uint64_t* __restri
         out[rowoff[x / cols] + coloff[x % cols]] = value;
 }
 
-template <int L>
-int launch_gemm_t(const GemmParams& p, int num_sms, cudaStream_t s) {
-    using Cfg = GemmCfg<L>;
+template <int L, bool NARROW>
+int launch_gemm_cfg(const GemmParams& p, int num_sms, cudaStream_t s) {
+    using Cfg = GemmCfg<L, NARROW>;
     const uint32_t tiles = p.Mt * p.Nt;
     const int grid = (int)(tiles < (uint32_t)num_sms ? tiles : (uint32_t)num_sms);
     const bool one_wave = tiles <= (uint32_t)num_sms;
     if constexpr (L == 2) {
         if (p.fold == 1 || p.fold == 2) {
-            if (p.fold == 1) return launch_pdl(one_wave, k_gemm<L, 1>, grid, Cfg::THREADS, Cfg::SMEM, s, p);
-            return launch_pdl(one_wave, k_gemm<L, 2>, grid, Cfg::THREADS, Cfg::SMEM, s, p);
+            if (p.fold == 1) return launch_pdl(one_wave, k_gemm<L, 1, NARROW>, grid, Cfg::THREADS, Cfg::SMEM, s, p);
+            return launch_pdl(one_wave, k_gemm<L, 2, NARROW>, grid, Cfg::THREADS, Cfg::SMEM, s, p);
         }
     }
-    return launch_pdl(one_wave, k_gemm<L>, grid, Cfg::THREADS, Cfg::SMEM, s, p);
+    return launch_pdl(one_wave, k_gemm<L, 3, NARROW>, grid, Cfg::THREADS, Cfg::SMEM, s, p);
+}
+
+template <int L>
+int launch_gemm_t(const GemmParams& p, int num_sms, cudaStream_t s) {
+    if constexpr (L <= 2) {
+        if (p.narrow) return launch_gemm_cfg<L, true>(p, num_sms, s);
+    }
+    return launch_gemm_cfg<L, false>(p, num_sms, s);
 }
 
 template <int L>

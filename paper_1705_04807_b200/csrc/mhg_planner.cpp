@@ -350,6 +350,12 @@ GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t c
     const int64_t kernel = option(kOptGemmKernel);
     g.pair = kernel == 0 ? lp.L >= 3 : kernel == 2;
     if (g.pair) g.Mt += g.Mt & 1u;  // pairs take two row tiles
+    // Problems of at most half a wave of 128 x 128 tiles (e.g. cfg1, n = 512: 16 tiles) are a
+    // single latency chain per CTA (load, MMA, drain, store): 128 x 64 tiles put twice as many
+    // SMs on it, each with half the chain (profiles/r02b/README.md).
+    g.narrow = !g.pair && lp.L <= 2 && option(kOptGemmKernel) != 1 &&
+               (uint64_t)g.Mt * ((cols + 127) / 128) <= 74;
+    if (g.narrow) g.W = 64;
     g.Nt = (uint32_t)((cols + g.W - 1) / g.W);
     g.Kt = (uint32_t)((inner + kBK - 1) / kBK);
     g.KC = (uint32_t)std::max<uint64_t>(1, lp.k_max / kBK);

@@ -64,6 +64,7 @@ Counters default_counters(const Kernel3& g);
 // -------------------------------------------------------------- task grid
 struct GemmGeometry {
     bool pair;            // CTA-pair kernel (k_gemm2); Mt is then even
+    bool narrow;          // 128 x 64 tiles for a problem of <= 74 128 x 128 tiles (1-2 limbs)
     bool udig;            // unsigned u8 digits (MHG_OPT_DIGITS = 1, the default)
     uint32_t L, W;        // limbs, output tile width
     uint32_t Mt, Nt, Kt;  // tiles along rows / cols / inner (128-byte K slices)
