@@ -789,7 +789,7 @@ __device__ __forceinline__ uint32_t fold_part(const int32_t (&acc)[C1 - C0][CW],
 #define MHG_XADDR_VOLATILE 1  // transpose-buffer addresses recomputed per use (fewer spills)
 #endif
 #ifndef MHG_COLD_MID
-#define MHG_COLD_MID 1  // pass 0's C_old requested between the two drain groups (A/B)
+#define MHG_COLD_MID 2  // C_old requested between the two drain groups: 1 = pass 0, 2 = both passes
 #endif
 // NARROW: 128 x 64 tiles for 1-2 limb primes (GemmGeometry::narrow), chosen for problems of
 // at most half a wave of 128 x 128 tiles: twice the CTAs, each with half the MMA and epilogue
@@ -1357,10 +1357,10 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
                 }
             }
         };
-        bool cold0_issued = false;
+        bool cold0_issued = false, cold1_issued = false;
         auto issue_cold = [&]() {
             if (!cold0_issued) issue_cold0();
-            issue_cold1();
+            if (!cold1_issued) issue_cold1();
         };
         if constexpr (XPOSE) {
             // the classes are folded from zero; C_old is loaded only after the tile's
@@ -1450,17 +1450,27 @@ __device__ __forceinline__ void epilogue_role(const GemmParams& p, uint32_t firs
                 if constexpr (L == 2) {
                     // lean split for q = 2^16 - small (e.g. 65521): the first group
                     // leaves cur unreduced (< 2^32 - 2^24); the second group finishes
+                    long long t_rel = 0;
                     drain_l2_small(tb, n, cur, acc_ph, [&]() {
+                        t_rel = diag_clock();
 #if MHG_COLD_MID
                         if constexpr (XPOSE) {
                             if (c + 1 == nchunks) {
                                 issue_cold0();
                                 cold0_issued = true;
+                                if constexpr (MHG_COLD_MID >= 2) {
+                                    issue_cold1();  // pass 1 too: its registers ride through the second drain
+                                    cold1_issued = true;
+                                }
                             }
                         }
 #endif
                     });
-                    epi_busy += diag_clock() - w1;
+                    // diagnostics: busy = the first drain group up to the TMEM release (what the
+                    // next job's MMAs wait for); the second group + C_old issue go to epi_ldw
+                    const long long t_end = diag_clock();
+                    epi_busy += t_rel - w1;
+                    epi_ldw += t_end - t_rel;
                     acc_ph ^= 1;
                     continue;
                 }
