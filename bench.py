@@ -393,6 +393,7 @@ def run_gpu(args, rank, world, local_rank):
     L = limbs_of(q)
     lay, mod = mh.Layout(n, t), mh.Modulus(q)
     stream = torch.cuda.current_stream()
+    shared_gpu = os.environ.get("MHG_BENCH_SHARED_GPU") == "1"
 
     # containers: full-size on every rank; each rank keeps its own 1/P Morton slice of
     # the reference's seed-0 stream (mh::Rng(0), gen_problem's fill order)
@@ -564,6 +565,29 @@ def run_gpu(args, rank, world, local_rank):
                              stream=stream)
         del old, old_f
         torch.cuda.empty_cache()
+    else:
+        # N > 1: every rank checks its own C block.  Freivalds needs the whole A row panel and
+        # B column panel as residues, so the 1/P slices are gathered into the (otherwise zero)
+        # full containers first; the step itself still exchanges the packed planes as timed.
+        torch.cuda.empty_cache()
+        room = torch.tensor([float(torch.cuda.mem_get_info()[0] > 4 * n * n * (world if shared_gpu else 1)
+                                   + (2 << 30))], dtype=torch.float64, device=dev)
+        dist.all_reduce(room, op=dist.ReduceOp.MIN)  # one decision for every rank
+        if room[0] > 0.5:
+            for f in (lhs_f, rhs_f):
+                for r in range(world):
+                    rb, re_ = slice_range(r, world, n)
+                    dist.broadcast(f[rb:re_], src=r)
+            old_f = out_f.clone()
+            old = mh.Matrix.wrap(lay, mod, old_f.data_ptr(), owner=old_f)
+            step()
+            ok = mh.verify(prob, mh.Sub(old, prob.a.origin, prob.a.rows, prob.a.cols), op, rounds=2,
+                           stream=stream)
+            v = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64, device=dev)
+            dist.all_reduce(v, op=dist.ReduceOp.MIN)
+            verified = bool(v[0] > 0.5)
+            del old, old_f
+            torch.cuda.empty_cache()
     if peer is not None:
         torch.cuda.synchronize()
         barrier()

@@ -327,16 +327,23 @@ class PeerPanels:
         self.pack_done = [ev() for _ in self.segs]
         self.copy_done = ev()
         exports = {}
-        for j, (sg, pl) in enumerate(zip(self.segs, plans)):
-            for which, owner in ((0, sg.a_owner), (1, sg.b_owner)):
-                ptr, nb = pl.pack_region(which)
-                if owner == rank and nb:
-                    h, off = mh.ipc_export(ptr)
-                    exports[(j, which)] = (h, off, nb)
-        mine = {"exports": exports, "pack_done": [e.ipc_handle() for e in self.pack_done],
-                "copy_done": self.copy_done.ipc_handle()}
+        mine = {"error": None}
+        try:  # an export that fails here is reported collectively below, like a failed mapping
+            for j, (sg, pl) in enumerate(zip(self.segs, plans)):
+                for which, owner in ((0, sg.a_owner), (1, sg.b_owner)):
+                    ptr, nb = pl.pack_region(which)
+                    if owner == rank and nb:
+                        h, off = mh.ipc_export(ptr)
+                        exports[(j, which)] = (h, off, nb)
+            mine.update({"exports": exports, "pack_done": [e.ipc_handle() for e in self.pack_done],
+                         "copy_done": self.copy_done.ipc_handle()})
+        except Exception as exc:  # noqa: BLE001
+            mine["error"] = f"rank {rank}: export failed: {exc}"
         infos = [None] * P
         dist.all_gather_object(infos, mine, group=host_group)
+        failed = [i["error"] for i in infos if i["error"]]
+        if failed:
+            raise PeerSetupError("; ".join(failed))
         # pulls[j] = [(owner, dst, src, bytes)]; one mapping per owner allocation
         self.pulls = [[] for _ in self.segs]
         owners = set()
