@@ -10,6 +10,7 @@
 //                                   mm_naive, mm_default, compatible_parts
 //   protocol      mh/bench.hpp      Config, Rng, gen_problem, run_trials, CSV writers
 //   fixtures      mh/io.hpp         load_matrix / save_matrix text format
+//   TU driver     mh/tu.hpp         schur_views, schur_update, SchurSweep (aliased Schur updates)
 //
 // Link with -lmhg (paper_1705_04807_b200/libmhg.so).
 #pragma once
@@ -23,3 +24,4 @@
 #include "mh/matrix.hpp"
 #include "mh/multiply.hpp"
 #include "mh/submatrix.hpp"
+#include "mh/tu.hpp"

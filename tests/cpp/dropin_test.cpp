@@ -593,6 +593,66 @@ void test_acceptance_partition() {  // acceptance_main.cpp:103-162 (criterion 2)
     CHECK(ok);
 }
 
+// TU/TURBO Schur-update driver (include/mh/tu.hpp): a right-looking
+// sweep on ONE parent with a misaligned panel width equals the dense elimination loop,
+// through the one-shot aliased update and through the planned sweep (run twice: the
+// second run continues from the first one's cells).
+void test_tu_schur_sweep() {
+    std::mt19937_64 eng(77);
+    const std::uint64_t n = 256, t = 32, block = 40;
+    const std::uint32_t q = 65521;
+    const mh::Modulus mod(q);
+    mh::Grid g = random_grid(n, q, eng);
+    auto dense_sweep = [&](mh::Grid& d) {
+        for (std::uint64_t k0 = 0; k0 + block < n; k0 += block) {
+            const std::uint64_t k1 = k0 + block, rest = n - k1;
+            const mh::Grid snap = d;  // operands are disjoint from the output: same as in place
+            dense_acc(d, snap, snap, k1, k1, k1, k0, k0, k1, rest, rest, block, q, true);
+        }
+    };
+    mh::Grid want = g;
+    dense_sweep(want);
+    // one-shot aliased updates
+    mh::Matrix A = mh::from_row_major(g, t, mod);
+    std::uint64_t macs = 0;
+    const auto steps = mh::tu::schur_views(A, block);
+    CHECK(steps.size() == 6);
+    for (const mh::Problem& p : steps) {
+        const mh::Counters c = mh::tu::schur_update(p);
+        CHECK(c.scalar_macs == p.a.rows * p.a.cols * p.b.cols);
+        CHECK(c.encode_calls == 0);
+        macs += c.scalar_macs;
+    }
+    CHECK(mh::to_row_major(A) == want);
+    // the reference's entry point still refuses the shared parent
+    CHECK(throws_as<std::logic_error>([&] { mh::mm_oblivious(steps[0]); }));
+    // planned sweep, replayed
+    mh::Matrix B = mh::from_row_major(g, t, mod);
+    mh::tu::SchurSweep sweep(B, block);
+    CHECK(sweep.steps() == 6 && sweep.macs() == macs);
+    CHECK(sweep.run() == macs);
+    CHECK(mh::to_row_major(B) == want);
+    mh::Grid want2 = want;
+    dense_sweep(want2);
+    B.set(0, 0, B.at(0, 0));  // a host-side touch between runs is uploaded, not lost
+    sweep.run();
+    CHECK(mh::to_row_major(B) == want2);
+    // add form and argument checks
+    mh::Matrix C = mh::from_row_major(g, t, mod);
+    mh::Grid want3 = g;
+    dense_acc(want3, g, g, 64, 64, 64, 0, 0, 64, 192, 192, 64, q, false);
+    mh::tu::schur_update(mh::Problem{mh::Sub{&C, mh::encode(C.layout(), 64, 64), 192, 192},
+                                     mh::Sub{&C, mh::encode(C.layout(), 64, 0), 192, 64},
+                                     mh::Sub{&C, mh::encode(C.layout(), 0, 64), 64, 192}},
+                         mh::Op::Add);
+    CHECK(mh::to_row_major(C) == want3);
+    CHECK(throws_as<std::invalid_argument>([&] { mh::tu::schur_views(C, 0); }));
+    CHECK(mh::tu::schur_views(C, n).empty());
+    CHECK(throws_as<std::logic_error>([&] {
+        mh::tu::schur_update(mh::Problem{mh::Sub{&C, 0, 8, 8}, mh::Sub{&C, 0, 8, 4}, mh::Sub{&C, 0, 5, 8}});
+    }));
+}
+
 }  // namespace
 
 int main() {
@@ -614,6 +674,7 @@ int main() {
         {"split_edge_cases", test_split_edge_cases},
         {"acceptance_codec", test_acceptance_codec},
         {"acceptance_partition", test_acceptance_partition},
+        {"tu_schur_sweep", test_tu_schur_sweep},
     };
     for (const auto& [name, fn] : tests) {
         const int before = g_fail;
