@@ -923,6 +923,9 @@ constexpr int kConvUnitBytes = 16384;
 // 4 units in flight per CTA x 3 CTAs per SM (more independent issuers measured faster
 // than fewer, deeper CTAs: profiles/r01_conversion_tma.txt)
 constexpr int kConvUnits = 4, kConvCtasPerSm = 3;
+#ifndef MHG_CONV_DEFER
+#define MHG_CONV_DEFER 1  // refill a buffer one unit after its store was issued
+#endif
 
 __device__ __forceinline__ void tma2d_load(uint32_t dst, const CUtensorMap* tm, int c0, int c1,
                                            uint64_t* bar) {
@@ -949,6 +952,9 @@ __device__ __forceinline__ void bulk_s2g(void* dst, uint32_t src, uint32_t bytes
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() {
     asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read1() {
+    asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
 }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
@@ -1014,10 +1020,24 @@ __global__ void __launch_bounds__(128) k_conv_tma(const __grid_constant__ CUtens
             if (to_mh) bulk_s2g(mh + zoff, src, ubytes);
             else tma2d_store(&tm, c0, c1, src);
             bulk_commit();
+#if MHG_CONV_DEFER
+            // refill the PREVIOUS unit's buffer: its store (every group but the one just
+            // committed) has read shared memory by now, so the issuer does not sit out this
+            // store's read before it can serve the next landed unit
+            if (k > 0) {
+                bulk_wait_read1();
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                // unit k - 1 + kConvBufs of this CTA (unit j >= kConvBufs is requested in
+                // iteration j - kConvBufs + 1, which always runs when unit j exists)
+                const uint64_t nu = u + (uint64_t)(kConvBufs - 1) * step;
+                if (nu < units) issue_load(nu, (int)((k - 1) % kConvBufs));
+            }
+#else
             bulk_wait_read0();  // the store has read buffer b
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             const uint64_t nu = u + (uint64_t)kConvBufs * step;
             if (nu < units) issue_load(nu, b);
+#endif
         }
     }
     if (issuer) bulk_wait0();
