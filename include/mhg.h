@@ -237,6 +237,44 @@ mhg_status mhg_plan_info(mhg_plan plan, uint64_t *launches, uint64_t *tiles, uin
 mhg_status mhg_plan_variant(mhg_plan plan, int *unsigned_digits, int *cta_group);
 mhg_status mhg_plan_destroy(mhg_plan plan);
 
+/* ---- multi-GPU partition (one process per GPU) ----
+ * C-stationary partition by top-level Morton blocks of the output: with P = 2^b ranks,
+ * rank r owns the r-th contiguous 1/P slice of every container's flat store (a rectangle:
+ * P = 2 halves, P = 4 quadrants, P = 8 n/4 x n/2 blocks) and updates only its own block
+ * C[R_r, C_r] -- disjoint output rectangles are independent (multiply.hpp:25-29), so no
+ * reduction is needed.  K is cut into mhg_dist_segment_count(P) segments; segment s needs
+ * A[R_r, k0:k1] -- a contiguous flat range of ONE rank's slice (a_owner) -- and
+ * B[k0:k1, C_r] -- the whole slice of ONE rank (b_owner).  The geometry calls are pure host
+ * code (usable without a GPU); the communication belongs to the host program (NCCL / MPI /
+ * peer copies): per segment the owner packs its part (mhg_plan_pack on the plan from
+ * mhg_dist_plan_create), the packed bytes (mhg_plan_pack_buffer) are broadcast inside the
+ * row group (A part) / column group (B part), and every rank runs mhg_plan_gemm.
+ * paper_1705_04807_b200/dist.py is such a host program (one Python process per GPU). */
+typedef struct {
+    uint32_t rank;
+    uint64_t i0, j0, rows, cols; /* the rank's block of every container */
+    uint32_t row_band, col_band; /* ranks sharing row_band form its row group, likewise columns */
+} mhg_dist_block_t;
+typedef struct {
+    uint32_t index;
+    uint64_t k0, k1;           /* inner range of the segment */
+    uint32_t a_owner;          /* rank holding A[R_r, k0:k1] */
+    uint64_t a_begin, a_end;   /* its flat cell range (inside a_owner's slice) */
+    uint32_t b_owner;          /* rank holding B[k0:k1, C_r] */
+    uint64_t b_begin, b_end;   /* its flat cell range (b_owner's whole slice) */
+} mhg_dist_segment_t;
+mhg_status mhg_dist_block(uint32_t nranks, uint32_t rank, uint64_t n, uint64_t t, mhg_dist_block_t *block);
+/* Flat [begin, end) of the rank's slice of an n x n store. */
+mhg_status mhg_dist_slice(uint32_t nranks, uint32_t rank, uint64_t n, uint64_t *begin, uint64_t *end);
+mhg_status mhg_dist_segment_count(uint32_t nranks, uint32_t *count);
+mhg_status mhg_dist_segment(uint32_t nranks, uint32_t rank, uint64_t n, uint64_t t, uint32_t index,
+                            mhg_dist_segment_t *segment);
+/* The rank's plan of one K segment: C[R_r, C_r] op= A[R_r, k0:k1] * B[k0:k1, C_r] on three
+ * full-size same-layout containers (out, lhs, rhs).  A SET update overwrites with segment 0
+ * only; later segments accumulate (the plan of segment index > 0 is created with ADD). */
+mhg_status mhg_dist_plan_create(mhg_matrix out, mhg_matrix lhs, mhg_matrix rhs, mhg_op op,
+                                uint32_t nranks, uint32_t rank, uint32_t index, mhg_plan *plan);
+
 /* ---- verification and seeded inputs ---- */
 /* Freivalds check of a finished multiply on the device: out_new == out_old op lhs*rhs
  * (views of matching shapes; out_old holds the output's cells from before the call,

@@ -37,6 +37,7 @@ __all__ = [
     "mm_oblivious", "mm_naive", "mm_default", "mm", "counters_oblivious", "counters_layout",
     "counters_geometry", "limb_params", "lib", "LIB_PATH", "KERNEL_NAIVE", "KERNEL_DEFAULT",
     "verify", "Rng",
+    "DistBlock", "DistSegment", "dist_block", "dist_slice", "dist_segments",
     "OP_ADD", "OP_SUB", "OP_SET", "set_option", "get_option", "options",
     "OPT_DIGITS", "OPT_GEMM_KERNEL", "OPT_MIN_FOLD_LEVEL", "OPT_MAX_KCHUNK", "OPT_UPLOAD_WIRE",
     "OPT_CONV_KERNEL", "OPT_GEMM_STATS", "OPT_UPLOAD_THREADS", "OPT_UPLOAD_ADAPTIVE",
@@ -83,6 +84,21 @@ class IpcHandle(C.Structure):
     """mhg_ipc_handle (include/mhg.h): a cudaIpcMemHandle_t as 64 opaque bytes."""
 
     _fields_ = [("bytes", C.c_ubyte * 64)]
+
+
+class DistBlock(C.Structure):
+    """mhg_dist_block_t: a rank's block of every container (include/mhg.h)."""
+
+    _fields_ = [("rank", C.c_uint32), ("i0", C.c_uint64), ("j0", C.c_uint64), ("rows", C.c_uint64),
+                ("cols", C.c_uint64), ("row_band", C.c_uint32), ("col_band", C.c_uint32)]
+
+
+class DistSegment(C.Structure):
+    """mhg_dist_segment_t: one K segment of a rank's update and the owners of its parts."""
+
+    _fields_ = [("index", C.c_uint32), ("k0", C.c_uint64), ("k1", C.c_uint64),
+                ("a_owner", C.c_uint32), ("a_begin", C.c_uint64), ("a_end", C.c_uint64),
+                ("b_owner", C.c_uint32), ("b_begin", C.c_uint64), ("b_end", C.c_uint64)]
 
 
 class Counters(C.Structure):
@@ -149,6 +165,11 @@ def lib():
         "mhg_ipc_open": ([P(IpcHandle), P(vp)], C.c_int),
         "mhg_ipc_close": ([vp], C.c_int),
         "mhg_copy_async": ([vp, vp, u64, vp], C.c_int),
+        "mhg_dist_block": ([u32, u32, u64, u64, P(DistBlock)], C.c_int),
+        "mhg_dist_slice": ([u32, u32, u64, P(u64), P(u64)], C.c_int),
+        "mhg_dist_segment_count": ([u32, P(u32)], C.c_int),
+        "mhg_dist_segment": ([u32, u32, u64, u64, u32, P(DistSegment)], C.c_int),
+        "mhg_dist_plan_create": ([vp, vp, vp, C.c_int, u32, u32, u32, P(vp)], C.c_int),
         "mhg_plan_counters": ([vp, P(Counters)], C.c_int),
         "mhg_verify": ([_View, _View, _View, _View, C.c_int, u32, u64, P(C.c_int), vp], C.c_int),
         "mhg_rng_create": ([u64, P(vp)], C.c_int),
@@ -500,6 +521,32 @@ def counters_geometry(kernel: int, geo_out, geo_lhs, geo_rhs, rows, inner, cols)
     return ctr
 
 
+def dist_block(nranks: int, rank: int, n: int, t: int) -> DistBlock:
+    """mhg_dist_block: the rank's block of the C-stationary Morton partition (host only)."""
+    b = DistBlock()
+    _check(lib().mhg_dist_block(nranks, rank, n, t, C.byref(b)))
+    return b
+
+
+def dist_slice(nranks: int, rank: int, n: int):
+    """mhg_dist_slice: flat [begin, end) of the rank's slice of an n x n store."""
+    b, e = C.c_uint64(), C.c_uint64()
+    _check(lib().mhg_dist_slice(nranks, rank, n, C.byref(b), C.byref(e)))
+    return b.value, e.value
+
+
+def dist_segments(nranks: int, rank: int, n: int, t: int):
+    """mhg_dist_segment for every K segment of the rank's update (host only)."""
+    cnt = C.c_uint32()
+    _check(lib().mhg_dist_segment_count(nranks, C.byref(cnt)))
+    out = []
+    for i in range(cnt.value):
+        g = DistSegment()
+        _check(lib().mhg_dist_segment(nranks, rank, n, t, i, C.byref(g)))
+        out.append(g)
+    return out
+
+
 def verify(problem: Problem, old: Sub, op: int = OP_ADD, rounds: int = 2, seed: int = 0x5EED,
            stream=None) -> bool:
     """Freivalds check on the device that problem.a now holds old op b*c (mhg_verify);
@@ -557,6 +604,18 @@ class Plan:
         self._problem = problem  # keep containers alive
         _check(lib().mhg_plan_create_ex(problem.a._c(), problem.b._c(), problem.c._c(), op,
                                         ALLOW_ALIAS if allow_alias else 0, C.byref(self._h)))
+
+    @classmethod
+    def for_segment(cls, out: "Matrix", lhs: "Matrix", rhs: "Matrix", op: int, nranks: int,
+                    rank: int, index: int) -> "Plan":
+        """mhg_dist_plan_create: rank `rank`'s plan of K segment `index` of the multi-GPU
+        partition over `nranks` ranks (C[R_r, C_r] op= A[R_r, k0:k1] B[k0:k1, C_r])."""
+        self = cls.__new__(cls)
+        self._h = C.c_void_p()
+        self._problem = (out, lhs, rhs)  # keep containers alive
+        _check(lib().mhg_dist_plan_create(out.handle, lhs.handle, rhs.handle, op, nranks, rank,
+                                          index, C.byref(self._h)))
+        return self
 
     def run(self, stream=None):
         _check(lib().mhg_plan_run(self._h, _stream_ptr(stream)))

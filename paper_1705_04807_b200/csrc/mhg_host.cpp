@@ -1401,4 +1401,75 @@ mhg_status mhg_plan_destroy(mhg_plan p) {
     });
 }
 
+// ------------------------------------------------------- multi-GPU partition
+namespace {
+void dist_fail(int e, const char* what) {
+    if (e == 1) fail(MHG_ERR_INVALID_ARGUMENT, std::string(what) + ": rank count must be a power of two");
+    if (e == 2) fail(MHG_ERR_OUT_OF_RANGE, std::string(what) + ": rank or segment index out of range");
+    if (e == 3) fail(MHG_ERR_INVALID_ARGUMENT, std::string(what) + ": fewer tiles than ranks");
+}
+}  // namespace
+
+mhg_status mhg_dist_block(uint32_t P, uint32_t rank, uint64_t n, uint64_t t, mhg_dist_block_t* block) {
+    mhg_status s = mhg_layout_check(n, t);
+    if (s) return s;
+    return guarded([&] {
+        if (!block) fail(MHG_ERR_INVALID_ARGUMENT, "dist_block: null output");
+        mhg::DistBlock b{};
+        dist_fail(mhg::dist_block(P, rank, n, t, b), "dist_block");
+        *block = mhg_dist_block_t{b.rank, b.i0, b.j0, b.rows, b.cols, b.row_band, b.col_band};
+    });
+}
+
+mhg_status mhg_dist_slice(uint32_t P, uint32_t rank, uint64_t n, uint64_t* begin, uint64_t* end) {
+    return guarded([&] {
+        if (!begin || !end) fail(MHG_ERR_INVALID_ARGUMENT, "dist_slice: null output");
+        if (P == 0 || (P & (P - 1))) dist_fail(1, "dist_slice");
+        if (rank >= P) dist_fail(2, "dist_slice");
+        const uint64_t per = n * n / P;
+        *begin = rank * per;
+        *end = (rank + 1) * per;
+    });
+}
+
+mhg_status mhg_dist_segment_count(uint32_t P, uint32_t* count) {
+    return guarded([&] {
+        if (!count) fail(MHG_ERR_INVALID_ARGUMENT, "dist_segment_count: null output");
+        const uint32_t c = mhg::dist_segment_count(P);
+        if (!c) dist_fail(1, "dist_segment_count");
+        *count = c;
+    });
+}
+
+mhg_status mhg_dist_segment(uint32_t P, uint32_t rank, uint64_t n, uint64_t t, uint32_t index,
+                            mhg_dist_segment_t* segment) {
+    mhg_status s = mhg_layout_check(n, t);
+    if (s) return s;
+    return guarded([&] {
+        if (!segment) fail(MHG_ERR_INVALID_ARGUMENT, "dist_segment: null output");
+        mhg::DistSegment g{};
+        dist_fail(mhg::dist_segment(P, rank, n, t, index, g), "dist_segment");
+        *segment = mhg_dist_segment_t{g.index, g.k0, g.k1, g.a_owner, g.a_begin, g.a_end,
+                                      g.b_owner, g.b_begin, g.b_end};
+    });
+}
+
+mhg_status mhg_dist_plan_create(mhg_matrix out, mhg_matrix lhs, mhg_matrix rhs, mhg_op op, uint32_t P,
+                                uint32_t rank, uint32_t index, mhg_plan* plan) {
+    mhg::DistBlock b{};
+    mhg::DistSegment g{};
+    mhg_status s = guarded([&] {
+        if (!out || !lhs || !rhs) fail(MHG_ERR_INVALID_ARGUMENT, "dist_plan_create: null container");
+        if (!plan) fail(MHG_ERR_INVALID_ARGUMENT, "dist_plan_create: null out");
+        dist_fail(mhg::dist_block(P, rank, out->n, out->t, b), "dist_plan_create");
+        dist_fail(mhg::dist_segment(P, rank, out->n, out->t, index, g), "dist_plan_create");
+    });
+    if (s) return s;
+    const uint64_t t = out->t;
+    const mhg_view vo{out, mhg::encode(t, b.i0, b.j0), b.rows, b.cols};
+    const mhg_view vl{lhs, mhg::encode(t, b.i0, g.k0), b.rows, g.k1 - g.k0};
+    const mhg_view vr{rhs, mhg::encode(t, g.k0, b.j0), g.k1 - g.k0, b.cols};
+    return mhg_plan_create(vo, vl, vr, (op == MHG_OP_SET && index > 0) ? MHG_OP_ADD : op, plan);
+}
+
 }  // extern "C"

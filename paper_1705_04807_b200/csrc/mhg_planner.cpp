@@ -381,4 +381,66 @@ GemmGeometry gemm_geometry(uint32_t q, uint64_t rows, uint64_t inner, uint64_t c
     return g;
 }
 
+// ------------------------------------------------- multi-GPU partition geometry
+namespace {
+int rank_bits(uint32_t P) {
+    if (P == 0 || (P & (P - 1))) return -1;
+    int b = 0;
+    while ((1u << b) < P) ++b;
+    return b;
+}
+}  // namespace
+
+int dist_block(uint32_t P, uint32_t rank, uint64_t n, uint64_t t, DistBlock& out) {
+    const int b = rank_bits(P);
+    if (b < 0) return 1;
+    if (rank >= P) return 2;
+    const uint64_t tiles = n / t;
+    if (tiles * tiles < P) return 3;
+    const int row_bits = (b + 1) / 2, col_bits = b / 2;
+    uint32_t rb = 0, cb = 0;
+    for (int k = 0; k < b; ++k) {  // from the most significant bit of rank
+        const uint32_t bit = (rank >> (b - 1 - k)) & 1u;
+        if (k % 2 == 0) rb = (rb << 1) | bit;
+        else cb = (cb << 1) | bit;
+    }
+    const uint64_t rows = n >> row_bits, cols = n >> col_bits;
+    out = DistBlock{rank, rb * rows, cb * cols, rows, cols, rb, cb};
+    return 0;
+}
+
+uint32_t dist_segment_count(uint32_t P) {
+    const int b = rank_bits(P);
+    return b < 0 ? 0u : 1u << ((b + 1) / 2);
+}
+
+int dist_segment(uint32_t P, uint32_t rank, uint64_t n, uint64_t t, uint32_t index, DistSegment& out) {
+    DistBlock blk{};
+    if (int e = dist_block(P, rank, n, t, blk)) return e;
+    const int b = rank_bits(P);
+    const int row_bits = (b + 1) / 2, col_bits = b / 2;
+    if (index >= (1u << row_bits)) return 2;
+    const uint64_t h = n >> row_bits, w = n >> col_bits;  // band height / width, w in {h, 2h}
+    // rank of the block at (row band, column band): interleave their bits back
+    auto owner = [&](uint32_t rband, uint32_t cband) {
+        uint32_t r = 0;
+        for (int k = 0; k < b; ++k) {
+            const uint32_t bit = (k % 2 == 0) ? (rband >> (row_bits - 1 - k / 2)) & 1u
+                                              : (cband >> (col_bits - 1 - k / 2)) & 1u;
+            r = (r << 1) | bit;
+        }
+        return r;
+    };
+    const uint64_t per = n * n / P;
+    const uint64_t k0 = (uint64_t)index * h;
+    const uint32_t a_owner = owner(blk.row_band, (uint32_t)(k0 / w));
+    const uint64_t lo = (uint64_t)a_owner * per;
+    const uint64_t half = per / (w / h);  // the slice is (w / h) h x h quadrants in Z order
+    const uint64_t part = (k0 % w) / h;
+    const uint32_t b_owner = owner(index, blk.col_band);
+    out = DistSegment{index, k0, k0 + h, a_owner, lo + part * half, lo + (part + 1) * half,
+                      b_owner, (uint64_t)b_owner * per, (uint64_t)(b_owner + 1) * per};
+    return 0;
+}
+
 }  // namespace mhg

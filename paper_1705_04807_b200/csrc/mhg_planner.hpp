@@ -84,4 +84,30 @@ int fold_level(uint32_t q, uint64_t k_chunk);
 // without the q-multiple bias (GemmParams::bias32 = 0) and the levels test uint32 range.
 int fold_level_u8(uint32_t q, uint64_t k_chunk);
 
+// ------------------------------------------------- multi-GPU partition geometry
+// C-stationary partition by top-level Morton blocks: with P = 2^b ranks,
+// rank r owns the r-th contiguous 1/P slice of every container's flat store -- a
+// rectangle, because the Z order visits quadrants NW, NE, SW, SE at every scale
+// (layout.hpp:42-48): the bits of r, most significant first, alternate row-half /
+// column-half choices.  Rank r updates C[R_r, C_r]; K is cut at row-band boundaries
+// into segments whose A part is a contiguous flat range of ONE row-group member's
+// slice and whose B part is the whole slice of ONE column-group member.
+struct DistBlock {
+    uint32_t rank;
+    uint64_t i0, j0, rows, cols;
+    uint32_t row_band, col_band;
+};
+struct DistSegment {
+    uint32_t index;
+    uint64_t k0, k1;
+    uint32_t a_owner;
+    uint64_t a_begin, a_end;  // flat cell range of A[R_r, k0:k1] (in a_owner's slice)
+    uint32_t b_owner;
+    uint64_t b_begin, b_end;  // flat cell range of B[k0:k1, C_r] (b_owner's whole slice)
+};
+// 0 on success; 1 = P not a power of two, 2 = rank out of range, 3 = fewer tiles than ranks
+int dist_block(uint32_t P, uint32_t rank, uint64_t n, uint64_t t, DistBlock& out);
+uint32_t dist_segment_count(uint32_t P);  // row bands = K segments per rank
+int dist_segment(uint32_t P, uint32_t rank, uint64_t n, uint64_t t, uint32_t index, DistSegment& out);
+
 }  // namespace mhg

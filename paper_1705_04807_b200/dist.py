@@ -33,6 +33,13 @@ class Block:
     col_band: int
 
 
+def _geom():
+    """The partition geometry lives in libmhg.so (mhg_dist_*, include/mhg.h: pure host code,
+    the same entry points a C++ host program would call)."""
+    import paper_1705_04807_b200 as mh
+    return mh
+
+
 def _bits(P: int) -> int:
     if P < 1 or P & (P - 1):
         raise ValueError(f"rank count must be a power of two, got {P}")
@@ -40,29 +47,20 @@ def _bits(P: int) -> int:
 
 
 def morton_block(rank: int, P: int, n: int, t: int) -> Block:
-    """Rectangle covered by the rank-th 1/P slice of an n x n Morton-hybrid store."""
-    b = _bits(P)
+    """Rectangle covered by the rank-th 1/P slice of an n x n Morton-hybrid store
+    (mhg_dist_block)."""
+    _bits(P)
     if not 0 <= rank < P:
         raise ValueError("rank out of range")
     if (n // t) ** 2 < P:
         raise ValueError("fewer tiles than ranks")
-    row_bits = (b + 1) // 2
-    col_bits = b // 2
-    rb = cb = 0
-    for k in range(b):  # from the most significant bit of rank
-        bit = (rank >> (b - 1 - k)) & 1
-        if k % 2 == 0:
-            rb = (rb << 1) | bit
-        else:
-            cb = (cb << 1) | bit
-    rows, cols = n >> row_bits, n >> col_bits
-    return Block(rank, rb * rows, cb * cols, rows, cols, rb, cb)
+    b = _geom().dist_block(P, rank, n, t)
+    return Block(rank, b.i0, b.j0, b.rows, b.cols, b.row_band, b.col_band)
 
 
 def slice_range(rank: int, P: int, n: int) -> Tuple[int, int]:
-    """Flat [begin, end) of the rank's slice of the Morton store."""
-    per = n * n // P
-    return rank * per, (rank + 1) * per
+    """Flat [begin, end) of the rank's slice of the Morton store (mhg_dist_slice)."""
+    return _geom().dist_slice(P, rank, n)
 
 
 def groups(P: int, n: int, t: int) -> Tuple[Dict[int, List[int]], Dict[int, List[int]]]:
@@ -95,23 +93,10 @@ class Segment:
 
 
 def segments(rank: int, P: int, n: int, t: int) -> List[Segment]:
-    b = _bits(P)
-    blk = morton_block(rank, P, n, t)
-    row_bits, col_bits = (b + 1) // 2, b // 2
-    h, w = n >> row_bits, n >> col_bits  # row-band height, column-band width (w in {h, 2h})
-    owners = {(morton_block(r, P, n, t).row_band, morton_block(r, P, n, t).col_band): r
-              for r in range(P)}
-    segs = []
-    for i in range(1 << row_bits):
-        k0, k1 = i * h, (i + 1) * h
-        a_owner = owners[(blk.row_band, k0 // w)]
-        lo, hi = slice_range(a_owner, P, n)
-        half = (hi - lo) // (w // h)  # the slice is (w // h) h x h quadrants, Z order
-        part = (k0 % w) // h
-        b_owner = owners[(i, blk.col_band)]
-        segs.append(Segment(i, k0, k1, a_owner, (lo + part * half, lo + (part + 1) * half),
-                            b_owner, slice_range(b_owner, P, n)))
-    return segs
+    """The K segments of the rank's update (mhg_dist_segment)."""
+    _bits(P)
+    return [Segment(g.index, g.k0, g.k1, g.a_owner, (g.a_begin, g.a_end), g.b_owner,
+                    (g.b_begin, g.b_end)) for g in _geom().dist_segments(P, rank, n, t)]
 
 
 class PanelExchange:
@@ -185,16 +170,7 @@ def segment_plans(mh, ex: PanelExchange, A, B, C, op: int):
     C[R_r, C_r] op= A[R_r, seg] * B[seg, C_r] (A = out, B = lhs, C = rhs in the
     reference's Problem order).  A SET update overwrites only with the first
     segment; the rest accumulate."""
-    lay = A.layout()
-    blk = ex.block
-    plans = []
-    for j, sg in enumerate(ex.segments()):
-        op_j = op if (op != mh.OP_SET or j == 0) else mh.OP_ADD
-        plans.append(mh.Plan(mh.Problem(
-            mh.Sub(A, mh.encode(lay, blk.i0, blk.j0), blk.rows, blk.cols),
-            mh.Sub(B, mh.encode(lay, blk.i0, sg.k0), blk.rows, sg.k1 - sg.k0),
-            mh.Sub(C, mh.encode(lay, sg.k0, blk.j0), sg.k1 - sg.k0, blk.cols)), op_j))
-    return plans
+    return [mh.Plan.for_segment(A, B, C, op, ex.P, ex.rank, j) for j in range(len(ex.segments()))]
 
 
 def rank_update(ex: PanelExchange, plans, lhs_flat, rhs_flat, stream=None):

@@ -653,6 +653,58 @@ void test_tu_schur_sweep() {
     }));
 }
 
+// Multi-GPU partition through the C ABI (mhg_dist_*), driven the way a C++ host
+// program would: every rank's K-segment plans (packs + GEMM run separately, as around a
+// broadcast of the packed bytes), here all on one device, make the whole multiply.
+void test_dist_segment_plans() {
+    std::mt19937_64 eng(404);
+    const std::uint64_t n = 256, t = 32;
+    const std::uint32_t q = 65521, P = 8;
+    const mh::Modulus mod(q);
+    const mh::Grid gc = random_grid(n, q, eng), ga = random_grid(n, q, eng), gb = random_grid(n, q, eng);
+    mh::Matrix C = mh::from_row_major(gc, t, mod), A = mh::from_row_major(ga, t, mod),
+               B = mh::from_row_major(gb, t, mod);
+    std::uint32_t nseg = 0;
+    CHECK(mhg_dist_segment_count(P, &nseg) == MHG_OK && nseg == 4);
+    std::uint64_t cells = 0, macs = 0;
+    for (std::uint32_t r = 0; r < P; ++r) {
+        mhg_dist_block_t blk{};
+        CHECK(mhg_dist_block(P, r, n, t, &blk) == MHG_OK);
+        std::uint64_t lo = 0, hi = 0;
+        CHECK(mhg_dist_slice(P, r, n, &lo, &hi) == MHG_OK);
+        CHECK(hi - lo == blk.rows * blk.cols && lo == mh::encode(C.layout(), blk.i0, blk.j0));
+        cells += hi - lo;
+        for (std::uint32_t s = 0; s < nseg; ++s) {
+            mhg_dist_segment_t sg{};
+            CHECK(mhg_dist_segment(P, r, n, t, s, &sg) == MHG_OK);
+            CHECK(sg.a_begin == mh::encode(A.layout(), blk.i0, sg.k0));
+            CHECK(sg.b_begin == mh::encode(B.layout(), sg.k0, blk.j0));
+            mhg_plan pl = nullptr;
+            CHECK(mhg_dist_plan_create(C.device(), A.device(), B.device(), MHG_OP_SUB, P, r, s, &pl) == MHG_OK);
+            if (!pl) continue;
+            mhg_counters c{};
+            CHECK(mhg_plan_counters(pl, &c) == MHG_OK);
+            macs += c.scalar_macs;
+            // the owner's packs, (the broadcast of mhg_plan_pack_buffer goes here), the GEMM
+            CHECK(mhg_plan_pack(pl, 0, nullptr) == MHG_OK && mhg_plan_pack(pl, 1, nullptr) == MHG_OK);
+            void* ptr = nullptr;
+            std::uint64_t bytes = 0;
+            CHECK(mhg_plan_pack_buffer(pl, 0, &ptr, &bytes) == MHG_OK && ptr && bytes);
+            CHECK(mhg_plan_gemm(pl, nullptr) == MHG_OK);
+            CHECK(mhg_synchronize(nullptr) == MHG_OK);
+            mhg_plan_destroy(pl);
+        }
+    }
+    C.device_written();
+    CHECK(cells == n * n && macs == n * n * n);
+    mh::Grid want = gc;
+    dense_acc(want, ga, gb, 0, 0, 0, 0, 0, 0, n, n, n, q, true);
+    CHECK(mh::to_row_major(C) == want);
+    mhg_dist_block_t blk{};
+    CHECK(mhg_dist_block(6, 0, n, t, &blk) == MHG_ERR_INVALID_ARGUMENT);
+    CHECK(mhg_dist_block(4, 4, n, t, &blk) == MHG_ERR_OUT_OF_RANGE);
+}
+
 }  // namespace
 
 int main() {
@@ -675,6 +727,7 @@ int main() {
         {"acceptance_codec", test_acceptance_codec},
         {"acceptance_partition", test_acceptance_partition},
         {"tu_schur_sweep", test_tu_schur_sweep},
+        {"dist_segment_plans", test_dist_segment_plans},
     };
     for (const auto& [name, fn] : tests) {
         const int before = g_fail;

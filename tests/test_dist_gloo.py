@@ -57,6 +57,71 @@ def test_segments_are_exact_flat_ranges(oracle):
                 assert za == set(range(*sg.a_range)) and zb == set(range(*sg.b_range))
 
 
+
+# ---- the C ABI's partition geometry (mhg_dist_*, include/mhg.h) against an independent
+# restatement of the same rules in Python
+def _py_block(rank, P, n):
+    b = P.bit_length() - 1
+    row_bits, col_bits = (b + 1) // 2, b // 2
+    rb = cb = 0
+    for k in range(b):  # from the most significant bit of rank
+        bit = (rank >> (b - 1 - k)) & 1
+        if k % 2 == 0:
+            rb = (rb << 1) | bit
+        else:
+            cb = (cb << 1) | bit
+    rows, cols = n >> row_bits, n >> col_bits
+    return rb * rows, cb * cols, rows, cols, rb, cb
+
+
+def _py_segments(rank, P, n):
+    b = P.bit_length() - 1
+    row_bits, col_bits = (b + 1) // 2, b // 2
+    h, w = n >> row_bits, n >> col_bits
+    per = n * n // P
+    owners = {_py_block(r, P, n)[4:]: r for r in range(P)}
+    _, _, _, _, rband, cband = _py_block(rank, P, n)
+    out = []
+    for i in range(1 << row_bits):
+        k0 = i * h
+        a_owner = owners[(rband, k0 // w)]
+        half = per // (w // h)
+        part = (k0 % w) // h
+        b_owner = owners[(i, cband)]
+        out.append((i, k0, k0 + h, a_owner, a_owner * per + part * half, a_owner * per + (part + 1) * half,
+                    b_owner, b_owner * per, (b_owner + 1) * per))
+    return out
+
+
+def test_c_abi_partition_geometry(mh):
+    for n, t in ((64, 4), (96, 3), (512, 32), (16384, 64), (32768, 64)):
+        for P in (1, 2, 4, 8, 16, 32, 64):
+            if (n // t) ** 2 < P:
+                continue
+            for r in range(P):
+                b = mh.dist_block(P, r, n, t)
+                assert (b.i0, b.j0, b.rows, b.cols, b.row_band, b.col_band) == _py_block(r, P, n)
+                assert b.rank == r
+                assert mh.dist_slice(P, r, n) == (r * (n * n // P), (r + 1) * (n * n // P))
+                got = [(g.index, g.k0, g.k1, g.a_owner, g.a_begin, g.a_end, g.b_owner, g.b_begin, g.b_end)
+                       for g in mh.dist_segments(P, r, n, t)]
+                assert got == _py_segments(r, P, n)
+    with pytest.raises(mh.InvalidArgument):
+        mh.dist_block(3, 0, 64, 4)          # not a power of two
+    with pytest.raises(mh.InvalidArgument):
+        mh.dist_block(0, 0, 64, 4)
+    with pytest.raises(mh.OutOfRange):
+        mh.dist_block(4, 4, 64, 4)          # rank out of range
+    with pytest.raises(mh.InvalidArgument):
+        mh.dist_block(32, 0, 16, 4)         # 16 tiles, 32 ranks
+    with pytest.raises(mh.InvalidArgument):
+        mh.dist_block(2, 0, 12, 4)          # not a layout
+    with pytest.raises(mh.OutOfRange):
+        mh.dist_slice(4, 7, 64)
+    with pytest.raises(mh.InvalidArgument):
+        mh.dist_segments(6, 0, 64, 4)
+
+
 def _seg_worker(rank, world, port, n, t, q, use_async):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist

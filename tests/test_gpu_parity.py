@@ -807,6 +807,40 @@ def test_split_plan_execution(gpu, mh, oracle):
         pl.pack(2)
 
 
+@pytest.mark.parametrize("P,op", [(2, "sub"), (4, "set"), (8, "add")])
+def test_dist_segment_plans_cover_the_multiply(gpu, mh, oracle, P, op):
+    """mhg_dist_plan_create (the C ABI's multi-GPU partition): every rank's K-segment plans,
+    run one after another on ONE device over full containers, make exactly the whole
+    multiply (SET overwrites with segment 0 and accumulates the rest) and their MACs sum
+    to n^3; the SET form rejects nothing the plain plan accepts."""
+    import torch
+
+    n, t, q = 512, 32, P16
+    out, lhs, rhs = _fill(oracle, 4200 + P, n, q)
+    A, B, Cm = _containers(mh, n, t, q, (out, lhs, rhs))
+    code = {"add": mh.OP_ADD, "sub": mh.OP_SUB, "set": mh.OP_SET}[op]
+    macs = 0
+    for r in range(P):
+        segs = mh.dist_segments(P, r, n, t)
+        blk = mh.dist_block(P, r, n, t)
+        assert sum(g.k1 - g.k0 for g in segs) == n
+        for g in segs:
+            pl = mh.Plan.for_segment(A, B, Cm, code, P, r, g.index)
+            assert pl.counters().scalar_macs == blk.rows * blk.cols * (g.k1 - g.k0)
+            macs += pl.counters().scalar_macs
+            pl.run()
+    torch.cuda.synchronize()
+    assert macs == n ** 3
+    want = out.copy()
+    full = _views_from(oracle, n, t, n, n, n, [0] * 6)
+    oracle.mm_dense(n, t, q, want, lhs, rhs, full, op={"add": OP_ADD, "sub": OP_SUB, "set": OP_SET}[op])
+    assert np.array_equal(A.cells(), want)
+    with pytest.raises(mh.OutOfRange):
+        mh.Plan.for_segment(A, B, Cm, code, P, P, 0)
+    with pytest.raises(mh.OutOfRange):
+        mh.Plan.for_segment(A, B, Cm, code, P, 0, 64)
+
+
 @pytest.mark.parametrize("n,t,q,bad", [
     (4096, 64, P16, ()),                   # 4 staging chunks, all cells on the 16-bit wire
     (6144, 96, P16, ()),                   # non-pow2 tile, partial last chunk
