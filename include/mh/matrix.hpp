@@ -32,8 +32,10 @@ public:
     }
 
     Matrix(Matrix&& o) noexcept
-        : lay_(o.lay_), mod_(o.mod_), host_(std::move(o.host_)), dev_(o.dev_), state_(o.state_) {
+        : lay_(o.lay_), mod_(o.mod_), host_(std::move(o.host_)), dev_(o.dev_), state_(o.state_),
+          pending_(o.pending_), stream_(o.stream_) {
         o.dev_ = nullptr;
+        o.pending_ = false;
     }
 
     Matrix& operator=(const Matrix& o) {
@@ -50,7 +52,10 @@ public:
     }
 
     ~Matrix() {
-        if (dev_) mhg_matrix_destroy(dev_);
+        if (dev_) {
+            if (pending_) mhg_synchronize(stream_);  // work in flight still uses the store
+            mhg_matrix_destroy(dev_);
+        }
     }
 
     const Layout& layout() const { return lay_; }
@@ -88,16 +93,41 @@ public:
     // ---- device side (used by the multiply entry points)
     /// Device container with any host-side edits uploaded first.
     mhg_matrix device() const {
+        settle();  // the caller works on the default stream, or synchronously
+        push();
+        return dev_;
+    }
+    /// The same for work about to be enqueued on `stream`: earlier asynchronous work on that
+    /// stream stays in flight (stream order covers it), work on another stream is awaited.
+    mhg_matrix device_on(void* stream) const {
+        if (pending_ && stream_ != stream) settle();
         push();
         return dev_;
     }
     /// Record that a kernel wrote the device copy.
     void device_written() { state_ = State::DeviceNewer; }
+    /// True when host-side edits are waiting to be uploaded (device() uploads them).
+    bool host_newer() const { return state_ == State::HostNewer; }
+    /// Record that work enqueued on `stream` (a cudaStream_t as void*) reads or writes the
+    /// device copy and may still be running (the asynchronous multiply): the next host-side
+    /// access or upload of this matrix waits for that stream first.
+    void in_flight_on(void* stream) const {
+        if (pending_ && stream_ != stream) settle();  // one stream is remembered at a time
+        pending_ = true;
+        stream_ = stream;
+    }
 
 private:
     enum class State { InSync, HostNewer, DeviceNewer };
 
+    void settle() const {
+        if (pending_) {
+            gpu::check(mhg_synchronize(stream_));
+            pending_ = false;
+        }
+    }
     void pull() const {
+        settle();
         if (state_ == State::DeviceNewer) {
             gpu::check(mhg_matrix_download(dev_, reinterpret_cast<std::uint32_t*>(host_.data()),
                                            nullptr));
@@ -107,6 +137,7 @@ private:
     }
     void push() const {
         if (state_ == State::HostNewer) {
+            settle();
             gpu::check(mhg_matrix_upload(dev_, reinterpret_cast<const std::uint32_t*>(host_.data()),
                                          nullptr));
             state_ = State::InSync;
@@ -118,6 +149,8 @@ private:
         std::swap(host_, o.host_);
         std::swap(dev_, o.dev_);
         std::swap(state_, o.state_);
+        std::swap(pending_, o.pending_);
+        std::swap(stream_, o.stream_);
     }
 
     Layout lay_;
@@ -125,6 +158,8 @@ private:
     mutable std::vector<Fp> host_;
     mhg_matrix dev_ = nullptr;
     mutable State state_ = State::InSync;
+    mutable bool pending_ = false;   // asynchronous work may still touch the device copy ...
+    mutable void* stream_ = nullptr; // ... on this stream
 };
 static_assert(sizeof(Fp) == sizeof(std::uint32_t), "Fp must be layout-compatible with uint32");
 

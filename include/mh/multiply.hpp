@@ -95,7 +95,39 @@ inline Counters run(const Problem& p, Op op, std::uint32_t flags = 0) {
     return to_counters(c);
 }
 
+/// Asynchronous form of run(): validation and Counters as usual, then the multiply is
+/// ENQUEUED on `stream` (a cudaStream_t passed as void*; nullptr = the default stream) and
+/// the call returns.  Pending host-side edits of the three matrices are uploaded first.
+/// The three matrices remember the stream: their next host-side access (operator[], at,
+/// cells(), ==) or upload waits for it, so results read through the Matrix API are always
+/// complete; mh::synchronize(stream) waits explicitly.  As in the reference, concurrent
+/// calls are allowed only on disjoint output rectangles (multiply.hpp:25-29) -- here:
+/// calls in flight on different streams.
+inline Counters run_async(const Problem& p, Op op, void* stream, std::uint32_t flags = 0) {
+    check_problem(p);
+    const bool uploads = p.a.mat->host_newer() || p.b.mat->host_newer() || p.c.mat->host_newer();
+    auto on = [&](const Sub& s) { return mhg_view{s.mat->device_on(stream), s.origin, s.rows, s.cols}; };
+    const mhg_view va = on(p.a), vb = on(p.b), vc = on(p.c);
+    if (uploads) gpu::check(mhg_synchronize(nullptr));  // uploads run on the default stream
+    mhg_counters c{};
+    gpu::check(mhg_mm_ex(va, vb, vc, static_cast<mhg_op>(op), flags, &c, stream));
+    p.a.mat->device_written();
+    p.a.mat->in_flight_on(stream);
+    p.b.mat->in_flight_on(stream);
+    p.c.mat->in_flight_on(stream);
+    return to_counters(c);
+}
+
 }  // namespace gpu
+
+/// Wait for `stream` (cudaStreamSynchronize for callers that do not link the CUDA runtime).
+inline void synchronize(void* stream = nullptr) { gpu::check(mhg_synchronize(stream)); }
+
+/// mm_oblivious enqueued on a stream (SURVEY 8(b) threading: the drop-in is synchronous by
+/// default, this is the explicit-stream variant); see gpu::run_async.
+inline Counters mm_oblivious_async(const Problem& p, Op op = Op::Add, void* stream = nullptr) {
+    return gpu::run_async(p, op, stream);
+}
 
 /// Drop-in for the reference's mm_oblivious (multiply.hpp:297-308).
 inline Counters mm_oblivious(const Problem& p) { return gpu::run(p, Op::Add); }

@@ -705,6 +705,38 @@ void test_dist_segment_plans() {
     CHECK(mhg_dist_block(4, 4, n, t, &blk) == MHG_ERR_OUT_OF_RANGE);
 }
 
+// The explicit-stream variant (SURVEY 8(b) threading): the call returns after enqueueing,
+// host-side reads of the output wait for it, host edits made after it are uploaded before
+// the next multiply, and a chain of asynchronous calls equals the synchronous results.
+void test_async_variant() {
+    std::mt19937_64 eng(909);
+    const std::uint64_t n = 256, t = 32;
+    const std::uint32_t q = 65521;
+    const mh::Modulus mod(q);
+    mh::Grid gc = random_grid(n, q, eng);
+    const mh::Grid ga = random_grid(n, q, eng), gb = random_grid(n, q, eng);
+    mh::Matrix C = mh::from_row_major(gc, t, mod), A = mh::from_row_major(ga, t, mod),
+               B = mh::from_row_major(gb, t, mod);
+    const mh::Problem p{mh::Sub{&C, mh::encode(C.layout(), 17, 40), 200, 150},
+                        mh::Sub{&A, mh::encode(A.layout(), 3, 9), 200, 120},
+                        mh::Sub{&B, mh::encode(B.layout(), 77, 5), 120, 150}};
+    const mh::Counters c1 = mh::mm_oblivious_async(p, mh::Op::Sub);
+    const mh::Counters c2 = mh::mm_oblivious_async(p);  // Add, same stream: ordered after the first
+    CHECK(c1.scalar_macs == 200ull * 150 * 120 && c2.base_case_calls == c1.base_case_calls);
+    CHECK(mh::to_row_major(C) == gc);  // -AB then +AB: back to the start; the read waited
+    // a host edit after the asynchronous calls reaches the device before the next one
+    C.set(17, 40, mh::Fp{5});
+    gc[17][40] = mh::Fp{5};
+    mh::mm_oblivious_async(p, mh::Op::Sub);
+    mh::synchronize();
+    dense_acc(gc, ga, gb, 17, 40, 3, 9, 77, 5, 200, 150, 120, q, true);
+    CHECK(mh::to_row_major(C) == gc);
+    // same validation as the synchronous entry point
+    CHECK(throws_as<std::logic_error>([&] {
+        mh::mm_oblivious_async(mh::Problem{p.a, mh::Sub{&C, 0, 200, 120}, p.c});
+    }));
+}
+
 }  // namespace
 
 int main() {
@@ -728,6 +760,7 @@ int main() {
         {"acceptance_partition", test_acceptance_partition},
         {"tu_schur_sweep", test_tu_schur_sweep},
         {"dist_segment_plans", test_dist_segment_plans},
+        {"async_variant", test_async_variant},
     };
     for (const auto& [name, fn] : tests) {
         const int before = g_fail;
