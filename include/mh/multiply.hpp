@@ -44,6 +44,25 @@ inline void check_problem(const Problem& p) {
         throw std::logic_error("problem: operands use different moduli");
 }
 
+namespace detail {
+
+/// Largest forward step between consecutive touches of one operand's cells -- the quantity
+/// behind Counters::max_consecutive_jump (reference: multiply.hpp:80-90).  The GPU engine
+/// returns that counter in closed form (libmhg.so's planner); this tracker is what a host
+/// walk uses to measure it, and the drop-in tests use it to check the closed forms.
+struct JumpTracker {
+    Index last = 0;
+    bool armed = false;
+
+    void touch(Index z, Counters& ctr) {
+        if (armed && z > last) ctr.max_consecutive_jump = std::max(ctr.max_consecutive_jump, z - last);
+        last = z;
+        armed = true;
+    }
+};
+
+}  // namespace detail
+
 /// A view plus its rectangle's position on the problem's shared axes.
 struct Framed {
     Sub view;

@@ -737,6 +737,38 @@ void test_async_variant() {
     }));
 }
 
+// detail::dilate / undilate (layout.hpp:15-33) against the codec, and detail::JumpTracker
+// (multiply.hpp:80-90) measuring base_case_mm's walk against its closed-form counter.
+void test_detail_helpers() {
+    const mh::Layout lay(64, 4);
+    for (std::uint64_t i = 0; i < 64; i += 3)
+        for (std::uint64_t j = 0; j < 64; j += 5) {
+            const std::uint64_t z = ((mh::detail::dilate(lay.tdiv(i)) << 1) | mh::detail::dilate(lay.tdiv(j))) * lay.tile +
+                                    lay.tmod(i) * lay.t + lay.tmod(j);
+            CHECK(z == mh::encode(lay, i, j));
+            CHECK(mh::detail::undilate(lay.tilediv(z) >> 1) == lay.tdiv(i));
+            CHECK(mh::detail::undilate(lay.tilediv(z)) == lay.tdiv(j));
+        }
+    // the walk of a contained leaf (out 3 x 2, inner 4, t = 8), tracked cell by cell
+    const mh::Modulus mod(97);
+    mh::Matrix A(mh::Layout(16, 8), mod), B(mh::Layout(16, 8), mod), C(mh::Layout(16, 8), mod);
+    const mh::Sub out{&A, mh::encode(A.layout(), 1, 2), 3, 2}, lhs{&B, mh::encode(B.layout(), 9, 1), 3, 4},
+        rhs{&C, mh::encode(C.layout(), 2, 10), 4, 2};
+    mh::Counters walked{}, closed{};
+    mh::detail::JumpTracker ja, jb, jc;
+    for (std::uint64_t x = 0; x < 3; ++x)
+        for (std::uint64_t y = 0; y < 2; ++y) {
+            ja.touch(out.origin + x * 8 + y, walked);
+            for (std::uint64_t z = 0; z < 4; ++z) {
+                jb.touch(lhs.origin + x * 8 + z, walked);
+                jc.touch(rhs.origin + z * 8 + y, walked);
+            }
+        }
+    mh::base_case_mm(out, lhs, rhs, closed);
+    CHECK(walked.max_consecutive_jump == closed.max_consecutive_jump);
+    CHECK(closed.max_consecutive_jump == 8);
+}
+
 }  // namespace
 
 int main() {
@@ -761,6 +793,7 @@ int main() {
         {"tu_schur_sweep", test_tu_schur_sweep},
         {"dist_segment_plans", test_dist_segment_plans},
         {"async_variant", test_async_variant},
+        {"detail_helpers", test_detail_helpers},
     };
     for (const auto& [name, fn] : tests) {
         const int before = g_fail;
