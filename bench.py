@@ -478,6 +478,50 @@ def run_gpu(args, rank, world, local_rank):
         else:
             rank_update_packed(ex, plans, stream)
 
+    gathered = [False]
+
+    def verify_ranked():
+        """N > 1: every rank checks its own C block on the device (Freivalds, mhg_verify).  That
+        needs the whole A row panel and B column panel as residues, so the 1/P slices are
+        gathered once into the (otherwise zero) full containers; the step itself still
+        exchanges the packed planes as timed.  Collective; returns the minimum over ranks
+        (None when memory is short: ranks sharing one GPU at n = 32768)."""
+        torch.cuda.empty_cache()
+        room = torch.tensor([float(torch.cuda.mem_get_info()[0] > 4 * n * n * (world if shared_gpu else 1)
+                                   + (2 << 30))], dtype=torch.float64, device=dev)
+        dist.all_reduce(room, op=dist.ReduceOp.MIN)  # one decision for every rank
+        if room[0] < 0.5:
+            return None
+        if not gathered[0]:
+            for f in (lhs_f, rhs_f):
+                for r in range(world):
+                    rb, re_ = slice_range(r, world, n)
+                    dist.broadcast(f[rb:re_], src=r)
+            gathered[0] = True
+        old_f = out_f.clone()
+        old = mh.Matrix.wrap(lay, mod, old_f.data_ptr(), owner=old_f)
+        step()
+        ok = mh.verify(prob, mh.Sub(old, prob.a.origin, prob.a.rows, prob.a.cols), op, rounds=2,
+                       stream=stream)
+        v = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64, device=dev)
+        dist.all_reduce(v, op=dist.ReduceOp.MIN)
+        del old, old_f
+        torch.cuda.empty_cache()
+        return bool(v[0] > 0.5)
+
+    # The copy-engine exchange orders ranks through CUDA IPC events and peer mappings: check
+    # one step of it on the device BEFORE timing; a wrong result (on any rank) sends every
+    # rank to the NCCL packed exchange instead.
+    if exchange == "p2p":
+        step()
+        # MHG_BENCH_FAIL_P2P_CHECK=1 (tests only) takes the fallback branch on a healthy exchange
+        if verify_ranked() is False or os.environ.get("MHG_BENCH_FAIL_P2P_CHECK") == "1":
+            torch.cuda.synchronize()
+            barrier()
+            peer.close()
+            peer = None
+            exchange, exchange_note = "nccl", "p2p failed the device verification, fell back to nccl"
+
     W = max(args.warmup, 3)
     w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     # the warm-up builds both graphs of every plan (plain and profiling, below): one profiled
@@ -589,28 +633,7 @@ def run_gpu(args, rank, world, local_rank):
         del old, old_f
         torch.cuda.empty_cache()
     else:
-        # N > 1: every rank checks its own C block.  Freivalds needs the whole A row panel and
-        # B column panel as residues, so the 1/P slices are gathered into the (otherwise zero)
-        # full containers first; the step itself still exchanges the packed planes as timed.
-        torch.cuda.empty_cache()
-        room = torch.tensor([float(torch.cuda.mem_get_info()[0] > 4 * n * n * (world if shared_gpu else 1)
-                                   + (2 << 30))], dtype=torch.float64, device=dev)
-        dist.all_reduce(room, op=dist.ReduceOp.MIN)  # one decision for every rank
-        if room[0] > 0.5:
-            for f in (lhs_f, rhs_f):
-                for r in range(world):
-                    rb, re_ = slice_range(r, world, n)
-                    dist.broadcast(f[rb:re_], src=r)
-            old_f = out_f.clone()
-            old = mh.Matrix.wrap(lay, mod, old_f.data_ptr(), owner=old_f)
-            step()
-            ok = mh.verify(prob, mh.Sub(old, prob.a.origin, prob.a.rows, prob.a.cols), op, rounds=2,
-                           stream=stream)
-            v = torch.tensor([1.0 if ok else 0.0], dtype=torch.float64, device=dev)
-            dist.all_reduce(v, op=dist.ReduceOp.MIN)
-            verified = bool(v[0] > 0.5)
-            del old, old_f
-            torch.cuda.empty_cache()
+        verified = verify_ranked()
     if peer is not None:
         torch.cuda.synchronize()
         barrier()

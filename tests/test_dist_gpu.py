@@ -108,6 +108,7 @@ def test_bench_two_ranks_runs_end_to_end(gpu, mh, tmp_path):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["scaling"] == "strong" and d["value"] > 0
     assert d["e2e"]["value"] > 0 and d["gpu_launches"] > 0
+    assert d["verified"] is True and d["exchange"]["mode"] == "p2p"
 
 
 def _fallback_worker(rank, world, port, outdir):
