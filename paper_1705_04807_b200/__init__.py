@@ -149,6 +149,9 @@ def lib():
         "mhg_matrix_download": ([vp, vp, vp], C.c_int),
         "mhg_rowmajor_to_mh": ([vp, vp, vp], C.c_int),
         "mhg_mh_to_rowmajor": ([vp, vp, vp], C.c_int),
+        "mhg_rowmajor_host_to_mh": ([vp, vp], C.c_int),
+        "mhg_mh_to_rowmajor_host": ([vp, vp], C.c_int),
+        "mhg_synchronize": ([vp], C.c_int),
         "mhg_mm": ([_View, _View, _View, C.c_int, P(Counters), vp], C.c_int),
         "mhg_mm_ex": ([_View, _View, _View, C.c_int, u32, P(Counters), vp], C.c_int),
         "mhg_plan_create_ex": ([_View, _View, _View, C.c_int, u32, P(vp)], C.c_int),

@@ -28,6 +28,14 @@ def test_library_exports_every_declared_symbol(mh):
     assert not missing, missing
 
 
+def test_python_binding_types_every_declared_entry_point(mh):
+    """Every function include/mhg.h declares has explicit ctypes argument / result types in
+    the Python mirror (an untyped call would pass 64-bit values as C ints)."""
+    L = mh.lib()
+    untyped = [n for n in _declared_symbols() if getattr(L, n).argtypes is None]
+    assert not untyped, untyped
+
+
 def test_no_torch_types_in_abi():
     src = open(os.path.join(ROOT, "include", "mhg.h")).read()
     assert "torch" not in src.split("*/", 1)[1]
