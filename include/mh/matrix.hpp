@@ -3,7 +3,8 @@
 // The authoritative copy lives in device memory (a libmhg container, same flat
 // order and bytes as the reference's std::vector<Fp>); a host mirror serves the
 // reference's element accessors.  Dirty tracking keeps them coherent:
-//   - non-const accessors (operator[], set, cells()) make the host copy newer;
+//   - non-const accessors (operator[], set, cells()) make the host copy newer in the flat
+//     range they touched (only that range is uploaded);
 //   - a kernel that writes the container makes the device copy newer;
 //   - whichever side is read next is refreshed first (one bulk copy).
 #pragma once
@@ -28,12 +29,12 @@ public:
         o.pull();
         host_ = o.host_;
         gpu::check(mhg_matrix_create(lay_.n, lay_.t, mod_.q, &dev_));
-        state_ = State::HostNewer;
+        touch(0, lay_.total);
     }
 
     Matrix(Matrix&& o) noexcept
         : lay_(o.lay_), mod_(o.mod_), host_(std::move(o.host_)), dev_(o.dev_), state_(o.state_),
-          pending_(o.pending_), stream_(o.stream_) {
+          dirty_lo_(o.dirty_lo_), dirty_hi_(o.dirty_hi_), pending_(o.pending_), stream_(o.stream_) {
         o.dev_ = nullptr;
         o.pending_ = false;
     }
@@ -67,7 +68,7 @@ public:
     }
     Fp& operator[](Index z) {
         pull();
-        state_ = State::HostNewer;
+        touch(z, z + 1);
         return host_[z];
     }
 
@@ -80,7 +81,7 @@ public:
     }
     std::vector<Fp>& cells() {
         pull();
-        state_ = State::HostNewer;
+        touch(0, lay_.total);
         return host_;
     }
 
@@ -135,11 +136,28 @@ private:
             state_ = State::InSync;
         }
     }
+    /// Non-const element access hands out a reference that MAY be written (the reference's
+    /// callers poke cells through operator[]): the touched flat range [lo, hi) is what the next
+    /// upload sends, so a few pokes -- or reads through a non-const Matrix -- do not re-upload
+    /// the whole container before the next multiply.
+    void touch(Index lo, Index hi) {
+        if (state_ != State::HostNewer) {
+            dirty_lo_ = lo;
+            dirty_hi_ = hi;
+        } else {
+            dirty_lo_ = lo < dirty_lo_ ? lo : dirty_lo_;
+            dirty_hi_ = hi > dirty_hi_ ? hi : dirty_hi_;
+        }
+        state_ = State::HostNewer;
+    }
     void push() const {
         if (state_ == State::HostNewer) {
             settle();
-            gpu::check(mhg_matrix_upload(dev_, reinterpret_cast<const std::uint32_t*>(host_.data()),
-                                         nullptr));
+            const Index lo = dirty_lo_ < lay_.total ? dirty_lo_ : lay_.total;
+            const Index hi = dirty_hi_ < lay_.total ? dirty_hi_ : lay_.total;
+            if (hi > lo)
+                gpu::check(mhg_matrix_upload_range(
+                    dev_, reinterpret_cast<const std::uint32_t*>(host_.data()) + lo, lo, hi - lo, nullptr));
             state_ = State::InSync;
         }
     }
@@ -149,6 +167,8 @@ private:
         std::swap(host_, o.host_);
         std::swap(dev_, o.dev_);
         std::swap(state_, o.state_);
+        std::swap(dirty_lo_, o.dirty_lo_);
+        std::swap(dirty_hi_, o.dirty_hi_);
         std::swap(pending_, o.pending_);
         std::swap(stream_, o.stream_);
     }
@@ -158,6 +178,7 @@ private:
     mutable std::vector<Fp> host_;
     mhg_matrix dev_ = nullptr;
     mutable State state_ = State::InSync;
+    Index dirty_lo_ = 0, dirty_hi_ = 0;  // flat range the host copy may differ in (HostNewer)
     mutable bool pending_ = false;   // asynchronous work may still touch the device copy ...
     mutable void* stream_ = nullptr; // ... on this stream
 };

@@ -215,6 +215,20 @@ void test_host_edits_and_copies() {
     const mh::Matrix& Ar = A;  // reads through the const overload: no host-newer marking
     const mh::Matrix& Cr = C;
     CHECK(Ar[5].v == Cr[5].v && Ar[6].v == (2 * Cr[6].v) % 97);
+    // only the touched flat range travels: two pokes 40 cells apart upload 41 cells, a read
+    // through the non-const overload one cell, an untouched matrix nothing
+    auto uploaded = [](const mh::Matrix& m) {
+        std::uint64_t b = 0;
+        CHECK(mhg_matrix_upload_bytes(m.device(), &b) == MHG_OK);
+        return b;
+    };
+    A[10] = mh::Fp{3};
+    A[50] = mh::Fp{4};
+    const std::uint32_t peek = C[7].v;  // non-const access, nothing written
+    mh::mm_oblivious({mh::Sub{&A, 0, 8, 8}, mh::Sub{&B, 0, 8, 8}, mh::Sub{&C, 0, 8, 8}});
+    CHECK(uploaded(A) == 41 * 4 && uploaded(C) == 4 && peek == 7);
+    CHECK(Ar[10].v == (3 + Cr[10].v) % 97 && Ar[50].v == (4 + Cr[50].v) % 97);
+    CHECK(Ar[11].v == (3 * Cr[11].v) % 97);  // cells between the pokes kept their device values
 }
 
 // ---- re-hosted from proj/tests/unit/multiply_test.cpp:308-437 -------------------------
