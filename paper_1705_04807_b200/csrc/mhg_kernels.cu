@@ -922,7 +922,13 @@ __device__ __forceinline__ void tmem_wait_st() {
 constexpr int kConvUnitBytes = 16384;
 // 4 units in flight per CTA x 3 CTAs per SM (more independent issuers measured faster
 // than fewer, deeper CTAs: profiles/r01_conversion_tma.txt)
-constexpr int kConvUnits = 4, kConvCtasPerSm = 3;
+#ifndef MHG_CONV_UNITS
+#define MHG_CONV_UNITS 4
+#endif
+#ifndef MHG_CONV_CTAS
+#define MHG_CONV_CTAS 3
+#endif
+constexpr int kConvUnits = MHG_CONV_UNITS, kConvCtasPerSm = MHG_CONV_CTAS;
 #ifndef MHG_CONV_DEFER
 #define MHG_CONV_DEFER 1  // refill a buffer one unit after its store was issued
 #endif
