@@ -451,7 +451,8 @@ def run_gpu(args, rank, world, local_rank):
         # CPU-only barriers for the IPC event ordering (never wait for the GPU)
         host_group = dist.new_group(backend="gloo") if dist.get_backend() != "gloo" else None
         try:
-            peer = PeerPanels(mh, ex, plans, host_group=host_group)
+            # ADD / SUB updates start with the segment of the rank's own row band (see PeerPanels)
+            peer = PeerPanels(mh, ex, plans, host_group=host_group, rotate=(op != mh.OP_SET))
         except PeerSetupError as exc:  # collective: every rank falls back together
             exchange, exchange_note = "nccl", f"p2p setup failed, fell back to nccl: {exc}"[:300]
     if exchange in ("p2p", "nccl"):

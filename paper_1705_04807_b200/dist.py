@@ -289,7 +289,7 @@ class PeerPanels:
     between the devices, IPC unsupported), every rank raises PeerSetupError and the
     caller can fall back to the NCCL exchange (rank_update_packed)."""
 
-    def __init__(self, mh, ex: PanelExchange, plans, host_group=None, device=None):
+    def __init__(self, mh, ex: PanelExchange, plans, host_group=None, device=None, rotate=False):
         import torch
         import torch.distributed as dist
 
@@ -298,6 +298,15 @@ class PeerPanels:
         self.group = host_group
         self.device = torch.device("cuda", torch.cuda.current_device()) if device is None else device
         self.segs = ex.segments()
+        # Processing order of the K segments.  rotate: start with the segment of the rank's own
+        # row band -- its B part is the rank's own slice (no pull) and its A part is what the
+        # row-group owner packs first, so the first GEMM waits for one small pull instead of
+        # two; B parts of the later segments belong to ranks that packed them first.  Sums
+        # commute, but a SET update must run segment 0 (the overwriting plan) first: callers
+        # rotate only ADD / SUB updates.
+        S = len(self.segs)
+        first = ex.block.row_band % S if rotate and S else 0
+        self.order = [(first + d) % S for d in range(S)]
         rank, P = ex.rank, ex.P
         ev = lambda: torch.cuda.Event(enable_timing=False, blocking=False, interprocess=True)
         self.pack_done = [ev() for _ in self.segs]
@@ -382,7 +391,8 @@ class PeerPanels:
         if self.steps:
             for e in self.peer_copy_done:
                 ps.wait_event(e)
-        for j, (sg, pl) in enumerate(zip(self.segs, self.plans)):
+        for j in self.order:
+            sg, pl = self.segs[j], self.plans[j]
             if sg.a_owner == rank:
                 pl.pack(0, ps)
             if sg.b_owner == rank:
@@ -393,7 +403,8 @@ class PeerPanels:
         self._barrier()  # every owner recorded pack_done of this step
         for cs in self.copy_streams.values():
             cs.wait_event(self.dst_free)
-        for j, pulls in enumerate(self.pulls):
+        for j in self.order:
+            pulls = self.pulls[j]
             used = []
             for owner, dst, src, nb in pulls:
                 cs = self.copy_streams[owner]

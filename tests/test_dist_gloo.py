@@ -122,6 +122,22 @@ def test_c_abi_partition_geometry(mh):
         mh.dist_segments(6, 0, 64, 4)
 
 
+def test_rotated_segment_order_starts_on_the_ranks_own_b_part(mh):
+    """PeerPanels(rotate=True) starts each rank on the K segment of its own row band: the
+    segment whose B part is the rank's own slice (nothing to pull for it) -- and every
+    row-group member starts on the same segment, so the A-part owner packs it first."""
+    from paper_1705_04807_b200.dist import segments
+    n, t = 256, 32
+    for P in (2, 4, 8, 16):
+        for r in range(P):
+            blk = morton_block(r, P, n, t)
+            segs = segments(r, P, n, t)
+            first = segs[blk.row_band % len(segs)]
+            assert first.b_owner == r and first.b_range == slice_range(r, P, n)
+            # the A part of that segment comes from the rank's own row group
+            assert morton_block(first.a_owner, P, n, t).row_band == blk.row_band
+
+
 def _seg_worker(rank, world, port, n, t, q, use_async):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch.distributed as dist

@@ -43,7 +43,8 @@ def _worker(rank, world, port, n, t, q, op, outdir, mode="u32", steps=1):
         A, B, C = (mh.Matrix.wrap(lay, mod, f.data_ptr(), owner=f) for f in flats)
         ex = PanelExchange(world, rank, n, t)
         plans = segment_plans(mh, ex, A, B, C, op)
-        peer = PeerPanels(mh, ex, plans) if mode == "p2p" else None
+        # ADD / SUB updates run the segments in each rank's rotated order (as bench.py does)
+        peer = PeerPanels(mh, ex, plans, rotate=(op != mh.OP_SET)) if mode == "p2p" else None
         for _ in range(steps):
             if mode == "p2p":
                 peer.update()
