@@ -16,8 +16,9 @@
 //                           for k0 = 0, block, ...: A[k1:, k1:] -= A[k1:, k0:k1] * A[k0:k1, k1:]
 //   schur_update(p, op)     one aliased update, synchronous; returns the Counters the
 //                           reference's mm_oblivious would return on three parents
-//   SchurSweep              every step planned once (mhg_plan: one CUDA graph of pack,
-//                           pack, GEMM per step); run() replays the whole sweep
+//   SchurSweep              every step planned once and the whole sequence captured into ONE
+//                           CUDA graph (mhg_sweep): run() is a single launch, no host work
+//                           between the steps
 #pragma once
 
 #include <cstdint>
@@ -64,9 +65,10 @@ inline Counters schur_update(const Problem& p, Op op = Op::Sub) {
     return gpu::to_counters(c);
 }
 
-/// A whole sweep planned once and replayed: run() enqueues every step's graph on the
-/// default stream and waits.  The parent must outlive the sweep; host-side edits of the
-/// parent between runs are uploaded by the next run().
+/// A whole sweep planned once and replayed: run() launches the one graph holding every
+/// step's packs and GEMM on the default stream and waits; run_async(stream) only enqueues
+/// it.  The parent must outlive the sweep; host-side edits of the parent between runs are
+/// uploaded by the next run.
 class SchurSweep {
 public:
     SchurSweep(Matrix& M, std::uint64_t block, Op op = Op::Sub) : mat_(&M) {
@@ -83,6 +85,8 @@ public:
                 gpu::check(mhg_plan_counters(pl, &c));
                 macs_ += c.scalar_macs;
             }
+            if (!plans_.empty())
+                gpu::check(mhg_sweep_create(plans_.data(), std::uint32_t(plans_.size()), &sweep_));
         } catch (...) {
             destroy();
             throw;
@@ -98,20 +102,33 @@ public:
 
     /// One sweep, in place; returns macs().
     std::uint64_t run() {
-        if (plans_.empty()) return 0;
-        mat_->device();  // upload pending host edits
-        for (mhg_plan pl : plans_) gpu::check(mhg_plan_run(pl, nullptr));
-        gpu::check(mhg_synchronize(nullptr));
+        run_async(nullptr);
+        if (sweep_) gpu::check(mhg_synchronize(nullptr));
+        return macs_;
+    }
+
+    /// The same, enqueued on `stream` (a cudaStream_t as void*): the parent remembers the
+    /// stream, and its next host-side access waits for it.
+    std::uint64_t run_async(void* stream) {
+        if (!sweep_) return 0;
+        const bool upload = mat_->host_newer();
+        (void)mat_->device_on(stream);  // pending host edits travel first (default stream)
+        if (upload) gpu::check(mhg_synchronize(nullptr));
+        gpu::check(mhg_sweep_run(sweep_, stream));
         mat_->device_written();
+        mat_->in_flight_on(stream);
         return macs_;
     }
 
 private:
     void destroy() {
+        if (sweep_) mhg_sweep_destroy(sweep_);
+        sweep_ = nullptr;
         for (mhg_plan pl : plans_) mhg_plan_destroy(pl);
         plans_.clear();
     }
     Matrix* mat_;
+    mhg_sweep sweep_ = nullptr;
     std::vector<mhg_plan> plans_;
     std::uint64_t macs_ = 0;
 };

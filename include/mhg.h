@@ -237,6 +237,19 @@ mhg_status mhg_plan_info(mhg_plan plan, uint64_t *launches, uint64_t *tiles, uin
 mhg_status mhg_plan_variant(mhg_plan plan, int *unsigned_digits, int *cta_group);
 mhg_status mhg_plan_destroy(mhg_plan plan);
 
+/* ---- plan sequences (TU/TURBO Schur sweeps) ----
+ * A sequence of plans captured, in order, into ONE CUDA graph: mhg_sweep_run replays every
+ * plan's packs and GEMM back to back with a single launch and no host work between the steps
+ * (the Schur-update sweep of a block elimination: each step reads what the previous one
+ * wrote, so the steps are serial on the device).  The plans must outlive the sweep, must not
+ * be empty, and must not be in profiling mode when the sweep is created. */
+typedef struct mhg_sweep_s *mhg_sweep;
+mhg_status mhg_sweep_create(const mhg_plan *plans, uint32_t count, mhg_sweep *sweep);
+mhg_status mhg_sweep_run(mhg_sweep sweep, void *stream);
+/* Sum of the plans' scalar_macs (the reference's work counter over the whole sweep). */
+mhg_status mhg_sweep_macs(mhg_sweep sweep, uint64_t *macs);
+mhg_status mhg_sweep_destroy(mhg_sweep sweep);
+
 /* ---- multi-GPU partition (one process per GPU) ----
  * C-stationary partition by top-level Morton blocks of the output: with P = 2^b ranks,
  * rank r owns the r-th contiguous 1/P slice of every container's flat store (a rectangle:

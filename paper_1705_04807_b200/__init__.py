@@ -37,7 +37,7 @@ __all__ = [
     "mm_oblivious", "mm_naive", "mm_default", "mm", "counters_oblivious", "counters_layout",
     "counters_geometry", "limb_params", "lib", "LIB_PATH", "KERNEL_NAIVE", "KERNEL_DEFAULT",
     "verify", "Rng",
-    "DistBlock", "DistSegment", "dist_block", "dist_slice", "dist_segments",
+    "Sweep", "DistBlock", "DistSegment", "dist_block", "dist_slice", "dist_segments",
     "OP_ADD", "OP_SUB", "OP_SET", "set_option", "get_option", "options",
     "OPT_DIGITS", "OPT_GEMM_KERNEL", "OPT_MIN_FOLD_LEVEL", "OPT_MAX_KCHUNK", "OPT_UPLOAD_WIRE",
     "OPT_CONV_KERNEL", "OPT_GEMM_STATS", "OPT_UPLOAD_THREADS", "OPT_UPLOAD_ADAPTIVE",
@@ -173,6 +173,10 @@ def lib():
         "mhg_dist_segment_count": ([u32, P(u32)], C.c_int),
         "mhg_dist_segment": ([u32, u32, u64, u64, u32, P(DistSegment)], C.c_int),
         "mhg_dist_plan_create": ([vp, vp, vp, C.c_int, u32, u32, u32, P(vp)], C.c_int),
+        "mhg_sweep_create": ([P(vp), u32, P(vp)], C.c_int),
+        "mhg_sweep_run": ([vp, vp], C.c_int),
+        "mhg_sweep_macs": ([vp, P(u64)], C.c_int),
+        "mhg_sweep_destroy": ([vp], C.c_int),
         "mhg_plan_counters": ([vp, P(Counters)], C.c_int),
         "mhg_verify": ([_View, _View, _View, _View, C.c_int, u32, u64, P(C.c_int), vp], C.c_int),
         "mhg_rng_create": ([u64, P(vp)], C.c_int),
@@ -522,6 +526,32 @@ def counters_geometry(kernel: int, geo_out, geo_lhs, geo_rhs, rows, inner, cols)
     _check(lib().mhg_counters_geometry(kernel, *geo_out, *geo_lhs, *geo_rhs, rows, inner, cols,
                                        C.byref(ctr)))
     return ctr
+
+
+class Sweep:
+    """mhg_sweep: a sequence of plans captured, in order, into ONE CUDA graph (include/mhg.h);
+    run(stream) replays every plan's packs and GEMM with a single launch."""
+
+    def __init__(self, plans):
+        self._plans = list(plans)  # keep the plans (and their containers) alive
+        self._h = C.c_void_p()
+        arr = (C.c_void_p * len(self._plans))(*[pl._h for pl in self._plans])
+        _check(lib().mhg_sweep_create(arr, len(self._plans), C.byref(self._h)))
+        m = C.c_uint64()
+        _check(lib().mhg_sweep_macs(self._h, C.byref(m)))
+        self.macs = m.value
+
+    def run(self, stream=None) -> int:
+        _check(lib().mhg_sweep_run(self._h, _stream_ptr(stream)))
+        return self.macs
+
+    def __del__(self):
+        try:
+            if self._h:
+                lib().mhg_sweep_destroy(self._h)
+                self._h = C.c_void_p()
+        except Exception:
+            pass
 
 
 def dist_block(nranks: int, rank: int, n: int, t: int) -> DistBlock:

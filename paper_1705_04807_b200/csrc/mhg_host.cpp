@@ -14,6 +14,7 @@
 #include <mutex>
 #include <random>
 #include <stdexcept>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -576,6 +577,13 @@ struct mhg_plan_s {
     cudaGraphExec_t pexec = nullptr;
     cudaGraphNode_t pnode[2] = {nullptr, nullptr};
     cudaEvent_t pev[2] = {nullptr, nullptr};
+};
+
+struct mhg_sweep_s {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    uint64_t macs = 0;
+    uint32_t steps = 0;
 };
 
 namespace {
@@ -1398,6 +1406,62 @@ mhg_status mhg_plan_destroy(mhg_plan p) {
         if (p->graph) cudaGraphDestroy(p->graph);
         if (p->mem) cudaFree(p->mem);
         delete p;
+    });
+}
+
+// ------------------------------------------------------------ plan sequences
+mhg_status mhg_sweep_create(const mhg_plan* plans, uint32_t count, mhg_sweep* sweep) {
+    return guarded([&] {
+        if (!sweep || (!plans && count)) fail(MHG_ERR_INVALID_ARGUMENT, "sweep_create: null pointer");
+        if (count == 0) fail(MHG_ERR_INVALID_ARGUMENT, "sweep_create: no plans");
+        for (uint32_t i = 0; i < count; ++i) {
+            if (!plans[i]) fail(MHG_ERR_INVALID_ARGUMENT, "sweep_create: null plan");
+            if (plans[i]->empty) fail(MHG_ERR_UNSUPPORTED, "sweep_create: empty plan in the sequence");
+            if (plans[i]->profiling) fail(MHG_ERR_UNSUPPORTED, "sweep_create: plan in profiling mode");
+        }
+        require_device();
+        auto sw = std::unique_ptr<mhg_sweep_s>(new mhg_sweep_s());
+        sw->steps = count;
+        for (uint32_t i = 0; i < count; ++i) sw->macs += plans[i]->ctr.scalar_macs;
+        sw->graph = capture_graph([&](cudaStream_t cap) {
+            for (uint32_t i = 0; i < count; ++i) {
+                const mhg_plan p = plans[i];
+                launch_multiply(p->buf, p->out, p->lhs, p->rhs, p->chk, p->geo, p->op, cap);
+            }
+        });
+        const cudaError_t e = cudaGraphInstantiate(&sw->exec, sw->graph, 0);
+        if (e != cudaSuccess) {
+            cudaGraphDestroy(sw->graph);
+            cuda_check(e, "sweep graph instantiate");
+        }
+        *sweep = sw.release();
+    });
+}
+
+mhg_status mhg_sweep_run(mhg_sweep sw, void* stream) {
+    return guarded([&] {
+        if (!sw) fail(MHG_ERR_INVALID_ARGUMENT, "sweep_run: null sweep");
+        cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+        cuda_check(cudaStreamIsCapturing((cudaStream_t)stream, &st), "capture query");
+        if (st != cudaStreamCaptureStatusNone)
+            fail(MHG_ERR_UNSUPPORTED, "sweep_run: the stream is capturing (run the plans themselves)");
+        cuda_check(cudaGraphLaunch(sw->exec, (cudaStream_t)stream), "sweep graph launch");
+    });
+}
+
+mhg_status mhg_sweep_macs(mhg_sweep sw, uint64_t* macs) {
+    return guarded([&] {
+        if (!sw || !macs) fail(MHG_ERR_INVALID_ARGUMENT, "sweep_macs: null pointer");
+        *macs = sw->macs;
+    });
+}
+
+mhg_status mhg_sweep_destroy(mhg_sweep sw) {
+    return guarded([&] {
+        if (!sw) return;
+        if (sw->exec) cudaGraphExecDestroy(sw->exec);
+        if (sw->graph) cudaGraphDestroy(sw->graph);
+        delete sw;
     });
 }
 

@@ -61,23 +61,18 @@ def schur_sweep(M: Matrix, block: int, op: int = OP_SUB, stream=None, plans=None
 
 
 class SweepGraph:
-    """A whole sweep captured into one CUDA graph (torch.cuda.CUDAGraph): `replay(stream)`
-    runs every step's pack and GEMM back to back with no host work in between.  The plans
-    (and their workspaces) must outlive the graph; the parent's cells are read and written
-    in place, so a replay is the same in-place update as schur_sweep."""
+    """A whole sweep captured into one CUDA graph (the C ABI's mhg_sweep): `replay(stream)`
+    runs every step's pack and GEMM back to back with one launch and no host work in
+    between.  The plans (and their workspaces) live as long as the graph; the parent's cells
+    are read and written in place, so a replay is the same in-place update as schur_sweep."""
 
     def __init__(self, M: Matrix, block: int, op: int = OP_SUB, plans=None):
-        import torch
+        from . import Sweep
         self.plans = plans if plans is not None else schur_plans(M, block, op)
-        self.macs = sweep_macs(self.plans)
-        self._stream = torch.cuda.Stream()
-        self._graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self._graph, stream=self._stream):
-            for pl in self.plans:
-                pl.run(self._stream)
+        self._sweep = Sweep(self.plans) if self.plans else None  # block >= n: nothing to do
+        self.macs = self._sweep.macs if self._sweep else 0
 
-    def replay(self) -> int:
-        """Launch the captured sweep (on the graph's capture stream ordering of the caller's
-        current stream, as torch.cuda.CUDAGraph.replay); returns GF(p) MACs done."""
-        self._graph.replay()
-        return self.macs
+    def replay(self, stream=None) -> int:
+        """Launch the captured sweep on `stream` (a torch stream or a raw handle; default: the
+        default stream, like Plan.run); returns GF(p) MACs done."""
+        return self._sweep.run(stream) if self._sweep else 0

@@ -563,6 +563,25 @@ def test_tu_sweep_graph(gpu, mh, oracle):
         torch.cuda.synchronize()
         assert np.array_equal(M.cells(), want), rep
     assert macs == sum(((n - k) ** 2) * block for k in range(block, n, block))
+    # the same sequence on a side stream; degenerate sequences
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    sg.replay(side)
+    side.synchronize()
+    assert not np.array_equal(M.cells(), want)  # a third sweep ran
+    assert SweepGraph(M, n).replay() == 0       # block >= n: no steps
+    with pytest.raises(mh.InvalidArgument):
+        mh.Sweep([])
+    pl = sg.plans[0]
+    pl.set_profiling(True)
+    with pytest.raises(mh.Unsupported):
+        mh.Sweep([pl])
+    pl.set_profiling(False)
+    g = torch.cuda.CUDAGraph()
+    cap = torch.cuda.Stream()
+    with pytest.raises(mh.Unsupported):       # a capturing stream takes the plans, not the sweep
+        with torch.cuda.graph(g, stream=cap):
+            sg.replay(cap)
 
 
 @pytest.mark.parametrize("kernel", [1, 2])
