@@ -36,6 +36,22 @@ def test_python_binding_types_every_declared_entry_point(mh):
     assert not untyped, untyped
 
 
+def test_header_is_plain_c(tmp_path):
+    """include/mhg.h is a C header (the drop-in boundary is a C ABI): it compiles as strict
+    C11 on its own, every struct and handle type usable from C."""
+    import subprocess
+    src = tmp_path / "abi.c"
+    src.write_text('#include "mhg.h"\n'
+                   "int main(void) { mhg_view v = {0, 0, 0, 0}; mhg_counters c; mhg_dist_block_t b;\n"
+                   "  mhg_dist_segment_t s; mhg_ipc_handle h; mhg_plan p = 0; mhg_sweep w = 0; mhg_matrix m = 0;\n"
+                   "  (void)v; (void)c; (void)b; (void)s; (void)h; (void)p; (void)w; (void)m;\n"
+                   "  return (int)MHG_OK; }\n")
+    r = subprocess.run(["gcc", "-std=c11", "-Wall", "-Wextra", "-pedantic", "-Werror", "-I",
+                        os.path.join(ROOT, "include"), "-fsyntax-only", str(src)],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+
+
 def test_no_torch_types_in_abi():
     src = open(os.path.join(ROOT, "include", "mhg.h")).read()
     assert "torch" not in src.split("*/", 1)[1]
