@@ -9,6 +9,7 @@
 //   - whichever side is read next is refreshed first (one bulk copy).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <utility>
@@ -34,9 +35,12 @@ public:
 
     Matrix(Matrix&& o) noexcept
         : lay_(o.lay_), mod_(o.mod_), host_(std::move(o.host_)), dev_(o.dev_), state_(o.state_),
-          dirty_lo_(o.dirty_lo_), dirty_hi_(o.dirty_hi_), pending_(o.pending_), stream_(o.stream_) {
+          dirty_lo_(o.dirty_lo_), dirty_hi_(o.dirty_hi_), writers_(std::move(o.writers_)),
+          readers_(std::move(o.readers_)), spare_(std::move(o.spare_)) {
         o.dev_ = nullptr;
-        o.pending_ = false;
+        o.writers_.clear();
+        o.readers_.clear();
+        o.spare_.clear();
     }
 
     Matrix& operator=(const Matrix& o) {
@@ -54,9 +58,12 @@ public:
 
     ~Matrix() {
         if (dev_) {
-            if (pending_) mhg_synchronize(stream_);  // work in flight still uses the store
+            for (void* ev : writers_) mhg_event_synchronize(ev);  // work in flight still uses the store
+            for (void* ev : readers_) mhg_event_synchronize(ev);
             mhg_matrix_destroy(dev_);
         }
+        for (std::vector<void*>* set : {&writers_, &readers_, &spare_})
+            for (void* ev : *set) mhg_event_destroy(ev);
     }
 
     const Layout& layout() const { return lay_; }
@@ -98,10 +105,15 @@ public:
         push();
         return dev_;
     }
-    /// The same for work about to be enqueued on `stream`: earlier asynchronous work on that
-    /// stream stays in flight (stream order covers it), work on another stream is awaited.
-    mhg_matrix device_on(void* stream) const {
-        if (pending_ && stream_ != stream) settle();
+    /// The same for work about to be enqueued on `stream`, which will write (`as_output`) or
+    /// only read the device copy.  Work still in flight from earlier asynchronous calls is
+    /// made a device-side dependency of `stream` (cudaStreamWaitEvent, no host wait) where a
+    /// sequential program implies one: a reader waits for the writers, a writer waits for the
+    /// readers.  Two writers are NOT ordered: concurrent multiplies may share an output
+    /// container as long as their output rectangles are disjoint (multiply.hpp:25-29) -- put
+    /// them on different streams and they overlap.
+    mhg_matrix device_on(void* stream, bool as_output) const {
+        for (void* ev : as_output ? readers_ : writers_) gpu::check(mhg_stream_wait_event(stream, ev));
         push();
         return dev_;
     }
@@ -109,22 +121,45 @@ public:
     void device_written() { state_ = State::DeviceNewer; }
     /// True when host-side edits are waiting to be uploaded (device() uploads them).
     bool host_newer() const { return state_ == State::HostNewer; }
-    /// Record that work enqueued on `stream` (a cudaStream_t as void*) reads or writes the
-    /// device copy and may still be running (the asynchronous multiply): the next host-side
-    /// access or upload of this matrix waits for that stream first.
-    void in_flight_on(void* stream) const {
-        if (pending_ && stream_ != stream) settle();  // one stream is remembered at a time
-        pending_ = true;
-        stream_ = stream;
+    /// Record that work just enqueued on `stream` (a cudaStream_t as void*) writes
+    /// (`as_output`) or reads the device copy: an event is recorded behind it, and the next
+    /// host-side access or upload of this matrix waits for that event.  (Events, not stream
+    /// handles: the caller may destroy the stream while the matrix lives on.)
+    void in_flight_on(void* stream, bool as_output) const {
+        std::vector<void*>& set = as_output ? writers_ : readers_;
+        for (std::size_t k = 0; k < set.size();) {  // recycle the events of finished work
+            int done = 0;
+            gpu::check(mhg_event_query(set[k], &done));
+            if (done) {
+                spare_.push_back(set[k]);
+                set[k] = set.back();
+                set.pop_back();
+            } else {
+                ++k;
+            }
+        }
+        void* ev = nullptr;
+        if (!spare_.empty()) {
+            ev = spare_.back();
+            spare_.pop_back();
+        } else {
+            gpu::check(mhg_event_create(&ev));
+        }
+        set.push_back(ev);
+        gpu::check(mhg_event_record(ev, stream));
     }
 
 private:
     enum class State { InSync, HostNewer, DeviceNewer };
 
+    /// Wait (on the host) for all asynchronous work in flight on this matrix.
     void settle() const {
-        if (pending_) {
-            gpu::check(mhg_synchronize(stream_));
-            pending_ = false;
+        for (std::vector<void*>* set : {&writers_, &readers_}) {
+            for (void* ev : *set) {
+                gpu::check(mhg_event_synchronize(ev));
+                spare_.push_back(ev);
+            }
+            set->clear();
         }
     }
     void pull() const {
@@ -169,8 +204,9 @@ private:
         std::swap(state_, o.state_);
         std::swap(dirty_lo_, o.dirty_lo_);
         std::swap(dirty_hi_, o.dirty_hi_);
-        std::swap(pending_, o.pending_);
-        std::swap(stream_, o.stream_);
+        std::swap(writers_, o.writers_);
+        std::swap(readers_, o.readers_);
+        std::swap(spare_, o.spare_);
     }
 
     Layout lay_;
@@ -179,8 +215,9 @@ private:
     mhg_matrix dev_ = nullptr;
     mutable State state_ = State::InSync;
     Index dirty_lo_ = 0, dirty_hi_ = 0;  // flat range the host copy may differ in (HostNewer)
-    mutable bool pending_ = false;   // asynchronous work may still touch the device copy ...
-    mutable void* stream_ = nullptr; // ... on this stream
+    // events recorded behind asynchronous work that writes / reads the device copy, and
+    // recycled events
+    mutable std::vector<void*> writers_, readers_, spare_;
 };
 static_assert(sizeof(Fp) == sizeof(std::uint32_t), "Fp must be layout-compatible with uint32");
 

@@ -119,21 +119,25 @@ inline Counters run(const Problem& p, Op op, std::uint32_t flags = 0) {
 /// the call returns.  Pending host-side edits of the three matrices are uploaded first.
 /// The three matrices remember the stream: their next host-side access (operator[], at,
 /// cells(), ==) or upload waits for it, so results read through the Matrix API are always
-/// complete; mh::synchronize(stream) waits explicitly.  As in the reference, concurrent
-/// calls are allowed only on disjoint output rectangles (multiply.hpp:25-29) -- here:
-/// calls in flight on different streams.
+/// complete; mh::synchronize(stream) waits explicitly.  Across streams the mirror inserts
+/// the waits a sequential program implies -- a call that reads a matrix waits for calls in
+/// flight that write it, a call that writes one waits for its readers -- except between two
+/// writers of one container: as in the reference, concurrent calls are allowed on disjoint
+/// output rectangles (multiply.hpp:25-29), here calls in flight on different streams.
 inline Counters run_async(const Problem& p, Op op, void* stream, std::uint32_t flags = 0) {
     check_problem(p);
     const bool uploads = p.a.mat->host_newer() || p.b.mat->host_newer() || p.c.mat->host_newer();
-    auto on = [&](const Sub& s) { return mhg_view{s.mat->device_on(stream), s.origin, s.rows, s.cols}; };
-    const mhg_view va = on(p.a), vb = on(p.b), vc = on(p.c);
+    auto on = [&](const Sub& s, bool as_output) {
+        return mhg_view{s.mat->device_on(stream, as_output), s.origin, s.rows, s.cols};
+    };
+    const mhg_view va = on(p.a, true), vb = on(p.b, false), vc = on(p.c, false);
     if (uploads) gpu::check(mhg_synchronize(nullptr));  // uploads run on the default stream
     mhg_counters c{};
     gpu::check(mhg_mm_ex(va, vb, vc, static_cast<mhg_op>(op), flags, &c, stream));
     p.a.mat->device_written();
-    p.a.mat->in_flight_on(stream);
-    p.b.mat->in_flight_on(stream);
-    p.c.mat->in_flight_on(stream);
+    p.a.mat->in_flight_on(stream, true);
+    p.b.mat->in_flight_on(stream, false);
+    p.c.mat->in_flight_on(stream, false);
     return to_counters(c);
 }
 

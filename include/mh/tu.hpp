@@ -112,11 +112,15 @@ public:
     std::uint64_t run_async(void* stream) {
         if (!sweep_) return 0;
         const bool upload = mat_->host_newer();
-        (void)mat_->device_on(stream);  // pending host edits travel first (default stream)
+        // the sweep reads and writes the parent: it waits for readers and writers on other
+        // streams, and later work on other streams waits for it either way
+        (void)mat_->device_on(stream, true);
+        (void)mat_->device_on(stream, false);  // pending host edits travel first (default stream)
         if (upload) gpu::check(mhg_synchronize(nullptr));
         gpu::check(mhg_sweep_run(sweep_, stream));
         mat_->device_written();
-        mat_->in_flight_on(stream);
+        mat_->in_flight_on(stream, true);
+        mat_->in_flight_on(stream, false);
         return macs_;
     }
 

@@ -147,6 +147,22 @@ mhg_status mhg_rowmajor_host_to_mh(mhg_matrix dst, const uint32_t *host_rows);
 mhg_status mhg_mh_to_rowmajor_host(mhg_matrix src, uint32_t *host_rows);
 /* cudaStreamSynchronize(stream) for callers that do not link the CUDA runtime. */
 mhg_status mhg_synchronize(void *stream);
+/* Streams for such callers: a cudaStream_t as void* on the current device (non_blocking != 0:
+ * cudaStreamNonBlocking, i.e. not ordered with the default stream).  The reference allows
+ * concurrent multiplies on disjoint output rectangles (multiply.hpp:25-29); here they run
+ * on different streams. */
+mhg_status mhg_stream_create(void **stream, int non_blocking);
+mhg_status mhg_stream_destroy(void *stream);
+/* Events (cudaEvent_t as void*, timing disabled) for the same callers: the C++ mirror's
+ * Matrix orders asynchronous multiplies on different streams with them.  An event stays
+ * valid after the stream it was recorded on is destroyed.  mhg_event_query: *done = 1 when
+ * the work captured by the last record has completed. */
+mhg_status mhg_event_create(void **event);
+mhg_status mhg_event_record(void *event, void *stream);
+mhg_status mhg_event_query(void *event, int *done);
+mhg_status mhg_event_synchronize(void *event);
+mhg_status mhg_stream_wait_event(void *stream, void *event);
+mhg_status mhg_event_destroy(void *event);
 
 /* ---- multiply (multiply.hpp) ---- */
 /* out op= lhs * rhs over the three views, computed on the GPU with the int8

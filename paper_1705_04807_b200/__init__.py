@@ -152,6 +152,14 @@ def lib():
         "mhg_rowmajor_host_to_mh": ([vp, vp], C.c_int),
         "mhg_mh_to_rowmajor_host": ([vp, vp], C.c_int),
         "mhg_synchronize": ([vp], C.c_int),
+        "mhg_stream_create": ([P(vp), C.c_int], C.c_int),
+        "mhg_stream_destroy": ([vp], C.c_int),
+        "mhg_event_create": ([P(vp)], C.c_int),
+        "mhg_event_record": ([vp, vp], C.c_int),
+        "mhg_event_query": ([vp, P(C.c_int)], C.c_int),
+        "mhg_event_synchronize": ([vp], C.c_int),
+        "mhg_stream_wait_event": ([vp, vp], C.c_int),
+        "mhg_event_destroy": ([vp], C.c_int),
         "mhg_mm": ([_View, _View, _View, C.c_int, P(Counters), vp], C.c_int),
         "mhg_mm_ex": ([_View, _View, _View, C.c_int, u32, P(Counters), vp], C.c_int),
         "mhg_plan_create_ex": ([_View, _View, _View, C.c_int, u32, P(vp)], C.c_int),

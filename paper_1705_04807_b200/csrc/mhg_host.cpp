@@ -865,6 +865,71 @@ mhg_status mhg_synchronize(void* stream) {
     });
 }
 
+mhg_status mhg_stream_create(void** stream, int non_blocking) {
+    return guarded([&] {
+        if (!stream) fail(MHG_ERR_INVALID_ARGUMENT, "stream_create: null output");
+        require_device();
+        cudaStream_t s = nullptr;
+        cuda_check(cudaStreamCreateWithFlags(&s, non_blocking ? cudaStreamNonBlocking : cudaStreamDefault),
+                   "stream create");
+        *stream = s;
+    });
+}
+
+mhg_status mhg_stream_destroy(void* stream) {
+    return guarded([&] {
+        if (!stream) return;
+        cuda_check(cudaStreamDestroy((cudaStream_t)stream), "stream destroy");
+    });
+}
+
+mhg_status mhg_event_create(void** event) {
+    return guarded([&] {
+        if (!event) fail(MHG_ERR_INVALID_ARGUMENT, "event_create: null output");
+        require_device();
+        cudaEvent_t e = nullptr;
+        cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event create");
+        *event = e;
+    });
+}
+
+mhg_status mhg_event_record(void* event, void* stream) {
+    return guarded([&] {
+        if (!event) fail(MHG_ERR_INVALID_ARGUMENT, "event_record: null event");
+        cuda_check(cudaEventRecord((cudaEvent_t)event, (cudaStream_t)stream), "event record");
+    });
+}
+
+mhg_status mhg_event_query(void* event, int* done) {
+    return guarded([&] {
+        if (!event || !done) fail(MHG_ERR_INVALID_ARGUMENT, "event_query: null pointer");
+        const cudaError_t e = cudaEventQuery((cudaEvent_t)event);
+        if (e != cudaSuccess && e != cudaErrorNotReady) cuda_check(e, "event query");
+        *done = e == cudaSuccess;
+    });
+}
+
+mhg_status mhg_event_synchronize(void* event) {
+    return guarded([&] {
+        if (!event) fail(MHG_ERR_INVALID_ARGUMENT, "event_synchronize: null event");
+        cuda_check(cudaEventSynchronize((cudaEvent_t)event), "event synchronize");
+    });
+}
+
+mhg_status mhg_stream_wait_event(void* stream, void* event) {
+    return guarded([&] {
+        if (!event) fail(MHG_ERR_INVALID_ARGUMENT, "stream_wait_event: null event");
+        cuda_check(cudaStreamWaitEvent((cudaStream_t)stream, (cudaEvent_t)event, 0), "stream wait event");
+    });
+}
+
+mhg_status mhg_event_destroy(void* event) {
+    return guarded([&] {
+        if (!event) return;
+        cuda_check(cudaEventDestroy((cudaEvent_t)event), "event destroy");
+    });
+}
+
 mhg_status mhg_rowmajor_host_to_mh(mhg_matrix dst, const uint32_t* host_rows) {
     return guarded([&] {
         if (!dst || !host_rows) fail(MHG_ERR_INVALID_ARGUMENT, "rowmajor_host_to_mh: null pointer");

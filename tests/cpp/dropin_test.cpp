@@ -749,6 +749,39 @@ void test_async_variant() {
     CHECK(throws_as<std::logic_error>([&] {
         mh::mm_oblivious_async(mh::Problem{p.a, mh::Sub{&C, 0, 200, 120}, p.c});
     }));
+    // the reference's concurrency contract (multiply.hpp:25-29): two multiplies on disjoint
+    // output rectangles of one container, in flight on two non-blocking streams
+    void *s1 = nullptr, *s2 = nullptr;
+    CHECK(mhg_stream_create(&s1, 1) == MHG_OK && mhg_stream_create(&s2, 1) == MHG_OK && s1 && s2);
+    mh::Matrix A2 = mh::from_row_major(ga, t, mod), B2 = mh::from_row_major(gb, t, mod);
+    mh::Grid want = mh::to_row_major(C);
+    const mh::Problem top{mh::Sub{&C, mh::encode(C.layout(), 0, 0), 100, 256},
+                          mh::Sub{&A, mh::encode(A.layout(), 5, 0), 100, 256},
+                          mh::Sub{&B, mh::encode(B.layout(), 0, 0), 256, 256}};
+    const mh::Problem bottom{mh::Sub{&C, mh::encode(C.layout(), 100, 0), 156, 256},
+                             mh::Sub{&A2, mh::encode(A2.layout(), 50, 0), 156, 256},
+                             mh::Sub{&B2, mh::encode(B2.layout(), 0, 0), 256, 256}};
+    for (int rep = 0; rep < 3; ++rep) {
+        mh::mm_oblivious_async(top, mh::Op::Add, s1);
+        mh::mm_oblivious_async(bottom, mh::Op::Sub, s2);  // both write C (disjoint rows): concurrent
+        dense_acc(want, ga, gb, 0, 0, 5, 0, 0, 0, 100, 256, 256, q, false);
+        dense_acc(want, ga, gb, 100, 0, 50, 0, 0, 0, 156, 256, 256, q, true);
+    }
+    CHECK(mh::to_row_major(C) == want);  // the read waits for both streams C is in flight on
+    // a dependent call on another stream: B2 = B2 + C * A2-like chain -- reading C on s2 waits
+    // for its writers on s1
+    mh::Matrix D = mh::from_row_major(gc, t, mod);
+    const mh::Problem into_c{mh::Sub{&C, 0, 64, 64}, mh::Sub{&A, 0, 64, 64}, mh::Sub{&B, 0, 64, 64}};
+    const mh::Problem from_c{mh::Sub{&D, 0, 64, 64}, mh::Sub{&C, 0, 64, 64}, mh::Sub{&B2, 0, 64, 64}};
+    mh::mm_oblivious_async(into_c, mh::Op::Add, s1);
+    mh::mm_oblivious_async(from_c, mh::Op::Add, s2);
+    dense_acc(want, ga, gb, 0, 0, 0, 0, 0, 0, 64, 64, 64, q, false);
+    mh::Grid want_d = gc;
+    dense_acc(want_d, want, gb, 0, 0, 0, 0, 0, 0, 64, 64, 64, q, false);
+    CHECK(mh::to_row_major(D) == want_d && mh::to_row_major(C) == want);
+    mh::synchronize(s1);
+    mh::synchronize(s2);
+    CHECK(mhg_stream_destroy(s1) == MHG_OK && mhg_stream_destroy(s2) == MHG_OK);
 }
 
 // detail::dilate / undilate (layout.hpp:15-33) against the codec, and detail::JumpTracker
@@ -818,6 +851,7 @@ int main() {
             std::fprintf(stderr, "FAIL %s: exception %s\n", name, e.what());
         }
         std::printf("%s %s\n", g_fail == before ? "PASS" : "FAIL", name);
+        std::fflush(stdout);  // keep the log if a later test dies
     }
     std::printf("%d checks, %d failures\n", g_checks, g_fail);
     return g_fail ? 1 : 0;
