@@ -110,8 +110,7 @@ public:
     /// made a device-side dependency of `stream` (cudaStreamWaitEvent, no host wait) where a
     /// sequential program implies one: a reader waits for the writers, a writer waits for the
     /// readers.  Two writers are NOT ordered: concurrent multiplies may share an output
-    /// container as long as their output rectangles are disjoint (multiply.hpp:25-29) -- put
-    /// them on different streams and they overlap.
+    /// container as long as their output rectangles are disjoint (multiply.hpp:25-29).
     mhg_matrix device_on(void* stream, bool as_output) const {
         for (void* ev : as_output ? readers_ : writers_) gpu::check(mhg_stream_wait_event(stream, ev));
         push();

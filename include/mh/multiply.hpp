@@ -123,7 +123,10 @@ inline Counters run(const Problem& p, Op op, std::uint32_t flags = 0) {
 /// the waits a sequential program implies -- a call that reads a matrix waits for calls in
 /// flight that write it, a call that writes one waits for its readers -- except between two
 /// writers of one container: as in the reference, concurrent calls are allowed on disjoint
-/// output rectangles (multiply.hpp:25-29), here calls in flight on different streams.
+/// output rectangles (multiply.hpp:25-29), here calls in flight on different streams.  (The
+/// engine's one-shot entry point packs into one workspace per device and orders its users
+/// with an event, so two such calls are both in flight but their kernels still run one
+/// after the other; plans -- mhg_plan, a workspace each -- are what overlaps on the GPU.)
 inline Counters run_async(const Problem& p, Op op, void* stream, std::uint32_t flags = 0) {
     check_problem(p);
     const bool uploads = p.a.mat->host_newer() || p.b.mat->host_newer() || p.c.mat->host_newer();
