@@ -7,7 +7,8 @@
 //                                   from_row_major / to_row_major (device kernels)
 //   views         mh/submatrix.hpp  Sub, Aligned, split_sub, quadrants, predicates
 //   multiply      mh/multiply.hpp   Problem, Counters, mm_oblivious (+ Op::Sub / Op::Set),
-//                                   mm_naive, mm_default, compatible_parts
+//                                   mm_naive, mm_default, base_case_mm, compatible_parts,
+//                                   mm_oblivious_async (explicit stream), synchronize
 //   protocol      mh/bench.hpp      Config, Rng, gen_problem, run_trials, CSV writers
 //   fixtures      mh/io.hpp         load_matrix / save_matrix text format
 //   TU driver     mh/tu.hpp         schur_views, schur_update, SchurSweep (aliased Schur updates)
